@@ -1,0 +1,312 @@
+/*
+ * lscat.h — C ABI of the B200-native LS-CAT hot path (arXiv 2103.14409).
+ *
+ * Citations: P:n = line n of the paper text (PAPER.md, final IEEE version P:46-324),
+ * S:n = SPEC.md line n (interfaces/test ideas only), DESIGN.md §x = this repo's readings.
+ *
+ * The hot path is the paper's thread-block-size sweep and the analysis of
+ * its runtime table:
+ *   register suite (a1) -> plan/shard (a2) -> launch (a3) + time (a4) -> emit table (a5)
+ *   -> per-group reduce (a6) -> global accumulate (a7) -> percentiles (a8)
+ *   -> multi-GPU merge (a9) -> finalize stats (a10).
+ *
+ * Conventions for every function below
+ *   - Returns lscat_status; LSCAT_OK == 0.  Never aborts the process, never prints.
+ *   - On LSCAT_ERR_INVALID_ARG no output is written (arguments are checked first).
+ *   - A sticky CUDA error (e.g. an illegal address) poisons the context: every later call
+ *     on it returns LSCAT_ERR_CUDA.  lscat_last_error() gives the message.
+ *   - `stream` is a cudaStream_t passed as an opaque pointer (NULL = legacy default stream).
+ *   - Device pointers are plain CUDA device addresses (e.g. torch tensor data_ptr()).
+ *     "CALLER-OWNED" buffers stay owned by the caller; the library never frees them.
+ *   - With world > 1 (lscat_comm_init), lscat_sweep, lscat_reduce_table and lscat_stats are
+ *     collective: every rank calls them in the same order with the same options.
+ *   - There is no CPU fallback: without a CUDA device every compute call returns
+ *     LSCAT_ERR_CUDA.  Host-only helpers (plan, work model, status strings) need no GPU.
+ */
+#ifndef LSCAT_H
+#define LSCAT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LSCAT_ABI_VERSION 1
+
+typedef enum {
+  LSCAT_OK = 0,
+  LSCAT_ERR_INVALID_ARG = 1, /* bad argument; nothing written (maps to SPEC exit 2) */
+  LSCAT_ERR_CUDA = 2,        /* CUDA runtime/driver error, or ctx poisoned */
+  LSCAT_ERR_OOM = 3,         /* device or pinned-host allocation failed */
+  LSCAT_ERR_NCCL = 4,        /* NCCL error during a collective */
+  LSCAT_ERR_STATE = 5,       /* call out of order (e.g. sweep before register_suite) */
+  LSCAT_ERR_UNSUPPORTED = 6  /* feature not built in / not available on this device */
+} lscat_status;
+
+/* Row status of one sweep point (S:233 RunOutcome; NaN runtime iff status != OK). */
+typedef enum {
+  LSCAT_ROW_OK = 0,
+  LSCAT_ROW_TIMEOUT = 1,        /* predicted or measured point time > timeout_s */
+  LSCAT_ROW_LAUNCH_ERROR = 2,   /* cudaLaunch* returned an error for this configuration */
+  LSCAT_ROW_INVALID_CONFIG = 3  /* the kernel has no implementation at this block size */
+} lscat_row_status;
+
+/* The self-written suite (the paper's scraped kernels are unavailable, its
+   only named kernel is euclidean_kernel). */
+typedef enum {
+  LSCAT_K_EUCLID = 0,    /* d[i] = sqrt(sum_j (A[i][j]-q[j])^2)                       */
+  LSCAT_K_MATVEC = 1,    /* y[i] = sum_j A[i][j] x[j]                                 */
+  LSCAT_K_GEMM_BF16 = 2, /* C = A Bt^T, bf16 in, fp32 accumulate (TMEM), bf16 out     */
+  LSCAT_K_TRANSPOSE = 3, /* B[j][i] = A[i][j]                                         */
+  LSCAT_K_AXPY = 4,      /* z = 0.5 x + y over N*N elements                           */
+  LSCAT_K_ROWSUM = 5,    /* r[i] = sum_j A[i][j]                                      */
+  LSCAT_K_COLSUM = 6,    /* c[j] = sum_i A[i][j]                                      */
+  LSCAT_K_STENCIL5 = 7,  /* 5-point average, interior; border copied                  */
+  LSCAT_K_COUNT = 8,
+  LSCAT_K_SPIN = 100     /* TEST ONLY: spins `spin_ns` ns per launch (timeout tests)  */
+} lscat_kernel;
+
+/* Suite buffer slots. in0 = A (or x for axpy), in1 = q / x / Bt / y, out = result. */
+typedef enum { LSCAT_SLOT_IN0 = 0, LSCAT_SLOT_IN1 = 1, LSCAT_SLOT_OUT = 2 } lscat_slot;
+
+typedef enum { LSCAT_MEM_DEVICE = 0, LSCAT_MEM_HOST = 1 } lscat_mem;
+typedef enum { LSCAT_LAUNCH_GRAPH = 0, LSCAT_LAUNCH_STREAM = 1 } lscat_launch_mode;
+typedef enum { LSCAT_SHARD_POINT_LPT = 0, LSCAT_SHARD_GROUP = 1 } lscat_shard;
+typedef enum { LSCAT_SKIPNA = 0, LSCAT_COMPLETE_ONLY = 1 } lscat_nan_policy;
+
+typedef struct lscat_ctx lscat_ctx; /* one per process/rank and device; opaque */
+
+/* ---------------------------------------------------------------- context ---------- */
+int lscat_abi_version(void);
+const char* lscat_status_string(lscat_status s);
+
+/* Create a context on CUDA device `device`.  `seed` seeds the on-device input generator
+   (DESIGN.md §6).  *out receives the context (CALLEE-OWNED; free with lscat_ctx_destroy). */
+lscat_status lscat_ctx_create(int device, uint64_t seed, lscat_ctx** out);
+void lscat_ctx_destroy(lscat_ctx* ctx);
+/* Message of the last failing call on ctx ("" if none).  Valid until the next call on ctx. */
+const char* lscat_last_error(const lscat_ctx* ctx);
+
+/* Multi-GPU (a9).  lscat_comm_unique_id writes a 128-byte ncclUniqueId into `out` (rank 0
+   calls it and broadcasts the bytes, e.g. with torch.distributed).  lscat_comm_init creates
+   the NCCL communicator of `world` ranks; world == 1 is valid and makes collectives no-ops. */
+lscat_status lscat_comm_unique_id(void* out /* 128 bytes */);
+lscat_status lscat_comm_init(lscat_ctx* ctx, const void* unique_id, int rank, int world);
+
+/* ------------------------------------------------------------- a1: suite ------------ */
+/* Materialise the inputs of every (kernel, N) pair: N x N row-major matrices (fp32, bf16 for
+   the GEMM) filled on the device with a counter-based generator, uniform in [-1, 1)
+   (reading R-15).  Outputs are allocated too.  The library owns these buffers until
+   lscat_ctx_destroy.  Re-registering replaces the previous suite.  Sizes: 1 <= N <= 16384.
+   (the generated main "initialize[s] all the needed variables".) */
+lscat_status lscat_register_suite(lscat_ctx* ctx, const uint32_t* kernels, uint32_t n_kernels,
+                                  const uint32_t* matrix_sizes, uint32_t n_sizes, void* stream);
+
+/* Device address and byte size of a registered suite buffer (for verification).  Returns
+   LSCAT_ERR_INVALID_ARG if the kernel/N/slot is not registered or the slot is unused. */
+lscat_status lscat_suite_buffer(lscat_ctx* ctx, uint32_t kernel, uint32_t n, uint32_t slot,
+                                void** dev_ptr, uint64_t* bytes);
+
+/* Overwrite a registered input slot from `src` (host or device per `src_mem`), `bytes` must
+   equal the slot size.  Host sources should be pinned for asynchronous copies. */
+lscat_status lscat_suite_upload(lscat_ctx* ctx, uint32_t kernel, uint32_t n, uint32_t slot,
+                                const void* src, uint64_t bytes, uint32_t src_mem, void* stream);
+
+/* ------------------------------------------------------------- a3: launch ----------- */
+/* One launch of suite kernel `kernel` over N at `block_threads` threads per block
+   (32..1024, multiple of 32: P:98).  Asynchronous.  Returns LSCAT_ERR_INVALID_ARG for
+   an illegal block and LSCAT_ERR_UNSUPPORTED when the kernel has no implementation at that
+   block size (the GEMM needs >= 128 threads; the sweep records such points as
+   LSCAT_ROW_INVALID_CONFIG). */
+lscat_status lscat_launch(lscat_ctx* ctx, uint32_t kernel, uint32_t n, uint32_t block_threads,
+                          void* stream);
+
+/* Algorithmic work of one launch: bytes that must cross HBM and FLOPs.
+   Host-only; needs no GPU. */
+lscat_status lscat_kernel_work(uint32_t kernel, uint32_t n, uint64_t* bytes, uint64_t* flops);
+
+/* ------------------------------------------------------------- a2: plan ------------- */
+typedef struct {
+  const uint32_t* kernels;  uint32_t n_kernels;   /* in sweep order                       */
+  const uint32_t* sizes;    uint32_t n_sizes;     /* ascending N                          */
+  const uint16_t* blocks;   uint32_t n_blocks;    /* threads; unique, ascending, %32 == 0, */
+                                                  /* 32..1024    */
+  uint32_t warmup, brackets, launches_per_bracket;/* paper: 1, 10, 1000    */
+  uint32_t shard;                                 /* lscat_shard                          */
+  double launch_overhead_s;                       /* cost model t_launch (0 -> 2e-6)      */
+  double hbm_bytes_per_s, tensor_flops_per_s;     /* cost model peaks (0 -> defaults)     */
+} lscat_plan_opts;
+
+/* Points are numbered p = (kernel_index * n_sizes + size_index) * n_blocks + block_index
+   (kernel-major canonical order); group g = p / n_blocks.  Writes the ids of the points owned
+   by `rank` of `world`, ascending, into out_points[cap]; *n_out = their count.  Sharding is
+   LPT on the cost model (W + K*R) * max(bytes/BW, flops/TC, t_launch), ties broken by point
+   id then rank for LSCAT_SHARD_POINT_LPT, or LPT over whole groups for
+   LSCAT_SHARD_GROUP.  Deterministic; host-only; needs no GPU.  ("By using
+   cudaSetDevice, the additional GPUs could run the script in parallel".) */
+lscat_status lscat_plan(const lscat_plan_opts* opts, int rank, int world, uint32_t* out_points,
+                        uint64_t cap, uint64_t* n_out);
+
+/* ------------------------------------------------------------- a4/a5: sweep --------- */
+typedef struct {
+  const uint16_t* blocks;   uint32_t n_blocks;    /* as lscat_plan_opts                   */
+  uint32_t warmup;                                /* preheat launches (1)          */
+  uint32_t brackets;                              /* K timed brackets (median: 10) */
+  uint32_t launches_per_bracket;                  /* R launches per bracket (1000) */
+  double timeout_s;                               /* per point (30; 2 on GTX 980)  */
+  uint32_t launch_mode;                           /* lscat_launch_mode                    */
+  uint32_t shard;                                 /* lscat_shard (world > 1)              */
+  double launch_overhead_s;                       /* cost model, as lscat_plan_opts       */
+  uint64_t spin_ns;                               /* LSCAT_K_SPIN only                    */
+  float* bracket_ms_host;                         /* optional [cap_rows * brackets] host  */
+} lscat_sweep_opts;
+
+/* Runtime table, structure of arrays (a5; the paper's dataframe rows).
+   Group g owns rows [group_offset[g], group_offset[g+1]), or rows [g*rows_per_group, ...)
+   when rows_per_group != 0 (then group_offset may be NULL).  Rows of a group need not be
+   sorted; (group, block_id) pairs must be unique.  Buffers are CALLER-OWNED and live in
+   device memory (mem == LSCAT_MEM_DEVICE) or host memory (LSCAT_MEM_HOST; the library
+   stages them through device scratch, copies counted in the e2e measurement). */
+typedef struct {
+  float* runtime_ms;        /* [cap_rows] per-launch milliseconds; NaN = no result        */
+  uint16_t* block_id;       /* [cap_rows] index into the block list (ascending threads)   */
+  uint8_t* status;          /* [cap_rows] lscat_row_status (written by sweep/gen; may be  */
+                            /*            NULL for reduce, which never reads it)          */
+  int64_t* group_offset;    /* [cap_groups + 1]                                           */
+  uint32_t* group_kernel;   /* [cap_groups] kernel id (may be NULL for reduce)           */
+  uint32_t* group_matrix;   /* [cap_groups] matrix-size index; NULL -> (first_group+g) %  */
+                            /*              n_matrices                                    */
+  uint64_t cap_rows, cap_groups;
+  uint64_t n_rows, n_groups;/* out of sweep/gen, in to reduce                             */
+  uint32_t rows_per_group;  /* != 0 -> uniform groups                                     */
+  uint32_t mem;             /* lscat_mem                                                  */
+  uint64_t first_group;     /* global index of this table's group 0 (group-aligned shards)*/
+} lscat_table;
+
+/* Run this rank's points: per point `warmup` launches, then `brackets` brackets of
+   `launches_per_bracket` launches each timed with CUDA events on `stream`; runtime = median
+   over brackets of (bracket ms / R) (even count -> midpoint).  A point
+   whose warm-up predicts, or whose measured brackets reach, more than timeout_s gets NaN +
+   TIMEOUT.  Writes ALL groups of the plan (n_groups = n_kernels * n_sizes, canonical order,
+   groups without local rows are empty) and this rank's rows, grouped, ascending block id.
+   Synchronous with respect to the host.  Requires lscat_register_suite for every kernel/N. */
+lscat_status lscat_sweep(lscat_ctx* ctx, const uint32_t* kernels, uint32_t n_kernels,
+                         const uint32_t* sizes, uint32_t n_sizes, const lscat_sweep_opts* opts,
+                         lscat_table* out, void* stream);
+
+/* ------------------------------------------------------------- a6-a9: reduce -------- */
+typedef struct {
+  uint32_t n_blocks;          /* |L|                                                        */
+  uint32_t largest_block_id;  /* l = id of the 1024-thread block             */
+  uint32_t n_matrices;        /* rows of best_block_hist                                    */
+  uint32_t nan_policy;        /* lscat_nan_policy; SKIPNA = pandas semantics        */
+  uint32_t bins_per_unit;     /* 100 -> 1 % bins                                            */
+  uint32_t gain_cap;          /* 10 -> gain bins [0, 10) + one overflow bin                 */
+  uint32_t gain_gt_num, gain_gt_den;   /* 1/5: "more than 20 %", strict             */
+  uint32_t perf_lt_num, perf_lt_den;   /* 17/20: "less than 85 %", strict           */
+  uint32_t band_lo_num, band_lo_den;   /* 2/5: "from 40 to 85 %", [2/5, 17/20)      */
+  uint32_t point_sharded;     /* 1 -> groups are split across ranks: per-group merge first  */
+} lscat_reduce_opts;
+
+/* Fills `opts` with the defaults above for a block list of n_blocks with largest id l. */
+void lscat_reduce_opts_default(lscat_reduce_opts* opts, uint32_t n_blocks, uint32_t n_matrices);
+
+/* Per-group outputs, device, CALLER-OWNED, each [n_groups] and each may be NULL. */
+typedef struct {
+  uint16_t* best_block_id;  /* argmin block id; 0xFFFF if the group is not defined        */
+  float* best_runtime;      /* min runtime; NaN if not defined                             */
+  double* perf;             /* RN(best / r_l); NaN unless ratio_defined           */
+  double* gain;             /* RN(RN(r_l / best) - 1); NaN unless ratio_defined    */
+  uint32_t* flags;          /* LSCAT_GF_* bits                                             */
+} lscat_reduce_out;
+
+#define LSCAT_GF_DEFINED 0x001u
+#define LSCAT_GF_COMPLETE 0x002u
+#define LSCAT_GF_ALL_NAN 0x004u
+#define LSCAT_GF_RATIO_DEFINED 0x008u
+#define LSCAT_GF_LARGEST_IS_BEST 0x010u
+#define LSCAT_GF_LARGEST_SLOWER 0x020u
+#define LSCAT_GF_GAIN_GT 0x040u
+#define LSCAT_GF_PERF_LT 0x080u
+#define LSCAT_GF_PERF_BAND 0x100u
+#define LSCAT_GF_LARGEST_MISSING 0x200u
+
+/* Number of uint64 words of the packed partial vector (the NCCL payload of a9). */
+size_t lscat_partials_len(const lscat_reduce_opts* opts);
+
+/* Reduce a runtime table to per-group results and packed integer partials (DESIGN.md §4,
+   steps O3.1-O3.9).  Integer outputs are exact and independent of row order, block order
+   within a group and shard count.  With world > 1 the partials are summed over ranks (and,
+   if point_sharded, per-group minima/maxima/counts are merged first) with NCCL.  The result
+   stays in the context for lscat_stats.  Asynchronous unless table->mem == HOST. */
+lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* table,
+                                const lscat_reduce_opts* opts, lscat_reduce_out* out,
+                                void* stream);
+
+/* ------------------------------------------------------------- a8/a10: stats -------- */
+typedef struct {
+  /* exact counters */
+  uint64_t n_rows, n_ok, n_nan, n_invalid;
+  uint64_t n_groups, n_defined, n_all_nan, n_complete, n_incomplete;
+  uint64_t n_largest_missing, n_ratio_defined;
+  uint64_t n_largest_is_best, n_largest_strictly_slower;
+  uint64_t n_gain_gt, n_perf_lt, n_perf_band;
+  /* fixed-point sums: sum floor(perf*2^52) and sum floor(min(gain,2^20)*2^32), each as
+     hi = sum(fx >> 21), lo = sum(fx & (2^21-1)) */
+  uint64_t perf_fx_hi, perf_fx_lo, gain_fx_hi, gain_fx_lo;
+  /* derived on the host */
+  double frac_nonnan;           /* n_ok / n_rows ("97% non NaN")                     */
+  double frac_largest_not_best; /* (ratio_defined - largest_is_best) / ratio_defined */
+  double frac_gain_gt;          /* n_gain_gt / n_ratio_defined ("10 %")             */
+  double frac_perf_lt;          /* n_perf_lt / n_ratio_defined ("12 %")             */
+  double frac_perf_band;        /* n_perf_band / n_ratio_defined ("1 %")            */
+  double mean_perf;             /* P:258 "98.7 %", "86 %"                           */
+  double mean_gain;             /* P:307 "6 %"                                            */
+  /* optional caller-owned HOST arrays (NULL to skip) */
+  uint64_t* perf_hist;          /* [bins_per_unit + 1]; bin k: k*t <= nb*b < (k+1)*t      */
+  uint64_t* gain_hist;          /* [gain_cap*bins_per_unit + 1]; last = overflow          */
+  uint64_t* best_block_hist;    /* [n_matrices * n_blocks]                                 */
+  const double* percentiles;    /* [n_percentiles] in [0, 1]; nearest rank                 */
+  uint32_t n_percentiles;       /* <= 64                                                   */
+  double* pct_perf;             /* [n_percentiles] out; NaN if no ratio-defined group     */
+  double* pct_gain;             /* [n_percentiles] out                                     */
+} lscat_stats_out;
+
+/* Finalize the statistics of the last lscat_reduce_table on ctx (a10) and, when
+   out->n_percentiles > 0, select the exact nearest-rank percentiles of perf and gain over
+   ratio-defined groups (a8).  Synchronizes `stream`; collective when world > 1. */
+lscat_status lscat_stats(lscat_ctx* ctx, const lscat_reduce_opts* opts, lscat_stats_out* out,
+                         void* stream);
+
+/* ------------------------------------------------- synthetic tables (test/bench) ---- */
+typedef enum { LSCAT_PRESET_T4 = 0, LSCAT_PRESET_GTX980 = 1 } lscat_preset;
+
+typedef struct {
+  uint64_t n_rows_global;   /* total rows of the global table (layout rule) */
+  uint32_t n_kernels;       /* kernel ids K                                                */
+  uint32_t n_blocks;        /* |L| (block ids 0..|L|-1, threads 32*(id+1))                 */
+  uint32_t largest_block_id;
+  uint32_t n_matrices;      /* matrix index = position within the kernel's groups         */
+  uint32_t preset;          /* lscat_preset                                                */
+  double nan_rate;          /* iid per row (3 %)                                    */
+  uint64_t seed;
+  /* shard selection: rows of global groups [group_begin, group_end) ...                   */
+  uint64_t group_begin, group_end;  /* group_end == 0 -> all groups                        */
+  uint32_t block_mod, block_rem;    /* ... keeping only block ids with id % mod == rem     */
+                                    /* (mod 0 or 1 -> all; point-sharded tables)           */
+} lscat_gen_opts;
+
+/* Write a synthetic runtime table shaped like the paper's dataset (planted-best runtime
+   model) into `out` (device memory).  Bit-identical to synth/tables.py. */
+lscat_status lscat_gen_table(lscat_ctx* ctx, const lscat_gen_opts* opts, lscat_table* out,
+                             void* stream);
+/* Sizes the buffers lscat_gen_table needs for `opts` (host-only). */
+lscat_status lscat_gen_table_shape(const lscat_gen_opts* opts, uint64_t* n_rows,
+                                   uint64_t* n_groups);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LSCAT_H */
