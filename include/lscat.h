@@ -18,8 +18,9 @@
  *   - `stream` is a cudaStream_t passed as an opaque pointer (NULL = legacy default stream).
  *   - Device pointers are plain CUDA device addresses (e.g. torch tensor data_ptr()).
  *     "CALLER-OWNED" buffers stay owned by the caller; the library never frees them.
- *   - With world > 1 (lscat_comm_init), lscat_sweep, lscat_reduce_table and lscat_stats are
- *     collective: every rank calls them in the same order with the same options.
+ *   - With world > 1 (lscat_comm_init), lscat_reduce_table and lscat_stats are collective:
+ *     every rank calls them in the same order with the same options.  lscat_sweep is not a
+ *     collective; each rank sweeps the points lscat_plan assigns to it.
  *   - There is no CPU fallback: without a CUDA device every compute call returns
  *     LSCAT_ERR_CUDA.  Host-only helpers (plan, work model, status strings) need no GPU.
  */
@@ -88,6 +89,9 @@ lscat_status lscat_ctx_create(int device, uint64_t seed, lscat_ctx** out);
 void lscat_ctx_destroy(lscat_ctx* ctx);
 /* Message of the last failing call on ctx ("" if none).  Valid until the next call on ctx. */
 const char* lscat_last_error(const lscat_ctx* ctx);
+/* Number of device kernels the library has launched on ctx so far (graph-launched kernels
+   counted one by one).  Used by bench.py for its gpu_launches claim. */
+lscat_status lscat_launch_count(const lscat_ctx* ctx, uint64_t* out);
 
 /* Multi-GPU (a9).  lscat_comm_unique_id writes a 128-byte ncclUniqueId into `out` (rank 0
    calls it and broadcasts the bytes, e.g. with torch.distributed).  lscat_comm_init creates
@@ -208,6 +212,8 @@ typedef struct {
   uint32_t perf_lt_num, perf_lt_den;   /* 17/20: "less than 85 %", strict           */
   uint32_t band_lo_num, band_lo_den;   /* 2/5: "from 40 to 85 %", [2/5, 17/20)      */
   uint32_t point_sharded;     /* 1 -> groups are split across ranks: per-group merge first  */
+  uint32_t keep_values;       /* 1 -> keep per-group perf/gain (caller arrays or ctx        */
+                              /*      scratch) for the percentiles of lscat_stats           */
 } lscat_reduce_opts;
 
 /* Fills `opts` with the defaults above for a block list of n_blocks with largest id l. */
@@ -220,7 +226,22 @@ typedef struct {
   double* perf;             /* RN(best / r_l); NaN unless ratio_defined           */
   double* gain;             /* RN(RN(r_l / best) - 1); NaN unless ratio_defined    */
   uint32_t* flags;          /* LSCAT_GF_* bits                                             */
+  uint64_t* partials;       /* [lscat_partials_len] merged packed partials, or NULL        */
+                            /* (the library keeps its own copy for lscat_stats either way) */
 } lscat_reduce_out;
+
+/* Layout of the packed partial vector (uint64 words), LSCAT_P_* counter slots first, then
+   perf_hist [bins_per_unit+1], gain_hist [gain_cap*bins_per_unit+1], best_block_hist
+   [n_matrices*n_blocks]. */
+enum {
+  LSCAT_P_ROWS = 0, LSCAT_P_OK, LSCAT_P_NAN, LSCAT_P_INVALID,
+  LSCAT_P_GROUPS, LSCAT_P_DEFINED, LSCAT_P_ALL_NAN, LSCAT_P_COMPLETE, LSCAT_P_INCOMPLETE,
+  LSCAT_P_LARGEST_MISSING, LSCAT_P_RATIO_DEFINED,
+  LSCAT_P_LARGEST_IS_BEST, LSCAT_P_LARGEST_SLOWER, LSCAT_P_GAIN_GT, LSCAT_P_PERF_LT,
+  LSCAT_P_PERF_BAND, LSCAT_P_PERF_FX_HI, LSCAT_P_PERF_FX_LO, LSCAT_P_GAIN_FX_HI,
+  LSCAT_P_GAIN_FX_LO,
+  LSCAT_P_NCOUNTERS = 24 /* padded */
+};
 
 #define LSCAT_GF_DEFINED 0x001u
 #define LSCAT_GF_COMPLETE 0x002u

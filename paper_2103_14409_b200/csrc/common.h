@@ -1,0 +1,126 @@
+// common.h — internal types of liblscat (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <map>
+#include <memory>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "lscat.h"
+
+namespace lscat {
+
+constexpr int kMaxBlockIdx = 32;  // block sizes 32..1024 in steps of 32
+
+// Device buffers of one registered (kernel, N) pair.
+struct SuiteEntry {
+  uint32_t kernel = 0, n = 0;
+  void* in0 = nullptr;
+  void* in1 = nullptr;
+  void* out = nullptr;
+  uint64_t in0_bytes = 0, in1_bytes = 0, out_bytes = 0;
+  void* scratch = nullptr;  // colsum: partials + tile counters; gemm: tensor maps
+  uint64_t scratch_bytes = 0;
+};
+
+struct LaunchArgs {
+  const SuiteEntry* e;
+  uint64_t spin_ns;
+};
+
+// One launch of a suite kernel at block index bi (threads = 32*(bi+1)).  Returns the
+// cudaGetLastError() of the launch (cudaSuccess on success).
+using LaunchFn = cudaError_t (*)(const LaunchArgs&, cudaStream_t);
+
+// Per-kernel dispatch: nullptr entries = no implementation at that block (INVALID_CONFIG).
+struct KernelTable {
+  LaunchFn fn[kMaxBlockIdx];
+};
+
+// registries filled by each kernel translation unit
+const KernelTable& table_euclid();
+const KernelTable& table_matvec();
+const KernelTable& table_rowsum();
+const KernelTable& table_colsum();
+const KernelTable& table_transpose();
+const KernelTable& table_axpy();
+const KernelTable& table_stencil5();
+const KernelTable& table_gemm();
+const KernelTable& table_spin();
+const KernelTable* kernel_table(uint32_t kernel);
+
+// suite buffer preparation that needs kernel-specific knowledge
+cudaError_t colsum_prepare(SuiteEntry& e);
+cudaError_t gemm_prepare(SuiteEntry& e);
+
+// reducer scratch kept between lscat_reduce_table and lscat_stats
+struct ReduceState {
+  bool valid = false;
+  lscat_reduce_opts opts{};
+  uint64_t n_groups = 0;       // groups of the reduced table
+  uint64_t own_lo = 0, own_hi = 0;  // groups whose values feed percentiles on this rank
+  double* perf = nullptr;      // device [n_groups] (caller's or scratch)
+  double* gain = nullptr;
+  uint64_t* partials = nullptr;  // device, len = partials_len (SUM-merged)
+  uint64_t* minmax = nullptr;    // device [4]: perf min, perf max, gain min, gain max keys
+};
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace lscat
+
+struct lscat_ctx {
+  int device = 0;
+  uint64_t seed = 0;
+  bool poisoned = false;
+  std::string err;
+  int sm_count = 0;
+  uint64_t launches = 0;  // device kernels launched (lscat_launch_count)
+  size_t l2_bytes = 0;
+  // suite
+  std::map<std::pair<uint32_t, uint32_t>, lscat::SuiteEntry> suite;
+  // graphs: (kernel, n, block_idx, chunk) -> exec
+  std::map<std::tuple<uint32_t, uint32_t, uint32_t, uint32_t>, cudaGraphExec_t> graphs;
+  cudaStream_t capture_stream = nullptr;
+  std::vector<cudaEvent_t> events;
+  // comm
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  // reducer scratch
+  lscat::ReduceState rs;
+  std::map<std::string, lscat::DevBuf> scratch;
+};
+
+namespace lscat {
+
+// error helpers ---------------------------------------------------------------------------
+lscat_status fail(lscat_ctx* ctx, lscat_status s, const char* fmt, ...);
+lscat_status cuda_fail(lscat_ctx* ctx, cudaError_t e, const char* what);
+bool is_sticky(cudaError_t e);
+// device scratch (grow-only) keyed by name
+void* scratch(lscat_ctx* ctx, const char* name, size_t bytes, cudaError_t* err);
+// host-side work model
+void kernel_work(uint32_t kernel, uint32_t n, uint64_t* bytes, uint64_t* flops);
+bool block_list_ok(const uint16_t* blocks, uint32_t n);
+
+}  // namespace lscat
+
+#define LSCAT_CHECK_CTX(ctx)                                                        \
+  do {                                                                              \
+    if (!(ctx)) return LSCAT_ERR_INVALID_ARG;                                       \
+    if ((ctx)->poisoned) return LSCAT_ERR_CUDA;                                     \
+  } while (0)
+
+#define LSCAT_CUDA(ctx, call)                                                       \
+  do {                                                                              \
+    cudaError_t e__ = (call);                                                       \
+    if (e__ != cudaSuccess) return lscat::cuda_fail((ctx), e__, #call);             \
+  } while (0)

@@ -1,0 +1,61 @@
+// kern_common.cuh — device helpers shared by the suite kernels (not by the reducer).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <utility>
+
+#include "common.h"
+
+namespace lscat {
+
+// Streaming 128-bit load: read-only path, no L1 allocation (each element is read once).
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float ld_stream(const float* p) {
+  float r;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
+  return r;
+}
+// Streaming store (evict-first in L2, the output is not re-read by this launch).
+__device__ __forceinline__ void st_stream(float4* p, float4 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(float* p, float v) { __stcs(p, v); }
+
+template <int B>
+__device__ __forceinline__ float block_sum(float v, float* red /* [B/32] smem */) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if constexpr (B == 32) {
+    return v;
+  } else {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    v = (l < B / 32) ? red[l] : 0.f;
+    if (w == 0) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    }
+    return v;  // valid in warp 0
+  }
+}
+
+// Builds a KernelTable whose entry i launches Launcher<32*(i+1)>::launch (or nullptr when
+// Launcher<B>::kSupported is false).
+template <template <int> class Launcher, int... Is>
+KernelTable make_table_impl(std::integer_sequence<int, Is...>) {
+  KernelTable t{};
+  ((t.fn[Is] = Launcher<32 * (Is + 1)>::kSupported ? &Launcher<32 * (Is + 1)>::launch : nullptr),
+   ...);
+  return t;
+}
+template <template <int> class Launcher>
+KernelTable make_table() {
+  return make_table_impl<Launcher>(std::make_integer_sequence<int, kMaxBlockIdx>{});
+}
+
+}  // namespace lscat

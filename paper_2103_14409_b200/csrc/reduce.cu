@@ -1,0 +1,533 @@
+// reduce.cu — a6 (per-group reduce), a7 (global accumulate), a9 (NCCL merge) and
+// a8/a10 (percentile selection, finalize) of the runtime-table analysis.
+//
+// The paper's statistics are group-wise: per (kernel, matrix size)
+// slice, the best block, the largest (1024) block's performance b/t and the optimal block's
+// gain t/b - 1; then shares, means and histograms over slices.  DESIGN.md §4 lists the exact
+// definitions (readings R-4..R-13) this kernel implements; the integer outputs (argmin ids,
+// counts, histograms, fixed-point sums) are exact and order independent, so they are
+// bit-identical to the CPU oracle and across shard counts.
+//
+// Kernel layout: persistent grid, a warp takes 32 consecutive groups at a
+// time; for each group the 32 lanes load one row each (one coalesced 128 B runtime load + 64 B
+// block ids, 8 groups' loads in flight per lane), find the minimum with two redux.sync.min
+// (runtime bits, then block id among the minima: positive finite fp32 bit patterns order like
+// their values), count with ballots, pick the largest block's row with a ballot; the result of
+// group j lands in lane j, and the 32 lanes then finalise their 32 groups in parallel (f64
+// ratios, exact bins, flags) into shared-memory histograms and per-thread counters, flushed
+// once per CTA with 64-bit atomics.  HBM: 6 B/row read (+16 B/group of perf/gain written).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "common.h"
+
+namespace lscat {
+namespace {
+
+enum { MODE_FUSED = 0, MODE_GROUP_PARTIALS = 1, MODE_FINALIZE_MERGED = 2 };
+constexpr int kNC = LSCAT_P_NCOUNTERS;
+
+struct RP {
+  const float* rt;
+  const uint16_t* bid;
+  const int64_t* off;
+  const uint32_t* gmat;
+  uint64_t n_groups, first_group;
+  uint32_t rpg;
+  uint64_t n_rows;
+  uint32_t L, ell, M, policy, nb, cap;
+  uint32_t ggn, ggd, pln, pld, bln, bld;
+  // per-group outputs (may be null)
+  uint16_t* o_best;
+  float* o_bestrt;
+  double* o_perf;
+  double* o_gain;
+  uint32_t* o_flags;
+  // accumulation
+  uint64_t* partials;
+  uint64_t* minmax;  // [4] perf min/max key, gain min/max key over accumulated groups
+  uint64_t acc_lo, acc_hi;
+  // point-sharded merge arrays
+  uint64_t* g_key;
+  uint64_t* g_lcode;
+  uint32_t* g_cnt;  // [3*G]: n_ok, n_nan, n_rows
+  int mode;
+  uint32_t smem_words;  // perf + gain + best-block histogram words in smem
+};
+
+struct GroupAcc {
+  uint32_t min_bits, min_bid;  // 0xFFFFFFFF if no ok row
+  uint32_t n_ok, n_nan, n_rows;
+  uint32_t lcode;  // 0 absent, 1 present but no result, 2 present with a result
+  uint32_t l_bits;
+};
+
+struct ThreadAcc {
+  uint64_t c[kNC];
+  uint64_t pmin, pmax, gmin, gmax;
+};
+
+__device__ __forceinline__ bool ok_bits(uint32_t b) { return b - 1u < 0x7F7FFFFFu; }  // 0 < b < 0x7F800000
+__device__ __forceinline__ bool nan_bits(uint32_t b) { return (b & 0x7FFFFFFFu) > 0x7F800000u; }
+
+// Fold one chunk of <= 32 rows (lane-distributed) into the warp-uniform accumulator.
+__device__ __forceinline__ void fold_chunk(GroupAcc& a, bool valid, uint32_t bits, uint32_t b,
+                                           uint32_t ell) {
+  const unsigned FULL = 0xffffffffu;
+  const bool ok = valid && ok_bits(bits);
+  const uint32_t m = __reduce_min_sync(FULL, ok ? bits : 0xFFFFFFFFu);
+  const uint32_t mb = __reduce_min_sync(FULL, (ok && bits == m) ? b : 0xFFFFFFFFu);
+  if (m < a.min_bits || (m == a.min_bits && mb < a.min_bid)) { a.min_bits = m; a.min_bid = mb; }
+  a.n_ok += __popc(__ballot_sync(FULL, ok));
+  a.n_nan += __popc(__ballot_sync(FULL, valid && nan_bits(bits)));
+  a.n_rows += __popc(__ballot_sync(FULL, valid));
+  const unsigned lb = __ballot_sync(FULL, valid && b == ell);
+  if (lb) {
+    const uint32_t lbits = __shfl_sync(FULL, bits, __ffs(lb) - 1);
+    a.lcode = ok_bits(lbits) ? 2u : 1u;
+    a.l_bits = lbits;
+  }
+}
+
+__device__ __forceinline__ uint64_t f64_key(double v) { return (uint64_t)__double_as_longlong(v); }
+
+// The paper's per-group statistics from the merged accumulator (O3 steps 3-9).
+__device__ void finalize_group(const RP& p, uint64_t g, const GroupAcc& a, ThreadAcc& t,
+                               uint32_t* sh_perf, uint32_t* sh_gain, uint32_t* sh_bb) {
+  const bool acc = g >= p.acc_lo && g < p.acc_hi;
+  const bool complete = a.n_rows == p.L && a.n_ok == a.n_rows;
+  const bool defined = p.policy ? complete : a.n_ok >= 1;
+  uint32_t flags = 0;
+  if (a.n_ok == 0) flags |= LSCAT_GF_ALL_NAN;
+  if (complete) flags |= LSCAT_GF_COMPLETE;
+  double perf = __longlong_as_double(0x7FF8000000000000ll), gain = perf;
+  if (defined) {
+    flags |= LSCAT_GF_DEFINED;
+    const uint32_t mat = p.gmat ? p.gmat[g] : (uint32_t)((p.first_group + g) % p.M);
+    if (acc) atomicAdd(&sh_bb[mat * p.L + a.min_bid], 1u);
+    if (a.lcode == 2) {
+      flags |= LSCAT_GF_RATIO_DEFINED;
+      const double b = (double)__uint_as_float(a.min_bits), tt = (double)__uint_as_float(a.l_bits);
+      perf = __ddiv_rn(b, tt);
+      gain = __dsub_rn(__ddiv_rn(tt, b), 1.0);
+      if (a.min_bid == p.ell) flags |= LSCAT_GF_LARGEST_IS_BEST;
+      if (tt > b) flags |= LSCAT_GF_LARGEST_SLOWER;
+      // exact rational predicates: products of an fp32 value and an integer < 2^29 are exact
+      if (__dmul_rn((double)p.ggd, tt) > __dmul_rn((double)(p.ggd + p.ggn), b)) flags |= LSCAT_GF_GAIN_GT;
+      const bool plt = __dmul_rn((double)p.pld, b) < __dmul_rn((double)p.pln, tt);
+      if (plt) flags |= LSCAT_GF_PERF_LT;
+      if (plt && __dmul_rn((double)p.bld, b) >= __dmul_rn((double)p.bln, tt)) flags |= LSCAT_GF_PERF_BAND;
+      if (acc) {
+        const double nbb = __dmul_rn((double)p.nb, b), nbt = __dmul_rn((double)p.nb, tt);
+        // perf bin: largest k with k t <= nb b (estimate, then exact fix-up)
+        int k = (int)floor(__ddiv_rn(nbb, tt));
+        while (__dmul_rn((double)(k + 1), tt) <= nbb) k++;
+        while (k > 0 && __dmul_rn((double)k, tt) > nbb) k--;
+        atomicAdd(&sh_perf[k], 1u);
+        // gain bin: overflow iff t >= (cap+1) b; else m - nb, m = largest with m b <= nb t
+        int gb;
+        if (tt >= __dmul_rn((double)(p.cap + 1), b)) {
+          gb = (int)(p.cap * p.nb);
+        } else {
+          int m = (int)floor(__ddiv_rn(nbt, b));
+          while (__dmul_rn((double)(m + 1), b) <= nbt) m++;
+          while (__dmul_rn((double)m, b) > nbt) m--;
+          gb = m - (int)p.nb;
+        }
+        atomicAdd(&sh_gain[gb], 1u);
+        const uint64_t fxp = (uint64_t)__dmul_rn(perf, 4503599627370496.0);  // floor(perf 2^52)
+        const double gc = gain < 1048576.0 ? gain : 1048576.0;
+        const uint64_t fxg = (uint64_t)__dmul_rn(gc, 4294967296.0);          // floor(gain 2^32)
+        t.c[LSCAT_P_PERF_FX_HI] += fxp >> 21;
+        t.c[LSCAT_P_PERF_FX_LO] += fxp & ((1ull << 21) - 1);
+        t.c[LSCAT_P_GAIN_FX_HI] += fxg >> 21;
+        t.c[LSCAT_P_GAIN_FX_LO] += fxg & ((1ull << 21) - 1);
+        const uint64_t kp = f64_key(perf), kg = f64_key(gain);
+        t.pmin = min(t.pmin, kp); t.pmax = max(t.pmax, kp);
+        t.gmin = min(t.gmin, kg); t.gmax = max(t.gmax, kg);
+      }
+    } else {
+      flags |= LSCAT_GF_LARGEST_MISSING;
+    }
+  }
+  if (acc) {
+    t.c[LSCAT_P_GROUPS] += 1;
+    t.c[LSCAT_P_ROWS] += a.n_rows;
+    t.c[LSCAT_P_OK] += a.n_ok;
+    t.c[LSCAT_P_NAN] += a.n_nan;
+    t.c[LSCAT_P_INVALID] += a.n_rows - a.n_ok - a.n_nan;
+    t.c[LSCAT_P_DEFINED] += (flags & LSCAT_GF_DEFINED) != 0;
+    t.c[LSCAT_P_ALL_NAN] += (flags & LSCAT_GF_ALL_NAN) != 0;
+    t.c[LSCAT_P_COMPLETE] += complete;
+    t.c[LSCAT_P_INCOMPLETE] += !complete;
+    t.c[LSCAT_P_LARGEST_MISSING] += (flags & LSCAT_GF_LARGEST_MISSING) != 0;
+    t.c[LSCAT_P_RATIO_DEFINED] += (flags & LSCAT_GF_RATIO_DEFINED) != 0;
+    t.c[LSCAT_P_LARGEST_IS_BEST] += (flags & LSCAT_GF_LARGEST_IS_BEST) != 0;
+    t.c[LSCAT_P_LARGEST_SLOWER] += (flags & LSCAT_GF_LARGEST_SLOWER) != 0;
+    t.c[LSCAT_P_GAIN_GT] += (flags & LSCAT_GF_GAIN_GT) != 0;
+    t.c[LSCAT_P_PERF_LT] += (flags & LSCAT_GF_PERF_LT) != 0;
+    t.c[LSCAT_P_PERF_BAND] += (flags & LSCAT_GF_PERF_BAND) != 0;
+  }
+  if (p.o_best) p.o_best[g] = defined ? (uint16_t)a.min_bid : (uint16_t)0xFFFF;
+  if (p.o_bestrt) p.o_bestrt[g] = defined ? __uint_as_float(a.min_bits) : __int_as_float(0x7FC00000);
+  if (p.o_perf) p.o_perf[g] = perf;
+  if (p.o_gain) p.o_gain[g] = gain;
+  if (p.o_flags) p.o_flags[g] = flags;
+}
+
+__device__ void flush(const RP& p, ThreadAcc& t, uint64_t* sh_c, uint32_t* sh) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int i = 0; i < kNC; i++) {
+    uint64_t v = t.c[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    if (lane == 0 && v) atomicAdd((unsigned long long*)&sh_c[i], (unsigned long long)v);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    t.pmin = min(t.pmin, (uint64_t)__shfl_xor_sync(FULL, t.pmin, o));
+    t.pmax = max(t.pmax, (uint64_t)__shfl_xor_sync(FULL, t.pmax, o));
+    t.gmin = min(t.gmin, (uint64_t)__shfl_xor_sync(FULL, t.gmin, o));
+    t.gmax = max(t.gmax, (uint64_t)__shfl_xor_sync(FULL, t.gmax, o));
+  }
+  if (lane == 0 && t.pmin <= t.pmax) {
+    atomicMin((unsigned long long*)&p.minmax[0], (unsigned long long)t.pmin);
+    atomicMax((unsigned long long*)&p.minmax[1], (unsigned long long)t.pmax);
+    atomicMin((unsigned long long*)&p.minmax[2], (unsigned long long)t.gmin);
+    atomicMax((unsigned long long*)&p.minmax[3], (unsigned long long)t.gmax);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kNC; i += blockDim.x)
+    if (sh_c[i]) atomicAdd((unsigned long long*)&p.partials[i], (unsigned long long)sh_c[i]);
+  for (uint32_t i = threadIdx.x; i < p.smem_words; i += blockDim.x)
+    if (sh[i]) atomicAdd((unsigned long long*)&p.partials[kNC + i], (unsigned long long)sh[i]);
+}
+
+__device__ __forceinline__ void init_shared(const RP& p, uint64_t* sh_c, uint32_t* sh, ThreadAcc& t) {
+  for (int i = threadIdx.x; i < kNC; i += blockDim.x) sh_c[i] = 0;
+  for (uint32_t i = threadIdx.x; i < p.smem_words; i += blockDim.x) sh[i] = 0;
+#pragma unroll
+  for (int i = 0; i < kNC; i++) t.c[i] = 0;
+  t.pmin = t.gmin = ~0ull;
+  t.pmax = t.gmax = 0;
+  __syncthreads();
+}
+
+constexpr int kU = 8;  // groups whose rows are in flight per lane
+
+__global__ void __launch_bounds__(256) reduce_groups_kernel(RP p) {
+  extern __shared__ uint64_t dyn[];
+  uint64_t* sh_c = dyn;
+  uint32_t* sh = reinterpret_cast<uint32_t*>(dyn + kNC);
+  uint32_t* sh_perf = sh;
+  uint32_t* sh_gain = sh + (p.nb + 1);
+  uint32_t* sh_bb = sh_gain + (p.cap * p.nb + 1);
+  ThreadAcc t;
+  init_shared(p, sh_c, sh, t);
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t base = warp * 32; base < p.n_groups; base += nwarps * 32) {
+    // group row ranges: lane l holds [lo, hi) of group base + l
+    const uint64_t gl = base + lane;
+    int64_t lo = 0, hi = 0;
+    if (gl < p.n_groups) {
+      if (p.rpg) {
+        lo = (int64_t)(gl * p.rpg);
+        hi = min((int64_t)(lo + p.rpg), (int64_t)p.n_rows);
+      } else {
+        lo = p.off[gl];
+        hi = p.off[gl + 1];
+      }
+    }
+    GroupAcc mine;
+    mine.min_bits = mine.min_bid = 0xFFFFFFFFu;
+    mine.n_ok = mine.n_nan = mine.n_rows = 0;
+    mine.lcode = 0;
+    mine.l_bits = 0;
+    const int nj = (int)min((uint64_t)32, p.n_groups - base);
+    for (int j0 = 0; j0 < nj; j0 += kU) {
+      uint32_t bits[kU], bb[kU];
+      int64_t r0[kU], r1[kU];
+#pragma unroll
+      for (int u = 0; u < kU; u++) {
+        r0[u] = __shfl_sync(FULL, lo, j0 + u);
+        r1[u] = __shfl_sync(FULL, hi, j0 + u);
+        const int64_t r = r0[u] + lane;
+        const bool v = (j0 + u < nj) && r < r1[u];
+        bits[u] = v ? __float_as_uint(__ldcs(p.rt + r)) : 0u;
+        bb[u] = v ? (uint32_t)__ldcs(p.bid + r) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; u++) {
+        if (j0 + u >= nj) break;
+        GroupAcc a;
+        a.min_bits = a.min_bid = 0xFFFFFFFFu;
+        a.n_ok = a.n_nan = a.n_rows = 0;
+        a.lcode = 0;
+        a.l_bits = 0;
+        fold_chunk(a, r0[u] + lane < r1[u], bits[u], bb[u], p.ell);
+        for (int64_t c = r0[u] + 32; c < r1[u]; c += 32) {  // groups of more than 32 rows
+          const int64_t r = c + lane;
+          const bool v = r < r1[u];
+          fold_chunk(a, v, v ? __float_as_uint(__ldcs(p.rt + r)) : 0u,
+                     v ? (uint32_t)__ldcs(p.bid + r) : 0u, p.ell);
+        }
+        if (lane == j0 + u) mine = a;
+      }
+    }
+    if (lane < nj) {
+      const uint64_t g = base + lane;
+      if (p.mode == MODE_FUSED) {
+        finalize_group(p, g, mine, t, sh_perf, sh_gain, sh_bb);
+      } else {  // MODE_GROUP_PARTIALS: per-group values for the NCCL MIN/MAX/SUM merge
+        p.g_key[g] = mine.min_bits == 0xFFFFFFFFu ? ~0ull
+                                                   : (((uint64_t)mine.min_bits << 32) | mine.min_bid);
+        p.g_lcode[g] = mine.lcode == 2 ? ((1ull << 32) | mine.l_bits) : (uint64_t)mine.lcode;
+        p.g_cnt[3 * g + 0] = mine.n_ok;
+        p.g_cnt[3 * g + 1] = mine.n_nan;
+        p.g_cnt[3 * g + 2] = mine.n_rows;
+      }
+    }
+  }
+  flush(p, t, sh_c, sh);
+}
+
+__global__ void __launch_bounds__(256) finalize_merged_kernel(RP p) {
+  extern __shared__ uint64_t dyn[];
+  uint64_t* sh_c = dyn;
+  uint32_t* sh = reinterpret_cast<uint32_t*>(dyn + kNC);
+  uint32_t* sh_perf = sh;
+  uint32_t* sh_gain = sh + (p.nb + 1);
+  uint32_t* sh_bb = sh_gain + (p.cap * p.nb + 1);
+  ThreadAcc t;
+  init_shared(p, sh_c, sh, t);
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < p.n_groups;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    GroupAcc a;
+    const uint64_t key = p.g_key[g], lc = p.g_lcode[g];
+    a.min_bits = key == ~0ull ? 0xFFFFFFFFu : (uint32_t)(key >> 32);
+    a.min_bid = key == ~0ull ? 0xFFFFFFFFu : (uint32_t)(key & 0xFFFFFFFFu);
+    a.n_ok = p.g_cnt[3 * g];
+    a.n_nan = p.g_cnt[3 * g + 1];
+    a.n_rows = p.g_cnt[3 * g + 2];
+    a.lcode = lc >> 32 ? 2u : (uint32_t)lc;
+    a.l_bits = (uint32_t)(lc & 0xFFFFFFFFu);
+    finalize_group(p, g, a, t, sh_perf, sh_gain, sh_bb);
+  }
+  flush(p, t, sh_c, sh);
+}
+
+__global__ void init_minmax(uint64_t* mm) {
+  mm[0] = ~0ull; mm[1] = 0; mm[2] = ~0ull; mm[3] = 0;
+}
+
+__global__ void init_group_merge(uint64_t* key, uint64_t* lc, uint32_t* cnt, uint64_t G) {
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < G;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    key[g] = ~0ull; lc[g] = 0; cnt[3 * g] = cnt[3 * g + 1] = cnt[3 * g + 2] = 0;
+  }
+}
+
+size_t partials_len(const lscat_reduce_opts& o) {
+  return (size_t)kNC + (o.bins_per_unit + 1) + ((size_t)o.gain_cap * o.bins_per_unit + 1) +
+         (size_t)o.n_matrices * o.n_blocks;
+}
+
+bool opts_ok(const lscat_reduce_opts* o) {
+  if (!o) return false;
+  if (o->n_blocks == 0 || o->n_blocks > 65535 || o->largest_block_id >= o->n_blocks) return false;
+  if (o->n_matrices == 0 || o->bins_per_unit == 0 || o->gain_cap == 0) return false;
+  if (o->bins_per_unit > 100000 || (uint64_t)o->gain_cap * o->bins_per_unit > 1000000) return false;
+  if (o->gain_gt_den == 0 || o->perf_lt_den == 0 || o->band_lo_den == 0) return false;
+  if ((uint64_t)o->gain_gt_den + o->gain_gt_num >= (1u << 29)) return false;
+  if (o->perf_lt_num >= (1u << 29) || o->perf_lt_den >= (1u << 29)) return false;
+  if (o->band_lo_num >= (1u << 29) || o->band_lo_den >= (1u << 29)) return false;
+  if (o->nan_policy > LSCAT_COMPLETE_ONLY) return false;
+  return true;
+}
+
+lscat_status nccl_check(lscat_ctx* ctx, ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return LSCAT_OK;
+  return fail(ctx, LSCAT_ERR_NCCL, "%s: %s", what, ncclGetErrorString(r));
+}
+
+}  // namespace
+}  // namespace lscat
+
+using namespace lscat;
+
+extern "C" {
+
+void lscat_reduce_opts_default(lscat_reduce_opts* o, uint32_t n_blocks, uint32_t n_matrices) {
+  if (!o) return;
+  memset(o, 0, sizeof *o);
+  o->n_blocks = n_blocks;
+  o->largest_block_id = n_blocks ? n_blocks - 1 : 0;
+  o->n_matrices = n_matrices;
+  o->nan_policy = LSCAT_SKIPNA;
+  o->bins_per_unit = 100;
+  o->gain_cap = 10;
+  o->gain_gt_num = 1; o->gain_gt_den = 5;
+  o->perf_lt_num = 17; o->perf_lt_den = 20;
+  o->band_lo_num = 2; o->band_lo_den = 5;
+  o->point_sharded = 0;
+  o->keep_values = 1;
+}
+
+size_t lscat_partials_len(const lscat_reduce_opts* o) { return opts_ok(o) ? partials_len(*o) : 0; }
+
+lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lscat_reduce_opts* o,
+                                lscat_reduce_out* out, void* stream) {
+  LSCAT_CHECK_CTX(ctx);
+  if (!T || !opts_ok(o)) return fail(ctx, LSCAT_ERR_INVALID_ARG, "reduce_table: bad table or options");
+  if (!T->runtime_ms || !T->block_id || (!T->rows_per_group && !T->group_offset) ||
+      T->mem > LSCAT_MEM_HOST)
+    return fail(ctx, LSCAT_ERR_INVALID_ARG, "reduce_table: table needs runtime_ms, block_id and offsets");
+  if (T->rows_per_group && (T->n_groups != (T->n_rows + T->rows_per_group - 1) / T->rows_per_group))
+    return fail(ctx, LSCAT_ERR_INVALID_ARG, "reduce_table: n_groups != ceil(n_rows / rows_per_group)");
+  const size_t sh_words = (o->bins_per_unit + 1) + ((size_t)o->gain_cap * o->bins_per_unit + 1) +
+                          (size_t)o->n_matrices * o->n_blocks;
+  const size_t smem = kNC * 8 + sh_words * 4;
+  if (smem > 200 * 1024)
+    return fail(ctx, LSCAT_ERR_UNSUPPORTED, "reduce_table: histograms need %zu B of shared memory", smem);
+  cudaStream_t s = (cudaStream_t)stream;
+  LSCAT_CUDA(ctx, cudaSetDevice(ctx->device));
+  const uint64_t G = T->n_groups, n = T->n_rows;
+  lscat_reduce_out dummy{};
+  if (!out) out = &dummy;
+  cudaError_t err;
+
+  RP p{};
+  // stage host tables through device scratch (e2e path)
+  if (T->mem == LSCAT_MEM_HOST) {
+    float* rt = (float*)scratch(ctx, "h_rt", n * 4, &err);
+    if (err) return cuda_fail(ctx, err, "reduce_table: scratch");
+    uint16_t* bid = (uint16_t*)scratch(ctx, "h_bid", n * 2, &err);
+    if (err) return cuda_fail(ctx, err, "reduce_table: scratch");
+    LSCAT_CUDA(ctx, cudaMemcpyAsync(rt, T->runtime_ms, n * 4, cudaMemcpyHostToDevice, s));
+    LSCAT_CUDA(ctx, cudaMemcpyAsync(bid, T->block_id, n * 2, cudaMemcpyHostToDevice, s));
+    p.rt = rt;
+    p.bid = bid;
+    if (!T->rows_per_group) {
+      int64_t* off = (int64_t*)scratch(ctx, "h_off", (G + 1) * 8, &err);
+      if (err) return cuda_fail(ctx, err, "reduce_table: scratch");
+      LSCAT_CUDA(ctx, cudaMemcpyAsync(off, T->group_offset, (G + 1) * 8, cudaMemcpyHostToDevice, s));
+      p.off = off;
+    }
+    if (T->group_matrix) {
+      uint32_t* gm = (uint32_t*)scratch(ctx, "h_gm", G * 4, &err);
+      if (err) return cuda_fail(ctx, err, "reduce_table: scratch");
+      LSCAT_CUDA(ctx, cudaMemcpyAsync(gm, T->group_matrix, G * 4, cudaMemcpyHostToDevice, s));
+      p.gmat = gm;
+    }
+  } else {
+    p.rt = T->runtime_ms;
+    p.bid = T->block_id;
+    p.off = T->group_offset;
+    p.gmat = T->group_matrix;
+  }
+  p.n_groups = G;
+  p.first_group = T->first_group;
+  p.rpg = T->rows_per_group;
+  p.n_rows = n;
+  p.L = o->n_blocks; p.ell = o->largest_block_id; p.M = o->n_matrices; p.policy = o->nan_policy;
+  p.nb = o->bins_per_unit; p.cap = o->gain_cap;
+  p.ggn = o->gain_gt_num; p.ggd = o->gain_gt_den; p.pln = o->perf_lt_num; p.pld = o->perf_lt_den;
+  p.bln = o->band_lo_num; p.bld = o->band_lo_den;
+  p.smem_words = (uint32_t)sh_words;
+  p.o_best = out->best_block_id;
+  p.o_bestrt = out->best_runtime;
+  p.o_perf = out->perf;
+  p.o_gain = out->gain;
+  p.o_flags = out->flags;
+  if (o->keep_values) {
+    if (!p.o_perf) { p.o_perf = (double*)scratch(ctx, "perf", G * 8, &err); if (err) return cuda_fail(ctx, err, "scratch"); }
+    if (!p.o_gain) { p.o_gain = (double*)scratch(ctx, "gain", G * 8, &err); if (err) return cuda_fail(ctx, err, "scratch"); }
+  }
+  const size_t plen = partials_len(*o);
+  p.partials = (uint64_t*)scratch(ctx, "partials", plen * 8, &err);
+  if (err) return cuda_fail(ctx, err, "reduce_table: scratch");
+  p.minmax = (uint64_t*)scratch(ctx, "minmax", 4 * 8, &err);
+  if (err) return cuda_fail(ctx, err, "reduce_table: scratch");
+  LSCAT_CUDA(ctx, cudaMemsetAsync(p.partials, 0, plen * 8, s));
+  init_minmax<<<1, 1, 0, s>>>(p.minmax);
+  ctx->launches++;
+  if (smem > 48 * 1024) {
+    LSCAT_CUDA(ctx, cudaFuncSetAttribute(reduce_groups_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    LSCAT_CUDA(ctx, cudaFuncSetAttribute(finalize_merged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
+  const bool merge = ctx->world > 1 && o->point_sharded;
+  const uint64_t warps_needed = (G + 31) / 32;
+  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)ctx->sm_count * 8, (warps_needed + 7) / 8));
+  p.acc_lo = 0;
+  p.acc_hi = G;
+  uint64_t own_lo = 0, own_hi = G;
+  if (!merge) {
+    p.mode = MODE_FUSED;
+    if (G) reduce_groups_kernel<<<grid, 256, smem, s>>>(p), ctx->launches++;
+    LSCAT_CUDA(ctx, cudaGetLastError());
+  } else {
+    // a9, point-sharded: per-group MIN(key) / MAX(l-code) / SUM(counts) over ranks, then each
+    // rank accumulates its contiguous share of the groups.
+    uint64_t* key = (uint64_t*)scratch(ctx, "g_key", G * 8, &err);
+    if (err) return cuda_fail(ctx, err, "scratch");
+    uint64_t* lc = (uint64_t*)scratch(ctx, "g_lcode", G * 8, &err);
+    if (err) return cuda_fail(ctx, err, "scratch");
+    uint32_t* cnt = (uint32_t*)scratch(ctx, "g_cnt", G * 12, &err);
+    if (err) return cuda_fail(ctx, err, "scratch");
+    init_group_merge<<<ctx->sm_count * 4, 256, 0, s>>>(key, lc, cnt, G);
+    p.g_key = key; p.g_lcode = lc; p.g_cnt = cnt;
+    p.mode = MODE_GROUP_PARTIALS;
+    if (G) reduce_groups_kernel<<<grid, 256, smem, s>>>(p);
+    LSCAT_CUDA(ctx, cudaGetLastError());
+    lscat_status ns;
+    if ((ns = nccl_check(ctx, ncclGroupStart(), "ncclGroupStart"))) return ns;
+    ncclAllReduce(key, key, G, ncclUint64, ncclMin, ctx->comm, s);
+    ncclAllReduce(lc, lc, G, ncclUint64, ncclMax, ctx->comm, s);
+    ncclAllReduce(cnt, cnt, 3 * G, ncclUint32, ncclSum, ctx->comm, s);
+    if ((ns = nccl_check(ctx, ncclGroupEnd(), "allreduce per-group merge"))) return ns;
+    own_lo = G * ctx->rank / ctx->world;
+    own_hi = G * (ctx->rank + 1) / ctx->world;
+    p.acc_lo = own_lo;
+    p.acc_hi = own_hi;
+    // reset accumulators written by the partial pass (none: partials untouched by mode 1
+    // except zero-valued flushes), then finalize all groups, accumulating the owned range
+    LSCAT_CUDA(ctx, cudaMemsetAsync(p.partials, 0, plen * 8, s));
+    init_minmax<<<1, 1, 0, s>>>(p.minmax);
+    p.mode = MODE_FINALIZE_MERGED;
+    const int g2 = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)ctx->sm_count * 4, (G + 255) / 256));
+    if (G) finalize_merged_kernel<<<g2, 256, smem, s>>>(p);
+    LSCAT_CUDA(ctx, cudaGetLastError());
+  }
+  if (ctx->world > 1) {
+    lscat_status ns;
+    if ((ns = nccl_check(ctx, ncclGroupStart(), "ncclGroupStart"))) return ns;
+    ncclAllReduce(p.partials, p.partials, plen, ncclUint64, ncclSum, ctx->comm, s);
+    ncclAllReduce(p.minmax, p.minmax, 1, ncclUint64, ncclMin, ctx->comm, s);
+    ncclAllReduce(p.minmax + 1, p.minmax + 1, 1, ncclUint64, ncclMax, ctx->comm, s);
+    ncclAllReduce(p.minmax + 2, p.minmax + 2, 1, ncclUint64, ncclMin, ctx->comm, s);
+    ncclAllReduce(p.minmax + 3, p.minmax + 3, 1, ncclUint64, ncclMax, ctx->comm, s);
+    if ((ns = nccl_check(ctx, ncclGroupEnd(), "allreduce partials"))) return ns;
+  }
+  if (out->partials) LSCAT_CUDA(ctx, cudaMemcpyAsync(out->partials, p.partials, plen * 8, cudaMemcpyDeviceToDevice, s));
+  ReduceState& rs = ctx->rs;
+  rs.valid = true;
+  rs.opts = *o;
+  rs.n_groups = G;
+  rs.own_lo = own_lo;
+  rs.own_hi = own_hi;
+  rs.perf = o->keep_values ? p.o_perf : out->perf;
+  rs.gain = o->keep_values ? p.o_gain : out->gain;
+  rs.partials = p.partials;
+  rs.minmax = p.minmax;
+  if (T->mem == LSCAT_MEM_HOST) LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
+  return LSCAT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,469 @@
+"""Thin ctypes binding of liblscat.so (include/lscat.h).
+
+Argument marshalling only: every step of the hot path runs in the library's CUDA kernels.
+Torch is used for device memory and streams (tensors own the table buffers).  There is no
+CPU fallback: if the shared library is missing or no GPU is present the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liblscat.so")
+
+# ---- enums (include/lscat.h)
+OK, ERR_INVALID_ARG, ERR_CUDA, ERR_OOM, ERR_NCCL, ERR_STATE, ERR_UNSUPPORTED = range(7)
+ROW_OK, ROW_TIMEOUT, ROW_LAUNCH_ERROR, ROW_INVALID_CONFIG = range(4)
+K_EUCLID, K_MATVEC, K_GEMM_BF16, K_TRANSPOSE, K_AXPY, K_ROWSUM, K_COLSUM, K_STENCIL5 = range(8)
+K_SPIN = 100
+KERNELS = {"euclid": K_EUCLID, "matvec": K_MATVEC, "gemm_bf16": K_GEMM_BF16,
+           "transpose": K_TRANSPOSE, "axpy": K_AXPY, "rowsum": K_ROWSUM, "colsum": K_COLSUM,
+           "stencil5": K_STENCIL5, "spin": K_SPIN}
+SLOT_IN0, SLOT_IN1, SLOT_OUT = 0, 1, 2
+MEM_DEVICE, MEM_HOST = 0, 1
+LAUNCH_GRAPH, LAUNCH_STREAM = 0, 1
+SHARD_POINT_LPT, SHARD_GROUP = 0, 1
+SKIPNA, COMPLETE_ONLY = 0, 1
+PRESET_T4, PRESET_GTX980 = 0, 1
+GF = dict(defined=0x1, complete=0x2, all_nan=0x4, ratio_defined=0x8, largest_is_best=0x10,
+          largest_slower=0x20, gain_gt=0x40, perf_lt=0x80, perf_band=0x100,
+          largest_missing=0x200)
+P_NCOUNTERS = 24
+COUNTERS = ["n_rows", "n_ok", "n_nan", "n_invalid", "n_groups", "n_defined", "n_all_nan",
+            "n_complete", "n_incomplete", "n_largest_missing", "n_ratio_defined",
+            "n_largest_is_best", "n_largest_strictly_slower", "n_gain_gt", "n_perf_lt",
+            "n_perf_band", "perf_fx_hi", "perf_fx_lo", "gain_fx_hi", "gain_fx_lo"]
+DERIVED = ["frac_nonnan", "frac_largest_not_best", "frac_gain_gt", "frac_perf_lt",
+           "frac_perf_band", "mean_perf", "mean_gain"]
+
+
+class LscatError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"lscat status {status}: {msg}")
+        self.status = status
+
+
+# ---- structs
+u8p, u16p, u32p, u64p = (C.c_void_p,) * 4
+
+
+class PlanOpts(C.Structure):
+    _fields_ = [("kernels", C.c_void_p), ("n_kernels", C.c_uint32),
+                ("sizes", C.c_void_p), ("n_sizes", C.c_uint32),
+                ("blocks", C.c_void_p), ("n_blocks", C.c_uint32),
+                ("warmup", C.c_uint32), ("brackets", C.c_uint32),
+                ("launches_per_bracket", C.c_uint32), ("shard", C.c_uint32),
+                ("launch_overhead_s", C.c_double), ("hbm_bytes_per_s", C.c_double),
+                ("tensor_flops_per_s", C.c_double)]
+
+
+class SweepOpts(C.Structure):
+    _fields_ = [("blocks", C.c_void_p), ("n_blocks", C.c_uint32), ("warmup", C.c_uint32),
+                ("brackets", C.c_uint32), ("launches_per_bracket", C.c_uint32),
+                ("timeout_s", C.c_double), ("launch_mode", C.c_uint32), ("shard", C.c_uint32),
+                ("launch_overhead_s", C.c_double), ("spin_ns", C.c_uint64),
+                ("bracket_ms_host", C.c_void_p)]
+
+
+class TableC(C.Structure):
+    _fields_ = [("runtime_ms", C.c_void_p), ("block_id", C.c_void_p), ("status", C.c_void_p),
+                ("group_offset", C.c_void_p), ("group_kernel", C.c_void_p),
+                ("group_matrix", C.c_void_p), ("cap_rows", C.c_uint64),
+                ("cap_groups", C.c_uint64), ("n_rows", C.c_uint64), ("n_groups", C.c_uint64),
+                ("rows_per_group", C.c_uint32), ("mem", C.c_uint32),
+                ("first_group", C.c_uint64)]
+
+
+class ReduceOpts(C.Structure):
+    _fields_ = [(n, C.c_uint32) for n in (
+        "n_blocks", "largest_block_id", "n_matrices", "nan_policy", "bins_per_unit", "gain_cap",
+        "gain_gt_num", "gain_gt_den", "perf_lt_num", "perf_lt_den", "band_lo_num",
+        "band_lo_den", "point_sharded", "keep_values")]
+
+
+class ReduceOutC(C.Structure):
+    _fields_ = [("best_block_id", C.c_void_p), ("best_runtime", C.c_void_p),
+                ("perf", C.c_void_p), ("gain", C.c_void_p), ("flags", C.c_void_p),
+                ("partials", C.c_void_p)]
+
+
+class StatsOutC(C.Structure):
+    _fields_ = ([(n, C.c_uint64) for n in COUNTERS] + [(n, C.c_double) for n in DERIVED] +
+                [("perf_hist", C.c_void_p), ("gain_hist", C.c_void_p),
+                 ("best_block_hist", C.c_void_p), ("percentiles", C.c_void_p),
+                 ("n_percentiles", C.c_uint32), ("pct_perf", C.c_void_p),
+                 ("pct_gain", C.c_void_p)])
+
+
+class GenOpts(C.Structure):
+    _fields_ = [("n_rows_global", C.c_uint64), ("n_kernels", C.c_uint32),
+                ("n_blocks", C.c_uint32), ("largest_block_id", C.c_uint32),
+                ("n_matrices", C.c_uint32), ("preset", C.c_uint32), ("nan_rate", C.c_double),
+                ("seed", C.c_uint64), ("group_begin", C.c_uint64), ("group_end", C.c_uint64),
+                ("block_mod", C.c_uint32), ("block_rem", C.c_uint32)]
+
+
+_lib = None
+
+EXPORTS = [
+    "lscat_abi_version", "lscat_status_string", "lscat_ctx_create", "lscat_ctx_destroy",
+    "lscat_last_error", "lscat_launch_count", "lscat_comm_unique_id", "lscat_comm_init", "lscat_register_suite",
+    "lscat_suite_buffer", "lscat_suite_upload", "lscat_launch", "lscat_kernel_work",
+    "lscat_plan", "lscat_sweep", "lscat_reduce_opts_default", "lscat_partials_len",
+    "lscat_reduce_table", "lscat_stats", "lscat_gen_table", "lscat_gen_table_shape",
+]
+
+
+def load(path: str = LIB_PATH):
+    """Load liblscat.so; raises (no fallback) if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built: run `python __graft_entry__.py build` "
+                          "(there is no CPU fallback)")
+    L = C.CDLL(path)
+    vp, u32, u64, i32 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int
+    sig = {
+        "lscat_abi_version": ([], C.c_int),
+        "lscat_status_string": ([i32], C.c_char_p),
+        "lscat_ctx_create": ([i32, u64, C.POINTER(vp)], i32),
+        "lscat_ctx_destroy": ([vp], None),
+        "lscat_last_error": ([vp], C.c_char_p),
+        "lscat_launch_count": ([vp, C.POINTER(u64)], i32),
+        "lscat_comm_unique_id": ([vp], i32),
+        "lscat_comm_init": ([vp, vp, i32, i32], i32),
+        "lscat_register_suite": ([vp, vp, u32, vp, u32, vp], i32),
+        "lscat_suite_buffer": ([vp, u32, u32, u32, C.POINTER(vp), C.POINTER(u64)], i32),
+        "lscat_suite_upload": ([vp, u32, u32, u32, vp, u64, u32, vp], i32),
+        "lscat_launch": ([vp, u32, u32, u32, vp], i32),
+        "lscat_kernel_work": ([u32, u32, C.POINTER(u64), C.POINTER(u64)], i32),
+        "lscat_plan": ([C.POINTER(PlanOpts), i32, i32, vp, u64, C.POINTER(u64)], i32),
+        "lscat_sweep": ([vp, vp, u32, vp, u32, C.POINTER(SweepOpts), C.POINTER(TableC), vp], i32),
+        "lscat_reduce_opts_default": ([C.POINTER(ReduceOpts), u32, u32], None),
+        "lscat_partials_len": ([C.POINTER(ReduceOpts)], C.c_size_t),
+        "lscat_reduce_table": ([vp, C.POINTER(TableC), C.POINTER(ReduceOpts),
+                                C.POINTER(ReduceOutC), vp], i32),
+        "lscat_stats": ([vp, C.POINTER(ReduceOpts), C.POINTER(StatsOutC), vp], i32),
+        "lscat_gen_table": ([vp, C.POINTER(GenOpts), C.POINTER(TableC), vp], i32),
+        "lscat_gen_table_shape": ([C.POINTER(GenOpts), C.POINTER(u64), C.POINTER(u64)], i32),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    if L.lscat_abi_version() != 1:
+        raise ImportError("liblscat ABI version mismatch")
+    _lib = L
+    return L
+
+
+def _arr(a, dtype):
+    a = np.ascontiguousarray(a, dtype=dtype)
+    return a, a.ctypes.data
+
+
+# ---------------------------------------------------------------- host-only helpers -------
+def kernel_work(kernel: int, n: int):
+    """Algorithmic (bytes, flops) of one launch."""
+    b, f = C.c_uint64(), C.c_uint64()
+    st = load().lscat_kernel_work(kernel, n, C.byref(b), C.byref(f))
+    if st:
+        raise LscatError(st, "kernel_work")
+    return b.value, f.value
+
+
+def plan(kernels, sizes, blocks, rank, world, warmup=1, brackets=10, launches=1000,
+         shard=SHARD_POINT_LPT, launch_overhead_s=0.0):
+    """Point ids owned by `rank` (a2).  Host-only."""
+    k, kp = _arr(kernels, np.uint32)
+    s, sp = _arr(sizes, np.uint32)
+    b, bp = _arr(blocks, np.uint16)
+    o = PlanOpts(kp, k.size, sp, s.size, bp, b.size, warmup, brackets, launches, shard,
+                 launch_overhead_s, 0.0, 0.0)
+    n = C.c_uint64()
+    st = load().lscat_plan(C.byref(o), rank, world, None, 0, C.byref(n))
+    if st:
+        raise LscatError(st, "plan")
+    out = np.zeros(n.value, np.uint32)
+    st = load().lscat_plan(C.byref(o), rank, world, out.ctypes.data, out.size, C.byref(n))
+    if st:
+        raise LscatError(st, "plan")
+    return out
+
+
+def comm_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    st = load().lscat_comm_unique_id(buf)
+    if st:
+        raise LscatError(st, "comm_unique_id")
+    return buf.raw
+
+
+def reduce_opts(n_blocks=32, n_matrices=8, **kw) -> ReduceOpts:
+    o = ReduceOpts()
+    load().lscat_reduce_opts_default(C.byref(o), n_blocks, n_matrices)
+    for k, v in kw.items():
+        if k in ("gain_gt", "perf_lt", "band_lo"):
+            setattr(o, k + "_num", v[0])
+            setattr(o, k + "_den", v[1])
+        else:
+            setattr(o, k, v)
+    return o
+
+
+def partials_len(o: ReduceOpts) -> int:
+    return int(load().lscat_partials_len(C.byref(o)))
+
+
+# ---------------------------------------------------------------- device-side objects -----
+class _CAI:
+    """__cuda_array_interface__ view of a library-owned device buffer (zero copy)."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr,
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+@dataclass
+class Table:
+    """Runtime table (a5): torch tensors on the device (or pinned host tensors)."""
+    runtime_ms: object
+    block_id: object          # int16 storage of uint16 ids
+    status: object
+    group_offset: object
+    group_kernel: object      # int32 storage of uint32
+    group_matrix: object
+    n_rows: int = 0
+    n_groups: int = 0
+    rows_per_group: int = 0
+    first_group: int = 0
+    mem: int = MEM_DEVICE
+
+    @staticmethod
+    def empty(cap_rows, cap_groups, device="cuda", pin=False):
+        import torch
+        kw = dict(device=device) if device != "cpu" else dict(pin_memory=pin)
+        return Table(torch.empty(max(cap_rows, 1), dtype=torch.float32, **kw),
+                     torch.empty(max(cap_rows, 1), dtype=torch.int16, **kw),
+                     torch.empty(max(cap_rows, 1), dtype=torch.uint8, **kw),
+                     torch.zeros(cap_groups + 1, dtype=torch.int64, **kw),
+                     torch.empty(max(cap_groups, 1), dtype=torch.int32, **kw),
+                     torch.empty(max(cap_groups, 1), dtype=torch.int32, **kw),
+                     mem=MEM_DEVICE if device != "cpu" else MEM_HOST)
+
+    def c(self, with_groups=True) -> TableC:
+        def p(t):
+            return None if t is None else t.data_ptr()
+        return TableC(p(self.runtime_ms), p(self.block_id), p(self.status),
+                      p(self.group_offset) if with_groups else None,
+                      p(self.group_kernel) if with_groups else None,
+                      p(self.group_matrix) if with_groups else None,
+                      self.runtime_ms.numel(), max(self.group_offset.numel() - 1, 0)
+                      if self.group_offset is not None else 0,
+                      self.n_rows, self.n_groups, self.rows_per_group, self.mem, self.first_group)
+
+    def to_numpy(self):
+        """Host copies (for the oracle and tests)."""
+        n, G = self.n_rows, self.n_groups
+        d = dict(runtime_ms=self.runtime_ms[:n].cpu().numpy(),
+                 block_id=self.block_id[:n].cpu().numpy().view(np.uint16),
+                 status=self.status[:n].cpu().numpy() if self.status is not None else None,
+                 n_rows=n, n_groups=G, rows_per_group=self.rows_per_group,
+                 first_group=self.first_group)
+        if self.group_offset is not None:
+            d["group_offset"] = self.group_offset[:G + 1].cpu().numpy()
+        if self.group_kernel is not None:
+            d["group_kernel"] = self.group_kernel[:G].cpu().numpy().view(np.uint32)
+        if self.group_matrix is not None:
+            d["group_matrix"] = self.group_matrix[:G].cpu().numpy().view(np.uint32)
+        return d
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(stream.cuda_stream)
+
+
+class Ctx:
+    """One lscat context per process/rank and device."""
+
+    def __init__(self, device: int = 0, seed: int = 0x15CA7):
+        self._lib = load()
+        h = C.c_void_p()
+        st = self._lib.lscat_ctx_create(device, seed, C.byref(h))
+        if st:
+            raise LscatError(st, f"ctx_create(device={device}) failed (no CUDA device?)")
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._lib.lscat_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _ck(self, st, what):
+        if st:
+            msg = self._lib.lscat_last_error(self.h)
+            raise LscatError(st, f"{what}: {msg.decode() if msg else ''}")
+
+    def launch_count(self) -> int:
+        n = C.c_uint64()
+        self._ck(self._lib.lscat_launch_count(self.h, C.byref(n)), "launch_count")
+        return n.value
+
+    # a9 plumbing
+    def comm_init(self, unique_id: bytes, rank: int, world: int):
+        buf = C.create_string_buffer(unique_id, 128) if unique_id else None
+        self._ck(self._lib.lscat_comm_init(self.h, buf, rank, world), "comm_init")
+
+    # a1
+    def register_suite(self, kernels, sizes, stream=None):
+        k, kp = _arr(kernels, np.uint32)
+        s, sp = _arr(sizes, np.uint32)
+        self._ck(self._lib.lscat_register_suite(self.h, kp, k.size, sp, s.size, _stream(stream)),
+                 "register_suite")
+
+    def suite_buffer(self, kernel, n, slot):
+        p, b = C.c_void_p(), C.c_uint64()
+        self._ck(self._lib.lscat_suite_buffer(self.h, kernel, n, slot, C.byref(p), C.byref(b)),
+                 "suite_buffer")
+        return p.value, b.value
+
+    def suite_tensor(self, kernel, n, slot):
+        """Zero-copy torch view of a suite buffer (fp32, or bf16 for the GEMM)."""
+        import torch
+        p, b = self.suite_buffer(kernel, n, slot)
+        if kernel == K_GEMM_BF16:
+            t = torch.as_tensor(_CAI(p, (b // 2,), "<i2"), device=f"cuda:{self.device}")
+            return t.view(torch.bfloat16)
+        return torch.as_tensor(_CAI(p, (b // 4,), "<f4"), device=f"cuda:{self.device}")
+
+    def suite_upload(self, kernel, n, slot, src, stream=None):
+        mem = MEM_DEVICE if src.is_cuda else MEM_HOST
+        nbytes = src.numel() * src.element_size()
+        self._ck(self._lib.lscat_suite_upload(self.h, kernel, n, slot, src.data_ptr(), nbytes,
+                                              mem, _stream(stream)), "suite_upload")
+
+    # a3
+    def launch(self, kernel, n, block, stream=None):
+        self._ck(self._lib.lscat_launch(self.h, kernel, n, block, _stream(stream)), "launch")
+
+    # a4/a5
+    def sweep(self, kernels, sizes, blocks, warmup=1, brackets=10, launches=1000,
+              timeout_s=30.0, launch_mode=LAUNCH_GRAPH, shard=SHARD_POINT_LPT, spin_ns=0,
+              table: Table | None = None, with_brackets=False, stream=None) -> Table:
+        k, kp = _arr(kernels, np.uint32)
+        s, sp = _arr(sizes, np.uint32)
+        b, bp = _arr(blocks, np.uint16)
+        npts = k.size * s.size * b.size
+        if table is None:
+            table = Table.empty(npts, k.size * s.size)
+        brk = np.full(npts * brackets, np.nan, np.float32) if with_brackets else None
+        o = SweepOpts(bp, b.size, warmup, brackets, launches, timeout_s, launch_mode, shard,
+                      0.0, spin_ns, None if brk is None else brk.ctypes.data)
+        tc = table.c()
+        self._ck(self._lib.lscat_sweep(self.h, kp, k.size, sp, s.size, C.byref(o), C.byref(tc),
+                                       _stream(stream)), "sweep")
+        table.n_rows, table.n_groups = tc.n_rows, tc.n_groups
+        table.rows_per_group, table.first_group = tc.rows_per_group, tc.first_group
+        if with_brackets:
+            table.brackets = brk[:tc.n_rows * brackets].reshape(tc.n_rows, brackets)
+        return table
+
+    # a6-a9
+    def reduce_table(self, table: Table, opts: ReduceOpts, per_group=True, partials=False,
+                     stream=None):
+        import torch
+        G = table.n_groups
+        dev = f"cuda:{self.device}"
+        out = {}
+        oc = ReduceOutC()
+        if per_group:
+            out = dict(best_block_id=torch.empty(max(G, 1), dtype=torch.int16, device=dev),
+                       best_runtime=torch.empty(max(G, 1), dtype=torch.float32, device=dev),
+                       perf=torch.empty(max(G, 1), dtype=torch.float64, device=dev),
+                       gain=torch.empty(max(G, 1), dtype=torch.float64, device=dev),
+                       flags=torch.empty(max(G, 1), dtype=torch.int32, device=dev))
+            for k, v in out.items():
+                setattr(oc, k, v.data_ptr())
+        if partials:
+            out["partials"] = torch.zeros(partials_len(opts), dtype=torch.int64, device=dev)
+            oc.partials = out["partials"].data_ptr()
+        tc = table.c(with_groups=not table.rows_per_group or table.group_offset is not None)
+        self._ck(self._lib.lscat_reduce_table(self.h, C.byref(tc), C.byref(opts), C.byref(oc),
+                                              _stream(stream)), "reduce_table")
+        return out
+
+    # a8/a10
+    def stats(self, opts: ReduceOpts, percentiles=(), hist=True, stream=None) -> dict:
+        so = StatsOutC()
+        nb, cap = opts.bins_per_unit, opts.gain_cap
+        ph = np.zeros(nb + 1, np.uint64)
+        gh = np.zeros(cap * nb + 1, np.uint64)
+        bh = np.zeros(opts.n_matrices * opts.n_blocks, np.uint64)
+        if hist:
+            so.perf_hist, so.gain_hist, so.best_block_hist = (ph.ctypes.data, gh.ctypes.data,
+                                                              bh.ctypes.data)
+        pc = np.ascontiguousarray(percentiles, dtype=np.float64)
+        pp = np.full(pc.size, np.nan)
+        pg = np.full(pc.size, np.nan)
+        if pc.size:
+            so.percentiles, so.n_percentiles = pc.ctypes.data, pc.size
+            so.pct_perf, so.pct_gain = pp.ctypes.data, pg.ctypes.data
+        self._ck(self._lib.lscat_stats(self.h, C.byref(opts), C.byref(so), _stream(stream)),
+                 "stats")
+        res = {k: int(getattr(so, k)) for k in COUNTERS}
+        res.update({k: float(getattr(so, k)) for k in DERIVED})
+        if hist:
+            res["perf_hist"], res["gain_hist"] = ph, gh
+            res["best_block_hist"] = bh.reshape(opts.n_matrices, opts.n_blocks)
+        if pc.size:
+            res["pct_perf"], res["pct_gain"] = pp.tolist(), pg.tolist()
+        return res
+
+    # synthetic tables
+    def gen_table(self, n_rows_global, n_kernels, n_blocks=32, largest_block_id=None,
+                  n_matrices=8, preset=PRESET_T4, nan_rate=0.03, seed=0, group_begin=0,
+                  group_end=0, block_mod=1, block_rem=0, offsets=True, stream=None) -> Table:
+        import torch
+        o = GenOpts(n_rows_global, n_kernels, n_blocks,
+                    n_blocks - 1 if largest_block_id is None else largest_block_id, n_matrices,
+                    preset, nan_rate, seed, group_begin, group_end, block_mod, block_rem)
+        nr, ng = C.c_uint64(), C.c_uint64()
+        st = self._lib.lscat_gen_table_shape(C.byref(o), C.byref(nr), C.byref(ng))
+        if st:
+            raise LscatError(st, "gen_table_shape")
+        dev = f"cuda:{self.device}"
+        t = Table(torch.empty(max(nr.value, 1), dtype=torch.float32, device=dev),
+                  torch.empty(max(nr.value, 1), dtype=torch.int16, device=dev),
+                  torch.empty(max(nr.value, 1), dtype=torch.uint8, device=dev),
+                  torch.empty(ng.value + 1, dtype=torch.int64, device=dev) if offsets else None,
+                  torch.empty(max(ng.value, 1), dtype=torch.int32, device=dev) if offsets else None,
+                  torch.empty(max(ng.value, 1), dtype=torch.int32, device=dev) if offsets else None)
+        tc = TableC(t.runtime_ms.data_ptr(), t.block_id.data_ptr(), t.status.data_ptr(),
+                    t.group_offset.data_ptr() if offsets else None,
+                    t.group_kernel.data_ptr() if offsets else None,
+                    t.group_matrix.data_ptr() if offsets else None,
+                    t.runtime_ms.numel(), ng.value, 0, 0, 0, MEM_DEVICE, 0)
+        self._ck(self._lib.lscat_gen_table(self.h, C.byref(o), C.byref(tc), _stream(stream)),
+                 "gen_table")
+        t.n_rows, t.n_groups = tc.n_rows, tc.n_groups
+        t.rows_per_group, t.first_group = tc.rows_per_group, tc.first_group
+        if not offsets and not t.rows_per_group:
+            raise LscatError(ERR_INVALID_ARG, "gen_table: ragged table needs offsets")
+        return t

@@ -1,0 +1,126 @@
+"""a3 parity: every suite kernel at every block size against the fp64 oracle (DESIGN.md §9
+tolerances: fp32 results within 1e-5 of the sum of |terms|, data movement bit-exact; the
+bf16 GEMM within 1e-2).  Sizes span several tiles, vector and scalar paths and ragged tails;
+N = 8192 (the bench configuration) is checked on sampled rows."""
+import numpy as np
+import pytest
+
+from oracle import kernels as OK
+from tests.gpu_util import ctx, require_gpu, to_np
+
+pytestmark = pytest.mark.gpu
+
+BLOCKS = list(range(32, 1025, 32))
+SIZES = [64, 96, 100, 257, 512]
+TOL = 1e-5
+
+
+def _setup(kernel, sizes):
+    c = ctx()
+    c.register_suite([kernel], sizes)
+    return c
+
+
+def _run(c, kernel, n, block):
+    import torch
+    out = c.suite_tensor(kernel, n, 2)
+    out.fill_(float("nan")) if out.dtype != torch.bfloat16 else out.fill_(0)
+    c.launch(kernel, n, block)
+    torch.cuda.synchronize()
+    return to_np(out)
+
+
+def _inputs(c, kernel, n):
+    A = to_np(c.suite_tensor(kernel, n, 0))
+    try:
+        v = to_np(c.suite_tensor(kernel, n, 1))
+    except Exception:
+        v = None
+    return A, v
+
+
+def _check_rel(out, ref, scale, tol=TOL):
+    err = np.abs(out.astype(np.float64) - ref)
+    bad = err > tol * scale
+    assert not bad.any(), f"{bad.sum()} elements off; worst {np.max(err / np.maximum(scale, 1e-300))}"
+
+
+@pytest.mark.parametrize("name", ["euclid", "matvec", "rowsum", "colsum"])
+def test_vector_outputs(name):
+    from paper_2103_14409_b200 import KERNELS
+    k = KERNELS[name]
+    c = _setup(k, SIZES)
+    for n in SIZES:
+        A, v = _inputs(c, k, n)
+        A = A.reshape(n, n)
+        ref, scale = {
+            "euclid": lambda: (OK.euclid(A, v), OK.euclid_abs_scale(A, v)),
+            "matvec": lambda: (OK.matvec(A, v), OK.matvec_abs_scale(A, v)),
+            "rowsum": lambda: (OK.rowsum(A), OK.rowsum_abs_scale(A)),
+            "colsum": lambda: (OK.colsum(A), OK.colsum_abs_scale(A)),
+        }[name]()
+        for b in BLOCKS:
+            out = _run(c, k, n, b)
+            assert np.isfinite(out).all(), (name, n, b)
+            _check_rel(out, ref, scale)
+
+
+def test_transpose_bit_exact():
+    from paper_2103_14409_b200 import K_TRANSPOSE
+    c = _setup(K_TRANSPOSE, SIZES)
+    for n in SIZES:
+        A, _ = _inputs(c, K_TRANSPOSE, n)
+        ref = OK.transpose(A.reshape(n, n))
+        for b in BLOCKS:
+            out = _run(c, K_TRANSPOSE, n, b).reshape(n, n)
+            assert (out.view(np.uint32) == ref.view(np.uint32)).all(), (n, b)
+
+
+def test_axpy():
+    from paper_2103_14409_b200 import K_AXPY
+    sizes = SIZES + [33]          # n = 1089 elements: scalar path
+    c = _setup(K_AXPY, sizes)
+    for n in sizes:
+        x, y = _inputs(c, K_AXPY, n)
+        ref, scale = OK.axpy(x, y), OK.axpy_abs_scale(x, y)
+        for b in BLOCKS:
+            _check_rel(_run(c, K_AXPY, n, b), ref, scale)
+
+
+def test_stencil5():
+    from paper_2103_14409_b200 import K_STENCIL5
+    c = _setup(K_STENCIL5, SIZES)
+    for n in SIZES:
+        A, _ = _inputs(c, K_STENCIL5, n)
+        A = A.reshape(n, n)
+        ref, scale = OK.stencil5(A), OK.stencil5_abs_scale(A)
+        border = np.zeros((n, n), bool)
+        border[0, :] = border[-1, :] = border[:, 0] = border[:, -1] = True
+        for b in BLOCKS:
+            out = _run(c, K_STENCIL5, n, b).reshape(n, n)
+            assert (out[border].view(np.uint32) == A[border].view(np.uint32)).all(), (n, b)
+            _check_rel(out[~border], ref[~border], scale[~border])
+
+
+def test_euclid_full_size_sampled():
+    """BASELINE configs[1] size N = 8192, the launch configuration bench.py times."""
+    import torch
+    from paper_2103_14409_b200 import K_EUCLID
+    n = 8192
+    c = _setup(K_EUCLID, [n])
+    A = c.suite_tensor(K_EUCLID, n, 0).view(n, n)
+    q = to_np(c.suite_tensor(K_EUCLID, n, 1))
+    rows = np.r_[0:8, np.random.default_rng(0).choice(n, 56, replace=False), n - 8:n]
+    Ar = A[torch.as_tensor(rows, device=A.device)].cpu().numpy()
+    ref = OK.euclid(Ar, q)
+    for b in (32, 128, 256, 512, 1024):
+        out = _run(c, K_EUCLID, n, b)[rows]
+        _check_rel(out, ref, ref)
+
+
+def test_launch_rejects_illegal_blocks():
+    from paper_2103_14409_b200 import K_EUCLID, LscatError
+    c = _setup(K_EUCLID, [64])
+    for b in (0, 16, 33, 1056, 2048):
+        with pytest.raises(LscatError):
+            c.launch(K_EUCLID, 64, b)

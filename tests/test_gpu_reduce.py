@@ -1,0 +1,156 @@
+"""a6-a10 parity: the CUDA table reducer against the C oracle on identical tables.
+
+Integer outputs (argmin block ids, every counter, every histogram bin, fixed-point sums) and
+the selected percentile values must be bit-exact; per-group perf/gain doubles too (one IEEE
+division each).  Tables: the generator's GTX 980- and T4-scale tables
+(BASELINE configs[2], [3]), ragged / point-sharded shapes, random tables with ties, NaN,
+inf, zero and negative runtimes."""
+import numpy as np
+import pytest
+
+from oracle import table as OT
+from synth import gen_table
+from tests.gpu_util import ctx
+from tests.test_oracle_table import _random_table
+
+pytestmark = pytest.mark.gpu
+
+PCTS = [0.0, 0.01, 0.05, 0.1, 0.25, 0.5, 0.75, 0.9, 0.95, 0.99, 1.0]
+
+
+def _device_table(t, host=False):
+    import torch
+    from paper_2103_14409_b200 import Table, MEM_HOST
+    dev = "cpu" if host else "cuda"
+    kw = dict(pin_memory=True) if host else dict(device=dev)
+
+    def T(a, dt):
+        x = torch.from_numpy(np.ascontiguousarray(a).view(dt))
+        return x.pin_memory() if host else x.to(dev)
+    tab = Table(T(t["runtime_ms"], np.float32), T(t["block_id"].astype(np.uint16), np.int16),
+                None, T(t["group_offset"].astype(np.int64), np.int64), None,
+                T(t["group_matrix"].astype(np.uint32), np.int32) if t.get("group_matrix") is not None else None,
+                n_rows=len(t["runtime_ms"]), n_groups=len(t["group_offset"]) - 1,
+                first_group=t.get("first_group", 0))
+    if host:
+        tab.mem = MEM_HOST
+    del kw
+    return tab
+
+
+def _opts_pair(L=32, M=8, ell=None, policy=0):
+    from paper_2103_14409_b200 import reduce_opts
+    ell = L - 1 if ell is None else ell
+    g = reduce_opts(L, M, largest_block_id=ell, nan_policy=policy)
+    o = OT.Opts(n_blocks=L, largest_block_id=ell, n_matrices=M, nan_policy=policy)
+    return g, o
+
+
+def _compare(t, L=32, M=8, ell=None, policy=0, host=False, pcts=PCTS):
+    c = ctx()
+    g_opts, o_opts = _opts_pair(L, M, ell, policy)
+    tab = _device_table(t, host=host)
+    out = c.reduce_table(tab, g_opts)
+    st = c.stats(g_opts, percentiles=pcts)
+    ref = OT.reduce_table(t["runtime_ms"], t["block_id"], t["group_offset"],
+                          group_matrix=t.get("group_matrix"), first_group=t.get("first_group", 0),
+                          opts=o_opts, percentiles=pcts)
+    for k, v in ref.counters.items():
+        assert st[k] == v, (k, st[k], v)
+    assert (st["perf_hist"] == ref.perf_hist).all()
+    assert (st["gain_hist"] == ref.gain_hist).all()
+    assert (st["best_block_hist"] == ref.best_block_hist).all()
+    for k, v in ref.derived.items():
+        assert (st[k] == v) or (np.isnan(st[k]) and np.isnan(v)), k
+    bb = out["best_block_id"].cpu().numpy().view(np.uint16)
+    assert (bb == ref.best_block).all()
+    br = out["best_runtime"].cpu().numpy()
+    assert (br.view(np.uint32) == ref.best_runtime.view(np.uint32)).all()
+    pf = out["perf"].cpu().numpy()
+    gn = out["gain"].cpu().numpy()
+    assert ((pf == ref.perf) | (np.isnan(pf) & np.isnan(ref.perf))).all()
+    assert ((gn == ref.gain) | (np.isnan(gn) & np.isnan(ref.gain))).all()
+    assert (out["flags"].cpu().numpy().view(np.uint32) == ref.flags).all()
+    if st["n_ratio_defined"]:
+        assert st["pct_perf"] == ref.percentiles["perf"]
+        assert st["pct_gain"] == ref.percentiles["gain"]
+    return st
+
+
+def test_gtx980_scale_table():
+    """BASELINE configs[2]: 2 140 796 rows, ~3 % NaN."""
+    t = gen_table(2_140_796, 8363, preset="gtx980", nan_rate=0.03, seed=980)
+    st = _compare(t)
+    assert st["n_rows"] == 2_140_796 and st["n_groups"] == 66_900
+
+
+@pytest.mark.parametrize("policy", [0, 1])
+def test_t4_scale_table(policy):
+    """BASELINE configs[3]: 5 028 536 runtimes over 19 683 kernel ids."""
+    t = gen_table(5_028_536, 19_683, preset="t4", nan_rate=0.03, seed=4)
+    _compare(t, policy=policy)
+
+
+def test_point_sharded_shape_and_host_table():
+    t = gen_table(200_000, 800, preset="t4", nan_rate=0.05, seed=5, block_mod=3, block_rem=1)
+    _compare(t)
+    _compare(t, host=True)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_tables_with_ties_and_invalid(seed):
+    rng = np.random.default_rng(100 + seed)
+    L = [4, 8, 32, 40][seed]
+    rt, bid, off, gm = _random_table(rng, 3000, L, dup_vals=seed % 2 == 0)
+    t = dict(runtime_ms=rt, block_id=bid, group_offset=off, group_matrix=gm)
+    _compare(t, L=L, ell=L // 2 if seed == 1 else None)
+
+
+def test_scale_invariance_on_gpu():
+    t = gen_table(100_000, 400, preset="gtx980", seed=9)
+    a = _compare(t)
+    t2 = dict(t, runtime_ms=(t["runtime_ms"] * np.float32(8.0)).astype(np.float32))
+    b = _compare(t2)
+    for k in ("n_ratio_defined", "n_gain_gt", "perf_fx_hi", "perf_fx_lo", "pct_perf"):
+        assert a[k] == b[k]
+
+
+def test_generator_twin_bit_exact():
+    """lscat_gen_table (CUDA) reproduces synth/tables.py bit for bit."""
+    c = ctx()
+    for kw in (dict(n_rows_global=2_140_796, n_kernels=8363, preset=1, seed=980),
+               dict(n_rows_global=5_028_536, n_kernels=19_683, preset=0, seed=4,
+                    block_mod=4, block_rem=3),
+               dict(n_rows_global=1_000_000, n_kernels=100, preset=0, seed=7, group_begin=5000,
+                    group_end=20000)):
+        g = c.gen_table(**kw).to_numpy()
+        pkw = dict(kw)
+        n, k = pkw.pop("n_rows_global"), pkw.pop("n_kernels")
+        pkw["preset"] = pkw["preset"]
+        h = gen_table(n, k, **pkw)
+        assert g["n_rows"] == h["n_rows"]
+        assert (g["runtime_ms"].view(np.uint32) == h["runtime_ms"].view(np.uint32)).all()
+        assert (g["block_id"] == h["block_id"]).all()
+        assert (g["status"] == h["status"]).all()
+        assert (g["group_offset"] == h["group_offset"]).all()
+        assert (g["group_kernel"] == h["group_kernel"]).all()
+        assert (g["group_matrix"] == h["group_matrix"]).all()
+
+
+def test_uniform_groups_without_offsets():
+    """configs[4] layout: uniform 32-row groups, no offset array, matrix = g mod 8."""
+    c = ctx()
+    from paper_2103_14409_b200 import reduce_opts
+    n = 32 * 50_000
+    tab = c.gen_table(n, 6250, preset=0, seed=10 ** 9, offsets=False)
+    assert tab.rows_per_group == 32
+    o = reduce_opts(32, 8)
+    c.reduce_table(tab, o, per_group=False)
+    st = c.stats(o, percentiles=PCTS)
+    h = gen_table(n, 6250, preset="t4", seed=10 ** 9)
+    ref = OT.reduce_table(h["runtime_ms"], h["block_id"], rows_per_group=32, opts=OT.Opts(),
+                          percentiles=PCTS)
+    for k, v in ref.counters.items():
+        assert st[k] == v, k
+    assert (st["best_block_hist"] == ref.best_block_hist).all()
+    assert st["pct_perf"] == ref.percentiles["perf"]

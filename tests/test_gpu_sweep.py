@@ -1,0 +1,105 @@
+"""a2-a5: the sweep engine end to end on the device (BASELINE configs[0]), its timeout /
+invalid-config / launch-mode behaviour, and stats of the swept table against the oracle."""
+import time
+
+import numpy as np
+import pytest
+
+from oracle import table as OT
+from tests.gpu_util import ctx
+
+pytestmark = pytest.mark.gpu
+
+TINY_K = None
+
+
+def _tiny():
+    from paper_2103_14409_b200 import K_EUCLID, K_MATVEC, K_AXPY
+    return [K_EUCLID, K_MATVEC, K_AXPY], [64, 128, 256, 512], [32, 64, 128, 256, 512, 1024]
+
+
+def test_tiny_sweep_and_stats():
+    """configs[0]: 3 kernels x 6 blocks x 4 matrices = 72 rows, 12 groups; stats bit-exact."""
+    from paper_2103_14409_b200 import reduce_opts, ROW_OK
+    c = ctx()
+    ks, ns, bs = _tiny()
+    c.register_suite(ks, ns)
+    tab = c.sweep(ks, ns, bs, warmup=1, brackets=10, launches=100, with_brackets=True)
+    t = tab.to_numpy()
+    assert t["n_rows"] == 72 and t["n_groups"] == 12                  # S:538 totality
+    assert (np.diff(t["group_offset"]) == 6).all()
+    assert (t["status"] == ROW_OK).all()
+    rt = t["runtime_ms"]
+    assert np.isfinite(rt).all() and (rt > 0).all()
+    assert (t["block_id"] == np.tile(np.arange(6), 12)).all()
+    assert (t["group_kernel"] == np.repeat(ks, 4)).all()
+    assert (t["group_matrix"] == np.tile(np.arange(4), 3)).all()
+    med = np.median(tab.brackets.astype(np.float64), axis=1).astype(np.float32)
+    assert np.allclose(med, rt, rtol=1e-6)                               # median of K
+    o = reduce_opts(6, 4)
+    c.reduce_table(tab, o, per_group=False)
+    st = c.stats(o, percentiles=[0.5, 0.9])
+    ref = OT.reduce_table(rt, t["block_id"], t["group_offset"], group_matrix=t["group_matrix"],
+                          opts=OT.Opts(n_blocks=6, n_matrices=4), percentiles=[0.5, 0.9])
+    for k, v in ref.counters.items():
+        assert st[k] == v, k
+    assert (st["best_block_hist"] == ref.best_block_hist).all()
+    assert st["pct_perf"] == ref.percentiles["perf"]
+
+
+def test_runtime_grows_with_n():
+    """Sanity: at fixed block the per-launch time does not shrink as the data grows 64x."""
+    from paper_2103_14409_b200 import K_AXPY
+    c = ctx()
+    c.register_suite([K_AXPY], [256, 2048])
+    t = c.sweep([K_AXPY], [256, 2048], [256], warmup=1, brackets=5, launches=50).to_numpy()
+    assert t["runtime_ms"][1] > t["runtime_ms"][0]
+
+
+def test_timeout_marks_nan_quickly():
+    """P:228 timeout -> NaN row (bounded wall time)."""
+    from paper_2103_14409_b200 import K_SPIN, ROW_TIMEOUT, ROW_OK, LAUNCH_STREAM
+    c = ctx()
+    t0 = time.time()
+    tab = c.sweep([K_SPIN], [1], [32, 64], warmup=1, brackets=10, launches=100, timeout_s=1.0,
+                  spin_ns=5_000_000, launch_mode=LAUNCH_STREAM)
+    wall = time.time() - t0
+    t = tab.to_numpy()
+    assert (t["status"] == ROW_TIMEOUT).all() and np.isnan(t["runtime_ms"]).all()
+    assert wall < 3.0
+    tab = c.sweep([K_SPIN], [1], [32], warmup=1, brackets=3, launches=2, timeout_s=1.0,
+                  spin_ns=100_000)
+    t = tab.to_numpy()
+    assert t["status"][0] == ROW_OK
+    assert 0.09 < t["runtime_ms"][0] < 0.5                                # ~0.1 ms per launch
+
+
+def test_gemm_small_blocks_invalid_config():
+    from paper_2103_14409_b200 import K_GEMM_BF16, ROW_INVALID_CONFIG
+    c = ctx()
+    c.register_suite([K_GEMM_BF16], [256])
+    t = c.sweep([K_GEMM_BF16], [256], [32, 64, 96], warmup=1, brackets=2, launches=2).to_numpy()
+    assert (t["status"] == ROW_INVALID_CONFIG).all() and np.isnan(t["runtime_ms"]).all()
+
+
+def test_stream_mode_and_host_table():
+    from paper_2103_14409_b200 import K_EUCLID, LAUNCH_STREAM, Table, ROW_OK
+    c = ctx()
+    c.register_suite([K_EUCLID], [128])
+    host = Table.empty(4, 1, device="cpu", pin=True)
+    t = c.sweep([K_EUCLID], [128], [32, 64, 128, 1024], brackets=3, launches=20,
+                launch_mode=LAUNCH_STREAM, table=host)
+    assert t.n_rows == 4
+    assert (t.status.numpy()[:4] == ROW_OK).all()
+    assert np.isfinite(t.runtime_ms.numpy()[:4]).all()
+
+
+def test_sweep_argument_errors():
+    from paper_2103_14409_b200 import K_EUCLID, LscatError
+    c = ctx()
+    c.register_suite([K_EUCLID], [64])
+    for bad in ([33], [32, 32], [1056], [64, 32]):
+        with pytest.raises(LscatError):
+            c.sweep([K_EUCLID], [64], bad, brackets=1, launches=1)
+    with pytest.raises(LscatError):
+        c.sweep([K_EUCLID], [128], [32], brackets=1, launches=1)       # not registered
