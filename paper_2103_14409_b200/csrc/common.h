@@ -24,8 +24,9 @@ struct SuiteEntry {
   void* in1 = nullptr;
   void* out = nullptr;
   uint64_t in0_bytes = 0, in1_bytes = 0, out_bytes = 0;
-  void* scratch = nullptr;  // colsum: partials + tile counters; gemm: tensor maps
+  void* scratch = nullptr;  // colsum: partials + tile counters
   uint64_t scratch_bytes = 0;
+  alignas(64) unsigned char host_blob[256] = {};  // gemm: the two TMA tensor maps
 };
 
 struct LaunchArgs {

@@ -1,11 +1,277 @@
-// gemm.cu — placeholder until the tcgen05 GEMM lands: no block size is implemented, so the
-// sweep records every GEMM point as LSCAT_ROW_INVALID_CONFIG.
-#include "common.h"
+// gemm.cu — the tensor-core member of the suite: C = A Bt^T, A and Bt N x N bf16 K-major,
+// fp32 accumulation in TMEM, bf16 output (R-17).  Tensor bound: 2N^3 FLOPs.
+//
+// sm_100a design, hand-written PTX (no CUTLASS): one CTA computes one 128 x 256 output tile.
+//   warp 0, one lane : TMA producer — cp.async.bulk.tensor 2D loads of the A (128 x 64) and
+//                      Bt (256 x 64) K-slices, 128-byte swizzle, into a kStages-deep ring of
+//                      shared-memory stages guarded by full/empty mbarriers;
+//   warp 1, one lane : MMA issuer — four tcgen05.mma.cta_group::1.kind::f16 (M=128, N=256,
+//                      K=16) per stage into a 256-column fp32 TMEM accumulator, tcgen05.commit
+//                      releases the stage back to the producer;
+//   all warps        : epilogue — tcgen05.ld 32 lanes x 32 columns per warp (lane quadrant
+//                      = warp % 4), convert to bf16, store 64 contiguous bytes per row.
+// The block size of the sweep sets how many warps share the epilogue; fewer than 128 threads
+// cannot cover the four TMEM lane quadrants, so those points are INVALID_CONFIG rows (the
+// paper's NaN rows for configurations a kernel does not support).
+// Requires N % 8 == 0 (TMA row pitch must be a multiple of 16 bytes).
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <cstring>
+
+#include "kern_common.cuh"
 
 namespace lscat {
-cudaError_t gemm_prepare(SuiteEntry&) { return cudaSuccess; }
-const KernelTable& table_gemm() {
-  static KernelTable t{};
-  return t;
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 64, UK = 16;
+constexpr int kStages = 4;
+constexpr int kStageA = BM * BK * 2;  // 16 KB
+constexpr int kStageB = BN * BK * 2;  // 32 KB
+constexpr int kSmem = kStages * (kStageA + kStageB) + 1024 /*align*/ + 256 /*barriers*/;
+constexpr uint32_t kTmemCols = 256;
+
+struct GemmMaps {
+  CUtensorMap a, b;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
 }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+// K-major, 128-byte swizzle smem matrix descriptor (SBO = 1024 B between 8-row groups).
+__device__ __forceinline__ uint64_t sw128_desc(const void* p) {
+  const uint64_t addr = smem_u32(p);
+  uint64_t d = 0;
+  d |= (addr >> 4) & 0x3FFFull;             // start address
+  d |= (uint64_t)1 << 16;                   // leading byte offset (unused for SW128 K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;         // stride byte offset
+  d |= (uint64_t)1 << 46;                   // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                   // SWIZZLE_128B
+  return d;
+}
+// kind::f16 instruction descriptor: D fp32, A/B bf16, both K-major, M = 128, N = 256.
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(ad), "l"(bd), "r"(kIdesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+template <int B>
+__global__ void __launch_bounds__(B, 1) gemm_kernel(const __grid_constant__ GemmMaps maps,
+                                                    __nv_bfloat16* __restrict__ C, int N) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kStages * kStageA;
+  uint64_t* full = (uint64_t*)(sB + kStages * kStageB);
+  uint64_t* empty = full + kStages;
+  uint64_t* tmem_full = empty + kStages;
+  uint32_t* tmem_slot = (uint32_t*)(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int kblocks = (N + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.b) : "memory");
+    for (int s = 0; s < kStages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer
+    for (int kb = 0; kb < kblocks; kb++) {
+      const int s = kb % kStages;
+      const uint32_t ph = (kb / kStages) & 1;
+      mbar_wait(&empty[s], ph ^ 1);
+      mbar_expect_tx(&full[s], kStageA + kStageB);
+      tma_load_2d(sA + s * kStageA, &maps.a, &full[s], kb * BK, m0);
+      tma_load_2d(sB + s * kStageB, &maps.b, &full[s], kb * BK, n0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer
+    for (int kb = 0; kb < kblocks; kb++) {
+      const int s = kb % kStages;
+      const uint32_t ph = (kb / kStages) & 1;
+      mbar_wait(&full[s], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint64_t ad = sw128_desc(sA + s * kStageA), bd = sw128_desc(sB + s * kStageB);
+#pragma unroll
+      for (int k = 0; k < BK / UK; k++) {
+        // advance the start address by k * 32 bytes inside the 128-byte swizzle atom
+        mma_bf16(tmem, ad + (uint64_t)(k * UK * 2 >> 4), bd + (uint64_t)(k * UK * 2 >> 4),
+                 (kb | k) != 0);
+      }
+      mma_commit(&empty[s]);
+    }
+    mma_commit(tmem_full);
+  }
+  __syncwarp();
+
+  // ---- epilogue: every warp, lane quadrant q = warp % 4, 32-column chunks round-robin
+  mbar_wait(tmem_full, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  constexpr int W = B / 32;
+  const int q = warp & 3;
+  const int nq = (W - q + 3) / 4;      // warps sharing quadrant q
+  const int iq = warp >> 2;            // this warp's index among them
+  const int row = m0 + q * 32 + lane;
+  for (int c = iq; c < BN / 32; c += nq) {
+    uint32_t v[32];
+    const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32);
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+          "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+          "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    const int col = n0 + c * 32;
+    if (row < N && col < N) {
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 16; i++) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+        pk[i] = *reinterpret_cast<uint32_t*>(&h);
+      }
+      __nv_bfloat16* dst = C + (size_t)row * N + col;
+      if (col + 32 <= N) {
+        uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+        for (int i = 0; i < 4; i++) d4[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+      } else {
+        for (int i = 0; i < 32 && col + i < N; i++) {
+          uint32_t w = pk[i >> 1];
+          uint16_t h = (i & 1) ? (uint16_t)(w >> 16) : (uint16_t)(w & 0xFFFF);
+          reinterpret_cast<uint16_t*>(dst)[i] = h;
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols)
+                 : "memory");
+  }
+}
+
+template <int B>
+struct GemmL {
+  static constexpr bool kSupported = B >= 128;
+  static cudaError_t launch(const LaunchArgs& a, cudaStream_t s) {
+    if constexpr (B >= 128) {
+      const SuiteEntry& e = *a.e;
+      static bool attr = false;
+      if (!attr) {
+        cudaError_t err = cudaFuncSetAttribute(gemm_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        if (err != cudaSuccess) return err;
+        attr = true;
+      }
+      const int N = (int)e.n;
+      dim3 grid((N + BM - 1) / BM, (N + BN - 1) / BN);
+      gemm_kernel<B><<<grid, B, kSmem, s>>>(*reinterpret_cast<const GemmMaps*>(e.host_blob),
+                                            (__nv_bfloat16*)e.out, N);
+      return cudaGetLastError();
+    } else {
+      return cudaErrorInvalidConfiguration;
+    }
+  }
+};
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+bool make_map(CUtensorMap* m, void* base, int n, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)n};           // {K, rows}
+  cuuint64_t strides[1] = {(cuuint64_t)n * 2};                   // row pitch in bytes
+  cuuint32_t box[2] = {BK, (cuuint32_t)box_rows};                // 64 bf16 = 128 B inner
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+cudaError_t gemm_prepare(SuiteEntry& e) {
+  static_assert(sizeof(GemmMaps) <= sizeof(e.host_blob), "host blob too small");
+  if (e.n % 8 != 0) return cudaErrorInvalidValue;  // TMA row pitch must be 16-byte aligned
+  GemmMaps* m = reinterpret_cast<GemmMaps*>(e.host_blob);
+  if (!make_map(&m->a, e.in0, (int)e.n, BM) || !make_map(&m->b, e.in1, (int)e.n, BN))
+    return cudaErrorInvalidValue;
+  return cudaSuccess;
+}
+
+const KernelTable& table_gemm() { static KernelTable t = make_table<GemmL>(); return t; }
+
 }  // namespace lscat

@@ -124,3 +124,60 @@ def test_launch_rejects_illegal_blocks():
     for b in (0, 16, 33, 1056, 2048):
         with pytest.raises(LscatError):
             c.launch(K_EUCLID, 64, b)
+
+
+GEMM_SIZES = [64, 200, 520]      # multiples of 8 (TMA pitch); ragged 128 x 256 tiles
+
+
+def test_gemm_bf16_all_blocks():
+    import torch
+    from paper_2103_14409_b200 import K_GEMM_BF16, LscatError
+    c = _setup(K_GEMM_BF16, GEMM_SIZES)
+    for n in GEMM_SIZES:
+        A, Bt = _inputs(c, K_GEMM_BF16, n)
+        A, Bt = A.reshape(n, n), Bt.reshape(n, n)
+        ref, scale = OK.gemm(A, Bt), OK.gemm_abs_scale(A, Bt)
+        for b in BLOCKS:
+            if b < 128:
+                with pytest.raises(LscatError):
+                    c.launch(K_GEMM_BF16, n, b)
+                continue
+            out = _run(c, K_GEMM_BF16, n, b).reshape(n, n)
+            _check_rel(out, ref, scale, tol=1e-2)
+
+
+def test_gemm_identity_bit_exact():
+    """Bt = I -> C = A exactly (one non-zero product per output, bf16 A exact)."""
+    import torch
+    from paper_2103_14409_b200 import K_GEMM_BF16
+    n = 256
+    c = _setup(K_GEMM_BF16, [n])
+    eye = torch.eye(n, dtype=torch.bfloat16, device="cuda").contiguous()
+    c.suite_upload(K_GEMM_BF16, n, 1, eye.view(-1))
+    A = c.suite_tensor(K_GEMM_BF16, n, 0).view(n, n).clone()
+    for b in (128, 256, 1024):
+        out = c.suite_tensor(K_GEMM_BF16, n, 2)
+        out.zero_()
+        c.launch(K_GEMM_BF16, n, b)
+        torch.cuda.synchronize()
+        assert torch.equal(out.view(n, n), A)
+
+
+def test_gemm_full_size_sampled():
+    import torch
+    from paper_2103_14409_b200 import K_GEMM_BF16
+    n = 8192
+    c = _setup(K_GEMM_BF16, [n])
+    A = c.suite_tensor(K_GEMM_BF16, n, 0).view(n, n)
+    Bt = c.suite_tensor(K_GEMM_BF16, n, 1).view(n, n)
+    rows = torch.as_tensor(np.r_[0:4, 127:131, 4090:4100, n - 4:n], device="cuda")
+    Ar = A[rows].float().cpu().numpy()
+    Bn = Bt.float().cpu().numpy()
+    ref, scale = OK.gemm(Ar, Bn), OK.gemm_abs_scale(Ar, Bn)
+    for b in (128, 256):
+        out = c.suite_tensor(K_GEMM_BF16, n, 2)
+        out.zero_()
+        c.launch(K_GEMM_BF16, n, b)
+        torch.cuda.synchronize()
+        got = out.view(n, n)[rows].float().cpu().numpy()
+        _check_rel(got, ref, scale, tol=1e-2)
