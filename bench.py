@@ -263,6 +263,13 @@ def main():
                 "share_of_step": round(sum(float(np.mean([b[lo + j].mean() for b in brackets_best]))
                                            for j in range(hi - lo)) * (W + K * R) / (dev_ms / args.steps), 4),
                 "all_blocks_gbs_min_max": [round(min(all_blocks_gbs), 1), round(max(all_blocks_gbs), 1)]}
+    per_n = {}
+    for gi, n in enumerate(SIZES):
+        a, b = tab["group_offset"][gi], tab["group_offset"][gi + 1]
+        if b > a:
+            v = tab["runtime_ms"][a:b] * 1e3
+            per_n[str(n)] = [round(float(np.nanmin(v)), 2), round(float(np.nanmedian(v)), 2),
+                             round(float(np.nanmax(v)), 2)]
     rooflines = None
     if world > 1:
         objs = [None] * world
@@ -305,6 +312,7 @@ def main():
                        "(512 MB write); N=8192 inputs (268 MB) exceed L2 (126 MB)"},
             "clocks": ck, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
             "e2e": e2e, "secondary": secondary,
+            "per_n_launch_us": per_n,
             "stats_last_step": {k: last[1][k] for k in ("n_rows", "n_ratio_defined",
                                                       "n_largest_is_best", "mean_perf",
                                                       "frac_largest_not_best")},

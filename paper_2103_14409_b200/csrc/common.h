@@ -98,6 +98,7 @@ struct lscat_ctx {
   // reducer scratch
   lscat::ReduceState rs;
   std::map<std::string, lscat::DevBuf> scratch;
+  std::map<std::string, lscat::DevBuf> pinned;  // cudaMallocHost staging
 };
 
 namespace lscat {
@@ -108,6 +109,8 @@ lscat_status cuda_fail(lscat_ctx* ctx, cudaError_t e, const char* what);
 bool is_sticky(cudaError_t e);
 // device scratch (grow-only) keyed by name
 void* scratch(lscat_ctx* ctx, const char* name, size_t bytes, cudaError_t* err);
+// pinned host staging (grow-only) keyed by name
+void* pinned(lscat_ctx* ctx, const char* name, size_t bytes, cudaError_t* err);
 // host-side work model
 void kernel_work(uint32_t kernel, uint32_t n, uint64_t* bytes, uint64_t* flops);
 bool block_list_ok(const uint16_t* blocks, uint32_t n);

@@ -63,6 +63,21 @@ void* scratch(lscat_ctx* ctx, const char* name, size_t bytes, cudaError_t* err) 
   return b.p;
 }
 
+void* pinned(lscat_ctx* ctx, const char* name, size_t bytes, cudaError_t* err) {
+  *err = cudaSuccess;
+  DevBuf& b = ctx->pinned[name];
+  if (b.bytes < bytes) {
+    if (b.p) cudaFreeHost(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    size_t want = std::max(bytes, (size_t)4096);
+    *err = cudaMallocHost(&b.p, want);
+    if (*err != cudaSuccess) return nullptr;
+    b.bytes = want;
+  }
+  return b.p;
+}
+
 // Algorithmic HBM bytes and FLOPs of one launch.
 void kernel_work(uint32_t k, uint32_t n, uint64_t* bytes, uint64_t* flops) {
   const uint64_t N = n, N2 = N * N;
@@ -163,6 +178,7 @@ void lscat_ctx_destroy(lscat_ctx* c) {
     cudaFree(kv.second.scratch);
   }
   for (auto& kv : c->scratch) cudaFree(kv.second.p);
+  for (auto& kv : c->pinned) cudaFreeHost(kv.second.p);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->capture_stream) cudaStreamDestroy(c->capture_stream);
   delete c;

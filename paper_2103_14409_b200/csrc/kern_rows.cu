@@ -2,9 +2,10 @@
 //
 // euclidean_kernel is the one kernel the paper names (Figs. 3/5).  Its source is
 // not given; this build reads it as the distance of every row of A to a query vector q
-// (reading R-14).  Mapping: one CTA of B threads per row, 128-bit
-// streaming loads of A with U independent loads in flight per thread, q/x through the
-// read-only cache (L2/L1 resident), fp32 accumulation, warp-shuffle + shared-memory tree.
+// (reading R-14).  Mapping: a CTA of B threads is split into teams of
+// warps, one team per row (one team per CTA for small blocks or long rows), 128-bit streaming
+// loads of A with U independent loads in flight per thread, q/x through the read-only cache
+// (L2/L1 resident), fp32 accumulation, warp shuffles + a fixed-order smem combine.
 // HBM bound: 4N^2 + 8N bytes per launch.
 #include "kern_common.cuh"
 
@@ -32,41 +33,75 @@ __device__ __forceinline__ float acc1(float s, float a, float v) {
   else return s + a;
 }
 
+// A CTA of B threads is split into teams of TW warps (TW divides B/32); each team reduces one
+// row at a time.  TW is chosen on the host so that a thread streams ~16 float4 of its row
+// (enough loads in flight) and small rows do not leave most of a large block idle.
 template <int OP, int B>
 __global__ void __launch_bounds__(B) row_kernel(const float* __restrict__ A,
                                                 const float* __restrict__ v,
-                                                float* __restrict__ out, int N) {
-  __shared__ float red[B / 32 > 0 ? B / 32 : 1];
-  const float* a = A + (size_t)blockIdx.x * N;
-  const int t = threadIdx.x;
+                                                float* __restrict__ out, int N, int TW) {
+  constexpr int W = B / 32;
+  __shared__ float red[W];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int team = warp / TW, tw = warp % TW;          // team index, warp within team
+  const int T = TW * 32, t = tw * 32 + lane;            // team size, thread within team
+  const int teams = W / TW;
+  const int row = blockIdx.x * teams + team;
+  const bool live = row < N;
+  const float* a = A + (size_t)(live ? row : 0) * N;
   float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-  if ((N & 3) == 0) {
-    constexpr int U = 4;
-    const float4* a4 = reinterpret_cast<const float4*>(a);
-    const float4* v4 = reinterpret_cast<const float4*>(v);
-    const int n4 = N >> 2;
-    for (int base = t; base < n4; base += U * B) {
-      float4 x[U], y[U];
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        const int j = base + u * B;
-        x[u] = j < n4 ? ld_stream(a4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      if constexpr (OP != kRowsum) {
+  if (live) {
+    if ((N & 3) == 0) {
+      constexpr int U = 4;
+      const float4* a4 = reinterpret_cast<const float4*>(a);
+      const float4* v4 = reinterpret_cast<const float4*>(v);
+      const int n4 = N >> 2;
+      for (int base = t; base < n4; base += U * T) {
+        float4 x[U], y[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
-          const int j = base + u * B;
-          y[u] = j < n4 ? __ldg(v4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+          const int j = base + u * T;
+          x[u] = j < n4 ? ld_stream(a4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-      }
+        if constexpr (OP != kRowsum) {
 #pragma unroll
-      for (int u = 0; u < U; u++) acc4<OP>(s, x[u], OP != kRowsum ? y[u] : x[u]);
+          for (int u = 0; u < U; u++) {
+            const int j = base + u * T;
+            y[u] = j < n4 ? __ldg(v4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) acc4<OP>(s, x[u], OP != kRowsum ? y[u] : x[u]);
+      }
+    } else {
+      for (int j = t; j < N; j += T) s.x = acc1<OP>(s.x, ld_stream(a + j), OP != kRowsum ? __ldg(v + j) : 0.f);
     }
-  } else {
-    for (int j = t; j < N; j += B) s.x = acc1<OP>(s.x, ld_stream(a + j), OP != kRowsum ? __ldg(v + j) : 0.f);
   }
-  float r = block_sum<B>((s.x + s.y) + (s.z + s.w), red);
-  if (t == 0) out[blockIdx.x] = (OP == kEuclid) ? sqrtf(r) : r;
+  float r = (s.x + s.y) + (s.z + s.w);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  if (TW > 1) {  // combine the team's warps in a fixed order
+    if (lane == 0) red[warp] = r;
+    __syncthreads();
+    if (tw == 0 && lane == 0) {
+      r = 0.f;
+      for (int k = 0; k < TW; k++) r += red[team * TW + k];
+    }
+  }
+  if (live && tw == 0 && lane == 0) out[row] = (OP == kEuclid) ? sqrtf(r) : r;
+}
+
+// Warps per team: the largest divisor of B/32 not above the warps that give each thread
+// ~16 float4 of the row.
+inline int team_warps(int N, int B) {
+  const int W = B / 32;
+  const int n4 = (N + 3) / 4;
+  int want = (n4 + 16 * 32 - 1) / (16 * 32);
+  if (want < 1) want = 1;
+  int best = 1;
+  for (int d = 1; d <= W; d++)
+    if (W % d == 0 && d <= want) best = d;
+  return best;
 }
 
 template <int OP>
@@ -76,8 +111,9 @@ struct RowLauncher {
     static constexpr bool kSupported = true;
     static cudaError_t launch(const LaunchArgs& a, cudaStream_t s) {
       const SuiteEntry& e = *a.e;
-      row_kernel<OP, B><<<e.n, B, 0, s>>>((const float*)e.in0, (const float*)e.in1,
-                                          (float*)e.out, (int)e.n);
+      const int N = (int)e.n, tw = team_warps(N, B), teams = B / 32 / tw;
+      row_kernel<OP, B><<<(N + teams - 1) / teams, B, 0, s>>>((const float*)e.in0, (const float*)e.in1,
+                                                             (float*)e.out, N, tw);
       return cudaGetLastError();
     }
   };

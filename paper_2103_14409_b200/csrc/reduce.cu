@@ -64,15 +64,42 @@ struct GroupAcc {
   uint32_t l_bits;
 };
 
+// Per-warp accumulators.  Counters are warp-uniform (built from ballots / redux, identical in
+// every lane, flushed by lane 0); fixed-point sums and percentile key bounds are per lane.
 struct ThreadAcc {
-  uint64_t c[kNC];
+  uint32_t c[LSCAT_P_PERF_FX_HI];  // counter slots 0..15
+  uint64_t fx[4];                  // perf hi, perf lo, gain hi, gain lo
   uint64_t pmin, pmax, gmin, gmax;
 };
 
 __device__ __forceinline__ bool ok_bits(uint32_t b) { return b - 1u < 0x7F7FFFFFu; }  // 0 < b < 0x7F800000
 __device__ __forceinline__ bool nan_bits(uint32_t b) { return (b & 0x7FFFFFFFu) > 0x7F800000u; }
 
-// Fold one chunk of <= 32 rows (lane-distributed) into the warp-uniform accumulator.
+__device__ __forceinline__ void acc_init(GroupAcc& a) {
+  a.min_bits = a.min_bid = 0xFFFFFFFFu;
+  a.n_ok = a.n_nan = a.n_rows = 0;
+  a.lcode = 0;
+  a.l_bits = 0;
+}
+
+// One row folded into a lane's own accumulator (staged path: one group per lane).
+__device__ __forceinline__ void fold_row(GroupAcc& a, uint32_t bits, uint32_t b, uint32_t ell) {
+  const bool ok = ok_bits(bits);
+  a.n_rows++;
+  a.n_ok += ok;
+  a.n_nan += nan_bits(bits);
+  if (ok && (bits < a.min_bits || (bits == a.min_bits && b < a.min_bid))) {
+    a.min_bits = bits;
+    a.min_bid = b;
+  }
+  if (b == ell) {
+    a.lcode = ok ? 2u : 1u;
+    a.l_bits = bits;
+  }
+}
+
+// Fold one chunk of <= 32 rows (lane-distributed) into a warp-uniform accumulator (fallback
+// path for groups of more than 32 rows).
 __device__ __forceinline__ void fold_chunk(GroupAcc& a, bool valid, uint32_t bits, uint32_t b,
                                            uint32_t ell) {
   const unsigned FULL = 0xffffffffu;
@@ -93,20 +120,29 @@ __device__ __forceinline__ void fold_chunk(GroupAcc& a, bool valid, uint32_t bit
 
 __device__ __forceinline__ uint64_t f64_key(double v) { return (uint64_t)__double_as_longlong(v); }
 
-// The paper's per-group statistics from the merged accumulator (O3 steps 3-9).
-__device__ void finalize_group(const RP& p, uint64_t g, const GroupAcc& a, ThreadAcc& t,
-                               uint32_t* sh_perf, uint32_t* sh_gain, uint32_t* sh_bb) {
-  const bool acc = g >= p.acc_lo && g < p.acc_hi;
+__device__ __forceinline__ void hist_add(uint32_t* h, int bin) {
+  // warp-aggregated shared-memory increment: lanes with the same bin add once
+  const unsigned peers = __match_any_sync(0xffffffffu, bin);
+  if (bin >= 0 && (__ffs(peers) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&h[bin], (uint32_t)__popc(peers));
+}
+
+// The paper's per-group statistics (O3 steps 3-9).  Warp-collective: all 32
+// lanes call it; `active` lanes hold group g's accumulator.
+__device__ void finalize_lane(const RP& p, uint64_t g, bool active, const GroupAcc& a,
+                              ThreadAcc& t, uint32_t* sh_perf, uint32_t* sh_gain, uint32_t* sh_bb) {
+  const unsigned FULL = 0xffffffffu;
+  const bool acc = active && g >= p.acc_lo && g < p.acc_hi;
   const bool complete = a.n_rows == p.L && a.n_ok == a.n_rows;
-  const bool defined = p.policy ? complete : a.n_ok >= 1;
+  const bool defined = active && (p.policy ? complete : a.n_ok >= 1);
   uint32_t flags = 0;
   if (a.n_ok == 0) flags |= LSCAT_GF_ALL_NAN;
   if (complete) flags |= LSCAT_GF_COMPLETE;
   double perf = __longlong_as_double(0x7FF8000000000000ll), gain = perf;
+  int pbin = -1, gbin = -1, bbi = -1;
   if (defined) {
     flags |= LSCAT_GF_DEFINED;
     const uint32_t mat = p.gmat ? p.gmat[g] : (uint32_t)((p.first_group + g) % p.M);
-    if (acc) atomicAdd(&sh_bb[mat * p.L + a.min_bid], 1u);
+    bbi = (int)(mat * p.L + a.min_bid);
     if (a.lcode == 2) {
       flags |= LSCAT_GF_RATIO_DEFINED;
       const double b = (double)__uint_as_float(a.min_bits), tt = (double)__uint_as_float(a.l_bits);
@@ -125,25 +161,23 @@ __device__ void finalize_group(const RP& p, uint64_t g, const GroupAcc& a, Threa
         int k = (int)floor(__ddiv_rn(nbb, tt));
         while (__dmul_rn((double)(k + 1), tt) <= nbb) k++;
         while (k > 0 && __dmul_rn((double)k, tt) > nbb) k--;
-        atomicAdd(&sh_perf[k], 1u);
+        pbin = k;
         // gain bin: overflow iff t >= (cap+1) b; else m - nb, m = largest with m b <= nb t
-        int gb;
         if (tt >= __dmul_rn((double)(p.cap + 1), b)) {
-          gb = (int)(p.cap * p.nb);
+          gbin = (int)(p.cap * p.nb);
         } else {
           int m = (int)floor(__ddiv_rn(nbt, b));
           while (__dmul_rn((double)(m + 1), b) <= nbt) m++;
           while (__dmul_rn((double)m, b) > nbt) m--;
-          gb = m - (int)p.nb;
+          gbin = m - (int)p.nb;
         }
-        atomicAdd(&sh_gain[gb], 1u);
         const uint64_t fxp = (uint64_t)__dmul_rn(perf, 4503599627370496.0);  // floor(perf 2^52)
         const double gc = gain < 1048576.0 ? gain : 1048576.0;
         const uint64_t fxg = (uint64_t)__dmul_rn(gc, 4294967296.0);          // floor(gain 2^32)
-        t.c[LSCAT_P_PERF_FX_HI] += fxp >> 21;
-        t.c[LSCAT_P_PERF_FX_LO] += fxp & ((1ull << 21) - 1);
-        t.c[LSCAT_P_GAIN_FX_HI] += fxg >> 21;
-        t.c[LSCAT_P_GAIN_FX_LO] += fxg & ((1ull << 21) - 1);
+        t.fx[0] += fxp >> 21;
+        t.fx[1] += fxp & ((1ull << 21) - 1);
+        t.fx[2] += fxg >> 21;
+        t.fx[3] += fxg & ((1ull << 21) - 1);
         const uint64_t kp = f64_key(perf), kg = f64_key(gain);
         t.pmin = min(t.pmin, kp); t.pmax = max(t.pmax, kp);
         t.gmin = min(t.gmin, kg); t.gmax = max(t.gmax, kg);
@@ -152,40 +186,50 @@ __device__ void finalize_group(const RP& p, uint64_t g, const GroupAcc& a, Threa
       flags |= LSCAT_GF_LARGEST_MISSING;
     }
   }
-  if (acc) {
-    t.c[LSCAT_P_GROUPS] += 1;
-    t.c[LSCAT_P_ROWS] += a.n_rows;
-    t.c[LSCAT_P_OK] += a.n_ok;
-    t.c[LSCAT_P_NAN] += a.n_nan;
-    t.c[LSCAT_P_INVALID] += a.n_rows - a.n_ok - a.n_nan;
-    t.c[LSCAT_P_DEFINED] += (flags & LSCAT_GF_DEFINED) != 0;
-    t.c[LSCAT_P_ALL_NAN] += (flags & LSCAT_GF_ALL_NAN) != 0;
-    t.c[LSCAT_P_COMPLETE] += complete;
-    t.c[LSCAT_P_INCOMPLETE] += !complete;
-    t.c[LSCAT_P_LARGEST_MISSING] += (flags & LSCAT_GF_LARGEST_MISSING) != 0;
-    t.c[LSCAT_P_RATIO_DEFINED] += (flags & LSCAT_GF_RATIO_DEFINED) != 0;
-    t.c[LSCAT_P_LARGEST_IS_BEST] += (flags & LSCAT_GF_LARGEST_IS_BEST) != 0;
-    t.c[LSCAT_P_LARGEST_SLOWER] += (flags & LSCAT_GF_LARGEST_SLOWER) != 0;
-    t.c[LSCAT_P_GAIN_GT] += (flags & LSCAT_GF_GAIN_GT) != 0;
-    t.c[LSCAT_P_PERF_LT] += (flags & LSCAT_GF_PERF_LT) != 0;
-    t.c[LSCAT_P_PERF_BAND] += (flags & LSCAT_GF_PERF_BAND) != 0;
+  if (active) {
+    if (p.o_best) p.o_best[g] = defined ? (uint16_t)a.min_bid : (uint16_t)0xFFFF;
+    if (p.o_bestrt) p.o_bestrt[g] = defined ? __uint_as_float(a.min_bits) : __int_as_float(0x7FC00000);
+    if (p.o_perf) p.o_perf[g] = perf;
+    if (p.o_gain) p.o_gain[g] = gain;
+    if (p.o_flags) p.o_flags[g] = flags;
   }
-  if (p.o_best) p.o_best[g] = defined ? (uint16_t)a.min_bid : (uint16_t)0xFFFF;
-  if (p.o_bestrt) p.o_bestrt[g] = defined ? __uint_as_float(a.min_bits) : __int_as_float(0x7FC00000);
-  if (p.o_perf) p.o_perf[g] = perf;
-  if (p.o_gain) p.o_gain[g] = gain;
-  if (p.o_flags) p.o_flags[g] = flags;
+  // warp-collective accumulation
+  if (!acc) { flags = 0; bbi = -1; }
+  t.c[LSCAT_P_GROUPS] += __popc(__ballot_sync(FULL, acc));
+  t.c[LSCAT_P_ROWS] += __reduce_add_sync(FULL, acc ? a.n_rows : 0u);
+  t.c[LSCAT_P_OK] += __reduce_add_sync(FULL, acc ? a.n_ok : 0u);
+  t.c[LSCAT_P_NAN] += __reduce_add_sync(FULL, acc ? a.n_nan : 0u);
+  t.c[LSCAT_P_INVALID] += __reduce_add_sync(FULL, acc ? a.n_rows - a.n_ok - a.n_nan : 0u);
+  t.c[LSCAT_P_DEFINED] += __popc(__ballot_sync(FULL, flags & LSCAT_GF_DEFINED));
+  t.c[LSCAT_P_ALL_NAN] += __popc(__ballot_sync(FULL, flags & LSCAT_GF_ALL_NAN));
+  t.c[LSCAT_P_COMPLETE] += __popc(__ballot_sync(FULL, flags & LSCAT_GF_COMPLETE));
+  t.c[LSCAT_P_INCOMPLETE] += __popc(__ballot_sync(FULL, acc && !(flags & LSCAT_GF_COMPLETE)));
+  t.c[LSCAT_P_LARGEST_MISSING] += __popc(__ballot_sync(FULL, flags & LSCAT_GF_LARGEST_MISSING));
+  t.c[LSCAT_P_RATIO_DEFINED] += __popc(__ballot_sync(FULL, flags & LSCAT_GF_RATIO_DEFINED));
+  t.c[LSCAT_P_LARGEST_IS_BEST] += __popc(__ballot_sync(FULL, flags & LSCAT_GF_LARGEST_IS_BEST));
+  t.c[LSCAT_P_LARGEST_SLOWER] += __popc(__ballot_sync(FULL, flags & LSCAT_GF_LARGEST_SLOWER));
+  t.c[LSCAT_P_GAIN_GT] += __popc(__ballot_sync(FULL, flags & LSCAT_GF_GAIN_GT));
+  t.c[LSCAT_P_PERF_LT] += __popc(__ballot_sync(FULL, flags & LSCAT_GF_PERF_LT));
+  t.c[LSCAT_P_PERF_BAND] += __popc(__ballot_sync(FULL, flags & LSCAT_GF_PERF_BAND));
+  hist_add(sh_perf, pbin);
+  hist_add(sh_gain, gbin);
+  hist_add(sh_bb, bbi);
 }
 
 __device__ void flush(const RP& p, ThreadAcc& t, uint64_t* sh_c, uint32_t* sh) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
+  if (lane == 0) {
 #pragma unroll
-  for (int i = 0; i < kNC; i++) {
-    uint64_t v = t.c[i];
+    for (int i = 0; i < LSCAT_P_PERF_FX_HI; i++)
+      if (t.c[i]) atomicAdd((unsigned long long*)&sh_c[i], (unsigned long long)t.c[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    uint64_t v = t.fx[i];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-    if (lane == 0 && v) atomicAdd((unsigned long long*)&sh_c[i], (unsigned long long)v);
+    if (lane == 0 && v) atomicAdd((unsigned long long*)&sh_c[LSCAT_P_PERF_FX_HI + i], (unsigned long long)v);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -211,32 +255,45 @@ __device__ __forceinline__ void init_shared(const RP& p, uint64_t* sh_c, uint32_
   for (int i = threadIdx.x; i < kNC; i += blockDim.x) sh_c[i] = 0;
   for (uint32_t i = threadIdx.x; i < p.smem_words; i += blockDim.x) sh[i] = 0;
 #pragma unroll
-  for (int i = 0; i < kNC; i++) t.c[i] = 0;
+  for (int i = 0; i < LSCAT_P_PERF_FX_HI; i++) t.c[i] = 0;
+#pragma unroll
+  for (int i = 0; i < 4; i++) t.fx[i] = 0;
   t.pmin = t.gmin = ~0ull;
   t.pmax = t.gmax = 0;
   __syncthreads();
 }
 
-constexpr int kU = 8;  // groups whose rows are in flight per lane
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kStageRows = 1024;                      // rows staged per warp batch
+constexpr int kStagePad = kStageRows + kStageRows / 32;  // + 1 word per 32 rows: no bank conflicts
+constexpr size_t kStageBytes = (size_t)kWarps * kStagePad * (4 + 2);
 
-__global__ void __launch_bounds__(256) reduce_groups_kernel(RP p) {
+// a6/a7: a warp takes 32 consecutive groups.  When every group has <= 32 rows and the batch
+// has <= 1024 rows (always, for the paper's tables), the rows are loaded with coalesced loads
+// (8 in flight per lane) into the warp's shared-memory stage and lane j then folds group j's
+// rows sequentially; otherwise the warp folds each group with redux/ballot (fallback).
+__global__ void __launch_bounds__(kThreads, 2) reduce_groups_kernel(RP p) {
   extern __shared__ uint64_t dyn[];
   uint64_t* sh_c = dyn;
   uint32_t* sh = reinterpret_cast<uint32_t*>(dyn + kNC);
   uint32_t* sh_perf = sh;
   uint32_t* sh_gain = sh + (p.nb + 1);
   uint32_t* sh_bb = sh_gain + (p.cap * p.nb + 1);
+  uint8_t* stage = reinterpret_cast<uint8_t*>(dyn) + kNC * 8 + ((p.smem_words * 4 + 15) & ~15u);
   ThreadAcc t;
   init_shared(p, sh_c, sh, t);
   const unsigned FULL = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint32_t* s_rt = reinterpret_cast<uint32_t*>(stage) + (size_t)wib * kStagePad;
+  uint16_t* s_id = reinterpret_cast<uint16_t*>(stage + (size_t)kWarps * kStagePad * 4) + (size_t)wib * kStagePad;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t base = warp * 32; base < p.n_groups; base += nwarps * 32) {
-    // group row ranges: lane l holds [lo, hi) of group base + l
+    const int nj = (int)min((uint64_t)32, p.n_groups - base);
     const uint64_t gl = base + lane;
     int64_t lo = 0, hi = 0;
-    if (gl < p.n_groups) {
+    if (lane < nj) {
       if (p.rpg) {
         lo = (int64_t)(gl * p.rpg);
         hi = min((int64_t)(lo + p.rpg), (int64_t)p.n_rows);
@@ -245,60 +302,66 @@ __global__ void __launch_bounds__(256) reduce_groups_kernel(RP p) {
         hi = p.off[gl + 1];
       }
     }
+    const int64_t R0 = __shfl_sync(FULL, lo, 0);
+    const int64_t R1 = __shfl_sync(FULL, hi, nj - 1);
+    const uint32_t maxlen = __reduce_max_sync(FULL, (uint32_t)(hi - lo));
+    const int64_t total = R1 - R0;
     GroupAcc mine;
-    mine.min_bits = mine.min_bid = 0xFFFFFFFFu;
-    mine.n_ok = mine.n_nan = mine.n_rows = 0;
-    mine.lcode = 0;
-    mine.l_bits = 0;
-    const int nj = (int)min((uint64_t)32, p.n_groups - base);
-    for (int j0 = 0; j0 < nj; j0 += kU) {
-      uint32_t bits[kU], bb[kU];
-      int64_t r0[kU], r1[kU];
+    acc_init(mine);
+    if (maxlen <= 32 && total >= 0 && total <= kStageRows) {
+      const int tot = (int)total;
+      constexpr int kU = 16;  // rows in flight per lane
+      for (int r0 = 0; r0 < tot; r0 += 32 * kU) {
+        uint32_t v[kU];
+        uint16_t b[kU];
 #pragma unroll
-      for (int u = 0; u < kU; u++) {
-        r0[u] = __shfl_sync(FULL, lo, j0 + u);
-        r1[u] = __shfl_sync(FULL, hi, j0 + u);
-        const int64_t r = r0[u] + lane;
-        const bool v = (j0 + u < nj) && r < r1[u];
-        bits[u] = v ? __float_as_uint(__ldcs(p.rt + r)) : 0u;
-        bb[u] = v ? (uint32_t)__ldcs(p.bid + r) : 0u;
-      }
-#pragma unroll
-      for (int u = 0; u < kU; u++) {
-        if (j0 + u >= nj) break;
-        GroupAcc a;
-        a.min_bits = a.min_bid = 0xFFFFFFFFu;
-        a.n_ok = a.n_nan = a.n_rows = 0;
-        a.lcode = 0;
-        a.l_bits = 0;
-        fold_chunk(a, r0[u] + lane < r1[u], bits[u], bb[u], p.ell);
-        for (int64_t c = r0[u] + 32; c < r1[u]; c += 32) {  // groups of more than 32 rows
-          const int64_t r = c + lane;
-          const bool v = r < r1[u];
-          fold_chunk(a, v, v ? __float_as_uint(__ldcs(p.rt + r)) : 0u,
-                     v ? (uint32_t)__ldcs(p.bid + r) : 0u, p.ell);
+        for (int u = 0; u < kU; u++) {
+          const int r = r0 + u * 32 + lane;
+          v[u] = r < tot ? __float_as_uint(__ldcs(p.rt + R0 + r)) : 0u;
+          b[u] = r < tot ? __ldcs(p.bid + R0 + r) : (uint16_t)0;
         }
-        if (lane == j0 + u) mine = a;
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+          const int r = r0 + u * 32 + lane;
+          if (r < tot) {
+            s_rt[r + (r >> 5)] = v[u];
+            s_id[r + (r >> 5)] = b[u];
+          }
+        }
+      }
+      __syncwarp();
+      if (lane < nj) {
+        const int a1 = (int)(hi - R0);
+        for (int r = (int)(lo - R0); r < a1; r++) fold_row(mine, s_rt[r + (r >> 5)], s_id[r + (r >> 5)], p.ell);
+      }
+      __syncwarp();
+    } else {
+      for (int j = 0; j < nj; j++) {
+        const int64_t r0 = __shfl_sync(FULL, lo, j), r1 = __shfl_sync(FULL, hi, j);
+        GroupAcc a;
+        acc_init(a);
+        for (int64_t c = r0; c < r1; c += 32) {
+          const int64_t r = c + lane;
+          const bool v = r < r1;
+          fold_chunk(a, v, v ? __float_as_uint(__ldcs(p.rt + r)) : 0u, v ? (uint32_t)__ldcs(p.bid + r) : 0u, p.ell);
+        }
+        if (lane == j) mine = a;
       }
     }
-    if (lane < nj) {
-      const uint64_t g = base + lane;
-      if (p.mode == MODE_FUSED) {
-        finalize_group(p, g, mine, t, sh_perf, sh_gain, sh_bb);
-      } else {  // MODE_GROUP_PARTIALS: per-group values for the NCCL MIN/MAX/SUM merge
-        p.g_key[g] = mine.min_bits == 0xFFFFFFFFu ? ~0ull
-                                                   : (((uint64_t)mine.min_bits << 32) | mine.min_bid);
-        p.g_lcode[g] = mine.lcode == 2 ? ((1ull << 32) | mine.l_bits) : (uint64_t)mine.lcode;
-        p.g_cnt[3 * g + 0] = mine.n_ok;
-        p.g_cnt[3 * g + 1] = mine.n_nan;
-        p.g_cnt[3 * g + 2] = mine.n_rows;
-      }
+    if (p.mode == MODE_FUSED) {
+      finalize_lane(p, gl, lane < nj, mine, t, sh_perf, sh_gain, sh_bb);
+    } else if (lane < nj) {  // MODE_GROUP_PARTIALS: per-group values for the NCCL MIN/MAX/SUM merge
+      p.g_key[gl] = mine.min_bits == 0xFFFFFFFFu ? ~0ull : (((uint64_t)mine.min_bits << 32) | mine.min_bid);
+      p.g_lcode[gl] = mine.lcode == 2 ? ((1ull << 32) | mine.l_bits) : (uint64_t)mine.lcode;
+      p.g_cnt[3 * gl + 0] = mine.n_ok;
+      p.g_cnt[3 * gl + 1] = mine.n_nan;
+      p.g_cnt[3 * gl + 2] = mine.n_rows;
     }
   }
   flush(p, t, sh_c, sh);
 }
 
-__global__ void __launch_bounds__(256) finalize_merged_kernel(RP p) {
+__global__ void __launch_bounds__(kThreads) finalize_merged_kernel(RP p) {
   extern __shared__ uint64_t dyn[];
   uint64_t* sh_c = dyn;
   uint32_t* sh = reinterpret_cast<uint32_t*>(dyn + kNC);
@@ -307,21 +370,29 @@ __global__ void __launch_bounds__(256) finalize_merged_kernel(RP p) {
   uint32_t* sh_bb = sh_gain + (p.cap * p.nb + 1);
   ThreadAcc t;
   init_shared(p, sh_c, sh, t);
-  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < p.n_groups;
-       g += (uint64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t base = warp * 32; base < p.n_groups; base += nwarps * 32) {
+    const uint64_t g = base + lane;
+    const bool active = g < p.n_groups;
     GroupAcc a;
-    const uint64_t key = p.g_key[g], lc = p.g_lcode[g];
-    a.min_bits = key == ~0ull ? 0xFFFFFFFFu : (uint32_t)(key >> 32);
-    a.min_bid = key == ~0ull ? 0xFFFFFFFFu : (uint32_t)(key & 0xFFFFFFFFu);
-    a.n_ok = p.g_cnt[3 * g];
-    a.n_nan = p.g_cnt[3 * g + 1];
-    a.n_rows = p.g_cnt[3 * g + 2];
-    a.lcode = lc >> 32 ? 2u : (uint32_t)lc;
-    a.l_bits = (uint32_t)(lc & 0xFFFFFFFFu);
-    finalize_group(p, g, a, t, sh_perf, sh_gain, sh_bb);
+    acc_init(a);
+    if (active) {
+      const uint64_t key = p.g_key[g], lc = p.g_lcode[g];
+      a.min_bits = key == ~0ull ? 0xFFFFFFFFu : (uint32_t)(key >> 32);
+      a.min_bid = key == ~0ull ? 0xFFFFFFFFu : (uint32_t)(key & 0xFFFFFFFFu);
+      a.n_ok = p.g_cnt[3 * g];
+      a.n_nan = p.g_cnt[3 * g + 1];
+      a.n_rows = p.g_cnt[3 * g + 2];
+      a.lcode = lc >> 32 ? 2u : (uint32_t)lc;
+      a.l_bits = (uint32_t)(lc & 0xFFFFFFFFu);
+    }
+    finalize_lane(p, g, active, a, t, sh_perf, sh_gain, sh_bb);
   }
   flush(p, t, sh_c, sh);
 }
+
 
 __global__ void init_minmax(uint64_t* mm) {
   mm[0] = ~0ull; mm[1] = 0; mm[2] = ~0ull; mm[3] = 0;
@@ -393,7 +464,8 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
     return fail(ctx, LSCAT_ERR_INVALID_ARG, "reduce_table: n_groups != ceil(n_rows / rows_per_group)");
   const size_t sh_words = (o->bins_per_unit + 1) + ((size_t)o->gain_cap * o->bins_per_unit + 1) +
                           (size_t)o->n_matrices * o->n_blocks;
-  const size_t smem = kNC * 8 + sh_words * 4;
+  const size_t smem_fin = kNC * 8 + sh_words * 4;
+  const size_t smem = kNC * 8 + ((sh_words * 4 + 15) & ~(size_t)15) + kStageBytes;
   if (smem > 200 * 1024)
     return fail(ctx, LSCAT_ERR_UNSUPPORTED, "reduce_table: histograms need %zu B of shared memory", smem);
   cudaStream_t s = (cudaStream_t)stream;
@@ -460,11 +532,13 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
   ctx->launches++;
   if (smem > 48 * 1024) {
     LSCAT_CUDA(ctx, cudaFuncSetAttribute(reduce_groups_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    LSCAT_CUDA(ctx, cudaFuncSetAttribute(finalize_merged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    LSCAT_CUDA(ctx, cudaFuncSetAttribute(finalize_merged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fin));
   }
   const bool merge = ctx->world > 1 && o->point_sharded;
   const uint64_t warps_needed = (G + 31) / 32;
-  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)ctx->sm_count * 8, (warps_needed + 7) / 8));
+  int occ = 0;
+  LSCAT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, reduce_groups_kernel, 256, smem));
+  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)ctx->sm_count * std::max(occ, 1), (warps_needed + 7) / 8));
   p.acc_lo = 0;
   p.acc_hi = G;
   uint64_t own_lo = 0, own_hi = G;
@@ -481,10 +555,9 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
     if (err) return cuda_fail(ctx, err, "scratch");
     uint32_t* cnt = (uint32_t*)scratch(ctx, "g_cnt", G * 12, &err);
     if (err) return cuda_fail(ctx, err, "scratch");
-    init_group_merge<<<ctx->sm_count * 4, 256, 0, s>>>(key, lc, cnt, G);
     p.g_key = key; p.g_lcode = lc; p.g_cnt = cnt;
     p.mode = MODE_GROUP_PARTIALS;
-    if (G) reduce_groups_kernel<<<grid, 256, smem, s>>>(p);
+    if (G) reduce_groups_kernel<<<grid, 256, smem, s>>>(p), ctx->launches++;
     LSCAT_CUDA(ctx, cudaGetLastError());
     lscat_status ns;
     if ((ns = nccl_check(ctx, ncclGroupStart(), "ncclGroupStart"))) return ns;
@@ -502,7 +575,7 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
     init_minmax<<<1, 1, 0, s>>>(p.minmax);
     p.mode = MODE_FINALIZE_MERGED;
     const int g2 = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)ctx->sm_count * 4, (G + 255) / 256));
-    if (G) finalize_merged_kernel<<<g2, 256, smem, s>>>(p);
+    if (G) finalize_merged_kernel<<<g2, 256, smem_fin, s>>>(p), ctx->launches++;
     LSCAT_CUDA(ctx, cudaGetLastError());
   }
   if (ctx->world > 1) {

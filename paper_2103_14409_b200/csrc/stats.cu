@@ -196,14 +196,31 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
           cands[r].insert(cands[r].end(), pk + 1, pk + 1 + pk[0]);
         }
     } else {
-      LSCAT_CUDA(ctx, cudaMemcpyAsync(hist.data(), d_hist, hist.size() * 4, cudaMemcpyDeviceToHost, s));
-      LSCAT_CUDA(ctx, cudaMemcpyAsync(ccnt.data(), d_ccnt, nr * 4, cudaMemcpyDeviceToHost, s));
+      // one D2H of histograms + counts, then one batch of candidate copies: <= 2 host syncs
+      uint32_t* h = (uint32_t*)pinned(ctx, "sel_h", (size_t)nr * kBins * 4 + kMaxRanges * 4, &err);
+      if (err) return cuda_fail(ctx, err, "stats: pinned");
+      uint32_t* hc = h + (size_t)nr * kBins;
+      LSCAT_CUDA(ctx, cudaMemcpyAsync(h, d_hist, (size_t)nr * kBins * 4, cudaMemcpyDeviceToHost, s));
+      LSCAT_CUDA(ctx, cudaMemcpyAsync(hc, d_ccnt, nr * 4, cudaMemcpyDeviceToHost, s));
       LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
-      for (int r = 0; r < nr; r++) {
-        if (!ranges[r].gather) continue;
-        const uint32_t c = std::min(ccnt[r], kCap);
-        cands[r].resize(c);
-        if (c) LSCAT_CUDA(ctx, cudaMemcpy(cands[r].data(), d_cand + (size_t)r * kCap, c * 8, cudaMemcpyDeviceToHost));
+      memcpy(hist.data(), h, (size_t)nr * kBins * 4);
+      size_t ncand = 0;
+      for (int r = 0; r < nr; r++) ccnt[r] = ranges[r].gather ? std::min(hc[r], kCap) : 0;
+      for (int r = 0; r < nr; r++) ncand += ccnt[r];
+      if (ncand) {
+        uint64_t* hk = (uint64_t*)pinned(ctx, "sel_k", ncand * 8, &err);
+        if (err) return cuda_fail(ctx, err, "stats: pinned");
+        size_t at = 0;
+        for (int r = 0; r < nr; r++) {
+          if (ccnt[r]) LSCAT_CUDA(ctx, cudaMemcpyAsync(hk + at, d_cand + (size_t)r * kCap, ccnt[r] * 8, cudaMemcpyDeviceToHost, s));
+          at += ccnt[r];
+        }
+        LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
+        at = 0;
+        for (int r = 0; r < nr; r++) {
+          cands[r].assign(hk + at, hk + at + ccnt[r]);
+          at += ccnt[r];
+        }
       }
     }
     for (int r = 0; r < nr; r++)
