@@ -26,6 +26,7 @@ namespace {
 
 constexpr int BM = 128, BN = 256, BK = 64, UK = 16;
 constexpr int kStages = 4;
+constexpr int kGroupM = 16;  // tile rows per rasterisation group
 constexpr int kStageA = BM * BK * 2;  // 16 KB
 constexpr int kStageB = BN * BK * 2;  // 32 KB
 constexpr int kSmem = kStages * (kStageA + kStageB) + 1024 /*align*/ + 256 /*barriers*/;
@@ -104,7 +105,15 @@ __global__ void __launch_bounds__(B, 1) gemm_kernel(const __grid_constant__ Gemm
   uint32_t* tmem_slot = (uint32_t*)(tmem_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  // grouped rasterisation: consecutive CTAs walk kGroupM tile rows before the next tile
+  // column, so a wave's A and Bt tiles stay L2-resident (A is re-read once per group, not per
+  // tile column)
+  const int mt = (N + BM - 1) / BM, nt = (N + BN - 1) / BN;
+  const int pid = blockIdx.x, per_group = kGroupM * nt;
+  const int first_m = (pid / per_group) * kGroupM;
+  const int gm = min(mt - first_m, kGroupM);
+  const int m0 = (first_m + (pid % per_group) % gm) * BM;
+  const int n0 = ((pid % per_group) / gm) * BN;
   const int kblocks = (N + BK - 1) / BK;
 
   if (warp == 0 && lane == 0) {
@@ -223,7 +232,7 @@ struct GemmL {
         attr = true;
       }
       const int N = (int)e.n;
-      dim3 grid((N + BM - 1) / BM, (N + BN - 1) / BN);
+      const int grid = ((N + BM - 1) / BM) * ((N + BN - 1) / BN);
       gemm_kernel<B><<<grid, B, kSmem, s>>>(*reinterpret_cast<const GemmMaps*>(e.host_blob),
                                             (__nv_bfloat16*)e.out, N);
       return cudaGetLastError();

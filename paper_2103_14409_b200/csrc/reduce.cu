@@ -55,6 +55,7 @@ struct RP {
   uint32_t* g_cnt;  // [3*G]: n_ok, n_nan, n_rows
   int mode;
   uint32_t smem_words;  // perf + gain + best-block histogram words in smem
+  uint32_t vec;         // runtime / block-id arrays are 16-byte aligned (vector path allowed)
 };
 
 struct GroupAcc {
@@ -67,7 +68,6 @@ struct GroupAcc {
 // Per-warp accumulators.  Counters are warp-uniform (built from ballots / redux, identical in
 // every lane, flushed by lane 0); fixed-point sums and percentile key bounds are per lane.
 struct ThreadAcc {
-  uint32_t c[LSCAT_P_PERF_FX_HI];  // counter slots 0..15
   uint64_t fx[4];                  // perf hi, perf lo, gain hi, gain lo
   uint64_t pmin, pmax, gmin, gmax;
 };
@@ -118,6 +118,11 @@ __device__ __forceinline__ void fold_chunk(GroupAcc& a, bool valid, uint32_t bit
   }
 }
 
+// warp-uniform counter increment: lane 0 adds to the CTA's shared counter slot
+__device__ __forceinline__ void wadd(uint64_t* sh_c, int slot, uint32_t v) {
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd((unsigned long long*)&sh_c[slot], (unsigned long long)v);
+}
+
 __device__ __forceinline__ uint64_t f64_key(double v) { return (uint64_t)__double_as_longlong(v); }
 
 __device__ __forceinline__ void hist_add(uint32_t* h, int bin) {
@@ -129,7 +134,8 @@ __device__ __forceinline__ void hist_add(uint32_t* h, int bin) {
 // The paper's per-group statistics (O3 steps 3-9).  Warp-collective: all 32
 // lanes call it; `active` lanes hold group g's accumulator.
 __device__ void finalize_lane(const RP& p, uint64_t g, bool active, const GroupAcc& a,
-                              ThreadAcc& t, uint32_t* sh_perf, uint32_t* sh_gain, uint32_t* sh_bb) {
+                              ThreadAcc& t, uint64_t* sh_c, uint32_t* sh_perf, uint32_t* sh_gain,
+                              uint32_t* sh_bb) {
   const unsigned FULL = 0xffffffffu;
   const bool acc = active && g >= p.acc_lo && g < p.acc_hi;
   const bool complete = a.n_rows == p.L && a.n_ok == a.n_rows;
@@ -157,8 +163,8 @@ __device__ void finalize_lane(const RP& p, uint64_t g, bool active, const GroupA
       if (plt && __dmul_rn((double)p.bld, b) >= __dmul_rn((double)p.bln, tt)) flags |= LSCAT_GF_PERF_BAND;
       if (acc) {
         const double nbb = __dmul_rn((double)p.nb, b), nbt = __dmul_rn((double)p.nb, tt);
-        // perf bin: largest k with k t <= nb b (estimate, then exact fix-up)
-        int k = (int)floor(__ddiv_rn(nbb, tt));
+        // perf bin: largest k with k t <= nb b (estimate from perf, then exact fix-up)
+        int k = (int)floor(__dmul_rn(perf, (double)p.nb));
         while (__dmul_rn((double)(k + 1), tt) <= nbb) k++;
         while (k > 0 && __dmul_rn((double)k, tt) > nbb) k--;
         pbin = k;
@@ -166,7 +172,7 @@ __device__ void finalize_lane(const RP& p, uint64_t g, bool active, const GroupA
         if (tt >= __dmul_rn((double)(p.cap + 1), b)) {
           gbin = (int)(p.cap * p.nb);
         } else {
-          int m = (int)floor(__ddiv_rn(nbt, b));
+          int m = (int)floor(__dmul_rn(__dadd_rn(gain, 1.0), (double)p.nb));
           while (__dmul_rn((double)(m + 1), b) <= nbt) m++;
           while (__dmul_rn((double)m, b) > nbt) m--;
           gbin = m - (int)p.nb;
@@ -195,22 +201,22 @@ __device__ void finalize_lane(const RP& p, uint64_t g, bool active, const GroupA
   }
   // warp-collective accumulation
   if (!acc) { flags = 0; bbi = -1; }
-  t.c[LSCAT_P_GROUPS] += __popc(__ballot_sync(FULL, acc));
-  t.c[LSCAT_P_ROWS] += __reduce_add_sync(FULL, acc ? a.n_rows : 0u);
-  t.c[LSCAT_P_OK] += __reduce_add_sync(FULL, acc ? a.n_ok : 0u);
-  t.c[LSCAT_P_NAN] += __reduce_add_sync(FULL, acc ? a.n_nan : 0u);
-  t.c[LSCAT_P_INVALID] += __reduce_add_sync(FULL, acc ? a.n_rows - a.n_ok - a.n_nan : 0u);
-  t.c[LSCAT_P_DEFINED] += __popc(__ballot_sync(FULL, flags & LSCAT_GF_DEFINED));
-  t.c[LSCAT_P_ALL_NAN] += __popc(__ballot_sync(FULL, flags & LSCAT_GF_ALL_NAN));
-  t.c[LSCAT_P_COMPLETE] += __popc(__ballot_sync(FULL, flags & LSCAT_GF_COMPLETE));
-  t.c[LSCAT_P_INCOMPLETE] += __popc(__ballot_sync(FULL, acc && !(flags & LSCAT_GF_COMPLETE)));
-  t.c[LSCAT_P_LARGEST_MISSING] += __popc(__ballot_sync(FULL, flags & LSCAT_GF_LARGEST_MISSING));
-  t.c[LSCAT_P_RATIO_DEFINED] += __popc(__ballot_sync(FULL, flags & LSCAT_GF_RATIO_DEFINED));
-  t.c[LSCAT_P_LARGEST_IS_BEST] += __popc(__ballot_sync(FULL, flags & LSCAT_GF_LARGEST_IS_BEST));
-  t.c[LSCAT_P_LARGEST_SLOWER] += __popc(__ballot_sync(FULL, flags & LSCAT_GF_LARGEST_SLOWER));
-  t.c[LSCAT_P_GAIN_GT] += __popc(__ballot_sync(FULL, flags & LSCAT_GF_GAIN_GT));
-  t.c[LSCAT_P_PERF_LT] += __popc(__ballot_sync(FULL, flags & LSCAT_GF_PERF_LT));
-  t.c[LSCAT_P_PERF_BAND] += __popc(__ballot_sync(FULL, flags & LSCAT_GF_PERF_BAND));
+  wadd(sh_c, LSCAT_P_GROUPS, __popc(__ballot_sync(FULL, acc)));
+  wadd(sh_c, LSCAT_P_ROWS, __reduce_add_sync(FULL, acc ? a.n_rows : 0u));
+  wadd(sh_c, LSCAT_P_OK, __reduce_add_sync(FULL, acc ? a.n_ok : 0u));
+  wadd(sh_c, LSCAT_P_NAN, __reduce_add_sync(FULL, acc ? a.n_nan : 0u));
+  wadd(sh_c, LSCAT_P_INVALID, __reduce_add_sync(FULL, acc ? a.n_rows - a.n_ok - a.n_nan : 0u));
+  wadd(sh_c, LSCAT_P_DEFINED, __popc(__ballot_sync(FULL, flags & LSCAT_GF_DEFINED)));
+  wadd(sh_c, LSCAT_P_ALL_NAN, __popc(__ballot_sync(FULL, flags & LSCAT_GF_ALL_NAN)));
+  wadd(sh_c, LSCAT_P_COMPLETE, __popc(__ballot_sync(FULL, flags & LSCAT_GF_COMPLETE)));
+  wadd(sh_c, LSCAT_P_INCOMPLETE, __popc(__ballot_sync(FULL, acc && !(flags & LSCAT_GF_COMPLETE))));
+  wadd(sh_c, LSCAT_P_LARGEST_MISSING, __popc(__ballot_sync(FULL, flags & LSCAT_GF_LARGEST_MISSING)));
+  wadd(sh_c, LSCAT_P_RATIO_DEFINED, __popc(__ballot_sync(FULL, flags & LSCAT_GF_RATIO_DEFINED)));
+  wadd(sh_c, LSCAT_P_LARGEST_IS_BEST, __popc(__ballot_sync(FULL, flags & LSCAT_GF_LARGEST_IS_BEST)));
+  wadd(sh_c, LSCAT_P_LARGEST_SLOWER, __popc(__ballot_sync(FULL, flags & LSCAT_GF_LARGEST_SLOWER)));
+  wadd(sh_c, LSCAT_P_GAIN_GT, __popc(__ballot_sync(FULL, flags & LSCAT_GF_GAIN_GT)));
+  wadd(sh_c, LSCAT_P_PERF_LT, __popc(__ballot_sync(FULL, flags & LSCAT_GF_PERF_LT)));
+  wadd(sh_c, LSCAT_P_PERF_BAND, __popc(__ballot_sync(FULL, flags & LSCAT_GF_PERF_BAND)));
   hist_add(sh_perf, pbin);
   hist_add(sh_gain, gbin);
   hist_add(sh_bb, bbi);
@@ -219,11 +225,6 @@ __device__ void finalize_lane(const RP& p, uint64_t g, bool active, const GroupA
 __device__ void flush(const RP& p, ThreadAcc& t, uint64_t* sh_c, uint32_t* sh) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
-  if (lane == 0) {
-#pragma unroll
-    for (int i = 0; i < LSCAT_P_PERF_FX_HI; i++)
-      if (t.c[i]) atomicAdd((unsigned long long*)&sh_c[i], (unsigned long long)t.c[i]);
-  }
 #pragma unroll
   for (int i = 0; i < 4; i++) {
     uint64_t v = t.fx[i];
@@ -255,8 +256,6 @@ __device__ __forceinline__ void init_shared(const RP& p, uint64_t* sh_c, uint32_
   for (int i = threadIdx.x; i < kNC; i += blockDim.x) sh_c[i] = 0;
   for (uint32_t i = threadIdx.x; i < p.smem_words; i += blockDim.x) sh[i] = 0;
 #pragma unroll
-  for (int i = 0; i < LSCAT_P_PERF_FX_HI; i++) t.c[i] = 0;
-#pragma unroll
   for (int i = 0; i < 4; i++) t.fx[i] = 0;
   t.pmin = t.gmin = ~0ull;
   t.pmax = t.gmax = 0;
@@ -268,6 +267,159 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kStageRows = 1024;                      // rows staged per warp batch
 constexpr int kStagePad = kStageRows + kStageRows / 32;  // + 1 word per 32 rows: no bank conflicts
 constexpr size_t kStageBytes = (size_t)kWarps * kStagePad * (4 + 2);
+
+
+constexpr size_t kUniStageBytes = (size_t)kWarps * 2 * (1024 * 4 + 1024 * 2);  // double buffer
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
+
+// Copy batch `base` (32 uniform groups = 1024 rows) into a warp stage buffer with cp.async:
+// 8 x 16 B of runtimes and 4 x 16 B of block ids per lane, coalesced, placed in an
+// XOR-swizzled layout (chunk c of group g at c ^ (g & 7) resp. c ^ ((g >> 1) & 3)) so that
+// the per-group 128-bit reads below (lane j <- group j) are bank-conflict free.
+__device__ __forceinline__ void uniform_prefetch(const RP& p, uint64_t base, float4* d, uint4* di, int lane) {
+  const float4* src = reinterpret_cast<const float4*>(p.rt + base * 32);
+  const uint4* isrc = reinterpret_cast<const uint4*>(p.bid + base * 32);
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    const int f = lane + 32 * i, g = f >> 3, c = f & 7;
+    cp_async16(d + g * 8 + (c ^ (g & 7)), src + f);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    const int h = lane + 32 * i, g = h >> 2, c = h & 3;
+    cp_async16(di + g * 4 + (c ^ ((g >> 1) & 3)), isrc + h);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+// Lane j folds group j of a staged batch.
+__device__ __forceinline__ void uniform_fold(const RP& p, const float4* d, const uint4* di, int lane,
+                                             GroupAcc& mine) {
+  uint32_t mkey = 0xFFFFFFFFu, nok = 0, nnan = 0;
+#pragma unroll 2
+  for (int c = 0; c < 8; c++) {
+    const float4 x = d[lane * 8 + (c ^ (lane & 7))];
+    const uint32_t b4[4] = {__float_as_uint(x.x), __float_as_uint(x.y), __float_as_uint(x.z),
+                            __float_as_uint(x.w)};
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const bool ok = ok_bits(b4[q]);
+      mkey = min(mkey, ok ? b4[q] : 0xFFFFFFFFu);
+      nok += ok;
+      nnan += nan_bits(b4[q]);
+    }
+  }
+  uint32_t mid = 0xFFFFFFFFu;
+#pragma unroll 1
+  for (int c = 0; c < 4; c++) {
+    const uint4 y = di[lane * 4 + (c ^ ((lane >> 1) & 3))];
+    const float4 x0 = d[lane * 8 + ((2 * c) ^ (lane & 7))];
+    const float4 x1 = d[lane * 8 + ((2 * c + 1) ^ (lane & 7))];
+    const uint32_t b8[8] = {__float_as_uint(x0.x), __float_as_uint(x0.y), __float_as_uint(x0.z),
+                            __float_as_uint(x0.w), __float_as_uint(x1.x), __float_as_uint(x1.y),
+                            __float_as_uint(x1.z), __float_as_uint(x1.w)};
+    const uint32_t iw[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const uint32_t id = (iw[q >> 1] >> (16 * (q & 1))) & 0xFFFFu;
+      if (mkey != 0xFFFFFFFFu && b8[q] == mkey) mid = min(mid, id);
+      if (id == p.ell) {
+        mine.lcode = ok_bits(b8[q]) ? 2u : 1u;
+        mine.l_bits = b8[q];
+      }
+    }
+  }
+  mine.min_bits = mkey;
+  mine.min_bid = mid;
+  mine.n_ok = nok;
+  mine.n_nan = nnan;
+  mine.n_rows = 32;
+}
+
+__device__ __forceinline__ void emit_group(const RP& p, uint64_t gl, bool active, const GroupAcc& mine,
+                                           ThreadAcc& t, uint64_t* sh_c, uint32_t* sh_perf,
+                                           uint32_t* sh_gain, uint32_t* sh_bb) {
+  if (p.mode == MODE_FUSED) {
+    finalize_lane(p, gl, active, mine, t, sh_c, sh_perf, sh_gain, sh_bb);
+  } else if (active) {  // MODE_GROUP_PARTIALS: per-group values for the NCCL MIN/MAX/SUM merge
+    p.g_key[gl] = mine.min_bits == 0xFFFFFFFFu ? ~0ull : (((uint64_t)mine.min_bits << 32) | mine.min_bid);
+    p.g_lcode[gl] = mine.lcode == 2 ? ((1ull << 32) | mine.l_bits) : (uint64_t)mine.lcode;
+    p.g_cnt[3 * gl + 0] = mine.n_ok;
+    p.g_cnt[3 * gl + 1] = mine.n_nan;
+    p.g_cnt[3 * gl + 2] = mine.n_rows;
+  }
+}
+
+// a6/a7 for tables of uniform 32-row groups with 16-byte aligned arrays (BASELINE configs[4]):
+// each warp streams its batches of 32 groups through a double-buffered cp.async stage (the
+// next batch is in flight while lane j folds group j of the current one).
+__global__ void __launch_bounds__(kThreads, 2) reduce_uniform32_kernel(RP p) {
+  extern __shared__ uint64_t dyn[];
+  uint64_t* sh_c = dyn;
+  uint32_t* sh = reinterpret_cast<uint32_t*>(dyn + kNC);
+  uint32_t* sh_perf = sh;
+  uint32_t* sh_gain = sh + (p.nb + 1);
+  uint32_t* sh_bb = sh_gain + (p.cap * p.nb + 1);
+  uint8_t* stage = reinterpret_cast<uint8_t*>(dyn) + kNC * 8 + ((p.smem_words * 4 + 15) & ~15u);
+  ThreadAcc t;
+  init_shared(p, sh_c, sh, t);
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  float4* d[2];
+  uint4* di[2];
+  for (int b = 0; b < 2; b++) {
+    uint8_t* w = stage + ((size_t)wib * 2 + b) * (1024 * 4 + 1024 * 2);
+    d[b] = reinterpret_cast<float4*>(w);
+    di[b] = reinterpret_cast<uint4*>(w + 1024 * 4);
+  }
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t full_batches = p.n_groups / 32;  // batches of 32 complete 32-row groups
+  uint64_t bi = warp;
+  int cur = 0;
+  if (bi < full_batches) uniform_prefetch(p, bi * 32, d[0], di[0], lane);
+  for (; bi < full_batches; bi += nwarps) {
+    const uint64_t nxt = bi + nwarps;
+    if (nxt < full_batches) {
+      uniform_prefetch(p, nxt * 32, d[cur ^ 1], di[cur ^ 1], lane);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncwarp();
+    GroupAcc mine;
+    acc_init(mine);
+    uniform_fold(p, d[cur], di[cur], lane, mine);
+    __syncwarp();
+    emit_group(p, bi * 32 + lane, true, mine, t, sh_c, sh_perf, sh_gain, sh_bb);
+    cur ^= 1;
+  }
+  // tail: the last < 32 groups (the last one possibly short), warp-per-group folding
+  const uint64_t tail0 = full_batches * 32;
+  if (tail0 < p.n_groups && warp == (full_batches % nwarps)) {
+    const int nj = (int)(p.n_groups - tail0);
+    GroupAcc mine;
+    acc_init(mine);
+    for (int j = 0; j < nj; j++) {
+      const int64_t r0 = (int64_t)(tail0 + j) * 32;
+      const int64_t r1 = min(r0 + 32, (int64_t)p.n_rows);
+      GroupAcc a;
+      acc_init(a);
+      const int64_t r = r0 + lane;
+      const bool v = r < r1;
+      fold_chunk(a, v, v ? __float_as_uint(__ldcs(p.rt + r)) : 0u, v ? (uint32_t)__ldcs(p.bid + r) : 0u, p.ell);
+      if (lane == j) mine = a;
+    }
+    emit_group(p, tail0 + lane, lane < nj, mine, t, sh_c, sh_perf, sh_gain, sh_bb);
+  }
+  (void)FULL;
+  flush(p, t, sh_c, sh);
+}
 
 // a6/a7: a warp takes 32 consecutive groups.  When every group has <= 32 rows and the batch
 // has <= 1024 rows (always, for the paper's tables), the rows are loaded with coalesced loads
@@ -349,7 +501,7 @@ __global__ void __launch_bounds__(kThreads, 2) reduce_groups_kernel(RP p) {
       }
     }
     if (p.mode == MODE_FUSED) {
-      finalize_lane(p, gl, lane < nj, mine, t, sh_perf, sh_gain, sh_bb);
+      finalize_lane(p, gl, lane < nj, mine, t, sh_c, sh_perf, sh_gain, sh_bb);
     } else if (lane < nj) {  // MODE_GROUP_PARTIALS: per-group values for the NCCL MIN/MAX/SUM merge
       p.g_key[gl] = mine.min_bits == 0xFFFFFFFFu ? ~0ull : (((uint64_t)mine.min_bits << 32) | mine.min_bid);
       p.g_lcode[gl] = mine.lcode == 2 ? ((1ull << 32) | mine.l_bits) : (uint64_t)mine.lcode;
@@ -388,7 +540,7 @@ __global__ void __launch_bounds__(kThreads) finalize_merged_kernel(RP p) {
       a.lcode = lc >> 32 ? 2u : (uint32_t)lc;
       a.l_bits = (uint32_t)(lc & 0xFFFFFFFFu);
     }
-    finalize_lane(p, g, active, a, t, sh_perf, sh_gain, sh_bb);
+    finalize_lane(p, g, active, a, t, sh_c, sh_perf, sh_gain, sh_bb);
   }
   flush(p, t, sh_c, sh);
 }
@@ -465,7 +617,8 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
   const size_t sh_words = (o->bins_per_unit + 1) + ((size_t)o->gain_cap * o->bins_per_unit + 1) +
                           (size_t)o->n_matrices * o->n_blocks;
   const size_t smem_fin = kNC * 8 + sh_words * 4;
-  const size_t smem = kNC * 8 + ((sh_words * 4 + 15) & ~(size_t)15) + kStageBytes;
+  const size_t smem_hist = kNC * 8 + ((sh_words * 4 + 15) & ~(size_t)15);
+  size_t smem = smem_hist + kStageBytes;
   if (smem > 200 * 1024)
     return fail(ctx, LSCAT_ERR_UNSUPPORTED, "reduce_table: histograms need %zu B of shared memory", smem);
   cudaStream_t s = (cudaStream_t)stream;
@@ -504,6 +657,7 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
     p.off = T->group_offset;
     p.gmat = T->group_matrix;
   }
+  p.vec = ((uintptr_t)p.rt % 16 == 0) && ((uintptr_t)p.bid % 16 == 0);
   p.n_groups = G;
   p.first_group = T->first_group;
   p.rpg = T->rows_per_group;
@@ -536,15 +690,21 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
   }
   const bool merge = ctx->world > 1 && o->point_sharded;
   const uint64_t warps_needed = (G + 31) / 32;
+  const bool uniform = p.vec && p.rpg == 32;
+  auto kern = uniform ? reduce_uniform32_kernel : reduce_groups_kernel;
+  if (uniform) {
+    smem = smem_hist + kUniStageBytes;
+    LSCAT_CUDA(ctx, cudaFuncSetAttribute(reduce_uniform32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
   int occ = 0;
-  LSCAT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, reduce_groups_kernel, 256, smem));
+  LSCAT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem));
   const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)ctx->sm_count * std::max(occ, 1), (warps_needed + 7) / 8));
   p.acc_lo = 0;
   p.acc_hi = G;
   uint64_t own_lo = 0, own_hi = G;
   if (!merge) {
     p.mode = MODE_FUSED;
-    if (G) reduce_groups_kernel<<<grid, 256, smem, s>>>(p), ctx->launches++;
+    if (G) kern<<<grid, 256, smem, s>>>(p), ctx->launches++;
     LSCAT_CUDA(ctx, cudaGetLastError());
   } else {
     // a9, point-sharded: per-group MIN(key) / MAX(l-code) / SUM(counts) over ranks, then each
@@ -557,7 +717,7 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
     if (err) return cuda_fail(ctx, err, "scratch");
     p.g_key = key; p.g_lcode = lc; p.g_cnt = cnt;
     p.mode = MODE_GROUP_PARTIALS;
-    if (G) reduce_groups_kernel<<<grid, 256, smem, s>>>(p), ctx->launches++;
+    if (G) kern<<<grid, 256, smem, s>>>(p), ctx->launches++;
     LSCAT_CUDA(ctx, cudaGetLastError());
     lscat_status ns;
     if ((ns = nccl_check(ctx, ncclGroupStart(), "ncclGroupStart"))) return ns;

@@ -154,3 +154,56 @@ def test_uniform_groups_without_offsets():
         assert st[k] == v, k
     assert (st["best_block_hist"] == ref.best_block_hist).all()
     assert st["pct_perf"] == ref.percentiles["perf"]
+
+
+def test_degenerate_tables():
+    """Empty groups, an all-NaN table, a single row, a zero-group table."""
+    c = ctx()
+    from paper_2103_14409_b200 import reduce_opts
+    # groups with 0 rows between regular ones
+    t = dict(runtime_ms=np.array([1.0, 2.0, np.nan, 3.0], np.float32),
+             block_id=np.array([0, 1, 0, 3], np.uint16),
+             group_offset=np.array([0, 0, 2, 2, 3, 4, 4], np.int64),
+             group_matrix=np.array([0, 1, 2, 3, 0, 1], np.uint32))
+    st = _compare(t, L=4, M=4)
+    assert st["n_groups"] == 6 and st["n_all_nan"] == 4
+    # all NaN
+    t = dict(runtime_ms=np.full(64, np.nan, np.float32), block_id=np.tile(np.arange(32), 2).astype(np.uint16),
+             group_offset=np.array([0, 32, 64], np.int64), group_matrix=np.array([0, 1], np.uint32))
+    st = _compare(t)
+    assert st["n_ratio_defined"] == 0 and np.isnan(st["mean_perf"])
+    assert all(np.isnan(v) for v in st["pct_perf"])
+    # one row, the largest block
+    t = dict(runtime_ms=np.array([0.5], np.float32), block_id=np.array([31], np.uint16),
+             group_offset=np.array([0, 1], np.int64), group_matrix=np.array([5], np.uint32))
+    st = _compare(t)
+    assert st["n_largest_is_best"] == 1 and st["pct_perf"][0] == 1.0
+    # zero groups
+    import torch
+    from paper_2103_14409_b200 import Table
+    tab = Table(torch.zeros(1, device="cuda"), torch.zeros(1, dtype=torch.int16, device="cuda"), None,
+                torch.zeros(1, dtype=torch.int64, device="cuda"), None, None, n_rows=0, n_groups=0)
+    o = reduce_opts(32, 8)
+    c.reduce_table(tab, o, per_group=False)
+    st = c.stats(o, percentiles=[0.5])
+    assert st["n_groups"] == 0 and st["n_rows"] == 0 and np.isnan(st["pct_perf"][0])
+
+
+def test_group_aligned_shard_without_matrix_array():
+    """A group-aligned shard (first_group != 0) with implicit matrix = (first_group + g) % M."""
+    c = ctx()
+    from paper_2103_14409_b200 import reduce_opts
+    n = 32 * 40_000
+    g0, g1 = 12_345, 30_000
+    tab = c.gen_table(n, 5000, preset=0, seed=77, group_begin=g0, group_end=g1, offsets=False)
+    assert tab.first_group == g0 and tab.rows_per_group == 32
+    o = reduce_opts(32, 8)
+    c.reduce_table(tab, o, per_group=False)
+    st = c.stats(o, percentiles=PCTS)
+    h = gen_table(n, 5000, preset="t4", seed=77, group_begin=g0, group_end=g1)
+    ref = OT.reduce_table(h["runtime_ms"], h["block_id"], rows_per_group=32, first_group=g0,
+                          opts=OT.Opts(), percentiles=PCTS)
+    for k, v in ref.counters.items():
+        assert st[k] == v, k
+    assert (st["best_block_hist"] == ref.best_block_hist).all()
+    assert st["pct_gain"] == ref.percentiles["gain"]

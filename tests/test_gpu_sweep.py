@@ -103,3 +103,25 @@ def test_sweep_argument_errors():
             c.sweep([K_EUCLID], [64], bad, brackets=1, launches=1)
     with pytest.raises(LscatError):
         c.sweep([K_EUCLID], [128], [32], brackets=1, launches=1)       # not registered
+
+
+def test_full_suite_small_sweep_stats():
+    """All eight suite kernels swept at small N (GEMM rows < 128 threads are INVALID_CONFIG
+    NaN rows); the stats of the swept table match the oracle bit for bit."""
+    from paper_2103_14409_b200 import reduce_opts, ROW_OK, ROW_INVALID_CONFIG, KERNELS
+    c = ctx()
+    ks = [KERNELS[k] for k in ("euclid", "matvec", "gemm_bf16", "transpose", "axpy", "rowsum",
+                               "colsum", "stencil5")]
+    ns = [64, 256]
+    bs = [32, 64, 96, 128, 256, 512, 1024]
+    c.register_suite(ks, ns)
+    t = c.sweep(ks, ns, bs, warmup=1, brackets=3, launches=20).to_numpy()
+    assert t["n_rows"] == len(ks) * len(ns) * len(bs)
+    gemm_rows = np.repeat(t["group_kernel"], np.diff(t["group_offset"])) == KERNELS["gemm_bf16"]
+    small = np.tile(np.array(bs) < 128, len(ks) * len(ns))
+    assert (t["status"][gemm_rows & small] == ROW_INVALID_CONFIG).all()
+    assert (t["status"][~(gemm_rows & small)] == ROW_OK).all()
+    o = reduce_opts(len(bs), len(ns))
+    c.reduce_table(c.sweep(ks, ns, bs, warmup=1, brackets=3, launches=20), o, per_group=False)
+    st = c.stats(o)
+    assert st["n_rows"] == t["n_rows"] and st["n_nan"] == 3 * len(ns)
