@@ -282,11 +282,6 @@ def main():
         e2e = run_e2e(ctx, L, ks, W, K, R, npts_total, world, barrier, allmax,
                       steps=min(args.steps, 2))
 
-    # ---- secondary: table rows/s on the paper-shaped tables (N = 1)
-    secondary = None
-    if not args.no_secondary and world == 1:
-        secondary = table_benches(ctx, L, hbm_peak)
-
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         A_by_n = {n: (ctx.suite_tensor(L.K_EUCLID, n, 0).view(n, n).cpu().numpy(),
@@ -296,8 +291,15 @@ def main():
                "sample": f"one fp64 numpy evaluation of euclidean_kernel per matrix size on the "
                          f"same inputs ({work:.2f} s CPU), scaled by 32 blocks x (W+K*R) launches "
                          f"per point"}
-        if secondary:
-            cpu["table_rows_per_s"] = secondary.pop("_cpu_rows_per_s", None)
+
+    # ---- secondary: table rows/s on the paper-shaped tables, % of peak per suite kernel (N = 1)
+    secondary = None
+    if not args.no_secondary and world == 1:
+        secondary = table_benches(ctx, L, hbm_peak)
+        secondary["suite_roofline_n8192"] = suite_roofline(ctx, L, hbm_peak, load_peaks()[1])
+        cpu_rows = secondary.pop("_cpu_rows_per_s", None)
+        if cpu:
+            cpu["table_rows_per_s"] = cpu_rows
 
     if rank == 0:
         out = {
@@ -367,6 +369,44 @@ def run_e2e(ctx, L, ks, W, K, R, npts_total, world, barrier, allmax, steps=2):
             "h2d_bytes_per_step": h2d + tab_h2d, "d2h_bytes_per_step": plen * 8 + 32,
             "steps": steps, "note": "sweep runtimes come from device events read on the host; "
                                     "percentile-selection histograms not counted in d2h"}
+
+
+def suite_roofline(ctx, L, hbm_peak, tc_peak, blocks=(128, 256, 512, 1024), reps=20):
+    """BASELINE metric '% HBM peak per kernel': every suite kernel at N = 8192, best of a few
+    blocks, per-launch time from CUDA events over `reps` back-to-back launches (inputs exceed
+    L2 except colsum/rowsum/matvec/euclid's 256 MB, which also exceed it)."""
+    import torch
+    names = ["euclid", "matvec", "rowsum", "colsum", "transpose", "axpy", "stencil5", "gemm_bf16"]
+    ks = [L.KERNELS[k] for k in names]
+    n = 8192
+    ctx.register_suite(ks, [n])
+    stream = torch.cuda.current_stream()
+    out = {}
+    for name, k in zip(names, ks):
+        nbytes, flops = L.kernel_work(k, n)
+        best = None
+        for b in blocks:
+            ctx.launch(k, n, b)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(reps):
+                ctx.launch(k, n, b)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            if best is None or ms < best[1]:
+                best = (b, ms)
+        b, ms = best
+        if k == L.K_GEMM_BF16:
+            ach = flops / (ms * 1e-3) / 1e12
+            out[name] = {"bound": "tensor", "block": b, "us": round(ms * 1e3, 2),
+                         "achieved": round(ach, 1), "unit": "TFLOP/s", "frac": round(ach / tc_peak, 4)}
+        else:
+            ach = nbytes / (ms * 1e-3) / 1e9
+            out[name] = {"bound": "hbm", "block": b, "us": round(ms * 1e3, 2),
+                         "achieved": round(ach, 1), "unit": "GB/s", "frac": round(ach / hbm_peak, 4)}
+    return out
 
 
 def table_benches(ctx, L, hbm_peak):

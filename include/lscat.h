@@ -98,6 +98,12 @@ lscat_status lscat_launch_count(const lscat_ctx* ctx, uint64_t* out);
    the NCCL communicator of `world` ranks; world == 1 is valid and makes collectives no-ops. */
 lscat_status lscat_comm_unique_id(void* out /* 128 bytes */);
 lscat_status lscat_comm_init(lscat_ctx* ctx, const void* unique_id, int rank, int world);
+/* TEST TRANSPORT: the `world` ranks are threads of this process (usually sharing one device)
+   that each own a ctx and call this with the same `name`.  The merge collectives of
+   lscat_reduce_table / lscat_stats then exchange buffers through host memory with a barrier
+   instead of NCCL; the merge code path is otherwise identical, so multi-rank merges can be
+   checked on a single GPU.  Not for production use. */
+lscat_status lscat_comm_init_local(lscat_ctx* ctx, const char* name, int rank, int world);
 
 /* ------------------------------------------------------------- a1: suite ------------ */
 /* Materialise the inputs of every (kernel, N) pair: N x N row-major matrices (fp32, bf16 for

@@ -11,6 +11,7 @@
 #include <tuple>
 #include <vector>
 
+#include "comm.h"
 #include "lscat.h"
 
 namespace lscat {
@@ -93,7 +94,7 @@ struct lscat_ctx {
   cudaStream_t capture_stream = nullptr;
   std::vector<cudaEvent_t> events;
   // comm
-  ncclComm_t comm = nullptr;
+  lscat::Comm* comm = nullptr;  // NCCL, or the local test transport (comm.h)
   int rank = 0, world = 1;
   // reducer scratch
   lscat::ReduceState rs;

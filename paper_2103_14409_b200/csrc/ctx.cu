@@ -179,7 +179,7 @@ void lscat_ctx_destroy(lscat_ctx* c) {
   }
   for (auto& kv : c->scratch) cudaFree(kv.second.p);
   for (auto& kv : c->pinned) cudaFreeHost(kv.second.p);
-  if (c->comm) ncclCommDestroy(c->comm);
+  delete c->comm;
   if (c->capture_stream) cudaStreamDestroy(c->capture_stream);
   delete c;
 }
@@ -205,21 +205,33 @@ lscat_status lscat_comm_init(lscat_ctx* c, const void* uid, int rank, int world)
   LSCAT_CHECK_CTX(c);
   if (world < 1 || rank < 0 || rank >= world || (world > 1 && !uid))
     return fail(c, LSCAT_ERR_INVALID_ARG, "comm_init: rank %d world %d", rank, world);
-  if (c->comm) {
-    ncclCommDestroy(c->comm);
-    c->comm = nullptr;
-  }
+  delete c->comm;
+  c->comm = nullptr;
   c->rank = rank;
   c->world = world;
   if (world == 1) return LSCAT_OK;
   LSCAT_CUDA(c, cudaSetDevice(c->device));
   ncclUniqueId id;
   memcpy(&id, uid, sizeof id);
-  ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
+  ncclComm_t nc = nullptr;
+  ncclResult_t r = ncclCommInitRank(&nc, world, id, rank);
   if (r != ncclSuccess) {
-    c->comm = nullptr;
+    c->world = 1;
+    c->rank = 0;
     return fail(c, LSCAT_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
   }
+  c->comm = make_nccl_comm(nc);
+  return LSCAT_OK;
+}
+
+lscat_status lscat_comm_init_local(lscat_ctx* c, const char* name, int rank, int world) {
+  LSCAT_CHECK_CTX(c);
+  if (!name || world < 1 || rank < 0 || rank >= world)
+    return fail(c, LSCAT_ERR_INVALID_ARG, "comm_init_local: rank %d world %d", rank, world);
+  delete c->comm;
+  c->comm = world > 1 ? make_local_comm(name, rank, world) : nullptr;
+  c->rank = rank;
+  c->world = world;
   return LSCAT_OK;
 }
 

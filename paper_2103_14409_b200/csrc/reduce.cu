@@ -575,10 +575,6 @@ bool opts_ok(const lscat_reduce_opts* o) {
   return true;
 }
 
-lscat_status nccl_check(lscat_ctx* ctx, ncclResult_t r, const char* what) {
-  if (r == ncclSuccess) return LSCAT_OK;
-  return fail(ctx, LSCAT_ERR_NCCL, "%s: %s", what, ncclGetErrorString(r));
-}
 
 }  // namespace
 }  // namespace lscat
@@ -719,12 +715,9 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
     p.mode = MODE_GROUP_PARTIALS;
     if (G) kern<<<grid, 256, smem, s>>>(p), ctx->launches++;
     LSCAT_CUDA(ctx, cudaGetLastError());
-    lscat_status ns;
-    if ((ns = nccl_check(ctx, ncclGroupStart(), "ncclGroupStart"))) return ns;
-    ncclAllReduce(key, key, G, ncclUint64, ncclMin, ctx->comm, s);
-    ncclAllReduce(lc, lc, G, ncclUint64, ncclMax, ctx->comm, s);
-    ncclAllReduce(cnt, cnt, 3 * G, ncclUint32, ncclSum, ctx->comm, s);
-    if ((ns = nccl_check(ctx, ncclGroupEnd(), "allreduce per-group merge"))) return ns;
+    lscat_status ns = ctx->comm->allreduce(ctx, {{key, G, DT::U64, Op::Min}, {lc, G, DT::U64, Op::Max},
+                                                 {cnt, 3 * G, DT::U32, Op::Sum}}, s);
+    if (ns) return ns;
     own_lo = G * ctx->rank / ctx->world;
     own_hi = G * (ctx->rank + 1) / ctx->world;
     p.acc_lo = own_lo;
@@ -739,14 +732,11 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
     LSCAT_CUDA(ctx, cudaGetLastError());
   }
   if (ctx->world > 1) {
-    lscat_status ns;
-    if ((ns = nccl_check(ctx, ncclGroupStart(), "ncclGroupStart"))) return ns;
-    ncclAllReduce(p.partials, p.partials, plen, ncclUint64, ncclSum, ctx->comm, s);
-    ncclAllReduce(p.minmax, p.minmax, 1, ncclUint64, ncclMin, ctx->comm, s);
-    ncclAllReduce(p.minmax + 1, p.minmax + 1, 1, ncclUint64, ncclMax, ctx->comm, s);
-    ncclAllReduce(p.minmax + 2, p.minmax + 2, 1, ncclUint64, ncclMin, ctx->comm, s);
-    ncclAllReduce(p.minmax + 3, p.minmax + 3, 1, ncclUint64, ncclMax, ctx->comm, s);
-    if ((ns = nccl_check(ctx, ncclGroupEnd(), "allreduce partials"))) return ns;
+    lscat_status ns = ctx->comm->allreduce(
+        ctx, {{p.partials, plen, DT::U64, Op::Sum}, {p.minmax, 1, DT::U64, Op::Min},
+              {p.minmax + 1, 1, DT::U64, Op::Max}, {p.minmax + 2, 1, DT::U64, Op::Min},
+              {p.minmax + 3, 1, DT::U64, Op::Max}}, s);
+    if (ns) return ns;
   }
   if (out->partials) LSCAT_CUDA(ctx, cudaMemcpyAsync(out->partials, p.partials, plen * 8, cudaMemcpyDeviceToDevice, s));
   ReduceState& rs = ctx->rs;

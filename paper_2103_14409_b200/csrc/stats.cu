@@ -95,10 +95,6 @@ uint32_t pick_shift(uint64_t lo, uint64_t hi) {
   return s;
 }
 
-lscat_status nccl_ok(lscat_ctx* ctx, ncclResult_t r, const char* what) {
-  if (r == ncclSuccess) return LSCAT_OK;
-  return fail(ctx, LSCAT_ERR_NCCL, "%s: %s", what, ncclGetErrorString(r));
-}
 
 lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct, uint64_t n_def,
                                 const uint64_t mm[4], double* out_perf, double* out_gain,
@@ -170,8 +166,7 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
     std::vector<std::vector<uint64_t>> cands(nr);
     if (ctx->world > 1) {
       lscat_status ns;
-      if ((ns = nccl_ok(ctx, ncclAllReduce(d_hist, d_hist, (size_t)nr * kBins, ncclUint32, ncclSum, ctx->comm, s), "select hist")))
-        return ns;
+      if ((ns = ctx->comm->allreduce(ctx, {{d_hist, (size_t)nr * kBins, DT::U32, Op::Sum}}, s))) return ns;
       // candidates: [count, keys...] per range, all-gathered
       uint64_t* d_pack = (uint64_t*)scratch(ctx, "sel_pack", (size_t)kMaxRanges * (kCap + 1) * 8, &err);
       if (err) return cuda_fail(ctx, err, "stats: scratch");
@@ -184,8 +179,7 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
         if (c) LSCAT_CUDA(ctx, cudaMemcpyAsync(d_pack + (size_t)r * (kCap + 1) + 1, d_cand + (size_t)r * kCap, c * 8, cudaMemcpyDeviceToDevice, s));
         LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
       }
-      if ((ns = nccl_ok(ctx, ncclAllGather(d_pack, d_gath, (size_t)nr * (kCap + 1), ncclUint64, ctx->comm, s), "select gather")))
-        return ns;
+      if ((ns = ctx->comm->allgather(ctx, d_pack, d_gath, (size_t)nr * (kCap + 1), DT::U64, s))) return ns;
       std::vector<uint64_t> g((size_t)ctx->world * nr * (kCap + 1));
       LSCAT_CUDA(ctx, cudaMemcpyAsync(g.data(), d_gath, g.size() * 8, cudaMemcpyDeviceToHost, s));
       LSCAT_CUDA(ctx, cudaMemcpyAsync(hist.data(), d_hist, hist.size() * 4, cudaMemcpyDeviceToHost, s));

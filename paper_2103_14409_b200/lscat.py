@@ -111,7 +111,8 @@ _lib = None
 
 EXPORTS = [
     "lscat_abi_version", "lscat_status_string", "lscat_ctx_create", "lscat_ctx_destroy",
-    "lscat_last_error", "lscat_launch_count", "lscat_comm_unique_id", "lscat_comm_init", "lscat_register_suite",
+    "lscat_last_error", "lscat_launch_count", "lscat_comm_unique_id", "lscat_comm_init",
+    "lscat_comm_init_local", "lscat_register_suite",
     "lscat_suite_buffer", "lscat_suite_upload", "lscat_launch", "lscat_kernel_work",
     "lscat_plan", "lscat_sweep", "lscat_reduce_opts_default", "lscat_partials_len",
     "lscat_reduce_table", "lscat_stats", "lscat_gen_table", "lscat_gen_table_shape",
@@ -137,6 +138,7 @@ def load(path: str = LIB_PATH):
         "lscat_launch_count": ([vp, C.POINTER(u64)], i32),
         "lscat_comm_unique_id": ([vp], i32),
         "lscat_comm_init": ([vp, vp, i32, i32], i32),
+        "lscat_comm_init_local": ([vp, C.c_char_p, i32, i32], i32),
         "lscat_register_suite": ([vp, vp, u32, vp, u32, vp], i32),
         "lscat_suite_buffer": ([vp, u32, u32, u32, C.POINTER(vp), C.POINTER(u64)], i32),
         "lscat_suite_upload": ([vp, u32, u32, u32, vp, u64, u32, vp], i32),
@@ -330,6 +332,11 @@ class Ctx:
     def comm_init(self, unique_id: bytes, rank: int, world: int):
         buf = C.create_string_buffer(unique_id, 128) if unique_id else None
         self._ck(self._lib.lscat_comm_init(self.h, buf, rank, world), "comm_init")
+
+    def comm_init_local(self, name: str, rank: int, world: int):
+        """Test transport: ranks are threads of this process (see include/lscat.h)."""
+        self._ck(self._lib.lscat_comm_init_local(self.h, name.encode(), rank, world),
+                 "comm_init_local")
 
     # a1
     def register_suite(self, kernels, sizes, stream=None):

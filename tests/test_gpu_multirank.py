@@ -1,0 +1,97 @@
+"""a9 merge on one GPU: W ranks are W threads, each with its own library context, joined by the
+library's local test transport (lscat_comm_init_local).  The merge code in reduce.cu /
+stats.cu is the same as with NCCL; only the byte transport differs.  Every rank must get
+results bit-identical to the oracle on the whole table, for point-sharded tables (per-group
+MIN/MAX/SUM merge) and group-aligned shards (partial-vector SUM), for W = 2, 3, 4."""
+import threading
+
+import numpy as np
+import pytest
+
+from oracle import table as OT
+from synth import gen_table
+from tests.gpu_util import require_gpu
+
+pytestmark = pytest.mark.gpu
+
+PCTS = [0.01, 0.1, 0.5, 0.9, 0.99]
+
+
+def _run_ranks(world, make_table, opts_kw, name):
+    import torch
+    import importlib
+    importlib.import_module("paper_2103_14409_b200.build").build()
+    import paper_2103_14409_b200 as L
+    results, errors = [None] * world, []
+
+    def rank_main(r):
+        try:
+            torch.cuda.set_device(0)
+            ctx = L.Ctx(0)
+            ctx.comm_init_local(name, r, world)
+            tab = make_table(ctx, r)
+            o = L.reduce_opts(32, 8, **opts_kw)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                out = ctx.reduce_table(tab, o, stream=s)
+                st = ctx.stats(o, percentiles=PCTS, stream=s)
+            s.synchronize()
+            results[r] = (st, {k: v.cpu().numpy() for k, v in out.items()})
+            ctx.close()
+        except Exception as e:  # noqa: BLE001
+            errors.append((r, repr(e)))
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errors, errors
+    return results
+
+
+def _check(results, ref):
+    for st, _ in results:
+        for k, v in ref.counters.items():
+            assert st[k] == v, k
+        assert (st["perf_hist"] == ref.perf_hist).all()
+        assert (st["gain_hist"] == ref.gain_hist).all()
+        assert (st["best_block_hist"] == ref.best_block_hist).all()
+        assert st["pct_perf"] == ref.percentiles["perf"]
+        assert st["pct_gain"] == ref.percentiles["gain"]
+        assert st["mean_perf"] == ref.derived["mean_perf"]
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_point_sharded_merge(world):
+    require_gpu()
+    n, K = 400_000, 1600
+    full = gen_table(n, K, preset="t4", seed=31)
+    ref = OT.reduce_table(full["runtime_ms"], full["block_id"], full["group_offset"],
+                          group_matrix=full["group_matrix"], percentiles=PCTS)
+
+    def make(ctx, r):
+        return ctx.gen_table(n, K, preset=0, seed=31, block_mod=world, block_rem=r)
+
+    res = _run_ranks(world, make, dict(point_sharded=1), f"ps{world}")
+    _check(res, ref)
+    # every rank holds the merged per-group argmin for all groups
+    for _, out in res:
+        assert (out["best_block_id"].view(np.uint16) == ref.best_block).all()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_group_aligned_merge(world):
+    require_gpu()
+    n, K = 32 * 120_000, 15_000
+    full = gen_table(n, K, preset="gtx980", seed=41)
+    ref = OT.reduce_table(full["runtime_ms"], full["block_id"], full["group_offset"],
+                          group_matrix=full["group_matrix"], percentiles=PCTS)
+    G = full["n_groups"]
+
+    def make(ctx, r):
+        return ctx.gen_table(n, K, preset=1, seed=41, group_begin=G * r // world,
+                             group_end=G * (r + 1) // world)
+
+    res = _run_ranks(world, make, {}, f"ga{world}")
+    _check(res, ref)
