@@ -270,6 +270,8 @@ def main():
             v = tab["runtime_ms"][a:b] * 1e3
             per_n[str(n)] = [round(float(np.nanmin(v)), 2), round(float(np.nanmedian(v)), 2),
                              round(float(np.nanmax(v)), 2)]
+            if n >= 4096:
+                per_n[f"{n}_by_block"] = [round(float(x), 1) for x in v]
     rooflines = None
     if world > 1:
         objs = [None] * world

@@ -297,15 +297,21 @@ __device__ __forceinline__ void uniform_prefetch(const RP& p, uint64_t base, flo
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-// Lane j folds group j of a staged batch.
-__device__ __forceinline__ void uniform_fold(const RP& p, const float4* d, const uint4* di, int lane,
+__device__ __forceinline__ uint4 lds128(uint32_t saddr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(saddr));
+  return v;
+}
+
+// Lane j folds group j of a staged batch (shared-space addresses of the runtime / id stage).
+__device__ __forceinline__ void uniform_fold(const RP& p, uint32_t srt, uint32_t sid, int lane,
                                              GroupAcc& mine) {
+  const uint32_t rbase = srt + lane * 128, ibase = sid + lane * 64;
   uint32_t mkey = 0xFFFFFFFFu, nok = 0, nnan = 0;
 #pragma unroll 2
   for (int c = 0; c < 8; c++) {
-    const float4 x = d[lane * 8 + (c ^ (lane & 7))];
-    const uint32_t b4[4] = {__float_as_uint(x.x), __float_as_uint(x.y), __float_as_uint(x.z),
-                            __float_as_uint(x.w)};
+    const uint4 x = lds128(rbase + 16 * (c ^ (lane & 7)));
+    const uint32_t b4[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
     for (int q = 0; q < 4; q++) {
       const bool ok = ok_bits(b4[q]);
@@ -317,12 +323,10 @@ __device__ __forceinline__ void uniform_fold(const RP& p, const float4* d, const
   uint32_t mid = 0xFFFFFFFFu;
 #pragma unroll 1
   for (int c = 0; c < 4; c++) {
-    const uint4 y = di[lane * 4 + (c ^ ((lane >> 1) & 3))];
-    const float4 x0 = d[lane * 8 + ((2 * c) ^ (lane & 7))];
-    const float4 x1 = d[lane * 8 + ((2 * c + 1) ^ (lane & 7))];
-    const uint32_t b8[8] = {__float_as_uint(x0.x), __float_as_uint(x0.y), __float_as_uint(x0.z),
-                            __float_as_uint(x0.w), __float_as_uint(x1.x), __float_as_uint(x1.y),
-                            __float_as_uint(x1.z), __float_as_uint(x1.w)};
+    const uint4 y = lds128(ibase + 16 * (c ^ ((lane >> 1) & 3)));
+    const uint4 x0 = lds128(rbase + 16 * ((2 * c) ^ (lane & 7)));
+    const uint4 x1 = lds128(rbase + 16 * ((2 * c + 1) ^ (lane & 7)));
+    const uint32_t b8[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
     const uint32_t iw[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll
     for (int q = 0; q < 8; q++) {
@@ -394,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, 2) reduce_uniform32_kernel(RP p) {
     __syncwarp();
     GroupAcc mine;
     acc_init(mine);
-    uniform_fold(p, d[cur], di[cur], lane, mine);
+    uniform_fold(p, (uint32_t)__cvta_generic_to_shared(d[cur]), (uint32_t)__cvta_generic_to_shared(di[cur]), lane, mine);
     __syncwarp();
     emit_group(p, bi * 32 + lane, true, mine, t, sh_c, sh_perf, sh_gain, sh_bb);
     cur ^= 1;

@@ -37,6 +37,12 @@ __device__ __forceinline__ int bin_of(const Range& r, uint64_t k) {
   return 1 + (int)((k - r.lo - 1) >> r.shift);
 }
 
+// kSmem: the histograms of all ranges fit in shared memory (nr <= kSmemRanges): per-CTA
+// privatised counts, flushed once (hot bins such as perf == 1.0 would otherwise serialise on
+// global atomics).
+constexpr int kSmemRanges = 4;
+
+template <bool kSmem>
 __global__ void __launch_bounds__(256) select_pass(const double* __restrict__ perf,
                                                    const double* __restrict__ gain, uint64_t lo,
                                                    uint64_t hi, const Range* __restrict__ ranges,
@@ -44,7 +50,11 @@ __global__ void __launch_bounds__(256) select_pass(const double* __restrict__ pe
                                                    uint64_t* __restrict__ cand,
                                                    uint32_t* __restrict__ cand_cnt) {
   __shared__ Range sr[kMaxRanges];
+  extern __shared__ uint32_t sh_hist[];
   for (int i = threadIdx.x; i < nr; i += blockDim.x) sr[i] = ranges[i];
+  if (kSmem)
+    for (int i = threadIdx.x; i < nr * kBins; i += blockDim.x) sh_hist[i] = 0;
+  uint32_t* H = kSmem ? sh_hist : hist;
   __syncthreads();
   const unsigned FULL = 0xffffffffu;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -70,10 +80,15 @@ __global__ void __launch_bounds__(256) select_pass(const double* __restrict__ pe
           const int b = hit ? bin_of(R, k) : -1;
           const unsigned peers = __match_any_sync(FULL, b);
           if (hit && (__ffs(peers) - 1) == (int)(threadIdx.x & 31))
-            atomicAdd(&hist[(size_t)r * kBins + b], (uint32_t)__popc(peers));
+            atomicAdd(&H[(size_t)r * kBins + b], (uint32_t)__popc(peers));
         }
       }
     }
+  }
+  if (kSmem) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < nr * kBins; i += blockDim.x)
+      if (sh_hist[i]) atomicAdd(&hist[i], sh_hist[i]);
   }
 }
 
@@ -158,8 +173,21 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
     LSCAT_CUDA(ctx, cudaMemsetAsync(d_ccnt, 0, nr * 4, s));
     const uint64_t n = rs.own_hi - rs.own_lo;
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)ctx->sm_count * 8, (n + 255) / 256));
-    if (n) select_pass<<<grid, 256, 0, s>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, d_ranges, nr,
-                                            d_hist, d_cand, d_ccnt), ctx->launches++;
+    int nhist = 0;
+    for (const auto& r : ranges) nhist += !r.gather;
+    if (n && nr <= kSmemRanges) {
+      const size_t sm = (size_t)nr * kBins * 4;
+      LSCAT_CUDA(ctx, cudaFuncSetAttribute(select_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      const int g2 = std::min(grid, ctx->sm_count * 2);
+      select_pass<true><<<g2, 256, sm, s>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, d_ranges, nr,
+                                              d_hist, d_cand, d_ccnt);
+      ctx->launches++;
+    } else if (n) {
+      select_pass<false><<<grid, 256, 0, s>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, d_ranges, nr,
+                                               d_hist, d_cand, d_ccnt);
+      ctx->launches++;
+    }
+    (void)nhist;
     LSCAT_CUDA(ctx, cudaGetLastError());
     std::vector<uint32_t> hist((size_t)nr * kBins);
     std::vector<uint32_t> ccnt(nr);
