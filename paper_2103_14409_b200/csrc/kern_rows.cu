@@ -7,6 +7,8 @@
 // loads of A with U independent loads in flight per thread, q/x through the read-only cache
 // (L2/L1 resident), fp32 accumulation, warp shuffles + a fixed-order smem combine.
 // HBM bound: 4N^2 + 8N bytes per launch.
+#include <cmath>
+
 #include "kern_common.cuh"
 
 namespace lscat {
@@ -91,16 +93,26 @@ __global__ void __launch_bounds__(B) row_kernel(const float* __restrict__ A,
   if (live && tw == 0 && lane == 0) out[row] = (OP == kEuclid) ? sqrtf(r) : r;
 }
 
-// Warps per team: the largest divisor of B/32 not above the warps that give each thread
-// ~16 float4 of the row.
-inline int team_warps(int N, int B) {
+// Warps per team (a divisor d of B/32).  Two effects decide: the tail of the last wave of
+// rows (C = resident teams, rows/C rounds, efficiency (N/C) / ceil(N/C)) and the loads in
+// flight per thread (a thread should stream >= ~8 float4 of its row).  Score both, pick the
+// best divisor.  `resident` = CTAs of this kernel resident per SM (occupancy API, cached).
+inline int team_warps(int N, int B, int sm_count, int resident) {
   const int W = B / 32;
-  const int n4 = (N + 3) / 4;
-  int want = (n4 + 16 * 32 - 1) / (16 * 32);
-  if (want < 1) want = 1;
+  const double n4 = (N + 3) / 4;
   int best = 1;
-  for (int d = 1; d <= W; d++)
-    if (W % d == 0 && d <= want) best = d;
+  double best_score = -1.0;
+  for (int d = 1; d <= W; d++) {
+    if (W % d) continue;
+    const double C = (double)sm_count * resident * (W / d);
+    const double R = N / C;
+    const double waves = R <= 1.0 ? 1.0 : std::ceil(R - 1e-9);
+    const double eff = R <= 1.0 ? 1.0 : R / waves;  // one partial wave: no tail to lose
+    const double f4 = n4 / (32.0 * d);
+    const double mlp = f4 >= 8.0 ? 1.0 : f4 / 8.0;
+    const double score = eff * (0.5 + 0.5 * mlp);
+    if (score > best_score + 1e-12) { best_score = score; best = d; }
+  }
   return best;
 }
 
@@ -111,7 +123,15 @@ struct RowLauncher {
     static constexpr bool kSupported = true;
     static cudaError_t launch(const LaunchArgs& a, cudaStream_t s) {
       const SuiteEntry& e = *a.e;
-      const int N = (int)e.n, tw = team_warps(N, B), teams = B / 32 / tw;
+      static int sm_count = 0, resident = 0;
+      if (!resident) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, row_kernel<OP, B>, B, 0);
+        if (resident < 1) resident = 1;
+      }
+      const int N = (int)e.n, tw = team_warps(N, B, sm_count, resident), teams = B / 32 / tw;
       row_kernel<OP, B><<<(N + teams - 1) / teams, B, 0, s>>>((const float*)e.in0, (const float*)e.in1,
                                                              (float*)e.out, N, tw);
       return cudaGetLastError();

@@ -78,9 +78,19 @@ __global__ void __launch_bounds__(256) select_pass(const double* __restrict__ pe
           }
         } else {
           const int b = hit ? bin_of(R, k) : -1;
-          const unsigned peers = __match_any_sync(FULL, b);
-          if (hit && (__ffs(peers) - 1) == (int)(threadIdx.x & 31))
-            atomicAdd(&H[(size_t)r * kBins + b], (uint32_t)__popc(peers));
+          // the two single-key end bins (e.g. perf == 1.0, gain == 0) are hot: count them with
+          // one ballot per warp; other bins spread, one atomic per lane
+          const unsigned e0 = __ballot_sync(FULL, b == 0), e1 = __ballot_sync(FULL, b == kBins - 1);
+          const int lane = threadIdx.x & 31;
+          if (lane == 0 && e0) atomicAdd(&H[(size_t)r * kBins], (uint32_t)__popc(e0));
+          if (lane == 0 && e1) atomicAdd(&H[(size_t)r * kBins + kBins - 1], (uint32_t)__popc(e1));
+          if (kSmem) {
+            if (b > 0 && b < kBins - 1) atomicAdd(&H[(size_t)r * kBins + b], 1u);
+          } else {
+            const bool mid = b > 0 && b < kBins - 1;
+            const unsigned peers = __match_any_sync(FULL, mid ? b : -1);
+            if (mid && (__ffs(peers) - 1) == lane) atomicAdd(&H[(size_t)r * kBins + b], (uint32_t)__popc(peers));
+          }
         }
       }
     }
