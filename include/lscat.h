@@ -220,6 +220,11 @@ typedef struct {
   uint32_t point_sharded;     /* 1 -> groups are split across ranks: per-group merge first  */
   uint32_t keep_values;       /* 1 -> keep per-group perf/gain (caller arrays or ctx        */
                               /*      scratch) for the percentiles of lscat_stats           */
+  uint32_t block_profile;     /* 1 -> also accumulate the block profile of Figs. 2/4        */
+                              /*      (P:240-247): per (matrix, block) the sum   */
+                              /*      of floor(RN(best / r_b) * 2^31) over the ok rows of   */
+                              /*      defined groups, and their count (R-22); one */
+                              /*      extra read of the table                               */
 } lscat_reduce_opts;
 
 /* Fills `opts` with the defaults above for a block list of n_blocks with largest id l. */
@@ -238,7 +243,8 @@ typedef struct {
 
 /* Layout of the packed partial vector (uint64 words), LSCAT_P_* counter slots first, then
    perf_hist [bins_per_unit+1], gain_hist [gain_cap*bins_per_unit+1], best_block_hist
-   [n_matrices*n_blocks]. */
+   [n_matrices*n_blocks], and with block_profile: profile_sum [n_matrices*n_blocks],
+   profile_count [n_matrices*n_blocks]. */
 enum {
   LSCAT_P_ROWS = 0, LSCAT_P_OK, LSCAT_P_NAN, LSCAT_P_INVALID,
   LSCAT_P_GROUPS, LSCAT_P_DEFINED, LSCAT_P_ALL_NAN, LSCAT_P_COMPLETE, LSCAT_P_INCOMPLETE,
@@ -299,6 +305,10 @@ typedef struct {
   uint32_t n_percentiles;       /* <= 64                                                   */
   double* pct_perf;             /* [n_percentiles] out; NaN if no ratio-defined group     */
   double* pct_gain;             /* [n_percentiles] out                                     */
+  /* with opts->block_profile (else untouched): [n_matrices * n_blocks], row-major by matrix */
+  double* profile_mean;         /* mean of best / r_b ((double)sum * 2^-31 / count); NaN  */
+                                /* where count == 0                                        */
+  uint64_t* profile_count;      /* number of rows averaged                                 */
 } lscat_stats_out;
 
 /* Finalize the statistics of the last lscat_reduce_table on ctx (a10) and, when

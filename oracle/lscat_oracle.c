@@ -26,6 +26,7 @@
  *      k*t <= nb*b), a per-matrix histogram of best block ids (Figs. 2/4 data).
  *   7. fixed-point sums floor(perf*2^52), floor(min(gain,2^20)*2^32) for exact means (R-13).
  *   8. nearest-rank percentiles of perf and gain over ratio-defined groups (R-13).
+ *   9. (optional) the block profile of Figs. 2/4: mean of best / r_b per (matrix, block) (R-22).
  *
  * Exactness argument used in steps 5-6: b and t are float32 values widened to double; every
  * product k*t with integer k < 2^29 has at most 24+29 = 53 significant bits, so it is exact
@@ -100,6 +101,8 @@ int oracle_reduce_table(const oracle_table* T, const oracle_opts* o, oracle_resu
   memset(R->perf_hist, 0, sizeof(uint64_t) * (nb + 1));
   memset(R->gain_hist, 0, sizeof(uint64_t) * ((size_t)o->gain_cap * nb + 1));
   memset(R->best_block_hist, 0, sizeof(uint64_t) * (size_t)o->n_matrices * L);
+  if (R->profile_sum) memset(R->profile_sum, 0, sizeof(uint64_t) * (size_t)o->n_matrices * L);
+  if (R->profile_count) memset(R->profile_count, 0, sizeof(uint64_t) * (size_t)o->n_matrices * L);
   uint64_t* C = R->counters;
   unsigned char* seen = (unsigned char*)malloc(L);
   if (!seen) return ORACLE_ENOMEM;
@@ -156,6 +159,17 @@ int oracle_reduce_table(const oracle_table* T, const oracle_opts* o, oracle_resu
       flags |= 0x001u;
       C[OC_N_DEFINED]++;
       R->best_block_hist[(size_t)matrix * L + best_block]++;
+      /* block profile (Figs. 2/4; reading R-22): performance best / r_b of every
+         block that has a result, as floor(RN(best / r_b) * 2^31), per (matrix, block) */
+      if (R->profile_sum && R->profile_count) {
+        for (uint64_t r = r0; r < r1; r++) {
+          if (!row_ok(T->runtime_ms[r])) continue;
+          double pb = (double)best / (double)T->runtime_ms[r];
+          size_t at = (size_t)matrix * L + T->block_id[r];
+          R->profile_sum[at] += (uint64_t)floor(pb * 2147483648.0);
+          R->profile_count[at] += 1;
+        }
+      }
       /* step 3: the largest block's row must exist and have a result */
       if (have_ell && ell_ok) {
         double b = (double)best, t = (double)t_ell;

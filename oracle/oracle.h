@@ -40,6 +40,8 @@ typedef struct {
   uint64_t* perf_hist;       /* [bins+1]            caller-owned */
   uint64_t* gain_hist;       /* [cap*bins+1]        caller-owned */
   uint64_t* best_block_hist; /* [n_matrices*n_blocks] caller-owned */
+  uint64_t* profile_sum;     /* [n_matrices*n_blocks] caller-owned, or NULL (no block profile) */
+  uint64_t* profile_count;   /* [n_matrices*n_blocks] caller-owned, or NULL */
 } oracle_result;
 
 typedef struct {

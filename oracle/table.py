@@ -50,7 +50,8 @@ class _Opts(C.Structure):
 
 class _Result(C.Structure):
     _fields_ = [("counters", C.c_uint64 * len(COUNTERS)), ("perf_hist", C.c_void_p),
-                ("gain_hist", C.c_void_p), ("best_block_hist", C.c_void_p)]
+                ("gain_hist", C.c_void_p), ("best_block_hist", C.c_void_p),
+                ("profile_sum", C.c_void_p), ("profile_count", C.c_void_p)]
 
 
 class _GroupOut(C.Structure):
@@ -93,6 +94,7 @@ class Opts:
     gain_gt: tuple = (1, 5)      # "more than 20 %"
     perf_lt: tuple = (17, 20)    # "less than 85 %"
     band_lo: tuple = (2, 5)      # "from 40 to 85 %"
+    block_profile: bool = False  # Figs. 2/4 block profile (R-22)
 
     def ell(self):
         return self.n_blocks - 1 if self.largest_block_id is None else self.largest_block_id
@@ -111,6 +113,9 @@ class Result:
     gain: np.ndarray
     flags: np.ndarray
     percentiles: dict = field(default_factory=dict)
+    profile_sum: np.ndarray | None = None
+    profile_count: np.ndarray | None = None
+    profile_mean: np.ndarray | None = None
 
 
 class OracleError(RuntimeError):
@@ -140,6 +145,11 @@ def reduce_table(runtime_ms, block_id, group_offset=None, rows_per_group=0, grou
     bh = np.zeros(o.n_matrices * o.n_blocks, np.uint64)
     R = _Result()
     R.perf_hist, R.gain_hist, R.best_block_hist = ph.ctypes.data, gh.ctypes.data, bh.ctypes.data
+    psum = pcnt = None
+    if o.block_profile:
+        psum = np.zeros(o.n_matrices * o.n_blocks, np.uint64)
+        pcnt = np.zeros(o.n_matrices * o.n_blocks, np.uint64)
+        R.profile_sum, R.profile_count = psum.ctypes.data, pcnt.ctypes.data
     bb = np.zeros(G, np.uint16)
     br = np.zeros(G, np.float32)
     pf = np.zeros(G, np.float64)
@@ -155,6 +165,12 @@ def reduce_table(runtime_ms, block_id, group_offset=None, rows_per_group=0, grou
     derived = {k: getattr(D, k) for k, _ in _Derived._fields_}
     res = Result(counters, ph, gh, bh.reshape(o.n_matrices, o.n_blocks), derived, bb, br, pf, gn,
                  fl)
+    if o.block_profile:
+        res.profile_sum = psum.reshape(o.n_matrices, o.n_blocks)
+        res.profile_count = pcnt.reshape(o.n_matrices, o.n_blocks)
+        with np.errstate(invalid="ignore", divide="ignore"):
+            res.profile_mean = (psum.astype(np.float64) * 2.0 ** -31 / pcnt).reshape(
+                o.n_matrices, o.n_blocks)
     if percentiles:
         rd = (fl & 0x008) != 0
         res.percentiles = {

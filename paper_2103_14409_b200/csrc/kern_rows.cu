@@ -35,9 +35,9 @@ __device__ __forceinline__ float acc1(float s, float a, float v) {
   else return s + a;
 }
 
-// A CTA of B threads is split into teams of TW warps (TW divides B/32); each team reduces one
-// row at a time.  TW is chosen on the host so that a thread streams ~16 float4 of its row
-// (enough loads in flight) and small rows do not leave most of a large block idle.
+// A CTA of B threads is split into floor(W/TW) teams of TW warps; each team reduces one row.
+// TW is chosen on the host (team_warps) from the wave tail, the loads in flight per thread and
+// the idle warps.
 template <int OP, int B>
 __global__ void __launch_bounds__(B) row_kernel(const float* __restrict__ A,
                                                 const float* __restrict__ v,
@@ -47,9 +47,9 @@ __global__ void __launch_bounds__(B) row_kernel(const float* __restrict__ A,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int team = warp / TW, tw = warp % TW;          // team index, warp within team
   const int T = TW * 32, t = tw * 32 + lane;            // team size, thread within team
-  const int teams = W / TW;
+  const int teams = W / TW;                            // warps beyond teams*TW idle
   const int row = blockIdx.x * teams + team;
-  const bool live = row < N;
+  const bool live = team < teams && row < N;
   const float* a = A + (size_t)(live ? row : 0) * N;
   float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
   if (live) {
@@ -87,31 +87,33 @@ __global__ void __launch_bounds__(B) row_kernel(const float* __restrict__ A,
     __syncthreads();
     if (tw == 0 && lane == 0) {
       r = 0.f;
-      for (int k = 0; k < TW; k++) r += red[team * TW + k];
+      if (team < teams)
+        for (int k = 0; k < TW; k++) r += red[team * TW + k];
     }
   }
   if (live && tw == 0 && lane == 0) out[row] = (OP == kEuclid) ? sqrtf(r) : r;
 }
 
-// Warps per team (a divisor d of B/32).  Two effects decide: the tail of the last wave of
-// rows (C = resident teams, rows/C rounds, efficiency (N/C) / ceil(N/C)) and the loads in
-// flight per thread (a thread should stream >= ~8 float4 of its row).  Score both, pick the
-// best divisor.  `resident` = CTAs of this kernel resident per SM (occupancy API, cached).
+// Warps per team d (1..B/32; floor(W/d) teams per CTA, leftover warps idle).  Scored on
+//   tail:  C = resident teams, N/C rounds of rows, efficiency (N/C) / ceil(N/C) (1 if one wave);
+//   MLP:   a thread streams n4/(32 d) float4 of its row, 4 in flight (U = 4): min(1, f4 / 4);
+//   idle:  fraction of the CTA's warps that have a team.
+// `resident` = CTAs of this kernel resident per SM (occupancy API, cached by the launcher).
 inline int team_warps(int N, int B, int sm_count, int resident) {
   const int W = B / 32;
   const double n4 = (N + 3) / 4;
   int best = 1;
   double best_score = -1.0;
   for (int d = 1; d <= W; d++) {
-    if (W % d) continue;
-    const double C = (double)sm_count * resident * (W / d);
+    const int teams = W / d;
+    const double C = (double)sm_count * resident * teams;
     const double R = N / C;
-    const double waves = R <= 1.0 ? 1.0 : std::ceil(R - 1e-9);
-    const double eff = R <= 1.0 ? 1.0 : R / waves;  // one partial wave: no tail to lose
+    const double eff = R <= 1.0 ? 1.0 : R / std::ceil(R - 1e-9);
     const double f4 = n4 / (32.0 * d);
-    const double mlp = f4 >= 8.0 ? 1.0 : f4 / 8.0;
-    const double score = eff * (0.5 + 0.5 * mlp);
-    if (score > best_score + 1e-12) { best_score = score; best = d; }
+    const double mlp = f4 >= 4.0 ? 1.0 : f4 / 4.0;
+    const double active = (double)(teams * d) / W;
+    const double score = eff * mlp * (0.75 + 0.25 * active);
+    if (score > best_score + 1e-9) { best_score = score; best = d; }
   }
   return best;
 }

@@ -563,7 +563,54 @@ __global__ void init_group_merge(uint64_t* key, uint64_t* lc, uint32_t* cnt, uin
 
 size_t partials_len(const lscat_reduce_opts& o) {
   return (size_t)kNC + (o.bins_per_unit + 1) + ((size_t)o.gain_cap * o.bins_per_unit + 1) +
-         (size_t)o.n_matrices * o.n_blocks;
+         (size_t)o.n_matrices * o.n_blocks * (o.block_profile ? 3 : 1);
+}
+
+// Block profile (Figs. 2/4; reading R-22): a second pass over this rank's rows once
+// every group's best runtime is final (after the a9 per-group merge when point-sharded).
+// Warp per group, lanes over rows; per ok row of a defined group the performance best / r_b
+// as floor(RN(best / r_b) * 2^31) is added to a shared (matrix, block) slot; one flush per CTA.
+__global__ void __launch_bounds__(256) profile_kernel(RP p, const float* __restrict__ best_rt,
+                                                      const uint32_t* __restrict__ gflags,
+                                                      uint64_t* __restrict__ prof_sum,
+                                                      uint64_t* __restrict__ prof_cnt) {
+  extern __shared__ uint64_t sp[];
+  const uint32_t ML = p.M * p.L;
+  uint64_t* s_sum = sp;
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(sp + ML);
+  for (uint32_t i = threadIdx.x; i < ML; i += blockDim.x) { s_sum[i] = 0; s_cnt[i] = 0; }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t g = warp; g < p.n_groups; g += nwarps) {
+    if (!(gflags[g] & LSCAT_GF_DEFINED)) continue;
+    const double b = (double)best_rt[g];
+    const uint32_t mat = p.gmat ? p.gmat[g] : (uint32_t)((p.first_group + g) % p.M);
+    int64_t r0, r1;
+    if (p.rpg) {
+      r0 = (int64_t)(g * p.rpg);
+      r1 = min(r0 + (int64_t)p.rpg, (int64_t)p.n_rows);
+    } else {
+      r0 = p.off[g];
+      r1 = p.off[g + 1];
+    }
+    for (int64_t r = r0 + lane; r < r1; r += 32) {
+      const float v = __ldcs(p.rt + r);
+      if (!ok_bits(__float_as_uint(v))) continue;
+      const uint32_t id = __ldcs(p.bid + r);
+      const uint64_t q = (uint64_t)__dmul_rn(__ddiv_rn(b, (double)v), 2147483648.0);
+      atomicAdd((unsigned long long*)&s_sum[mat * p.L + id], (unsigned long long)q);
+      atomicAdd(&s_cnt[mat * p.L + id], 1u);
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < ML; i += blockDim.x) {
+    if (s_cnt[i]) {
+      atomicAdd((unsigned long long*)&prof_sum[i], (unsigned long long)s_sum[i]);
+      atomicAdd((unsigned long long*)&prof_cnt[i], (unsigned long long)s_cnt[i]);
+    }
+  }
 }
 
 bool opts_ok(const lscat_reduce_opts* o) {
@@ -576,6 +623,7 @@ bool opts_ok(const lscat_reduce_opts* o) {
   if (o->perf_lt_num >= (1u << 29) || o->perf_lt_den >= (1u << 29)) return false;
   if (o->band_lo_num >= (1u << 29) || o->band_lo_den >= (1u << 29)) return false;
   if (o->nan_policy > LSCAT_COMPLETE_ONLY) return false;
+  if (o->block_profile && (uint64_t)o->n_matrices * o->n_blocks * 12 > 200 * 1024) return false;
   return true;
 }
 
@@ -672,6 +720,10 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
   p.o_perf = out->perf;
   p.o_gain = out->gain;
   p.o_flags = out->flags;
+  if (o->block_profile) {
+    if (!p.o_bestrt) { p.o_bestrt = (float*)scratch(ctx, "bestrt", G * 4, &err); if (err) return cuda_fail(ctx, err, "scratch"); }
+    if (!p.o_flags) { p.o_flags = (uint32_t*)scratch(ctx, "gflags", G * 4, &err); if (err) return cuda_fail(ctx, err, "scratch"); }
+  }
   if (o->keep_values) {
     if (!p.o_perf) { p.o_perf = (double*)scratch(ctx, "perf", G * 8, &err); if (err) return cuda_fail(ctx, err, "scratch"); }
     if (!p.o_gain) { p.o_gain = (double*)scratch(ctx, "gain", G * 8, &err); if (err) return cuda_fail(ctx, err, "scratch"); }
@@ -733,6 +785,17 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
     p.mode = MODE_FINALIZE_MERGED;
     const int g2 = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)ctx->sm_count * 4, (G + 255) / 256));
     if (G) finalize_merged_kernel<<<g2, 256, smem_fin, s>>>(p), ctx->launches++;
+    LSCAT_CUDA(ctx, cudaGetLastError());
+  }
+  if (o->block_profile && G) {
+    const size_t ML = (size_t)o->n_matrices * o->n_blocks;
+    uint64_t* prof = p.partials + kNC + sh_words;  // [sum ML][count ML]
+    const size_t psm = ML * 12;
+    if (psm > 48 * 1024)
+      LSCAT_CUDA(ctx, cudaFuncSetAttribute(profile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
+    const int g3 = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)ctx->sm_count * 8, (G + 7) / 8));
+    profile_kernel<<<g3, 256, psm, s>>>(p, p.o_bestrt, p.o_flags, prof, prof + ML);
+    ctx->launches++;
     LSCAT_CUDA(ctx, cudaGetLastError());
   }
   if (ctx->world > 1) {

@@ -69,7 +69,8 @@ __global__ void __launch_bounds__(256) select_pass(const double* __restrict__ pe
       const uint64_t k = def ? (uint64_t)__double_as_longlong(v) : 0;
       for (int r = 0; r < nr; r++) {
         const Range& R = sr[r];
-        const bool hit = def && R.which == (uint32_t)w && k >= R.lo && k <= R.hi;
+        if (R.which != (uint32_t)w) continue;  // warp-uniform
+        const bool hit = def && k >= R.lo && k <= R.hi;
         if (!__any_sync(FULL, hit)) continue;
         if (R.gather) {
           if (hit) {
@@ -321,7 +322,7 @@ extern "C" lscat_status lscat_stats(lscat_ctx* ctx, const lscat_reduce_opts* o, 
   cudaStream_t s = (cudaStream_t)stream;
   LSCAT_CUDA(ctx, cudaSetDevice(ctx->device));
   const size_t nb = o->bins_per_unit, ng = (size_t)o->gain_cap * nb, nbb = (size_t)o->n_matrices * o->n_blocks;
-  const size_t plen = LSCAT_P_NCOUNTERS + (nb + 1) + (ng + 1) + nbb;
+  const size_t plen = LSCAT_P_NCOUNTERS + (nb + 1) + (ng + 1) + nbb * (o->block_profile ? 3 : 1);
   std::vector<uint64_t> P(plen);
   uint64_t mm[4];
   LSCAT_CUDA(ctx, cudaMemcpyAsync(P.data(), rs.partials, plen * 8, cudaMemcpyDeviceToHost, s));
@@ -353,6 +354,14 @@ extern "C" lscat_status lscat_stats(lscat_ctx* ctx, const lscat_reduce_opts* o, 
   if (out->perf_hist) memcpy(out->perf_hist, H, (nb + 1) * 8);
   if (out->gain_hist) memcpy(out->gain_hist, H + nb + 1, (ng + 1) * 8);
   if (out->best_block_hist) memcpy(out->best_block_hist, H + nb + 1 + ng + 1, nbb * 8);
+  if (o->block_profile) {  // R-22: mean of best / r_b per (matrix, block)
+    const uint64_t* ps = H + nb + 1 + ng + 1 + nbb;
+    const uint64_t* pc = ps + nbb;
+    for (size_t i = 0; i < nbb; i++) {
+      if (out->profile_count) out->profile_count[i] = pc[i];
+      if (out->profile_mean) out->profile_mean[i] = pc[i] ? ((double)ps[i] * 0x1p-31) / (double)pc[i] : NAN;
+    }
+  }
   if (out->n_percentiles) {
     if (out->n_ratio_defined == 0) {
       for (uint32_t i = 0; i < out->n_percentiles; i++) out->pct_perf[i] = out->pct_gain[i] = NAN;

@@ -82,7 +82,7 @@ class ReduceOpts(C.Structure):
     _fields_ = [(n, C.c_uint32) for n in (
         "n_blocks", "largest_block_id", "n_matrices", "nan_policy", "bins_per_unit", "gain_cap",
         "gain_gt_num", "gain_gt_den", "perf_lt_num", "perf_lt_den", "band_lo_num",
-        "band_lo_den", "point_sharded", "keep_values")]
+        "band_lo_den", "point_sharded", "keep_values", "block_profile")]
 
 
 class ReduceOutC(C.Structure):
@@ -96,7 +96,8 @@ class StatsOutC(C.Structure):
                 [("perf_hist", C.c_void_p), ("gain_hist", C.c_void_p),
                  ("best_block_hist", C.c_void_p), ("percentiles", C.c_void_p),
                  ("n_percentiles", C.c_uint32), ("pct_perf", C.c_void_p),
-                 ("pct_gain", C.c_void_p)])
+                 ("pct_gain", C.c_void_p), ("profile_mean", C.c_void_p),
+                 ("profile_count", C.c_void_p)])
 
 
 class GenOpts(C.Structure):
@@ -432,6 +433,10 @@ class Ctx:
         if pc.size:
             so.percentiles, so.n_percentiles = pc.ctypes.data, pc.size
             so.pct_perf, so.pct_gain = pp.ctypes.data, pg.ctypes.data
+        pm = np.full(opts.n_matrices * opts.n_blocks, np.nan)
+        pn = np.zeros(opts.n_matrices * opts.n_blocks, np.uint64)
+        if opts.block_profile:
+            so.profile_mean, so.profile_count = pm.ctypes.data, pn.ctypes.data
         self._ck(self._lib.lscat_stats(self.h, C.byref(opts), C.byref(so), _stream(stream)),
                  "stats")
         res = {k: int(getattr(so, k)) for k in COUNTERS}
@@ -441,6 +446,9 @@ class Ctx:
             res["best_block_hist"] = bh.reshape(opts.n_matrices, opts.n_blocks)
         if pc.size:
             res["pct_perf"], res["pct_gain"] = pp.tolist(), pg.tolist()
+        if opts.block_profile:
+            res["profile_mean"] = pm.reshape(opts.n_matrices, opts.n_blocks)
+            res["profile_count"] = pn.reshape(opts.n_matrices, opts.n_blocks)
         return res
 
     # synthetic tables

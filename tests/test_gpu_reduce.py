@@ -207,3 +207,34 @@ def test_group_aligned_shard_without_matrix_array():
         assert st[k] == v, k
     assert (st["best_block_hist"] == ref.best_block_hist).all()
     assert st["pct_gain"] == ref.percentiles["gain"]
+
+
+@pytest.mark.parametrize("policy", [0, 1])
+def test_block_profile(policy):
+    """Figs. 2/4 block profile (R-22): per (matrix, block) sums of floor(RN(best/r_b) 2^31) and
+    counts, bit-exact vs the oracle, on a ragged table and on a uniform one."""
+    c = ctx()
+    from paper_2103_14409_b200 import reduce_opts
+    t = gen_table(300_000, 1200, preset="t4", nan_rate=0.05, seed=12, block_mod=2, block_rem=0)
+    o = reduce_opts(32, 8, nan_policy=policy, block_profile=1)
+    c.reduce_table(_device_table(t), o, per_group=False)
+    st = c.stats(o)
+    ref = OT.reduce_table(t["runtime_ms"], t["block_id"], t["group_offset"],
+                          group_matrix=t["group_matrix"],
+                          opts=OT.Opts(nan_policy=policy, block_profile=True))
+    assert (st["profile_count"] == ref.profile_count).all()
+    m = ~np.isnan(ref.profile_mean)
+    assert (st["profile_mean"][m] == ref.profile_mean[m]).all()
+    assert np.isnan(st["profile_mean"][~m]).all()
+    for k, v in ref.counters.items():
+        assert st[k] == v, k
+    # uniform 32-row layout (vector reducer path)
+    n = 32 * 30_000
+    tab = c.gen_table(n, 3750, preset=0, seed=99, offsets=False)
+    c.reduce_table(tab, o, per_group=False)
+    st = c.stats(o)
+    h = gen_table(n, 3750, preset="t4", seed=99)
+    ref = OT.reduce_table(h["runtime_ms"], h["block_id"], rows_per_group=32,
+                          opts=OT.Opts(nan_policy=policy, block_profile=True))
+    assert (st["profile_count"] == ref.profile_count).all()
+    assert (st["profile_mean"] == ref.profile_mean).all()

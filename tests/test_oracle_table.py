@@ -267,3 +267,27 @@ def test_duplicate_rows_rejected(oracle_lib):
     with pytest.raises(oracle_lib.OracleError):
         oracle_lib.reduce_table(np.array([1, 2], np.float32), np.array([0, 0]),
                                 np.array([0, 2]), opts=oracle_lib.Opts(n_blocks=2))
+
+
+def test_block_profile_brute_force(oracle_lib):
+    """R-22 block profile == Fraction brute force: per (matrix, block) floor(RN(best/r)*2^31)."""
+    rng = np.random.default_rng(5)
+    rt, bid, off, gm = _random_table(rng, 400, 8, dup_vals=False)
+    r = oracle_lib.reduce_table(rt, bid, off, group_matrix=gm,
+                                opts=oracle_lib.Opts(n_blocks=8, block_profile=True))
+    ps = np.zeros((8, 8), object)
+    pc = np.zeros((8, 8), np.int64)
+    for g in range(len(off) - 1):
+        rows = range(off[g], off[g + 1])
+        okr = [i for i in rows if np.isfinite(rt[i]) and rt[i] > 0]
+        if not okr:
+            continue
+        best = min(float(rt[i]) for i in okr)
+        for i in okr:
+            q = float(best) / float(rt[i])                    # RN(best / r)
+            ps[gm[g], bid[i]] += math.floor(Fraction(q) * 2 ** 31)
+            pc[gm[g], bid[i]] += 1
+    assert (r.profile_count == pc).all()
+    assert all(int(r.profile_sum[i, j]) == int(ps[i, j]) for i in range(8) for j in range(8))
+    # the best block of a group with a unique minimum contributes exactly 2^31 (perf 1)
+    assert r.profile_mean.max() <= 1.0
