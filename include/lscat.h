@@ -317,6 +317,38 @@ typedef struct {
 lscat_status lscat_stats(lscat_ctx* ctx, const lscat_reduce_opts* opts, lscat_stats_out* out,
                          void* stream);
 
+/* ------------------------------------------------- side analyses (8f #4) ----------- */
+/* The block the CUDA occupancy calculator picks for `kernel` among `blocks`:
+   the most resident warps per SM, ties -> the larger block (cudaOccupancyMaxPotentialBlockSize
+   semantics).  Independent of N by construction ("insensitive to matrix sizes").
+   *out_block_id = its index in `blocks`; warps_per_sm (HOST [n_blocks], may be NULL) receives
+   the occupancy of every candidate.  Evaluate its quality with lscat_reduce_table by setting
+   largest_block_id to this id. */
+lscat_status lscat_occupancy_block(lscat_ctx* ctx, uint32_t kernel, const uint16_t* blocks,
+                                   uint32_t n_blocks, uint32_t* out_block_id, uint32_t* warps_per_sm);
+
+/* Timeout economics ("for two seconds of timeout around one third of the kernels had
+   enough time to execute"): counts[i] (HOST) = number of rows of the (device) table that have
+   a result and whose point time (warmup + brackets * launches_per_bracket) x runtime_ms x 1e-3
+   (computed in double, rounded per operation) is <= taus[i] seconds (HOST, <= 64 values). */
+lscat_status lscat_timeout_curve(lscat_ctx* ctx, const lscat_table* table, uint32_t warmup,
+                                 uint32_t brackets, uint32_t launches_per_bracket,
+                                 const double* taus, uint32_t n_taus, uint64_t* counts,
+                                 void* stream);
+
+/* ------------------------------------------------- aggregation experiment (8f #2) --- */
+/* The paper's choice of the median: from a pool of runtimes (device, n_pool fp32)
+   draw `reps` samples of k values without replacement (Floyd's algorithm on a counter-based
+   generator seeded by `seed`), aggregate each with the five methods {mean, median, min, max,
+   20 % trimmed mean} and report per method the variation = population standard deviation of
+   its reps aggregates divided by their mean (R-23).  spread[5] and
+   mean_of_aggregates[5] (may be NULL) are HOST arrays; aggregates (may be NULL) is a DEVICE
+   array [5 * reps], method-major.  1 <= k <= 64 <= ... k <= n_pool.  Synchronizes `stream`. */
+lscat_status lscat_aggregation_experiment(lscat_ctx* ctx, const float* pool, uint64_t n_pool,
+                                          uint32_t k, uint32_t reps, uint64_t seed,
+                                          double* spread, double* mean_of_aggregates,
+                                          double* aggregates, void* stream);
+
 /* ------------------------------------------------- synthetic tables (test/bench) ---- */
 typedef enum { LSCAT_PRESET_T4 = 0, LSCAT_PRESET_GTX980 = 1 } lscat_preset;
 

@@ -40,8 +40,12 @@ struct LaunchArgs {
 using LaunchFn = cudaError_t (*)(const LaunchArgs&, cudaStream_t);
 
 // Per-kernel dispatch: nullptr entries = no implementation at that block (INVALID_CONFIG).
+// Resident warps per SM of the kernel at one block size (occupancy API), for lscat_occupancy_block.
+using OccFn = int (*)();
+
 struct KernelTable {
   LaunchFn fn[kMaxBlockIdx];
+  OccFn occ[kMaxBlockIdx];
 };
 
 // registries filled by each kernel translation unit

@@ -222,6 +222,14 @@ __global__ void __launch_bounds__(B, 1) gemm_kernel(const __grid_constant__ Gemm
 template <int B>
 struct GemmL {
   static constexpr bool kSupported = B >= 128;
+  static int occupancy() {
+    if constexpr (B >= 128) {
+      cudaFuncSetAttribute(gemm_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+      return occupancy_warps(gemm_kernel<B>, B, kSmem);
+    } else {
+      return 0;
+    }
+  }
   static cudaError_t launch(const LaunchArgs& a, cudaStream_t s) {
     if constexpr (B >= 128) {
       const SuiteEntry& e = *a.e;

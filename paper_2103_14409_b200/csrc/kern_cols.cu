@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(B) colsum_kernel(const float* __restrict__ A,
 template <int B>
 struct ColsumL {
   static constexpr bool kSupported = true;
+  static int occupancy() { return occupancy_warps(colsum_kernel<B, 4>, B); }
   static cudaError_t launch(const LaunchArgs& a, cudaStream_t s) {
     const SuiteEntry& e = *a.e;
     const int N = (int)e.n;

@@ -44,12 +44,22 @@ __device__ __forceinline__ float block_sum(float v, float* red /* [B/32] smem */
   }
 }
 
+// Resident warps per SM of `kernel` launched with B threads and `smem` dynamic bytes.
+template <typename F>
+inline int occupancy_warps(F kernel, int B, size_t smem = 0) {
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, B, smem) != cudaSuccess) return 0;
+  return nb * B / 32;
+}
+
 // Builds a KernelTable whose entry i launches Launcher<32*(i+1)>::launch (or nullptr when
 // Launcher<B>::kSupported is false).
 template <template <int> class Launcher, int... Is>
 KernelTable make_table_impl(std::integer_sequence<int, Is...>) {
   KernelTable t{};
   ((t.fn[Is] = Launcher<32 * (Is + 1)>::kSupported ? &Launcher<32 * (Is + 1)>::launch : nullptr),
+   ...);
+  ((t.occ[Is] = Launcher<32 * (Is + 1)>::kSupported ? &Launcher<32 * (Is + 1)>::occupancy : nullptr),
    ...);
   return t;
 }

@@ -33,6 +33,7 @@ __global__ void __launch_bounds__(B) transpose_kernel(const float* __restrict__ 
 template <int B>
 struct TransposeL {
   static constexpr bool kSupported = true;
+  static int occupancy() { return occupancy_warps(transpose_kernel<B>, B); }
   static cudaError_t launch(const LaunchArgs& a, cudaStream_t s) {
     const SuiteEntry& e = *a.e;
     const int N = (int)e.n;
@@ -85,6 +86,7 @@ __global__ void __launch_bounds__(B) axpy_kernel1(const float* __restrict__ x,
 template <int B>
 struct AxpyL {
   static constexpr bool kSupported = true;
+  static int occupancy() { return occupancy_warps(axpy_kernel4<B>, B); }
   static cudaError_t launch(const LaunchArgs& a, cudaStream_t s) {
     const SuiteEntry& e = *a.e;
     const size_t n = (size_t)e.n * e.n;
@@ -183,6 +185,7 @@ __global__ void __launch_bounds__(B) stencil_kernel(const float* __restrict__ A,
 template <int B>
 struct StencilL {
   static constexpr bool kSupported = true;
+  static int occupancy() { return occupancy_warps(stencil_kernel<B, 4>, B); }
   static cudaError_t launch(const LaunchArgs& a, cudaStream_t s) {
     const SuiteEntry& e = *a.e;
     const int N = (int)e.n;
@@ -212,6 +215,7 @@ __global__ void __launch_bounds__(B) spin_kernel(uint64_t ns) {
 template <int B>
 struct SpinL {
   static constexpr bool kSupported = true;
+  static int occupancy() { return occupancy_warps(spin_kernel<B>, B); }
   static cudaError_t launch(const LaunchArgs& a, cudaStream_t s) {
     spin_kernel<B><<<1, B, 0, s>>>(a.spin_ns);
     return cudaGetLastError();

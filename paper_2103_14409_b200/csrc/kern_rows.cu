@@ -7,6 +7,7 @@
 // loads of A with U independent loads in flight per thread, q/x through the read-only cache
 // (L2/L1 resident), fp32 accumulation, warp shuffles + a fixed-order smem combine.
 // HBM bound: 4N^2 + 8N bytes per launch.
+#include <algorithm>
 #include <cmath>
 
 #include "kern_common.cuh"
@@ -127,15 +128,23 @@ struct RowLauncher {
   template <int B>
   struct L {
     static constexpr bool kSupported = true;
+    static int occupancy() { return occupancy_warps(row_kernel<OP, B>, B); }
     static cudaError_t launch(const LaunchArgs& a, cudaStream_t s) {
       const SuiteEntry& e = *a.e;
+      // CTAs resident per SM from threads (2048), CTAs (32) and registers (64K, allocated per
+      // warp in units of 256); shared memory (< 1 KB) never binds
       static int sm_count = 0, resident = 0;
       if (!resident) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, row_kernel<OP, B>, B, 0);
-        if (resident < 1) resident = 1;
+        if (sm_count < 1) sm_count = 148;
+        cudaFuncAttributes fa{};
+        int regs = 32;
+        if (cudaFuncGetAttributes(&fa, row_kernel<OP, B>) == cudaSuccess && fa.numRegs > 0) regs = fa.numRegs;
+        cudaGetLastError();
+        const int per_warp = ((regs * 32 + 255) / 256) * 256;
+        resident = std::max(1, std::min({32, 2048 / B, 65536 / (per_warp * (B / 32))}));
       }
       const int N = (int)e.n, tw = team_warps(N, B, sm_count, resident), teams = B / 32 / tw;
       row_kernel<OP, B><<<(N + teams - 1) / teams, B, 0, s>>>((const float*)e.in0, (const float*)e.in1,

@@ -117,6 +117,7 @@ EXPORTS = [
     "lscat_suite_buffer", "lscat_suite_upload", "lscat_launch", "lscat_kernel_work",
     "lscat_plan", "lscat_sweep", "lscat_reduce_opts_default", "lscat_partials_len",
     "lscat_reduce_table", "lscat_stats", "lscat_gen_table", "lscat_gen_table_shape",
+    "lscat_aggregation_experiment", "lscat_occupancy_block", "lscat_timeout_curve",
 ]
 
 
@@ -154,6 +155,9 @@ def load(path: str = LIB_PATH):
         "lscat_stats": ([vp, C.POINTER(ReduceOpts), C.POINTER(StatsOutC), vp], i32),
         "lscat_gen_table": ([vp, C.POINTER(GenOpts), C.POINTER(TableC), vp], i32),
         "lscat_gen_table_shape": ([C.POINTER(GenOpts), C.POINTER(u64), C.POINTER(u64)], i32),
+        "lscat_aggregation_experiment": ([vp, vp, u64, u32, u32, u64, vp, vp, vp, vp], i32),
+        "lscat_occupancy_block": ([vp, u32, vp, u32, C.POINTER(u32), vp], i32),
+        "lscat_timeout_curve": ([vp, C.POINTER(TableC), u32, u32, u32, vp, u32, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -450,6 +454,45 @@ class Ctx:
             res["profile_mean"] = pm.reshape(opts.n_matrices, opts.n_blocks)
             res["profile_count"] = pn.reshape(opts.n_matrices, opts.n_blocks)
         return res
+
+    # occupancy-API block and timeout economics
+    def occupancy_block(self, kernel, blocks):
+        """(index into blocks of the occupancy calculator's choice, warps/SM per candidate)."""
+        b, bp = _arr(blocks, np.uint16)
+        w = np.zeros(b.size, np.uint32)
+        out = C.c_uint32()
+        self._ck(self._lib.lscat_occupancy_block(self.h, kernel, bp, b.size, C.byref(out),
+                                                 w.ctypes.data), "occupancy_block")
+        return out.value, w
+
+    def timeout_curve(self, table: Table, taus, warmup=1, brackets=10, launches=1000,
+                      stream=None):
+        t, tp = _arr(taus, np.float64)
+        cnt = np.zeros(t.size, np.uint64)
+        tc = table.c()
+        self._ck(self._lib.lscat_timeout_curve(self.h, C.byref(tc), warmup, brackets, launches,
+                                               tp, t.size, cnt.ctypes.data, _stream(stream)),
+                 "timeout_curve")
+        return cnt
+
+    # SURVEY 8(f) #2: the paper's aggregation experiment (P:205)
+    AGG_METHODS = ("mean", "median", "min", "max", "trimmed_mean_20")
+
+    def aggregation_experiment(self, pool, k=10, reps=10_000, seed=0, aggregates=False,
+                               stream=None):
+        """pool: 1-D float32 CUDA tensor.  Returns {method: spread} (+ per-rep aggregates)."""
+        import torch
+        sp = np.zeros(5)
+        mn = np.zeros(5)
+        agg = torch.empty(5 * reps, dtype=torch.float64, device=pool.device) if aggregates else None
+        self._ck(self._lib.lscat_aggregation_experiment(
+            self.h, pool.data_ptr(), pool.numel(), k, reps, seed, sp.ctypes.data, mn.ctypes.data,
+            None if agg is None else agg.data_ptr(), _stream(stream)), "aggregation_experiment")
+        out = {"spread": dict(zip(self.AGG_METHODS, sp.tolist())),
+               "mean": dict(zip(self.AGG_METHODS, mn.tolist()))}
+        if aggregates:
+            out["aggregates"] = agg.view(5, reps).cpu().numpy()
+        return out
 
     # synthetic tables
     def gen_table(self, n_rows_global, n_kernels, n_blocks=32, largest_block_id=None,
