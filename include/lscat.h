@@ -317,6 +317,19 @@ typedef struct {
 lscat_status lscat_stats(lscat_ctx* ctx, const lscat_reduce_opts* opts, lscat_stats_out* out,
                          void* stream);
 
+/* ------------------------------------------------- table ingest (8f #3) ------------ */
+/* Group an unordered runtime dataframe (the paper's Pandas rows) into a table: DEVICE
+   inputs [n] kernel id, matrix index, block id, runtime (status may be NULL); `out` (device,
+   CALLER-OWNED, cap_rows >= n, cap_groups >= number of distinct (kernel, matrix)) receives
+   groups in ascending (kernel, matrix) order, rows ascending by block id (a stable radix sort,
+   so equal keys keep their input order), group_offset / group_kernel / group_matrix (the
+   latter two may be NULL).  n < 2^32.  Duplicated (kernel, matrix, block) rows violate the
+   table precondition: the table is still written, *n_duplicates (may be NULL) counts them,
+   and LSCAT_ERR_INVALID_ARG is returned.  Synchronous. */
+lscat_status lscat_ingest(lscat_ctx* ctx, const uint32_t* kernel, const uint32_t* matrix,
+                          const uint16_t* block_id, const float* runtime, const uint8_t* status,
+                          uint64_t n, lscat_table* out, uint64_t* n_duplicates, void* stream);
+
 /* ------------------------------------------------- side analyses (8f #4) ----------- */
 /* The block the CUDA occupancy calculator picks for `kernel` among `blocks`:
    the most resident warps per SM, ties -> the larger block (cudaOccupancyMaxPotentialBlockSize

@@ -9,6 +9,7 @@
 // HBM bound: 4N^2 + 8N bytes per launch.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "kern_common.cuh"
 
@@ -146,7 +147,13 @@ struct RowLauncher {
         const int per_warp = ((regs * 32 + 255) / 256) * 256;
         resident = std::max(1, std::min({32, 2048 / B, 65536 / (per_warp * (B / 32))}));
       }
-      const int N = (int)e.n, tw = team_warps(N, B, sm_count, resident), teams = B / 32 / tw;
+      static const int tw_env = [] {  // LSCAT_ROW_TEAM_WARPS: tuning override (profiling only)
+        const char* v = getenv("LSCAT_ROW_TEAM_WARPS");
+        return v ? atoi(v) : 0;
+      }();
+      const int N = (int)e.n;
+      const int tw = (tw_env > 0 && tw_env <= B / 32) ? tw_env : team_warps(N, B, sm_count, resident);
+      const int teams = B / 32 / tw;
       row_kernel<OP, B><<<(N + teams - 1) / teams, B, 0, s>>>((const float*)e.in0, (const float*)e.in1,
                                                              (float*)e.out, N, tw);
       return cudaGetLastError();

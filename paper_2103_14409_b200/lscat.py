@@ -118,6 +118,7 @@ EXPORTS = [
     "lscat_plan", "lscat_sweep", "lscat_reduce_opts_default", "lscat_partials_len",
     "lscat_reduce_table", "lscat_stats", "lscat_gen_table", "lscat_gen_table_shape",
     "lscat_aggregation_experiment", "lscat_occupancy_block", "lscat_timeout_curve",
+    "lscat_ingest",
 ]
 
 
@@ -158,6 +159,7 @@ def load(path: str = LIB_PATH):
         "lscat_aggregation_experiment": ([vp, vp, u64, u32, u32, u64, vp, vp, vp, vp], i32),
         "lscat_occupancy_block": ([vp, u32, vp, u32, C.POINTER(u32), vp], i32),
         "lscat_timeout_curve": ([vp, C.POINTER(TableC), u32, u32, u32, vp, u32, vp, vp], i32),
+        "lscat_ingest": ([vp, vp, vp, vp, vp, vp, u64, C.POINTER(TableC), C.POINTER(u64), vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -454,6 +456,23 @@ class Ctx:
             res["profile_mean"] = pm.reshape(opts.n_matrices, opts.n_blocks)
             res["profile_count"] = pn.reshape(opts.n_matrices, opts.n_blocks)
         return res
+
+    # group an unordered dataframe into a table
+    def ingest(self, kernel, matrix, block_id, runtime, status=None, stream=None) -> Table:
+        """CUDA tensors [n]: kernel (int32/uint32), matrix (int32), block_id (int16), runtime
+        (float32), status (uint8, optional).  Returns the grouped Table."""
+        n = runtime.numel()
+        table = Table.empty(n, n)
+        tc = table.c()
+        dups = C.c_uint64()
+        st = self._lib.lscat_ingest(self.h, kernel.data_ptr(), matrix.data_ptr(),
+                                    block_id.data_ptr(), runtime.data_ptr(),
+                                    None if status is None else status.data_ptr(), n,
+                                    C.byref(tc), C.byref(dups), _stream(stream))
+        table.n_rows, table.n_groups = tc.n_rows, tc.n_groups
+        table.duplicates = dups.value
+        self._ck(st, "ingest")
+        return table
 
     # SURVEY 8(f) #4: occupancy-API block (P:230-231, P:309) and timeout economics (P:228)
     def occupancy_block(self, kernel, blocks):
