@@ -147,15 +147,41 @@ struct RowLauncher {
         const int per_warp = ((regs * 32 + 255) / 256) * 256;
         resident = std::max(1, std::min({32, 2048 / B, 65536 / (per_warp * (B / 32))}));
       }
-      static const int tw_env = [] {  // LSCAT_ROW_TEAM_WARPS: tuning override (profiling only)
+      // tuning overrides (profiling only): LSCAT_ROW_TEAM_WARPS, LSCAT_ROW_WARPS_PER_SM
+      static const int tw_env = [] {
         const char* v = getenv("LSCAT_ROW_TEAM_WARPS");
         return v ? atoi(v) : 0;
       }();
+      static const int cap_env = [] {
+        const char* v = getenv("LSCAT_ROW_WARPS_PER_SM");
+        return v ? atoi(v) : -1;
+      }();
+      // Resident warps per SM are capped (default 32) by reserving dynamic shared memory: with
+      // more warps streaming rows at once, HBM efficiency drops (measured on B200: 64 warps/SM
+      // 40-70 % slower than 32 at N = 8192).
+      static int smem_cap = -1;
+      if (smem_cap < 0) {
+        const int cap = cap_env >= 0 ? cap_env : 32;
+        const int W = B / 32;
+        smem_cap = 0;
+        if (cap > 0 && resident * W > cap) {
+          const int ctas = std::max(1, cap / W);
+          smem_cap = (227 * 1024) / ctas - 1024;  // leaves room for the static red[] array
+          smem_cap = std::min(smem_cap, 227 * 1024 - 2048);
+          if (cudaFuncSetAttribute(row_kernel<OP, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap) !=
+              cudaSuccess) {
+            cudaGetLastError();
+            smem_cap = 0;
+          } else {
+            resident = ctas;
+          }
+        }
+      }
       const int N = (int)e.n;
       const int tw = (tw_env > 0 && tw_env <= B / 32) ? tw_env : team_warps(N, B, sm_count, resident);
       const int teams = B / 32 / tw;
-      row_kernel<OP, B><<<(N + teams - 1) / teams, B, 0, s>>>((const float*)e.in0, (const float*)e.in1,
-                                                             (float*)e.out, N, tw);
+      row_kernel<OP, B><<<(N + teams - 1) / teams, B, smem_cap, s>>>((const float*)e.in0, (const float*)e.in1,
+                                                                     (float*)e.out, N, tw);
       return cudaGetLastError();
     }
   };
