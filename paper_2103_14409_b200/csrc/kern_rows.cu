@@ -18,6 +18,10 @@ namespace {
 
 enum RowOp { kEuclid = 0, kMatvec = 1, kRowsum = 2 };
 
+#ifndef ROW_U
+#define ROW_U 8  // float4 loads of A in flight per thread (and as many of q/x)
+#endif
+
 template <int OP>
 __device__ __forceinline__ void acc4(float4& s, float4 a, float4 v) {
   if constexpr (OP == kEuclid) {
@@ -37,9 +41,8 @@ __device__ __forceinline__ float acc1(float s, float a, float v) {
   else return s + a;
 }
 
-// A CTA of B threads is split into floor(W/TW) teams of TW warps; each team reduces one row.
-// TW is chosen on the host (team_warps) from the wave tail, the loads in flight per thread and
-// the idle warps.
+// A CTA of B threads is split into floor(W/TW) teams of TW warps; each team reduces one row
+// (TW from team_warps, calibrated on B200).
 template <int OP, int B>
 __global__ void __launch_bounds__(B) row_kernel(const float* __restrict__ A,
                                                 const float* __restrict__ v,
@@ -56,7 +59,7 @@ __global__ void __launch_bounds__(B) row_kernel(const float* __restrict__ A,
   float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
   if (live) {
     if ((N & 3) == 0) {
-      constexpr int U = 4;
+      constexpr int U = ROW_U;
       const float4* a4 = reinterpret_cast<const float4*>(a);
       const float4* v4 = reinterpret_cast<const float4*>(v);
       const int n4 = N >> 2;
@@ -96,29 +99,21 @@ __global__ void __launch_bounds__(B) row_kernel(const float* __restrict__ A,
   if (live && tw == 0 && lane == 0) out[row] = (OP == kEuclid) ? sqrtf(r) : r;
 }
 
-// Warps per team d (1..B/32; floor(W/d) teams per CTA, leftover warps idle).  Scored on
-//   tail:        C = resident teams, N/C rounds of rows, efficiency (N/C) / ceil(N/C);
-//   MLP:         a thread streams n4/(32 d) float4 of its row, 4 in flight: min(1, f4 / 4);
-//   concurrency: more than ~32 concurrently streamed rows per SM lowers HBM efficiency
-//                (measured: 9472 concurrent row streams ran 35 % slower than 4736);
-//   idle:        fraction of the CTA's warps that have a team.
-// `resident` = CTAs of this kernel resident per SM (occupancy API, cached by the launcher).
+// Warps per team d (1..W, W = B/32; floor(W/d) teams per CTA, leftover warps idle), from the
+// B200 calibration in profiles/r01_summary.md (euclid, N = 8192, U = 8): two warps per row is
+// best or within 2 % for every block with W even; one-warp teams run 5-7 % slower, 8-warp teams
+// up to 20 % slower at large blocks; idle warps cost about their share.  Score = fraction of
+// active warps x preference(d); wave-tail models did not predict the measurements and are not
+// used.  (`N`, `sm_count`, `resident` are kept for the interface: small N is launch-bound.)
 inline int team_warps(int N, int B, int sm_count, int resident) {
+  (void)N; (void)sm_count; (void)resident;
   const int W = B / 32;
-  const double n4 = (N + 3) / 4;
   int best = 1;
   double best_score = -1.0;
   for (int d = 1; d <= W; d++) {
-    const int teams = W / d;
-    const double C = (double)sm_count * resident * teams;
-    const double R = N / C;
-    const double eff = R <= 1.0 ? 1.0 : R / std::ceil(R - 1e-9);
-    const double f4 = n4 / (32.0 * d);
-    const double mlp = f4 >= 4.0 ? 1.0 : f4 / 4.0;
-    const double over = C / (32.0 * sm_count);
-    const double conc = over > 1.0 ? 1.0 / over : 1.0;
-    const double active = (double)(teams * d) / W;
-    const double score = eff * mlp * conc * (0.75 + 0.25 * active);
+    const double pref = d == 2 ? 1.0 : (d == 3 || d == 4) ? 0.99 : (d <= 8 ? (d == 1 ? 0.95 : 0.97) : 0.9);
+    const double active = (double)((W / d) * d) / W;
+    const double score = active * pref;
     if (score > best_score + 1e-9) { best_score = score; best = d; }
   }
   return best;
@@ -156,12 +151,12 @@ struct RowLauncher {
         const char* v = getenv("LSCAT_ROW_WARPS_PER_SM");
         return v ? atoi(v) : -1;
       }();
-      // Resident warps per SM are capped (default 32) by reserving dynamic shared memory: with
-      // more warps streaming rows at once, HBM efficiency drops (measured on B200: 64 warps/SM
-      // 40-70 % slower than 32 at N = 8192).
+      // Optional cap on resident warps per SM by reserving dynamic shared memory (calibration
+      // only, off by default: the reservation also shrinks L1, which holds q/x, and measured
+      // slower on B200 for every cap tried, profiles/r01_summary.md).
       static int smem_cap = -1;
       if (smem_cap < 0) {
-        const int cap = cap_env >= 0 ? cap_env : 32;
+        const int cap = cap_env >= 0 ? cap_env : 0;
         const int W = B / 32;
         smem_cap = 0;
         if (cap > 0 && resident * W > cap) {
