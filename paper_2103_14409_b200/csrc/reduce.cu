@@ -304,28 +304,67 @@ __device__ __forceinline__ uint4 lds128(uint32_t saddr) {
 }
 
 // Lane j folds group j of a staged batch (shared-space addresses of the runtime / id stage).
+__device__ __forceinline__ uint32_t lds32(uint32_t saddr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr));
+  return v;
+}
+
+// Lane j folds group j of a staged batch (shared-space addresses of the runtime / id stage).
+// Fast path when the group's block ids are 0..31 in order (every table the sweep or the
+// generator writes): one pass tracks the first minimum (= the smallest block id among equal
+// minima), the largest block's row is read directly.  Otherwise a second pass over ids.
 __device__ __forceinline__ void uniform_fold(const RP& p, uint32_t srt, uint32_t sid, int lane,
                                              GroupAcc& mine) {
   const uint32_t rbase = srt + lane * 128, ibase = sid + lane * 64;
-  uint32_t mkey = 0xFFFFFFFFu, nok = 0, nnan = 0;
+  const int sw = lane & 7, swi = (lane >> 1) & 3;
+  bool sorted = true;
+#pragma unroll
+  for (int c = 0; c < 4; c++) {  // ids 8c .. 8c+7 packed in pairs: word w = (2w+1) << 16 | 2w
+    const uint4 y = lds128(ibase + 16 * (c ^ swi));
+    const uint32_t w0 = 8 * c;
+    sorted &= y.x == (((w0 + 1) << 16) | w0) && y.y == (((w0 + 3) << 16) | (w0 + 2)) &&
+              y.z == (((w0 + 5) << 16) | (w0 + 4)) && y.w == (((w0 + 7) << 16) | (w0 + 6));
+  }
+  uint32_t mkey = 0xFFFFFFFFu, mpos = 0xFFFFFFFFu, okm = 0;
 #pragma unroll 2
   for (int c = 0; c < 8; c++) {
-    const uint4 x = lds128(rbase + 16 * (c ^ (lane & 7)));
+    const uint4 x = lds128(rbase + 16 * (c ^ sw));
     const uint32_t b4[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
     for (int q = 0; q < 4; q++) {
       const bool ok = ok_bits(b4[q]);
-      mkey = min(mkey, ok ? b4[q] : 0xFFFFFFFFu);
-      nok += ok;
-      nnan += nan_bits(b4[q]);
+      const bool lt = ok && b4[q] < mkey;  // strict: ties keep the earlier row
+      mkey = lt ? b4[q] : mkey;
+      mpos = lt ? (uint32_t)(4 * c + q) : mpos;
+      okm |= ok ? (1u << (4 * c + q)) : 0u;
     }
+  }
+  uint32_t nnan = 0;
+  for (uint32_t m = ~okm; m; m &= m - 1) {  // rows without a result (rare): NaN or invalid
+    const int j = __ffs(m) - 1;
+    nnan += nan_bits(lds32(rbase + 16 * ((j >> 2) ^ sw) + 4 * (j & 3)));
+  }
+  mine.min_bits = mkey;
+  mine.n_ok = __popc(okm);
+  mine.n_nan = nnan;
+  mine.n_rows = 32;
+  if (sorted) {
+    mine.min_bid = mkey != 0xFFFFFFFFu ? mpos : 0xFFFFFFFFu;
+    if (p.ell < 32) {
+      const int j = (int)p.ell;
+      const uint32_t lb = lds32(rbase + 16 * ((j >> 2) ^ sw) + 4 * (j & 3));
+      mine.lcode = ok_bits(lb) ? 2u : 1u;
+      mine.l_bits = lb;
+    }
+    return;
   }
   uint32_t mid = 0xFFFFFFFFu;
 #pragma unroll 1
   for (int c = 0; c < 4; c++) {
-    const uint4 y = lds128(ibase + 16 * (c ^ ((lane >> 1) & 3)));
-    const uint4 x0 = lds128(rbase + 16 * ((2 * c) ^ (lane & 7)));
-    const uint4 x1 = lds128(rbase + 16 * ((2 * c + 1) ^ (lane & 7)));
+    const uint4 y = lds128(ibase + 16 * (c ^ swi));
+    const uint4 x0 = lds128(rbase + 16 * ((2 * c) ^ sw));
+    const uint4 x1 = lds128(rbase + 16 * ((2 * c + 1) ^ sw));
     const uint32_t b8[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
     const uint32_t iw[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll
@@ -338,11 +377,7 @@ __device__ __forceinline__ void uniform_fold(const RP& p, uint32_t srt, uint32_t
       }
     }
   }
-  mine.min_bits = mkey;
   mine.min_bid = mid;
-  mine.n_ok = nok;
-  mine.n_nan = nnan;
-  mine.n_rows = 32;
 }
 
 __device__ __forceinline__ void emit_group(const RP& p, uint64_t gl, bool active, const GroupAcc& mine,
@@ -374,23 +409,20 @@ __global__ void __launch_bounds__(kThreads, 2) reduce_uniform32_kernel(RP p) {
   init_shared(p, sh_c, sh, t);
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  float4* d[2];
-  uint4* di[2];
-  for (int b = 0; b < 2; b++) {
-    uint8_t* w = stage + ((size_t)wib * 2 + b) * (1024 * 4 + 1024 * 2);
-    d[b] = reinterpret_cast<float4*>(w);
-    di[b] = reinterpret_cast<uint4*>(w + 1024 * 4);
-  }
+  // two stage buffers per warp: [runtimes 4 KB | ids 2 KB] x 2
+  uint8_t* wstage = stage + (size_t)wib * 2 * (1024 * 4 + 1024 * 2);
+  auto D = [&](int b) { return reinterpret_cast<float4*>(wstage + b * (1024 * 4 + 1024 * 2)); };
+  auto DI = [&](int b) { return reinterpret_cast<uint4*>(wstage + b * (1024 * 4 + 1024 * 2) + 1024 * 4); };
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t full_batches = p.n_groups / 32;  // batches of 32 complete 32-row groups
   uint64_t bi = warp;
   int cur = 0;
-  if (bi < full_batches) uniform_prefetch(p, bi * 32, d[0], di[0], lane);
+  if (bi < full_batches) uniform_prefetch(p, bi * 32, D(0), DI(0), lane);
   for (; bi < full_batches; bi += nwarps) {
     const uint64_t nxt = bi + nwarps;
     if (nxt < full_batches) {
-      uniform_prefetch(p, nxt * 32, d[cur ^ 1], di[cur ^ 1], lane);
+      uniform_prefetch(p, nxt * 32, D(cur ^ 1), DI(cur ^ 1), lane);
       asm volatile("cp.async.wait_group 1;" ::: "memory");
     } else {
       asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -398,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, 2) reduce_uniform32_kernel(RP p) {
     __syncwarp();
     GroupAcc mine;
     acc_init(mine);
-    uniform_fold(p, (uint32_t)__cvta_generic_to_shared(d[cur]), (uint32_t)__cvta_generic_to_shared(di[cur]), lane, mine);
+    uniform_fold(p, (uint32_t)__cvta_generic_to_shared(D(cur)), (uint32_t)__cvta_generic_to_shared(DI(cur)), lane, mine);
     __syncwarp();
     emit_group(p, bi * 32 + lane, true, mine, t, sh_c, sh_perf, sh_gain, sh_bb);
     cur ^= 1;

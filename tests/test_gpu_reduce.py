@@ -238,3 +238,34 @@ def test_block_profile(policy):
                           opts=OT.Opts(nan_policy=policy, block_profile=True))
     assert (st["profile_count"] == ref.profile_count).all()
     assert (st["profile_mean"] == ref.profile_mean).all()
+
+
+@pytest.mark.parametrize("ell", [31, 7])
+def test_uniform_groups_unsorted_rows(ell):
+    """Uniform 32-row groups whose rows are NOT in block order (the vector reducer's
+    general second pass), with NaN/inf/zero rows, vs the oracle."""
+    import torch
+    from paper_2103_14409_b200 import Table, reduce_opts
+    c = ctx()
+    rng = np.random.default_rng(ell)
+    h = gen_table(32 * 20_000, 2500, preset="t4", seed=21, nan_rate=0.05)
+    rt, bid = h["runtime_ms"].copy(), h["block_id"].copy()
+    G = h["n_groups"]
+    perm = np.argsort(rng.random((G, 32)), axis=1) + (np.arange(G) * 32)[:, None]
+    sel = rng.random(G) < 0.5                      # half the groups permuted, half sorted
+    idx = np.where(sel[:, None], perm, (np.arange(G) * 32)[:, None] + np.arange(32)).ravel()
+    rt, bid = rt[idx], bid[idx]
+    bad = rng.random(rt.size) < 0.01
+    rt[bad] = rng.choice(np.array([np.inf, 0.0, -1.0], np.float32), size=int(bad.sum()))
+    tab = Table(torch.from_numpy(rt).cuda(), torch.from_numpy(bid.view(np.int16)).cuda(), None, None,
+                None, None, n_rows=rt.size, n_groups=G, rows_per_group=32)
+    o = reduce_opts(32, 8, largest_block_id=ell)
+    out = c.reduce_table(tab, o)
+    st = c.stats(o, percentiles=PCTS)
+    ref = OT.reduce_table(rt, bid, rows_per_group=32, opts=OT.Opts(largest_block_id=ell),
+                          percentiles=PCTS)
+    for k, v in ref.counters.items():
+        assert st[k] == v, k
+    assert (out["best_block_id"].cpu().numpy().view(np.uint16) == ref.best_block).all()
+    assert (out["flags"].cpu().numpy().view(np.uint32) == ref.flags).all()
+    assert st["pct_perf"] == ref.percentiles["perf"]
