@@ -292,13 +292,13 @@ lscat_status lscat_plan(const lscat_plan_opts* o, int rank, int world, uint32_t*
     heap.push({l.first + ucost[u], l.second});
   }
   uint64_t cnt = 0;
-  for (uint64_t p = 0; p < npts; p++) {
-    if (owner[by_group ? p / nb : p] != rank) continue;
-    if (out && cnt < cap) out[cnt] = (uint32_t)p;
-    cnt++;
-  }
+  for (uint64_t p = 0; p < npts; p++) cnt += owner[by_group ? p / nb : p] == rank;
   *n_out = cnt;
-  if (out && cnt > cap) return LSCAT_ERR_INVALID_ARG;
+  if (!out) return LSCAT_OK;
+  if (cnt > cap) return LSCAT_ERR_INVALID_ARG;  // nothing written
+  uint64_t i = 0;
+  for (uint64_t p = 0; p < npts; p++)
+    if (owner[by_group ? p / nb : p] == rank) out[i++] = (uint32_t)p;
   return LSCAT_OK;
 }
 

@@ -586,13 +586,6 @@ __global__ void init_minmax(uint64_t* mm) {
   mm[0] = ~0ull; mm[1] = 0; mm[2] = ~0ull; mm[3] = 0;
 }
 
-__global__ void init_group_merge(uint64_t* key, uint64_t* lc, uint32_t* cnt, uint64_t G) {
-  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < G;
-       g += (uint64_t)gridDim.x * blockDim.x) {
-    key[g] = ~0ull; lc[g] = 0; cnt[3 * g] = cnt[3 * g + 1] = cnt[3 * g + 2] = 0;
-  }
-}
-
 size_t partials_len(const lscat_reduce_opts& o) {
   return (size_t)kNC + (o.bins_per_unit + 1) + ((size_t)o.gain_cap * o.bins_per_unit + 1) +
          (size_t)o.n_matrices * o.n_blocks * (o.block_profile ? 3 : 1);

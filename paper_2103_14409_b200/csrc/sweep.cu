@@ -117,7 +117,6 @@ extern "C" lscat_status lscat_sweep(lscat_ctx* ctx, const uint32_t* kernels, uin
     return fail(ctx, LSCAT_ERR_INVALID_ARG, "sweep: table capacity %llu rows / %llu groups < %llu / %llu",
                 (unsigned long long)out->cap_rows, (unsigned long long)out->cap_groups,
                 (unsigned long long)npts, (unsigned long long)G);
-  if (o->bracket_ms_host == nullptr) {}
   cudaStream_t s = (cudaStream_t)stream;
   LSCAT_CUDA(ctx, cudaSetDevice(ctx->device));
 
