@@ -101,19 +101,22 @@ __global__ void __launch_bounds__(B) row_kernel(const float* __restrict__ A,
 
 // Warps per team d (1..W, W = B/32; floor(W/d) teams per CTA, leftover warps idle), from the
 // B200 calibration in profiles/r01_summary.md (euclid, N = 8192, U = 8): two warps per row is
-// best or within 2 % for every block with W even; one-warp teams run 5-7 % slower, 8-warp teams
-// up to 20 % slower at large blocks; idle warps cost about their share.  Score = fraction of
-// active warps x preference(d); wave-tail models did not predict the measurements and are not
-// used.  (`N`, `sm_count`, `resident` are kept for the interface: small N is launch-bound.)
+// best or within 2 % for every block with W even; one-warp teams run 5-7 % slower, 8+-warp
+// teams up to 20 % slower at large blocks; idle warps cost about their share; a grid that
+// needs just over one (or two) waves of resident CTAs loses most of a wave (B = 352, 416,
+// 544: 70 us instead of 45).  Score = active fraction x preference(d) x tail penalty.
 inline int team_warps(int N, int B, int sm_count, int resident) {
-  (void)N; (void)sm_count; (void)resident;
   const int W = B / 32;
+  const double slots = (double)sm_count * resident;
   int best = 1;
   double best_score = -1.0;
   for (int d = 1; d <= W; d++) {
-    const double pref = d == 2 ? 1.0 : (d == 3 || d == 4) ? 0.99 : (d <= 8 ? (d == 1 ? 0.95 : 0.97) : 0.9);
-    const double active = (double)((W / d) * d) / W;
-    const double score = active * pref;
+    const int teams = W / d;
+    const double pref = d == 2 ? 1.0 : (d == 3 || d == 4) ? 0.99 : d == 1 ? 0.96 : (d <= 8 ? 0.97 : 0.93);
+    const double active = (double)(teams * d) / W;
+    const double waves = std::ceil((double)N / teams) / slots;
+    const double tail = (waves > 1.0 && waves < 1.3) ? 0.5 : (waves > 2.0 && waves < 2.3) ? 0.8 : 1.0;
+    const double score = active * pref * tail;
     if (score > best_score + 1e-9) { best_score = score; best = d; }
   }
   return best;
