@@ -31,7 +31,7 @@ sys.path.insert(0, ROOT)
 
 SIZES = [64, 128, 256, 512, 1024, 2048, 4096, 8192]
 BLOCKS = list(range(32, 1025, 32))
-POLICIES = {"paper": (1, 10, 1000), "fast": (1, 5, 20)}   # (W, K, R): P:203
+POLICIES = {"paper": (1, 10, 1000), "fast": (1, 5, 20), "tiny": (1, 2, 2)}  # (W, K, R): P:203; tiny = ncu launch lists
 METRIC = "sweep points/s (euclidean_kernel, 32 blocks x 8 matrix sizes)"
 PCTS = [0.01, 0.05, 0.1, 0.25, 0.5, 0.75, 0.9, 0.95, 0.99]
 

@@ -9,13 +9,18 @@
 // bit-identical to the CPU oracle and across shard counts.
 //
 // Kernel layout: persistent grid, a warp takes 32 consecutive groups at a
-// time; for each group the 32 lanes load one row each (one coalesced 128 B runtime load + 64 B
-// block ids, 8 groups' loads in flight per lane), find the minimum with two redux.sync.min
-// (runtime bits, then block id among the minima: positive finite fp32 bit patterns order like
-// their values), count with ballots, pick the largest block's row with a ballot; the result of
-// group j lands in lane j, and the 32 lanes then finalise their 32 groups in parallel (f64
-// ratios, exact bins, flags) into shared-memory histograms and per-thread counters, flushed
-// once per CTA with 64-bit atomics.  HBM: 6 B/row read (+16 B/group of perf/gain written).
+// time and lane j ends up owning group j.  Three ways to get there:
+//   * uniform 32-row tables (configs[4]): cp.async 16-byte copies into an XOR-swizzled warp
+//     stage, lane j folds group j in one pass when its block ids are 0..31 in order (first
+//     minimum = smallest id among equal minima; positive finite fp32 bit patterns order like
+//     their values), else a second pass over the ids; the next batch streams in while this
+//     one is finalised;
+//   * ragged tables with groups of <= 32 rows: coalesced loads into a padded stage, lane j
+//     folds group j's rows;
+//   * longer groups: the warp folds each group with redux.sync.min / ballots.
+// The 32 lanes then finalise their groups in parallel (f64 ratios, exact bins, flags) into
+// shared-memory histograms and CTA counters, flushed once per CTA with 64-bit atomics.
+// HBM: 6 B/row read (+16 B/group of perf/gain written).
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -125,12 +130,6 @@ __device__ __forceinline__ void wadd(uint64_t* sh_c, int slot, uint32_t v) {
 
 __device__ __forceinline__ uint64_t f64_key(double v) { return (uint64_t)__double_as_longlong(v); }
 
-__device__ __forceinline__ void hist_add(uint32_t* h, int bin) {
-  // warp-aggregated shared-memory increment: lanes with the same bin add once
-  const unsigned peers = __match_any_sync(0xffffffffu, bin);
-  if (bin >= 0 && (__ffs(peers) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&h[bin], (uint32_t)__popc(peers));
-}
-
 // The paper's per-group statistics (O3 steps 3-9).  Warp-collective: all 32
 // lanes call it; `active` lanes hold group g's accumulator.
 __device__ void finalize_lane(const RP& p, uint64_t g, bool active, const GroupAcc& a,
@@ -217,9 +216,18 @@ __device__ void finalize_lane(const RP& p, uint64_t g, bool active, const GroupA
   wadd(sh_c, LSCAT_P_GAIN_GT, __popc(__ballot_sync(FULL, flags & LSCAT_GF_GAIN_GT)));
   wadd(sh_c, LSCAT_P_PERF_LT, __popc(__ballot_sync(FULL, flags & LSCAT_GF_PERF_LT)));
   wadd(sh_c, LSCAT_P_PERF_BAND, __popc(__ballot_sync(FULL, flags & LSCAT_GF_PERF_BAND)));
-  hist_add(sh_perf, pbin);
-  hist_add(sh_gain, gbin);
-  hist_add(sh_bb, bbi);
+  // histogram increments: the hot bins (perf == 1: bin nb; gain == 0: bin 0) by one ballot per
+  // warp, every other bin by a plain shared atomic (spread bins rarely collide in a warp)
+  {
+    const unsigned hp = __ballot_sync(FULL, pbin == (int)p.nb), hg = __ballot_sync(FULL, gbin == 0);
+    if ((threadIdx.x & 31) == 0) {
+      if (hp) atomicAdd(&sh_perf[p.nb], (uint32_t)__popc(hp));
+      if (hg) atomicAdd(&sh_gain[0], (uint32_t)__popc(hg));
+    }
+    if (pbin >= 0 && pbin != (int)p.nb) atomicAdd(&sh_perf[pbin], 1u);
+    if (gbin > 0) atomicAdd(&sh_gain[gbin], 1u);
+    if (bbi >= 0) atomicAdd(&sh_bb[bbi], 1u);
+  }
 }
 
 __device__ void flush(const RP& p, ThreadAcc& t, uint64_t* sh_c, uint32_t* sh) {
@@ -269,7 +277,7 @@ constexpr int kStagePad = kStageRows + kStageRows / 32;  // + 1 word per 32 rows
 constexpr size_t kStageBytes = (size_t)kWarps * kStagePad * (4 + 2);
 
 
-constexpr size_t kUniStageBytes = (size_t)kWarps * 2 * (1024 * 4 + 1024 * 2);  // double buffer
+constexpr size_t kUniStageBytes = (size_t)kWarps * (1024 * 4 + 1024 * 2);  // one stage per warp
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
@@ -395,9 +403,9 @@ __device__ __forceinline__ void emit_group(const RP& p, uint64_t gl, bool active
 }
 
 // a6/a7 for tables of uniform 32-row groups with 16-byte aligned arrays (BASELINE configs[4]):
-// each warp streams its batches of 32 groups through a double-buffered cp.async stage (the
-// next batch is in flight while lane j folds group j of the current one).
-__global__ void __launch_bounds__(kThreads, 2) reduce_uniform32_kernel(RP p) {
+// each warp streams its batches of 32 groups through a cp.async stage; as soon as lane j has
+// folded group j the next batch is requested, so its loads fly while the batch is finalised.
+__global__ void __launch_bounds__(kThreads, 3) reduce_uniform32_kernel(RP p) {
   extern __shared__ uint64_t dyn[];
   uint64_t* sh_c = dyn;
   uint32_t* sh = reinterpret_cast<uint32_t*>(dyn + kNC);
@@ -409,31 +417,26 @@ __global__ void __launch_bounds__(kThreads, 2) reduce_uniform32_kernel(RP p) {
   init_shared(p, sh_c, sh, t);
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  // two stage buffers per warp: [runtimes 4 KB | ids 2 KB] x 2
-  uint8_t* wstage = stage + (size_t)wib * 2 * (1024 * 4 + 1024 * 2);
+  // one stage per warp: [runtimes 4 KB | ids 2 KB]
+  uint8_t* wstage = stage + (size_t)wib * (1024 * 4 + 1024 * 2);
   auto D = [&](int b) { return reinterpret_cast<float4*>(wstage + b * (1024 * 4 + 1024 * 2)); };
   auto DI = [&](int b) { return reinterpret_cast<uint4*>(wstage + b * (1024 * 4 + 1024 * 2) + 1024 * 4); };
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t full_batches = p.n_groups / 32;  // batches of 32 complete 32-row groups
   uint64_t bi = warp;
-  int cur = 0;
   if (bi < full_batches) uniform_prefetch(p, bi * 32, D(0), DI(0), lane);
   for (; bi < full_batches; bi += nwarps) {
-    const uint64_t nxt = bi + nwarps;
-    if (nxt < full_batches) {
-      uniform_prefetch(p, nxt * 32, D(cur ^ 1), DI(cur ^ 1), lane);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncwarp();
     GroupAcc mine;
     acc_init(mine);
-    uniform_fold(p, (uint32_t)__cvta_generic_to_shared(D(cur)), (uint32_t)__cvta_generic_to_shared(DI(cur)), lane, mine);
+    uniform_fold(p, (uint32_t)__cvta_generic_to_shared(D(0)), (uint32_t)__cvta_generic_to_shared(DI(0)), lane, mine);
     __syncwarp();
+    // the stage is free again: the next batch streams in while this one is finalised
+    const uint64_t nxt = bi + nwarps;
+    if (nxt < full_batches) uniform_prefetch(p, nxt * 32, D(0), DI(0), lane);
     emit_group(p, bi * 32 + lane, true, mine, t, sh_c, sh_perf, sh_gain, sh_bb);
-    cur ^= 1;
   }
   // tail: the last < 32 groups (the last one possibly short), warp-per-group folding
   const uint64_t tail0 = full_batches * 32;
