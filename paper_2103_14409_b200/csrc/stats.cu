@@ -58,39 +58,50 @@ __global__ void __launch_bounds__(256) select_pass(const double* __restrict__ pe
   __syncthreads();
   const unsigned FULL = 0xffffffffu;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  // whole warps iterate together so that __match_any_sync sees every lane
-  for (uint64_t base = lo + (blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u)); base < hi;
-       base += stride) {
-    const uint64_t g = base + (threadIdx.x & 31);
-    const bool in = g < hi;
-    for (int w = 0; w < 2; w++) {
-      const double v = in ? (w ? gain[g] : perf[g]) : __longlong_as_double(0x7FF8000000000000ll);
-      const bool def = in && !isnan(v);
-      const uint64_t k = def ? (uint64_t)__double_as_longlong(v) : 0;
-      for (int r = 0; r < nr; r++) {
-        const Range& R = sr[r];
-        if (R.which != (uint32_t)w) continue;  // warp-uniform
-        const bool hit = def && k >= R.lo && k <= R.hi;
-        if (!__any_sync(FULL, hit)) continue;
-        if (R.gather) {
-          if (hit) {
-            const uint32_t idx = atomicAdd(&cand_cnt[r], 1u);
-            if (idx < kCap) cand[(size_t)r * kCap + idx] = k;
-          }
-        } else {
-          const int b = hit ? bin_of(R, k) : -1;
-          // the two single-key end bins (e.g. perf == 1.0, gain == 0) are hot: count them with
-          // one ballot per warp; other bins spread, one atomic per lane
-          const unsigned e0 = __ballot_sync(FULL, b == 0), e1 = __ballot_sync(FULL, b == kBins - 1);
-          const int lane = threadIdx.x & 31;
-          if (lane == 0 && e0) atomicAdd(&H[(size_t)r * kBins], (uint32_t)__popc(e0));
-          if (lane == 0 && e1) atomicAdd(&H[(size_t)r * kBins + kBins - 1], (uint32_t)__popc(e1));
-          if (kSmem) {
-            if (b > 0 && b < kBins - 1) atomicAdd(&H[(size_t)r * kBins + b], 1u);
+  // A warp takes 4 chunks of 32 consecutive groups per iteration and issues all 8 loads
+  // (perf, gain) before using them; whole warps iterate together (ballots, match.any).
+  constexpr int kU = 4;
+  const int lane = threadIdx.x & 31;
+  const uint64_t wstride = stride * kU;
+  for (uint64_t base = lo + (blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u)) * kU; base < hi;
+       base += wstride) {
+    double pv[kU], gv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+      const uint64_t g = base + 32 * u + lane;
+      pv[u] = g < hi ? perf[g] : __longlong_as_double(0x7FF8000000000000ll);
+      gv[u] = g < hi ? gain[g] : __longlong_as_double(0x7FF8000000000000ll);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+      for (int w = 0; w < 2; w++) {
+        const double v = w ? gv[u] : pv[u];
+        const bool def = !isnan(v);
+        const uint64_t k = def ? (uint64_t)__double_as_longlong(v) : 0;
+        for (int r = 0; r < nr; r++) {
+          const Range& R = sr[r];
+          if (R.which != (uint32_t)w) continue;  // warp-uniform
+          const bool hit = def && k >= R.lo && k <= R.hi;
+          if (!__any_sync(FULL, hit)) continue;
+          if (R.gather) {
+            if (hit) {
+              const uint32_t idx = atomicAdd(&cand_cnt[r], 1u);
+              if (idx < kCap) cand[(size_t)r * kCap + idx] = k;
+            }
           } else {
-            const bool mid = b > 0 && b < kBins - 1;
-            const unsigned peers = __match_any_sync(FULL, mid ? b : -1);
-            if (mid && (__ffs(peers) - 1) == lane) atomicAdd(&H[(size_t)r * kBins + b], (uint32_t)__popc(peers));
+            const int b = hit ? bin_of(R, k) : -1;
+            // the two single-key end bins (e.g. perf == 1.0, gain == 0) are hot: count them with
+            // one ballot per warp; other bins spread, one atomic per lane
+            const unsigned e0 = __ballot_sync(FULL, b == 0), e1 = __ballot_sync(FULL, b == kBins - 1);
+            if (lane == 0 && e0) atomicAdd(&H[(size_t)r * kBins], (uint32_t)__popc(e0));
+            if (lane == 0 && e1) atomicAdd(&H[(size_t)r * kBins + kBins - 1], (uint32_t)__popc(e1));
+            if (kSmem) {
+              if (b > 0 && b < kBins - 1) atomicAdd(&H[(size_t)r * kBins + b], 1u);
+            } else {
+              const bool mid = b > 0 && b < kBins - 1;
+              const unsigned peers = __match_any_sync(FULL, mid ? b : -1);
+              if (mid && (__ffs(peers) - 1) == lane) atomicAdd(&H[(size_t)r * kBins + b], (uint32_t)__popc(peers));
+            }
           }
         }
       }
@@ -183,22 +194,26 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
     LSCAT_CUDA(ctx, cudaMemsetAsync(d_hist, 0, (size_t)nr * kBins * 4, s));
     LSCAT_CUDA(ctx, cudaMemsetAsync(d_ccnt, 0, nr * 4, s));
     const uint64_t n = rs.own_hi - rs.own_lo;
-    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)ctx->sm_count * 8, (n + 255) / 256));
-    int nhist = 0;
-    for (const auto& r : ranges) nhist += !r.gather;
+    // grid: every resident CTA once (occupancy API), capped by the work (1024 groups per CTA
+    // iteration)
+    const uint64_t want = std::max<uint64_t>(1, (n + 1023) / 1024);
     if (n && nr <= kSmemRanges) {
       const size_t sm = (size_t)nr * kBins * 4;
       LSCAT_CUDA(ctx, cudaFuncSetAttribute(select_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      const int g2 = std::min(grid, ctx->sm_count * 2);
+      int occ = 1;
+      LSCAT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, select_pass<true>, 256, sm));
+      const int g2 = (int)std::min<uint64_t>(want, (uint64_t)ctx->sm_count * std::max(occ, 1));
       select_pass<true><<<g2, 256, sm, s>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, d_ranges, nr,
                                               d_hist, d_cand, d_ccnt);
       ctx->launches++;
     } else if (n) {
-      select_pass<false><<<grid, 256, 0, s>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, d_ranges, nr,
+      int occ = 1;
+      LSCAT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, select_pass<false>, 256, 0));
+      const int g2 = (int)std::min<uint64_t>(want, (uint64_t)ctx->sm_count * std::max(occ, 1));
+      select_pass<false><<<g2, 256, 0, s>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, d_ranges, nr,
                                                d_hist, d_cand, d_ccnt);
       ctx->launches++;
     }
-    (void)nhist;
     LSCAT_CUDA(ctx, cudaGetLastError());
     std::vector<uint32_t> hist((size_t)nr * kBins);
     std::vector<uint32_t> ccnt(nr);
