@@ -117,6 +117,7 @@ __global__ void __launch_bounds__(kTPB) radix_scatter(const uint64_t* __restrict
     const int d = j < n ? (int)((k[c] >> shift) & 255) : -1;
     const unsigned peers = __match_any_sync(0xffffffffu, d);
     if (d >= 0 && (__ffs(peers) - 1) == lane) wc[w][d] += __popc(peers);
+    __syncwarp();  // the next chunk's leader for d may be another lane
   }
   __syncthreads();
   {  // exclusive prefix over the CTA's warps, per digit
@@ -143,6 +144,7 @@ __global__ void __launch_bounds__(kTPB) radix_scatter(const uint64_t* __restrict
       kout[pos] = k[c];
       vout[pos] = v[c];
     }
+    __syncwarp();
   }
 }
 
