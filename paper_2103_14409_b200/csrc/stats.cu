@@ -2,17 +2,26 @@
 // nearest-rank percentiles of perf and gain over ratio-defined groups, R-13).
 //
 // Percentile selection is a multi-level radix select over the IEEE bit patterns of the
-// positive doubles (bit order == value order): a level splits a key range [lo, hi] into
-// 4096 bins (bin 0 = {lo}, last bin = {hi}, the rest partition (lo, hi) by a shift), one pass
-// over the keys builds the histograms of every still-open range (warp-aggregated atomics),
-// the host picks the bin holding each target rank; ranges holding <= kCap keys are gathered
-// and sorted on the host instead.  Single-key bins (e.g. the many perf == 1.0 groups, the
-// upper extreme) resolve immediately.  With world > 1 the histograms are NCCL-summed and the
-// gathered candidates all-gathered, so every rank selects the same value.
+// positive doubles (bit order == value order), run entirely on the device:
+//   sel_init    targets k = clamp(ceil(p * n_def)) from the merged partials, level-0 ranges
+//               [min key, max key] per quantity (perf, gain);
+//   sel_pass    one pass over the keys: for each open range (disjoint, sorted by lo; located by
+//               binary search) either histogram the key into 8192 bins (bin 0 = {lo}, bin 1 =
+//               (lo, base), bins 2.. uniform in key from base by a shift, last bin = {hi}) or,
+//               when the range holds <= cap keys, gather it;
+//   sel_resolve one CTA per range: scan its histogram (narrow each target to its bin) or sort
+//               its gathered keys (bitonic, shared memory) and pick each target's rank;
+//   sel_plan    merge the open targets into the next level's ranges.
+// The host launches levels in batches of three and reads the state once per batch (one sync
+// for the common case).  `base` skips the empty low binades of a level-0 range whose minimum
+// is far below its maximum (gain = 0 next to gains of order 1).  With world > 1 the histograms
+// are summed and the gathered keys all-gathered between sel_pass and sel_resolve, so every
+// rank takes the same decisions.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
-#include <map>
 #include <vector>
 
 #include "common.h"
@@ -20,296 +29,431 @@
 namespace lscat {
 namespace {
 
-constexpr int kBins = 4096;
-constexpr uint32_t kCap = 4096;
-constexpr int kMaxRanges = 128;
+constexpr int kBins = 8192;           // bins per range and level
+constexpr int kMaxT = 128;            // targets: 2 x <= 64 percentiles
+constexpr int kMaxR = kMaxT;          // open ranges per level (<= open targets)
+static_assert(kMaxR <= 128, "sel_pass range search covers 128 ranges");
+constexpr int kSmemRanges = 2;        // histograms privatised in shared memory up to this many
+constexpr int kLevelsPerBatch = 3;
+constexpr uint64_t kGapKeys = 32ull << 52;  // 32 binades: keys below hi - kGapKeys share bin 1
+constexpr uint64_t kNaNKey = 0x7FF8000000000000ull;
 
 struct Range {
   uint64_t lo, hi;   // inclusive key range
-  uint32_t shift;
-  uint32_t which;    // 0 perf, 1 gain
-  uint32_t gather;   // 1 -> collect keys instead of a histogram
+  uint64_t base;     // first key of the uniform bins
+  uint64_t count;    // keys inside [lo, hi] over all ranks
+  uint32_t shift, which, gather, pad;
 };
 
-__device__ __forceinline__ int bin_of(const Range& r, uint64_t k) {
-  if (k == r.lo) return 0;
-  if (k == r.hi) return kBins - 1;
-  return 1 + (int)((k - r.lo - 1) >> r.shift);
+struct Tgt {
+  uint64_t lo, hi;   // current inclusive key range of the target
+  uint64_t k;        // 1-based rank inside [lo, hi]
+  uint64_t count;    // keys inside [lo, hi] over all ranks
+  uint64_t key;      // result when done
+  uint32_t which, done, range, pad;
+};
+
+struct SelState {
+  uint32_t nt, nr, nw0, err;  // targets, open ranges, ranges of perf (sorted first), error code
+  uint32_t open, pad[3];      // targets still open after the last plan
+  Range r[kMaxR];
+  Tgt t[kMaxT];
+};
+
+struct PctArg {
+  double p[kMaxT / 2];
+};
+
+__device__ __forceinline__ int bin_of(const Range& R, uint64_t k) {
+  if (k == R.lo) return 0;
+  if (k == R.hi) return kBins - 1;
+  if (k < R.base) return 1;
+  return 2 + (int)((k - R.base) >> R.shift);
 }
 
-// kSmem: the histograms of all ranges fit in shared memory (nr <= kSmemRanges): per-CTA
-// privatised counts, flushed once (hot bins such as perf == 1.0 would otherwise serialise on
-// global atomics).
-constexpr int kSmemRanges = 4;
+__device__ Range make_range(uint64_t lo, uint64_t hi, uint64_t count, uint32_t which, uint32_t cap) {
+  Range R;
+  R.lo = lo;
+  R.hi = hi;
+  R.count = count;
+  R.which = which;
+  R.gather = count <= cap;
+  R.pad = 0;
+  R.base = (hi > kGapKeys && hi - kGapKeys > lo + 1) ? hi - kGapKeys : lo + 1;
+  uint32_t s = 0;
+  if (R.base < hi) {
+    const uint64_t span = hi - 1 - R.base;  // largest (k - base) of a middle key
+    while ((span >> s) > (uint64_t)(kBins - 4)) s++;
+  }
+  R.shift = s;
+  return R;
+}
 
-template <bool kSmem>
-__global__ void __launch_bounds__(256) select_pass(const double* __restrict__ perf,
-                                                   const double* __restrict__ gain, uint64_t lo,
-                                                   uint64_t hi, const Range* __restrict__ ranges,
-                                                   int nr, uint32_t* __restrict__ hist,
-                                                   uint64_t* __restrict__ cand,
-                                                   uint32_t* __restrict__ cand_cnt) {
-  __shared__ Range sr[kMaxRanges];
+// Merge the open targets into disjoint ranges sorted by (which, lo).  One CTA; thread i < nt
+// owns target i.  Called by sel_init and sel_plan.
+__device__ void plan_ranges(SelState* st, uint32_t cap) {
+  __shared__ uint64_t slo[kMaxT], shi[kMaxT];
+  __shared__ uint32_t sw[kMaxT], sopen[kMaxT], sfirst[kMaxT];
+  const int i = threadIdx.x;
+  const int nt = (int)st->nt;
+  bool open = false;
+  if (i < nt) {
+    Tgt& t = st->t[i];
+    if (!t.done && t.lo == t.hi) { t.done = 1; t.key = t.lo; }
+    open = !t.done;
+    slo[i] = t.lo;
+    shi[i] = t.hi;
+    sw[i] = t.which;
+  }
+  if (i < kMaxT) sopen[i] = open;
+  __syncthreads();
+  bool first = open;
+  if (open)
+    for (int j = 0; j < i; j++)
+      if (sopen[j] && sw[j] == sw[i] && slo[j] == slo[i] && shi[j] == shi[i]) { first = false; break; }
+  if (i < kMaxT) sfirst[i] = first;
+  __syncthreads();
+  uint32_t rank = 0, nr = 0, nw0 = 0, nopen = 0;
+  for (int j = 0; j < nt; j++) {
+    nopen += sopen[j];
+    if (!sfirst[j]) continue;
+    nr++;
+    nw0 += sw[j] == 0;
+    if (open && (sw[j] < sw[i] || (sw[j] == sw[i] && slo[j] < slo[i]))) rank++;
+  }
+  if (open) {
+    Tgt& t = st->t[i];
+    t.range = rank;
+    if (first) st->r[rank] = make_range(t.lo, t.hi, t.count, t.which, cap);
+  }
+  if (i == 0) {
+    st->nr = nr;
+    st->nw0 = nw0;
+    st->open = nopen;
+  }
+}
+
+__global__ void __launch_bounds__(kMaxT) sel_init(SelState* st, const uint64_t* __restrict__ partials,
+                                                  const uint64_t* __restrict__ mm, PctArg pct, uint32_t npct,
+                                                  uint32_t cap) {
+  const int i = threadIdx.x;
+  const uint64_t n_def = partials[LSCAT_P_RATIO_DEFINED];
+  if (i == 0) { st->nt = 2 * npct; st->err = 0; }
+  if (i < (int)(2 * npct)) {
+    Tgt t{};
+    t.which = i >= (int)npct;
+    const double r = ceil(pct.p[i % npct] * (double)n_def);  // nearest rank (R-13)
+    t.k = r < 1.0 ? 1 : (r > (double)n_def ? n_def : (uint64_t)r);
+    t.lo = mm[2 * t.which];
+    t.hi = mm[2 * t.which + 1];
+    t.count = n_def;
+    t.done = n_def == 0;
+    t.key = kNaNKey;
+    st->t[i] = t;
+  }
+  __syncthreads();
+  plan_ranges(st, cap);
+}
+
+__global__ void __launch_bounds__(kMaxT) sel_plan(SelState* st, uint32_t cap) {
+  if (st->nr == 0) return;
+  plan_ranges(st, cap);
+}
+
+// One pass over this rank's values.  cand = [kMaxR counts][kMaxR x cap keys].
+// kSmem (level 0 only: one range per quantity): histograms privatised in shared memory, the two
+// single-key end bins (perf == 1.0, gain == 0, the extremes) counted with one ballot per warp.
+// Otherwise (levels >= 1: narrow ranges, few hits) global atomics aggregated per warp over
+// equal bins (match.any), so a heavily repeated value does not serialise on one address.
+template <bool kSmem, int kT>
+__global__ void __launch_bounds__(kT) sel_pass(const double* __restrict__ perf, const double* __restrict__ gain,
+                                               uint64_t lo, uint64_t hi, SelState* __restrict__ st,
+                                               uint32_t* __restrict__ hist, unsigned long long* __restrict__ cand,
+                                               uint32_t cap) {
+  __shared__ Range sr[kMaxR];
   extern __shared__ uint32_t sh_hist[];
-  for (int i = threadIdx.x; i < nr; i += blockDim.x) sr[i] = ranges[i];
+  const uint32_t nr = st->nr;
+  if (nr == 0) return;
+  const uint32_t nw0 = st->nw0, nw1 = nr - nw0;
+  if (kSmem && (nw0 > 1 || nw1 > 1)) {  // host contract: level 0 only
+    if (threadIdx.x == 0) atomicOr(&st->err, 8u);
+    return;
+  }
+  for (uint32_t i = threadIdx.x; i < nr; i += kT) sr[i] = st->r[i];
   if (kSmem)
-    for (int i = threadIdx.x; i < nr * kBins; i += blockDim.x) sh_hist[i] = 0;
-  uint32_t* H = kSmem ? sh_hist : hist;
+    for (uint32_t i = threadIdx.x; i < nr * kBins; i += kT) sh_hist[i] = 0;
   __syncthreads();
   const unsigned FULL = 0xffffffffu;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  // A warp takes 4 chunks of 32 consecutive groups per iteration and issues all 8 loads
-  // (perf, gain) before using them; whole warps iterate together (ballots, match.any).
-  constexpr int kU = 4;
   const int lane = threadIdx.x & 31;
-  const uint64_t wstride = stride * kU;
-  for (uint64_t base = lo + (blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u)) * kU; base < hi;
+  // A warp takes kU chunks of 32 consecutive groups per iteration and issues all loads before
+  // using them; arrays with no open range are not read.
+  constexpr int kU = 8;
+  const uint64_t wstride = (uint64_t)gridDim.x * kT * kU;
+  for (uint64_t base = lo + (blockIdx.x * (uint64_t)kT + (threadIdx.x & ~31u)) * kU; base < hi;
        base += wstride) {
-    double pv[kU], gv[kU];
+    double v[2][kU];
 #pragma unroll
-    for (int u = 0; u < kU; u++) {
-      const uint64_t g = base + 32 * u + lane;
-      pv[u] = g < hi ? perf[g] : __longlong_as_double(0x7FF8000000000000ll);
-      gv[u] = g < hi ? gain[g] : __longlong_as_double(0x7FF8000000000000ll);
+    for (int w = 0; w < 2; w++) {
+      const double* src = w ? gain : perf;
+      const bool rd = w ? nw1 : nw0;
+#pragma unroll
+      for (int u = 0; u < kU; u++) {
+        const uint64_t g = base + 32 * u + lane;
+        v[w][u] = (rd && g < hi) ? src[g] : __longlong_as_double((long long)kNaNKey);
+      }
     }
 #pragma unroll
     for (int u = 0; u < kU; u++) {
+#pragma unroll
       for (int w = 0; w < 2; w++) {
-        const double v = w ? gv[u] : pv[u];
-        const bool def = !isnan(v);
-        const uint64_t k = def ? (uint64_t)__double_as_longlong(v) : 0;
-        for (int r = 0; r < nr; r++) {
-          const Range& R = sr[r];
-          if (R.which != (uint32_t)w) continue;  // warp-uniform
-          const bool hit = def && k >= R.lo && k <= R.hi;
-          if (!__any_sync(FULL, hit)) continue;
-          if (R.gather) {
-            if (hit) {
-              const uint32_t idx = atomicAdd(&cand_cnt[r], 1u);
-              if (idx < kCap) cand[(size_t)r * kCap + idx] = k;
-            }
-          } else {
-            const int b = hit ? bin_of(R, k) : -1;
-            // the two single-key end bins (e.g. perf == 1.0, gain == 0) are hot: count them with
-            // one ballot per warp; other bins spread, one atomic per lane
-            const unsigned e0 = __ballot_sync(FULL, b == 0), e1 = __ballot_sync(FULL, b == kBins - 1);
-            if (lane == 0 && e0) atomicAdd(&H[(size_t)r * kBins], (uint32_t)__popc(e0));
-            if (lane == 0 && e1) atomicAdd(&H[(size_t)r * kBins + kBins - 1], (uint32_t)__popc(e1));
-            if (kSmem) {
-              if (b > 0 && b < kBins - 1) atomicAdd(&H[(size_t)r * kBins + b], 1u);
-            } else {
-              const bool mid = b > 0 && b < kBins - 1;
-              const unsigned peers = __match_any_sync(FULL, mid ? b : -1);
-              if (mid && (__ffs(peers) - 1) == lane) atomicAdd(&H[(size_t)r * kBins + b], (uint32_t)__popc(peers));
-            }
+        const uint32_t nw = w ? nw1 : nw0;
+        if (!nw) continue;  // uniform
+        const double x = v[w][u];
+        const bool def = !isnan(x);
+        const uint64_t k = def ? (uint64_t)__double_as_longlong(x) : 0;
+        const uint32_t b0 = w ? nw0 : 0;
+        uint32_t r = b0;
+        if (!kSmem) {
+          // last range with lo <= k: fixed-length branch-free search (ranges sorted by lo)
+#pragma unroll
+          for (int sh = 6; sh >= 0; sh--) {
+            if ((1u << sh) >= nw) continue;  // uniform
+            const uint32_t q = r + (1u << sh);
+            const bool ok = q < b0 + nw;
+            const uint64_t ql = sr[ok ? q : r].lo;
+            r = (ok && ql <= k) ? q : r;
           }
+        }
+        const Range& R = sr[r];
+        const bool hit = def && k >= R.lo && k <= R.hi;
+        if (!__any_sync(FULL, hit)) continue;
+        // lanes may sit in different ranges (gathered or histogrammed): no early exit before
+        // the warp collectives below
+        if (hit && R.gather) {  // <= cap keys in the whole range: rare
+          const unsigned long long idx = atomicAdd(&cand[r], 1ull);
+          if (idx < cap) cand[kMaxR + (size_t)r * cap + idx] = k;
+        }
+        const bool counted = hit && !R.gather;
+        const int b = counted ? bin_of(R, k) : -1;
+        if (kSmem) {  // R is warp-uniform here (one range per quantity)
+          const unsigned e0 = __ballot_sync(FULL, b == 0), e1 = __ballot_sync(FULL, b == kBins - 1);
+          if (lane == 0 && e0) atomicAdd(&sh_hist[r * kBins], (uint32_t)__popc(e0));
+          if (lane == 0 && e1) atomicAdd(&sh_hist[r * kBins + kBins - 1], (uint32_t)__popc(e1));
+          if (b > 0 && b < kBins - 1) atomicAdd(&sh_hist[r * kBins + b], 1u);
+        } else {
+          const int key = counted ? (int)(r * kBins) + b : -1;
+          const unsigned peers = __match_any_sync(FULL, key);
+          if (counted && (__ffs(peers) - 1) == lane) atomicAdd(&hist[key], (uint32_t)__popc(peers));
         }
       }
     }
   }
   if (kSmem) {
     __syncthreads();
-    for (int i = threadIdx.x; i < nr * kBins; i += blockDim.x)
+    for (uint32_t i = threadIdx.x; i < nr * kBins; i += kT)
       if (sh_hist[i]) atomicAdd(&hist[i], sh_hist[i]);
   }
 }
 
-struct Target {
-  int which;       // 0 perf, 1 gain
-  int out_index;
-  uint64_t lo, hi;  // current inclusive range
-  uint64_t k;       // 1-based rank inside the range
-  uint64_t count;   // keys inside the range (global)
-  bool done;
-  uint64_t key;
-};
-
-uint32_t pick_shift(uint64_t lo, uint64_t hi) {
-  if (hi - lo < 2) return 0;
-  const uint64_t span = hi - lo - 2;  // max of (k - lo - 1)
-  uint32_t s = 0;
-  while ((span >> s) > (uint64_t)(kBins - 3)) s++;
-  return s;
+// One CTA per open range.  Histogram ranges: narrow every target of the range to the bin that
+// holds its rank, then zero the histogram for the next level.  Gathered ranges: sort the keys
+// of all ranks and pick.  cand_all = world x [kMaxR counts][kMaxR x cap keys].
+__global__ void __launch_bounds__(1024) sel_resolve(SelState* st, uint32_t* __restrict__ hist,
+                                                    const unsigned long long* __restrict__ cand_all,
+                                                    unsigned long long* __restrict__ cand_own, int world,
+                                                    uint32_t cap) {
+  extern __shared__ unsigned long long sk[];
+  __shared__ unsigned long long wsum[32];
+  __shared__ unsigned long long s_total;
+  __shared__ unsigned long long s_k[kMaxT];
+  const uint32_t r = blockIdx.x;
+  if (r >= st->nr) return;
+  const Range R = st->r[r];
+  const int nt = (int)st->nt;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (!R.gather) {
+    constexpr int kPer = kBins / 1024;
+    uint32_t* h = hist + (size_t)r * kBins;
+    uint32_t c[kPer];
+    unsigned long long sum = 0;
+#pragma unroll
+    for (int j = 0; j < kPer; j++) { c[j] = h[tid * kPer + j]; sum += c[j]; }
+#pragma unroll
+    for (int j = 0; j < kPer; j++) h[tid * kPer + j] = 0;
+    unsigned long long inc = sum;  // block-wide inclusive scan of the per-thread sums
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      unsigned long long x = wsum[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      wsum[lane] = x;
+      if (lane == 31) s_total = x;
+    }
+    __syncthreads();
+    const unsigned long long ex = inc - sum + (warp ? wsum[warp - 1] : 0ull);
+    if (tid == 0 && s_total != R.count) atomicOr(&st->err, 1u);  // keys lost or double-counted
+    // snapshot the ranks before any thread rewrites a target
+    if (tid < nt) {
+      const Tgt& t = st->t[tid];
+      s_k[tid] = (t.done || t.range != r) ? 0ull : t.k;
+    }
+    __syncthreads();
+    for (int i = 0; i < nt; i++) {
+      const uint64_t k = s_k[i];
+      if (!(k && ex < k && k <= ex + sum)) continue;
+      Tgt& t = st->t[i];
+      unsigned long long cum = ex;
+      int j = 0;
+      while (cum + c[j] < k) cum += c[j++];
+      const int b = tid * kPer + j;
+      t.k = k - cum;
+      t.count = c[j];
+      if (b == 0) {
+        t.lo = t.hi = R.lo;
+      } else if (b == kBins - 1) {
+        t.lo = t.hi = R.hi;
+      } else if (b == 1) {
+        t.lo = R.lo + 1;
+        t.hi = R.base - 1;
+      } else {
+        t.lo = R.base + ((uint64_t)(b - 2) << R.shift);
+        const uint64_t top = R.base + ((uint64_t)(b - 1) << R.shift) - 1;  // may wrap only past hi
+        t.hi = (top < t.lo || top > R.hi - 1) ? R.hi - 1 : top;
+      }
+    }
+  } else {
+    const size_t stride = (size_t)kMaxR * (cap + 1);
+    unsigned long long total = 0;
+    for (int w = 0; w < world; w++) total += min(cand_all[(size_t)w * stride + r], (unsigned long long)cap);
+    if (total != R.count || total > cap) {
+      if (tid == 0) atomicOr(&st->err, 2u);
+      return;
+    }
+    uint32_t P = 1;
+    while (P < total) P <<= 1;
+    uint32_t at = 0;
+    for (int w = 0; w < world; w++) {
+      const unsigned long long* seg = cand_all + (size_t)w * stride;
+      const uint32_t c = (uint32_t)min(seg[r], (unsigned long long)cap);
+      for (uint32_t i = tid; i < c; i += blockDim.x) sk[at + i] = seg[kMaxR + (size_t)r * cap + i];
+      at += c;
+    }
+    for (uint32_t i = at + tid; i < P; i += blockDim.x) sk[i] = ~0ull;
+    __syncthreads();
+    for (uint32_t kk = 2; kk <= P; kk <<= 1)
+      for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+        for (uint32_t i = tid; i < P; i += blockDim.x) {
+          const uint32_t ixj = i ^ j;
+          if (ixj > i) {
+            const unsigned long long a = sk[i], b = sk[ixj];
+            if ((a > b) == ((i & kk) == 0)) { sk[i] = b; sk[ixj] = a; }
+          }
+        }
+        __syncthreads();
+      }
+    if (tid == 0) {
+      for (int i = 0; i < nt; i++) {
+        Tgt& t = st->t[i];
+        if (t.done || t.range != r) continue;
+        if (t.k == 0 || t.k > total) { atomicOr(&st->err, 4u); continue; }
+        t.key = sk[t.k - 1];
+        t.lo = t.hi = t.key;
+        t.done = 1;
+      }
+      cand_own[r] = 0;
+    }
+  }
 }
 
-
-lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct, uint64_t n_def,
-                                const uint64_t mm[4], double* out_perf, double* out_gain,
-                                cudaStream_t s) {
-  std::vector<Target> tg;
-  for (int w = 0; w < 2; w++) {
-    for (uint32_t i = 0; i < npct; i++) {
-      Target t{};
-      t.which = w;
-      t.out_index = (int)i;
-      double r = ceil(pct[i] * (double)n_def);  // nearest rank (R-13)
-      t.k = r < 1.0 ? 1 : (r > (double)n_def ? n_def : (uint64_t)r);
-      t.lo = mm[2 * w];
-      t.hi = mm[2 * w + 1];
-      t.count = n_def;
-      t.done = false;
-      tg.push_back(t);
-    }
-  }
+lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct, double* out_perf,
+                                double* out_gain, cudaStream_t s) {
   const ReduceState& rs = ctx->rs;
+  const int world = ctx->world;
+  const uint32_t cap = world > 1 ? 1024 : 8192;
+  const size_t cand_len = (size_t)kMaxR * (cap + 1);
   cudaError_t err;
-  Range* d_ranges = (Range*)scratch(ctx, "sel_ranges", sizeof(Range) * kMaxRanges, &err);
+  SelState* st = (SelState*)scratch(ctx, "sel_state", sizeof(SelState), &err);
   if (err) return cuda_fail(ctx, err, "stats: scratch");
-  uint32_t* d_hist = (uint32_t*)scratch(ctx, "sel_hist", (size_t)kMaxRanges * kBins * 4, &err);
+  uint32_t* hist = (uint32_t*)scratch(ctx, "sel_hist", (size_t)kMaxR * kBins * 4, &err);
   if (err) return cuda_fail(ctx, err, "stats: scratch");
-  uint64_t* d_cand = (uint64_t*)scratch(ctx, "sel_cand", (size_t)kMaxRanges * kCap * 8, &err);
+  auto* cand = (unsigned long long*)scratch(ctx, "sel_cand", cand_len * 8, &err);
   if (err) return cuda_fail(ctx, err, "stats: scratch");
-  uint32_t* d_ccnt = (uint32_t*)scratch(ctx, "sel_ccnt", kMaxRanges * 4, &err);
-  if (err) return cuda_fail(ctx, err, "stats: scratch");
-  uint64_t* d_gath = nullptr;
-  if (ctx->world > 1) {
-    d_gath = (uint64_t*)scratch(ctx, "sel_gath", (size_t)ctx->world * kMaxRanges * (kCap + 1) * 8, &err);
+  unsigned long long* cand_all = cand;
+  if (world > 1) {
+    cand_all = (unsigned long long*)scratch(ctx, "sel_cand_all", (size_t)world * cand_len * 8, &err);
     if (err) return cuda_fail(ctx, err, "stats: scratch");
   }
-  for (int level = 0; level < 16; level++) {
-    // resolve trivially known targets
-    for (auto& t : tg)
-      if (!t.done && (t.lo == t.hi)) { t.done = true; t.key = t.lo; }
-    // unique open ranges
-    std::vector<Range> ranges;
-    std::map<std::tuple<int, uint64_t, uint64_t>, int> idx;
-    std::vector<int> tr(tg.size(), -1);
-    for (size_t i = 0; i < tg.size(); i++) {
-      Target& t = tg[i];
-      if (t.done) continue;
-      auto key = std::make_tuple(t.which, t.lo, t.hi);
-      auto it = idx.find(key);
-      if (it == idx.end()) {
-        Range r{t.lo, t.hi, pick_shift(t.lo, t.hi), (uint32_t)t.which, t.count <= kCap ? 1u : 0u};
-        idx[key] = (int)ranges.size();
-        tr[i] = (int)ranges.size();
-        ranges.push_back(r);
-      } else {
-        tr[i] = it->second;
-      }
-    }
-    if (ranges.empty()) break;
-    const int nr = (int)ranges.size();
-    LSCAT_CUDA(ctx, cudaMemcpyAsync(d_ranges, ranges.data(), sizeof(Range) * nr, cudaMemcpyHostToDevice, s));
-    LSCAT_CUDA(ctx, cudaMemsetAsync(d_hist, 0, (size_t)nr * kBins * 4, s));
-    LSCAT_CUDA(ctx, cudaMemsetAsync(d_ccnt, 0, nr * 4, s));
-    const uint64_t n = rs.own_hi - rs.own_lo;
-    // grid: every resident CTA once (occupancy API), capped by the work (1024 groups per CTA
-    // iteration)
-    const uint64_t want = std::max<uint64_t>(1, (n + 1023) / 1024);
-    if (n && nr <= kSmemRanges) {
-      const size_t sm = (size_t)nr * kBins * 4;
-      LSCAT_CUDA(ctx, cudaFuncSetAttribute(select_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      int occ = 1;
-      LSCAT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, select_pass<true>, 256, sm));
-      const int g2 = (int)std::min<uint64_t>(want, (uint64_t)ctx->sm_count * std::max(occ, 1));
-      select_pass<true><<<g2, 256, sm, s>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, d_ranges, nr,
-                                              d_hist, d_cand, d_ccnt);
+  SelState* hst = (SelState*)pinned(ctx, "sel_state_h", sizeof(SelState), &err);
+  if (err) return cuda_fail(ctx, err, "stats: pinned");
+  constexpr int kT0 = 512, kT1 = 256;
+  const int pass_smem = kSmemRanges * kBins * 4, res_smem = (int)cap * 8;
+  LSCAT_CUDA(ctx, cudaFuncSetAttribute(sel_pass<true, kT0>, cudaFuncAttributeMaxDynamicSharedMemorySize, pass_smem));
+  LSCAT_CUDA(ctx, cudaFuncSetAttribute(sel_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, res_smem));
+  // grids: every resident CTA once (occupancy API), capped by the work (kU x 32 groups per warp)
+  const uint64_t n = rs.own_hi - rs.own_lo;
+  int occ0 = 1, occ1 = 1;
+  LSCAT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ0, sel_pass<true, kT0>, kT0, pass_smem));
+  LSCAT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, sel_pass<false, kT1>, kT1, 0));
+  const int grid0 = (int)std::min<uint64_t>(std::max<uint64_t>(1, (n + kT0 * 8 - 1) / (kT0 * 8)),
+                                             (uint64_t)ctx->sm_count * std::max(occ0, 1));
+  const int grid1 = (int)std::min<uint64_t>(std::max<uint64_t>(1, (n + kT1 * 8 - 1) / (kT1 * 8)),
+                                             (uint64_t)ctx->sm_count * std::max(occ1, 1));
+  PctArg pa{};
+  for (uint32_t i = 0; i < npct; i++) pa.p[i] = pct[i];
+  LSCAT_CUDA(ctx, cudaMemsetAsync(hist, 0, (size_t)kMaxR * kBins * 4, s));
+  LSCAT_CUDA(ctx, cudaMemsetAsync(cand, 0, (size_t)kMaxR * 8, s));
+  sel_init<<<1, kMaxT, 0, s>>>(st, rs.partials, rs.minmax, pa, npct, cap);
+  ctx->launches++;
+  LSCAT_CUDA(ctx, cudaGetLastError());
+  for (int batch = 0;; batch++) {
+    if (batch == 8) return fail(ctx, LSCAT_ERR_STATE, "stats: percentile selection did not converge");
+    for (int level = 0; level < kLevelsPerBatch; level++) {
+      if (batch == 0 && level == 0)
+        sel_pass<true, kT0><<<grid0, kT0, pass_smem, s>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, st, hist, cand, cap);
+      else
+        sel_pass<false, kT1><<<grid1, kT1, 0, s>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, st, hist, cand, cap);
       ctx->launches++;
-    } else if (n) {
-      int occ = 1;
-      LSCAT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, select_pass<false>, 256, 0));
-      const int g2 = (int)std::min<uint64_t>(want, (uint64_t)ctx->sm_count * std::max(occ, 1));
-      select_pass<false><<<g2, 256, 0, s>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, d_ranges, nr,
-                                               d_hist, d_cand, d_ccnt);
+      LSCAT_CUDA(ctx, cudaGetLastError());
+      if (world > 1) {
+        lscat_status ns;
+        if ((ns = ctx->comm->allreduce(ctx, {{hist, (size_t)kMaxR * kBins, DT::U32, Op::Sum}}, s))) return ns;
+        if ((ns = ctx->comm->allgather(ctx, cand, cand_all, cand_len, DT::U64, s))) return ns;
+      }
+      sel_resolve<<<kMaxR, 1024, res_smem, s>>>(st, hist, cand_all, cand, world, cap);
       ctx->launches++;
-    }
-    LSCAT_CUDA(ctx, cudaGetLastError());
-    std::vector<uint32_t> hist((size_t)nr * kBins);
-    std::vector<uint32_t> ccnt(nr);
-    std::vector<std::vector<uint64_t>> cands(nr);
-    if (ctx->world > 1) {
-      lscat_status ns;
-      if ((ns = ctx->comm->allreduce(ctx, {{d_hist, (size_t)nr * kBins, DT::U32, Op::Sum}}, s))) return ns;
-      // candidates: [count, keys...] per range, all-gathered
-      uint64_t* d_pack = (uint64_t*)scratch(ctx, "sel_pack", (size_t)kMaxRanges * (kCap + 1) * 8, &err);
-      if (err) return cuda_fail(ctx, err, "stats: scratch");
-      std::vector<uint32_t> lc(nr);
-      LSCAT_CUDA(ctx, cudaMemcpyAsync(lc.data(), d_ccnt, nr * 4, cudaMemcpyDeviceToHost, s));
-      LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
-      for (int r = 0; r < nr; r++) {
-        uint64_t c = std::min<uint64_t>(lc[r], kCap);
-        LSCAT_CUDA(ctx, cudaMemcpyAsync(d_pack + (size_t)r * (kCap + 1), &c, 8, cudaMemcpyHostToDevice, s));
-        if (c) LSCAT_CUDA(ctx, cudaMemcpyAsync(d_pack + (size_t)r * (kCap + 1) + 1, d_cand + (size_t)r * kCap, c * 8, cudaMemcpyDeviceToDevice, s));
+      LSCAT_CUDA(ctx, cudaGetLastError());
+      sel_plan<<<1, kMaxT, 0, s>>>(st, cap);
+      ctx->launches++;
+      LSCAT_CUDA(ctx, cudaGetLastError());
+      if (getenv("LSCAT_SEL_DEBUG")) {
+        LSCAT_CUDA(ctx, cudaMemcpyAsync(hst, st, sizeof(SelState), cudaMemcpyDeviceToHost, s));
         LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
-      }
-      if ((ns = ctx->comm->allgather(ctx, d_pack, d_gath, (size_t)nr * (kCap + 1), DT::U64, s))) return ns;
-      std::vector<uint64_t> g((size_t)ctx->world * nr * (kCap + 1));
-      LSCAT_CUDA(ctx, cudaMemcpyAsync(g.data(), d_gath, g.size() * 8, cudaMemcpyDeviceToHost, s));
-      LSCAT_CUDA(ctx, cudaMemcpyAsync(hist.data(), d_hist, hist.size() * 4, cudaMemcpyDeviceToHost, s));
-      LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
-      for (int w = 0; w < ctx->world; w++)
-        for (int r = 0; r < nr; r++) {
-          const uint64_t* pk = g.data() + ((size_t)w * nr + r) * (kCap + 1);
-          cands[r].insert(cands[r].end(), pk + 1, pk + 1 + pk[0]);
-        }
-    } else {
-      // one D2H of histograms + counts, then one batch of candidate copies: <= 2 host syncs
-      uint32_t* h = (uint32_t*)pinned(ctx, "sel_h", (size_t)nr * kBins * 4 + kMaxRanges * 4, &err);
-      if (err) return cuda_fail(ctx, err, "stats: pinned");
-      uint32_t* hc = h + (size_t)nr * kBins;
-      LSCAT_CUDA(ctx, cudaMemcpyAsync(h, d_hist, (size_t)nr * kBins * 4, cudaMemcpyDeviceToHost, s));
-      LSCAT_CUDA(ctx, cudaMemcpyAsync(hc, d_ccnt, nr * 4, cudaMemcpyDeviceToHost, s));
-      LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
-      memcpy(hist.data(), h, (size_t)nr * kBins * 4);
-      size_t ncand = 0;
-      for (int r = 0; r < nr; r++) ccnt[r] = ranges[r].gather ? std::min(hc[r], kCap) : 0;
-      for (int r = 0; r < nr; r++) ncand += ccnt[r];
-      if (ncand) {
-        uint64_t* hk = (uint64_t*)pinned(ctx, "sel_k", ncand * 8, &err);
-        if (err) return cuda_fail(ctx, err, "stats: pinned");
-        size_t at = 0;
-        for (int r = 0; r < nr; r++) {
-          if (ccnt[r]) LSCAT_CUDA(ctx, cudaMemcpyAsync(hk + at, d_cand + (size_t)r * kCap, ccnt[r] * 8, cudaMemcpyDeviceToHost, s));
-          at += ccnt[r];
-        }
-        LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
-        at = 0;
-        for (int r = 0; r < nr; r++) {
-          cands[r].assign(hk + at, hk + at + ccnt[r]);
-          at += ccnt[r];
-        }
+        fprintf(stderr, "sel batch %d level %d: nt %u nr %u nw0 %u open %u err %u\n", batch, level, hst->nt,
+                hst->nr, hst->nw0, hst->open, hst->err);
+        for (uint32_t i = 0; i < hst->nr; i++)
+          fprintf(stderr, "  range %u: which %u lo %016llx hi %016llx base %016llx count %llu shift %u gather %u\n", i,
+                  hst->r[i].which, (unsigned long long)hst->r[i].lo, (unsigned long long)hst->r[i].hi,
+                  (unsigned long long)hst->r[i].base, (unsigned long long)hst->r[i].count, hst->r[i].shift,
+                  hst->r[i].gather);
       }
     }
-    for (int r = 0; r < nr; r++)
-      if (ranges[r].gather) std::sort(cands[r].begin(), cands[r].end());
-    for (size_t i = 0; i < tg.size(); i++) {
-      Target& t = tg[i];
-      if (t.done) continue;
-      const int r = tr[i];
-      const Range& R = ranges[r];
-      if (R.gather) {
-        if (cands[r].size() != t.count || t.k == 0 || t.k > t.count)
-          return fail(ctx, LSCAT_ERR_STATE, "stats: percentile candidates %zu != expected %llu",
-                      cands[r].size(), (unsigned long long)t.count);
-        t.key = cands[r][t.k - 1];
-        t.done = true;
-        continue;
-      }
-      const uint32_t* h = hist.data() + (size_t)r * kBins;
-      uint64_t cum = 0;
-      int b = 0;
-      for (; b < kBins; b++) {
-        if (cum + h[b] >= t.k) break;
-        cum += h[b];
-      }
-      if (b == kBins) return fail(ctx, LSCAT_ERR_STATE, "stats: percentile histogram lost keys");
-      t.k -= cum;
-      t.count = h[b];
-      if (b == 0) { t.done = true; t.key = R.lo; continue; }
-      if (b == kBins - 1) { t.done = true; t.key = R.hi; continue; }
-      const uint64_t nlo = R.lo + 1 + ((uint64_t)(b - 1) << R.shift);
-      uint64_t nhi = R.lo + ((uint64_t)b << R.shift);
-      if (nhi > R.hi - 1) nhi = R.hi - 1;
-      t.lo = nlo;
-      t.hi = nhi;
-    }
+    LSCAT_CUDA(ctx, cudaMemcpyAsync(hst, st, sizeof(SelState), cudaMemcpyDeviceToHost, s));
+    LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
+    if (hst->err) return fail(ctx, LSCAT_ERR_STATE, "stats: percentile selection lost keys (code %u)", hst->err);
+    if (!hst->open) break;
   }
-  for (auto& t : tg) {
-    if (!t.done) return fail(ctx, LSCAT_ERR_STATE, "stats: percentile selection did not converge");
+  for (uint32_t i = 0; i < 2 * npct; i++) {
+    const Tgt& t = hst->t[i];
     double v;
     memcpy(&v, &t.key, 8);
-    (t.which ? out_gain : out_perf)[t.out_index] = v;
+    (t.which ? out_gain : out_perf)[i % npct] = v;
   }
   return LSCAT_OK;
 }
@@ -338,11 +482,19 @@ extern "C" lscat_status lscat_stats(lscat_ctx* ctx, const lscat_reduce_opts* o, 
   LSCAT_CUDA(ctx, cudaSetDevice(ctx->device));
   const size_t nb = o->bins_per_unit, ng = (size_t)o->gain_cap * nb, nbb = (size_t)o->n_matrices * o->n_blocks;
   const size_t plen = LSCAT_P_NCOUNTERS + (nb + 1) + (ng + 1) + nbb * (o->block_profile ? 3 : 1);
-  std::vector<uint64_t> P(plen);
-  uint64_t mm[4];
-  LSCAT_CUDA(ctx, cudaMemcpyAsync(P.data(), rs.partials, plen * 8, cudaMemcpyDeviceToHost, s));
-  LSCAT_CUDA(ctx, cudaMemcpyAsync(mm, rs.minmax, sizeof mm, cudaMemcpyDeviceToHost, s));
-  LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
+  cudaError_t err;
+  uint64_t* hP = (uint64_t*)pinned(ctx, "stats_partials", plen * 8, &err);
+  if (err) return cuda_fail(ctx, err, "stats: pinned");
+  LSCAT_CUDA(ctx, cudaMemcpyAsync(hP, rs.partials, plen * 8, cudaMemcpyDeviceToHost, s));
+  if (out->n_percentiles) {
+    // a8 on the device; its first host sync also completes the partials copy above
+    lscat_status st = select_percentiles(ctx, out->percentiles, out->n_percentiles, out->pct_perf,
+                                         out->pct_gain, s);
+    if (st) return st;
+  } else {
+    LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
+  }
+  std::vector<uint64_t> P(hP, hP + plen);
   const uint64_t* C = P.data();
   out->n_rows = C[LSCAT_P_ROWS]; out->n_ok = C[LSCAT_P_OK]; out->n_nan = C[LSCAT_P_NAN];
   out->n_invalid = C[LSCAT_P_INVALID]; out->n_groups = C[LSCAT_P_GROUPS];
@@ -375,15 +527,6 @@ extern "C" lscat_status lscat_stats(lscat_ctx* ctx, const lscat_reduce_opts* o, 
     for (size_t i = 0; i < nbb; i++) {
       if (out->profile_count) out->profile_count[i] = pc[i];
       if (out->profile_mean) out->profile_mean[i] = pc[i] ? ((double)ps[i] * 0x1p-31) / (double)pc[i] : NAN;
-    }
-  }
-  if (out->n_percentiles) {
-    if (out->n_ratio_defined == 0) {
-      for (uint32_t i = 0; i < out->n_percentiles; i++) out->pct_perf[i] = out->pct_gain[i] = NAN;
-    } else {
-      lscat_status st = select_percentiles(ctx, out->percentiles, out->n_percentiles,
-                                           out->n_ratio_defined, mm, out->pct_perf, out->pct_gain, s);
-      if (st) return st;
     }
   }
   return LSCAT_OK;

@@ -269,3 +269,24 @@ def test_uniform_groups_unsorted_rows(ell):
     assert (out["best_block_id"].cpu().numpy().view(np.uint16) == ref.best_block).all()
     assert (out["flags"].cpu().numpy().view(np.uint32) == ref.flags).all()
     assert st["pct_perf"] == ref.percentiles["perf"]
+
+
+def test_percentiles_wide_key_span_many_targets():
+    """a8 with 64 percentiles over perf/gain spanning > 200 binades (gain from 2^-23 to 1e60,
+    perf down to 1e-60), exact ties at perf == 1 / gain == 0: exercises the level-0 range whose
+    low binades share one bin, multi-level refinement and many targets per range."""
+    rng = np.random.default_rng(7)
+    G = 200_000
+    b = rng.uniform(0.5, 2.0, G).astype(np.float32)
+    kind = rng.integers(0, 5, G)
+    b = np.where(kind == 1, np.float32(1e-30), b).astype(np.float32)
+    t = np.where(kind == 0, np.nextafter(b, np.float32(np.inf)),
+                 np.where(kind == 1, np.float32(1e30),
+                          np.where(kind == 2, b, b * rng.uniform(1.0, 3.0, G).astype(np.float32))))
+    rt = np.empty(2 * G, np.float32)
+    rt[0::2], rt[1::2] = b, t.astype(np.float32)
+    tab = dict(runtime_ms=rt, block_id=np.tile(np.array([0, 1], np.uint16), G),
+               group_offset=np.arange(0, 2 * G + 1, 2, dtype=np.int64),
+               group_matrix=np.zeros(G, np.uint32))
+    st = _compare(tab, L=2, M=1, ell=1, pcts=list(np.linspace(0.0, 1.0, 64)))
+    assert st["pct_gain"][-1] > 1e59 and st["pct_perf"][0] < 1e-59
