@@ -37,11 +37,15 @@ constexpr int kSmemRanges = 2;        // histograms privatised in shared memory 
 constexpr int kLevelsPerBatch = 3;
 constexpr uint64_t kGapKeys = 32ull << 52;  // 32 binades: keys below hi - kGapKeys share bin 1
 constexpr uint64_t kNaNKey = 0x7FF8000000000000ull;
+// Once the open ranges hold at most this many keys per quantity (and at most half of them), one
+// pass copies them out and later levels read the copies instead of the full perf/gain arrays.
+constexpr uint64_t kCompactCap = 1ull << 22;
 
 struct Range {
   uint64_t lo, hi;   // inclusive key range
   uint64_t base;     // first key of the uniform bins
   uint64_t count;    // keys inside [lo, hi] over all ranks
+  uint64_t span, g;  // hi - lo, base - lo (the pass works on d = k - lo)
   uint32_t shift, which, gather, pad;
 };
 
@@ -55,7 +59,12 @@ struct Tgt {
 
 struct SelState {
   uint32_t nt, nr, nw0, err;  // targets, open ranges, ranges of perf (sorted first), error code
-  uint32_t open, pad[3];      // targets still open after the last plan
+  uint32_t open;              // targets still open after the last plan
+  uint32_t src;               // 0: passes read perf/gain; 1: the compacted keys
+  uint32_t compact;           // 1: the next pass also copies the keys it counts (src 0 only)
+  uint32_t pad;
+  unsigned long long nc[2];   // compacted keys per quantity
+  uint64_t n_def;
   Range r[kMaxR];
   Tgt t[kMaxT];
 };
@@ -64,11 +73,12 @@ struct PctArg {
   double p[kMaxT / 2];
 };
 
-__device__ __forceinline__ int bin_of(const Range& R, uint64_t k) {
-  if (k == R.lo) return 0;
-  if (k == R.hi) return kBins - 1;
-  if (k < R.base) return 1;
-  return 2 + (int)((k - R.base) >> R.shift);
+// bin of a key inside the range, from d = k - lo (0 <= d <= span)
+__device__ __forceinline__ int bin_of_d(const Range& R, uint64_t d) {
+  if (d == 0) return 0;
+  if (d == R.span) return kBins - 1;
+  if (d < R.g) return 1;
+  return 2 + (int)((d - R.g) >> R.shift);
 }
 
 __device__ Range make_range(uint64_t lo, uint64_t hi, uint64_t count, uint32_t which, uint32_t cap) {
@@ -86,8 +96,12 @@ __device__ Range make_range(uint64_t lo, uint64_t hi, uint64_t count, uint32_t w
     while ((span >> s) > (uint64_t)(kBins - 4)) s++;
   }
   R.shift = s;
+  R.span = hi - lo;
+  R.g = R.base - lo;
   return R;
 }
+
+__device__ __forceinline__ uint64_t t_count(const SelState* st, int i) { return st->t[i].count; }
 
 // Merge the open targets into disjoint ranges sorted by (which, lo).  One CTA; thread i < nt
 // owns target i.  Called by sel_init and sel_plan.
@@ -126,10 +140,23 @@ __device__ void plan_ranges(SelState* st, uint32_t cap) {
     t.range = rank;
     if (first) st->r[rank] = make_range(t.lo, t.hi, t.count, t.which, cap);
   }
+  __shared__ unsigned long long s_keys[2];
+  if (i < 2) s_keys[i] = 0;
+  __syncthreads();
+  if (open && first && !st->r[rank].gather) atomicAdd(&s_keys[st->r[rank].which], (unsigned long long)t_count(st, i));
+  __syncthreads();
   if (i == 0) {
     st->nr = nr;
     st->nw0 = nw0;
     st->open = nopen;
+    if (st->compact) {  // the pass that just ran copied the keys: read the copies from now on
+      st->src = 1;
+      st->compact = 0;
+    } else if (st->src == 0 && nr > 0 && s_keys[0] <= kCompactCap && s_keys[1] <= kCompactCap &&
+               2 * (s_keys[0] + s_keys[1]) <= st->n_def) {
+      st->compact = 1;
+      st->nc[0] = st->nc[1] = 0;
+    }
   }
 }
 
@@ -138,7 +165,13 @@ __global__ void __launch_bounds__(kMaxT) sel_init(SelState* st, const uint64_t* 
                                                   uint32_t cap) {
   const int i = threadIdx.x;
   const uint64_t n_def = partials[LSCAT_P_RATIO_DEFINED];
-  if (i == 0) { st->nt = 2 * npct; st->err = 0; }
+  if (i == 0) {
+    st->nt = 2 * npct;
+    st->err = 0;
+    st->src = 0;
+    st->compact = 0;
+    st->n_def = n_def;
+  }
   if (i < (int)(2 * npct)) {
     Tgt t{};
     t.which = i >= (int)npct;
@@ -160,16 +193,50 @@ __global__ void __launch_bounds__(kMaxT) sel_plan(SelState* st, uint32_t cap) {
   plan_ranges(st, cap);
 }
 
-// One pass over this rank's values.  cand = [kMaxR counts][kMaxR x cap keys].
+// One pass over this rank's values (src 0: perf/gain[lo, hi); src 1: the compacted keys).
+// cand = [kMaxR counts][kMaxR x cap keys]; cbuf = [2][kCompactCap] compacted keys.
 // kSmem (level 0 only: one range per quantity): histograms privatised in shared memory, the two
 // single-key end bins (perf == 1.0, gain == 0, the extremes) counted with one ballot per warp.
 // Otherwise (levels >= 1: narrow ranges, few hits) global atomics aggregated per warp over
 // equal bins (match.any), so a heavily repeated value does not serialise on one address.
+// Keys are the raw bit patterns: NaN (undefined group) patterns exceed every finite range.
+// largest power of two < n (0 for n <= 1): the first step of the range search
+__device__ __forceinline__ uint32_t top_step(uint32_t n) { return n > 1 ? 1u << (31 - __clz(n - 1)) : 0u; }
+
+// Levels >= 1, a warp with at least one key inside an open range (rare): gather, histogram
+// (match.any-aggregated global atomics) and compaction.  Out of line so the unrolled scan loop
+// of sel_pass stays small enough for the instruction cache.  Called by all 32 lanes.
+__device__ __noinline__ void hit_slow(const Range* sr, uint32_t r, uint64_t k, uint64_t d, bool hit, int w,
+                                      int lane, uint32_t* __restrict__ hist,
+                                      unsigned long long* __restrict__ cand, uint32_t cap, bool compact,
+                                      SelState* __restrict__ st, double* __restrict__ cbuf) {
+  const unsigned FULL = 0xffffffffu;
+  const Range& R = sr[r];
+  // lanes may sit in different ranges (gathered or histogrammed): no early exit before the
+  // warp collectives below
+  if (hit && R.gather) {  // <= cap keys in the whole range
+    const unsigned long long idx = atomicAdd(&cand[r], 1ull);
+    if (idx < cap) cand[kMaxR + (size_t)r * cap + idx] = k;
+  }
+  const bool counted = hit && !R.gather;
+  const int key = counted ? (int)(r * kBins) + bin_of_d(R, d) : -1;
+  const unsigned peers = __match_any_sync(FULL, key);
+  if (counted && (__ffs(peers) - 1) == lane) atomicAdd(&hist[key], (uint32_t)__popc(peers));
+  if (compact) {  // copy the counted keys out for the next levels (warp-aggregated)
+    const unsigned m = __ballot_sync(FULL, counted);
+    unsigned long long at = 0;
+    if (m && lane == 0) at = atomicAdd(&st->nc[w], (unsigned long long)__popc(m));
+    at = __shfl_sync(FULL, at, 0);
+    const unsigned long long pos = at + __popc(m & ((1u << lane) - 1u));
+    if (counted && pos < kCompactCap) reinterpret_cast<uint64_t*>(cbuf)[(size_t)w * kCompactCap + pos] = k;
+  }
+}
+
 template <bool kSmem, int kT>
-__global__ void __launch_bounds__(kT) sel_pass(const double* __restrict__ perf, const double* __restrict__ gain,
+__global__ void __launch_bounds__(kT, kSmem ? 2 : 4) sel_pass(const double* __restrict__ perf, const double* __restrict__ gain,
                                                uint64_t lo, uint64_t hi, SelState* __restrict__ st,
                                                uint32_t* __restrict__ hist, unsigned long long* __restrict__ cand,
-                                               uint32_t cap) {
+                                               uint32_t cap, double* __restrict__ cbuf) {
   __shared__ Range sr[kMaxR];
   extern __shared__ uint32_t sh_hist[];
   const uint32_t nr = st->nr;
@@ -179,28 +246,44 @@ __global__ void __launch_bounds__(kT) sel_pass(const double* __restrict__ perf, 
     if (threadIdx.x == 0) atomicOr(&st->err, 8u);
     return;
   }
+  const bool compact = !kSmem && st->compact;
+  uint64_t hi0 = hi, hi1 = hi;
+  if (!kSmem && st->src) {
+    perf = cbuf;
+    gain = cbuf + kCompactCap;
+    lo = 0;
+    hi0 = st->nc[0];
+    hi1 = st->nc[1];
+  }
   for (uint32_t i = threadIdx.x; i < nr; i += kT) sr[i] = st->r[i];
   if (kSmem)
     for (uint32_t i = threadIdx.x; i < nr * kBins; i += kT) sh_hist[i] = 0;
   __syncthreads();
+  uint32_t c0[2] = {0, 0}, cL[2] = {0, 0};  // level 0: end-bin counts per thread
+  Range sr0[2];  // level 0: the range of each quantity, kept in registers
+  if (kSmem) {
+    sr0[0] = sr[0];
+    sr0[1] = sr[nw0 ? nw0 : 0];
+  }
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
-  // A warp takes kU chunks of 32 consecutive groups per iteration and issues all loads before
+  const uint64_t end = hi0 > hi1 ? hi0 : hi1;
+  // A warp takes kU chunks of 32 consecutive keys per iteration and issues all loads before
   // using them; arrays with no open range are not read.
   constexpr int kU = 8;
   const uint64_t wstride = (uint64_t)gridDim.x * kT * kU;
-  for (uint64_t base = lo + (blockIdx.x * (uint64_t)kT + (threadIdx.x & ~31u)) * kU; base < hi;
+  for (uint64_t base = lo + (blockIdx.x * (uint64_t)kT + (threadIdx.x & ~31u)) * kU; base < end;
        base += wstride) {
-    double v[2][kU];
+    uint64_t v[2][kU];
 #pragma unroll
     for (int w = 0; w < 2; w++) {
-      const double* src = w ? gain : perf;
-      const bool rd = w ? nw1 : nw0;
+      const uint64_t* src = reinterpret_cast<const uint64_t*>(w ? gain : perf) + base + lane;
+      const uint64_t hw = (w ? hi1 : hi0) - base;  // keys left in this array (if > 0)
+      const bool rd = (w ? nw1 : nw0) && (w ? hi1 : hi0) > base;
+      const bool full = rd && hw >= 32 * kU;
 #pragma unroll
-      for (int u = 0; u < kU; u++) {
-        const uint64_t g = base + 32 * u + lane;
-        v[w][u] = (rd && g < hi) ? src[g] : __longlong_as_double((long long)kNaNKey);
-      }
+      for (int u = 0; u < kU; u++)
+        v[w][u] = (full || (rd && (uint64_t)(32 * u + lane) < hw)) ? __ldg(src + 32 * u) : kNaNKey;
     }
 #pragma unroll
     for (int u = 0; u < kU; u++) {
@@ -208,47 +291,56 @@ __global__ void __launch_bounds__(kT) sel_pass(const double* __restrict__ perf, 
       for (int w = 0; w < 2; w++) {
         const uint32_t nw = w ? nw1 : nw0;
         if (!nw) continue;  // uniform
-        const double x = v[w][u];
-        const bool def = !isnan(x);
-        const uint64_t k = def ? (uint64_t)__double_as_longlong(x) : 0;
+        const uint64_t k = v[w][u];
         const uint32_t b0 = w ? nw0 : 0;
-        uint32_t r = b0;
-        if (!kSmem) {
-          // last range with lo <= k: fixed-length branch-free search (ranges sorted by lo)
-#pragma unroll
-          for (int sh = 6; sh >= 0; sh--) {
-            if ((1u << sh) >= nw) continue;  // uniform
-            const uint32_t q = r + (1u << sh);
-            const bool ok = q < b0 + nw;
-            const uint64_t ql = sr[ok ? q : r].lo;
-            r = (ok && ql <= k) ? q : r;
+        if (kSmem) {
+          // level 0: one range per quantity (registers); end bins counted per thread
+          const Range& R = sr0[w];
+          const uint64_t d = k - R.lo;
+          const bool hit = d <= R.span;  // k < lo wraps d past every span (< 2^63)
+          if (R.gather) {                // uniform
+            if (hit) {
+              const unsigned long long idx = atomicAdd(&cand[b0], 1ull);
+              if (idx < cap) cand[kMaxR + (size_t)b0 * cap + idx] = k;
+            }
+            continue;
           }
+          int b = 2 + (int)((d - R.g) >> R.shift);
+          b = d < R.g ? 1 : b;
+          const bool is0 = hit && d == 0, isL = hit && d == R.span;
+          c0[w] += is0;
+          cL[w] += isL;
+          if (hit && !is0 && !isL) atomicAdd(&sh_hist[b0 * kBins + b], 1u);
+          continue;
+        }
+        // last range with lo <= k (ranges sorted by lo): binary lifting with a warp-uniform
+        // trip count, not unrolled (keeps the 16 unrolled copies small)
+        uint32_t r = b0;
+#pragma unroll 1
+        for (uint32_t h = top_step(nw); h; h >>= 1) {
+          const uint32_t q = r + h;
+          const bool ok = q < b0 + nw;
+          const uint64_t ql = sr[ok ? q : r].lo;
+          r = (ok && ql <= k) ? q : r;
         }
         const Range& R = sr[r];
-        const bool hit = def && k >= R.lo && k <= R.hi;
+        const uint64_t d = k - R.lo;
+        const bool hit = d <= R.span;  // k < lo wraps d past every span (< 2^63)
         if (!__any_sync(FULL, hit)) continue;
-        // lanes may sit in different ranges (gathered or histogrammed): no early exit before
-        // the warp collectives below
-        if (hit && R.gather) {  // <= cap keys in the whole range: rare
-          const unsigned long long idx = atomicAdd(&cand[r], 1ull);
-          if (idx < cap) cand[kMaxR + (size_t)r * cap + idx] = k;
-        }
-        const bool counted = hit && !R.gather;
-        const int b = counted ? bin_of(R, k) : -1;
-        if (kSmem) {  // R is warp-uniform here (one range per quantity)
-          const unsigned e0 = __ballot_sync(FULL, b == 0), e1 = __ballot_sync(FULL, b == kBins - 1);
-          if (lane == 0 && e0) atomicAdd(&sh_hist[r * kBins], (uint32_t)__popc(e0));
-          if (lane == 0 && e1) atomicAdd(&sh_hist[r * kBins + kBins - 1], (uint32_t)__popc(e1));
-          if (b > 0 && b < kBins - 1) atomicAdd(&sh_hist[r * kBins + b], 1u);
-        } else {
-          const int key = counted ? (int)(r * kBins) + b : -1;
-          const unsigned peers = __match_any_sync(FULL, key);
-          if (counted && (__ffs(peers) - 1) == lane) atomicAdd(&hist[key], (uint32_t)__popc(peers));
-        }
+        hit_slow(sr, r, k, d, hit, w, lane, hist, cand, cap, compact, st, cbuf);
       }
     }
   }
   if (kSmem) {
+#pragma unroll
+    for (int w = 0; w < 2; w++) {
+      const uint32_t a = __reduce_add_sync(FULL, c0[w]), z = __reduce_add_sync(FULL, cL[w]);
+      const uint32_t b0 = w ? nw0 : 0;
+      if (lane == 0 && (w ? nw1 : nw0)) {
+        if (a) atomicAdd(&sh_hist[b0 * kBins], a);
+        if (z) atomicAdd(&sh_hist[b0 * kBins + kBins - 1], z);
+      }
+    }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < nr * kBins; i += kT)
       if (sh_hist[i]) atomicAdd(&hist[i], sh_hist[i]);
@@ -390,6 +482,8 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
     cand_all = (unsigned long long*)scratch(ctx, "sel_cand_all", (size_t)world * cand_len * 8, &err);
     if (err) return cuda_fail(ctx, err, "stats: scratch");
   }
+  double* cbuf = (double*)scratch(ctx, "sel_cbuf", 2 * kCompactCap * 8, &err);
+  if (err) return cuda_fail(ctx, err, "stats: scratch");
   SelState* hst = (SelState*)pinned(ctx, "sel_state_h", sizeof(SelState), &err);
   if (err) return cuda_fail(ctx, err, "stats: pinned");
   constexpr int kT0 = 512, kT1 = 256;
@@ -416,9 +510,9 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
     if (batch == 8) return fail(ctx, LSCAT_ERR_STATE, "stats: percentile selection did not converge");
     for (int level = 0; level < kLevelsPerBatch; level++) {
       if (batch == 0 && level == 0)
-        sel_pass<true, kT0><<<grid0, kT0, pass_smem, s>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, st, hist, cand, cap);
+        sel_pass<true, kT0><<<grid0, kT0, pass_smem, s>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, st, hist, cand, cap, cbuf);
       else
-        sel_pass<false, kT1><<<grid1, kT1, 0, s>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, st, hist, cand, cap);
+        sel_pass<false, kT1><<<grid1, kT1, 0, s>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, st, hist, cand, cap, cbuf);
       ctx->launches++;
       LSCAT_CUDA(ctx, cudaGetLastError());
       if (world > 1) {
@@ -435,8 +529,9 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
       if (getenv("LSCAT_SEL_DEBUG")) {
         LSCAT_CUDA(ctx, cudaMemcpyAsync(hst, st, sizeof(SelState), cudaMemcpyDeviceToHost, s));
         LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
-        fprintf(stderr, "sel batch %d level %d: nt %u nr %u nw0 %u open %u err %u\n", batch, level, hst->nt,
-                hst->nr, hst->nw0, hst->open, hst->err);
+        fprintf(stderr, "sel batch %d level %d: nt %u nr %u nw0 %u open %u err %u src %u compact %u nc %llu %llu\n",
+                batch, level, hst->nt, hst->nr, hst->nw0, hst->open, hst->err, hst->src, hst->compact,
+                hst->nc[0], hst->nc[1]);
         for (uint32_t i = 0; i < hst->nr; i++)
           fprintf(stderr, "  range %u: which %u lo %016llx hi %016llx base %016llx count %llu shift %u gather %u\n", i,
                   hst->r[i].which, (unsigned long long)hst->r[i].lo, (unsigned long long)hst->r[i].hi,

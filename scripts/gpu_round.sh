@@ -14,6 +14,7 @@ for job in "$@"; do
     ncu_euclid) timeout 600 ncu --set full --clock-control none --import-source on -k regex:row_kernel -c 2 -o gpurun_out/prof_euclid -f python scripts/profile_kernels.py euclid8192 512 > gpurun_out/ncu_euclid.log 2>&1; echo "ncu_euclid rc=$?" ;;
     ncu_gemm) timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_kernel -c 1 -o gpurun_out/prof_gemm -f python scripts/profile_kernels.py gemm8192 256 > gpurun_out/ncu_gemm.log 2>&1; echo "ncu_gemm rc=$?" ;;
     launches) timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --policy tiny --steps 1 --warmup 0 --no-e2e --no-secondary --no-cpu > gpurun_out/launches_bench.log 2>&1; echo "launches rc=$?" ;;
+    ncu_select) timeout 900 ncu --set full --clock-control none --import-source on -k regex:sel_pass -c 3 -o gpurun_out/prof_select -f python scripts/profile_kernels.py reduce 1000000000 > gpurun_out/ncu_select.log 2>&1; echo "ncu_select rc=$?" ;;
     stats_list) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/stats_list.csv python scripts/profile_kernels.py reduce 1000000000 > gpurun_out/ncu_stats.log 2>&1; echo "stats_list rc=$?" ;;
     suite) timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/suite8192.csv python scripts/profile_kernels.py suite8192 > gpurun_out/ncu_suite.log 2>&1; echo "suite rc=$?" ;;
   esac

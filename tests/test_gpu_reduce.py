@@ -290,3 +290,22 @@ def test_percentiles_wide_key_span_many_targets():
                group_matrix=np.zeros(G, np.uint32))
     st = _compare(tab, L=2, M=1, ell=1, pcts=list(np.linspace(0.0, 1.0, 64)))
     assert st["pct_gain"][-1] > 1e59 and st["pct_perf"][0] < 1e-59
+
+
+def test_percentiles_dense_bin_compaction():
+    """a8 where one level-0 bin holds ~35 % of the ratio-defined groups as distinct keys
+    (perf = 1 - j * 2^-20): the level-1 range is too large to gather, so the device copies the
+    keys of the open ranges out and refines on the copies (percentile select)."""
+    rng = np.random.default_rng(11)
+    G = 400_000
+    b = rng.uniform(0.5, 2.0, G).astype(np.float32)
+    dense = rng.random(G) < 0.35
+    j = rng.integers(1, 1 << 8, G).astype(np.float32)
+    t = np.where(dense, b * (np.float32(1) + j * np.float32(2.0 ** -20)),
+                 b * rng.uniform(1.0, 4.0, G).astype(np.float32)).astype(np.float32)
+    rt = np.empty(2 * G, np.float32)
+    rt[0::2], rt[1::2] = b, t
+    tab = dict(runtime_ms=rt, block_id=np.tile(np.array([0, 1], np.uint16), G),
+               group_offset=np.arange(0, 2 * G + 1, 2, dtype=np.int64),
+               group_matrix=np.zeros(G, np.uint32))
+    _compare(tab, L=2, M=1, ell=1, pcts=[0.01, 0.2, 0.5, 0.7, 0.8, 0.9, 0.95, 0.99])
