@@ -75,7 +75,14 @@ struct GroupAcc {
 struct ThreadAcc {
   uint64_t fx[4];                  // perf hi, perf lo, gain hi, gain lo
   uint64_t pmin, pmax, gmin, gmax;
+  // Per-lane counters since the last flush_counters (every kPkGroups groups per lane): 14
+  // packed 4-bit fields (the 12 flag counters LSCAT_P_GROUPS.., the perf == 1 and gain == 0
+  // histogram bins) and the row counts (groups of < 2^28 rows).
+  uint64_t pk;
+  uint32_t rows, ok, nan;
+  uint32_t n;                      // groups finalised since the last flush (warp-uniform)
 };
+constexpr uint32_t kPkGroups = 15;  // 4-bit fields: at most 15 increments between flushes
 
 __device__ __forceinline__ bool ok_bits(uint32_t b) { return b - 1u < 0x7F7FFFFFu; }  // 0 < b < 0x7F800000
 __device__ __forceinline__ bool nan_bits(uint32_t b) { return (b & 0x7FFFFFFFu) > 0x7F800000u; }
@@ -129,6 +136,38 @@ __device__ __forceinline__ void wadd(uint64_t* sh_c, int slot, uint32_t v) {
 }
 
 __device__ __forceinline__ uint64_t f64_key(double v) { return (uint64_t)__double_as_longlong(v); }
+
+__device__ __forceinline__ uint64_t warp_sum64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Warp-collective: add the lanes' packed counters and row counts to the CTA's shared counters.
+__device__ __forceinline__ void flush_counters(const RP& p, ThreadAcc& t, uint64_t* sh_c, uint32_t* sh_perf,
+                                            uint32_t* sh_gain) {
+  const unsigned FULL = 0xffffffffu;
+  const bool l0 = (threadIdx.x & 31) == 0;
+#pragma unroll
+  for (int i = 0; i < 12; i++) {
+    const uint32_t v = __reduce_add_sync(FULL, (uint32_t)(t.pk >> (4 * i)) & 15u);
+    if (l0 && v) atomicAdd((unsigned long long*)&sh_c[LSCAT_P_GROUPS + i], (unsigned long long)v);
+  }
+  const uint32_t hp = __reduce_add_sync(FULL, (uint32_t)(t.pk >> 48) & 15u);
+  const uint32_t hg = __reduce_add_sync(FULL, (uint32_t)(t.pk >> 52) & 15u);
+  if (l0 && hp) atomicAdd(&sh_perf[p.nb], hp);
+  if (l0 && hg) atomicAdd(&sh_gain[0], hg);
+  const uint64_t r = warp_sum64(t.rows), o = warp_sum64(t.ok), n = warp_sum64(t.nan);
+  if (l0 && r) {
+    atomicAdd((unsigned long long*)&sh_c[LSCAT_P_ROWS], (unsigned long long)r);
+    atomicAdd((unsigned long long*)&sh_c[LSCAT_P_OK], (unsigned long long)o);
+    atomicAdd((unsigned long long*)&sh_c[LSCAT_P_NAN], (unsigned long long)n);
+    atomicAdd((unsigned long long*)&sh_c[LSCAT_P_INVALID], (unsigned long long)(r - o - n));
+  }
+  t.pk = 0;
+  t.rows = t.ok = t.nan = 0;
+  t.n = 0;
+}
 
 // The paper's per-group statistics (O3 steps 3-9).  Warp-collective: all 32
 // lanes call it; `active` lanes hold group g's accumulator.
@@ -198,41 +237,36 @@ __device__ void finalize_lane(const RP& p, uint64_t g, bool active, const GroupA
     if (p.o_gain) p.o_gain[g] = gain;
     if (p.o_flags) p.o_flags[g] = flags;
   }
-  // warp-collective accumulation
+  // per-lane accumulation: packed flag counters and row counts, flushed every kPkGroups groups
   if (!acc) { flags = 0; bbi = -1; }
-  wadd(sh_c, LSCAT_P_GROUPS, __popc(__ballot_sync(FULL, acc)));
-  wadd(sh_c, LSCAT_P_ROWS, __reduce_add_sync(FULL, acc ? a.n_rows : 0u));
-  wadd(sh_c, LSCAT_P_OK, __reduce_add_sync(FULL, acc ? a.n_ok : 0u));
-  wadd(sh_c, LSCAT_P_NAN, __reduce_add_sync(FULL, acc ? a.n_nan : 0u));
-  wadd(sh_c, LSCAT_P_INVALID, __reduce_add_sync(FULL, acc ? a.n_rows - a.n_ok - a.n_nan : 0u));
-  wadd(sh_c, LSCAT_P_DEFINED, __popc(__ballot_sync(FULL, flags & LSCAT_GF_DEFINED)));
-  wadd(sh_c, LSCAT_P_ALL_NAN, __popc(__ballot_sync(FULL, flags & LSCAT_GF_ALL_NAN)));
-  wadd(sh_c, LSCAT_P_COMPLETE, __popc(__ballot_sync(FULL, flags & LSCAT_GF_COMPLETE)));
-  wadd(sh_c, LSCAT_P_INCOMPLETE, __popc(__ballot_sync(FULL, acc && !(flags & LSCAT_GF_COMPLETE))));
-  wadd(sh_c, LSCAT_P_LARGEST_MISSING, __popc(__ballot_sync(FULL, flags & LSCAT_GF_LARGEST_MISSING)));
-  wadd(sh_c, LSCAT_P_RATIO_DEFINED, __popc(__ballot_sync(FULL, flags & LSCAT_GF_RATIO_DEFINED)));
-  wadd(sh_c, LSCAT_P_LARGEST_IS_BEST, __popc(__ballot_sync(FULL, flags & LSCAT_GF_LARGEST_IS_BEST)));
-  wadd(sh_c, LSCAT_P_LARGEST_SLOWER, __popc(__ballot_sync(FULL, flags & LSCAT_GF_LARGEST_SLOWER)));
-  wadd(sh_c, LSCAT_P_GAIN_GT, __popc(__ballot_sync(FULL, flags & LSCAT_GF_GAIN_GT)));
-  wadd(sh_c, LSCAT_P_PERF_LT, __popc(__ballot_sync(FULL, flags & LSCAT_GF_PERF_LT)));
-  wadd(sh_c, LSCAT_P_PERF_BAND, __popc(__ballot_sync(FULL, flags & LSCAT_GF_PERF_BAND)));
-  // histogram increments: the hot bins (perf == 1: bin nb; gain == 0: bin 0) by one ballot per
-  // warp, every other bin by a plain shared atomic (spread bins rarely collide in a warp)
   {
-    const unsigned hp = __ballot_sync(FULL, pbin == (int)p.nb), hg = __ballot_sync(FULL, gbin == 0);
-    if ((threadIdx.x & 31) == 0) {
-      if (hp) atomicAdd(&sh_perf[p.nb], (uint32_t)__popc(hp));
-      if (hg) atomicAdd(&sh_gain[0], (uint32_t)__popc(hg));
-    }
-    if (pbin >= 0 && pbin != (int)p.nb) atomicAdd(&sh_perf[pbin], 1u);
-    if (gbin > 0) atomicAdd(&sh_gain[gbin], 1u);
-    if (bbi >= 0) atomicAdd(&sh_bb[bbi], 1u);
+    uint64_t inc = acc ? 1ull : 0ull;  // field 0: LSCAT_P_GROUPS
+    inc |= (uint64_t)((flags & LSCAT_GF_DEFINED) != 0) << 4;
+    inc |= (uint64_t)((flags & LSCAT_GF_ALL_NAN) != 0) << 8;
+    inc |= (uint64_t)((flags & LSCAT_GF_COMPLETE) != 0) << 12;
+    inc |= (uint64_t)(acc && !(flags & LSCAT_GF_COMPLETE)) << 16;
+    inc |= (uint64_t)((flags & LSCAT_GF_LARGEST_MISSING) != 0) << 20;
+    inc |= (uint64_t)((flags & LSCAT_GF_RATIO_DEFINED) != 0) << 24;
+    inc |= (uint64_t)((flags & LSCAT_GF_LARGEST_IS_BEST) != 0) << 28;
+    inc |= (uint64_t)((flags & LSCAT_GF_LARGEST_SLOWER) != 0) << 32;
+    inc |= (uint64_t)((flags & LSCAT_GF_GAIN_GT) != 0) << 36;
+    inc |= (uint64_t)((flags & LSCAT_GF_PERF_LT) != 0) << 40;
+    inc |= (uint64_t)((flags & LSCAT_GF_PERF_BAND) != 0) << 44;
+    inc |= (uint64_t)(pbin == (int)p.nb) << 48;  // hot bins: perf == 1, gain == 0
+    inc |= (uint64_t)(gbin == 0) << 52;
+    t.pk += inc;
+    if (acc) { t.rows += a.n_rows; t.ok += a.n_ok; t.nan += a.n_nan; }
   }
+  if (pbin >= 0 && pbin != (int)p.nb) atomicAdd(&sh_perf[pbin], 1u);
+  if (gbin > 0) atomicAdd(&sh_gain[gbin], 1u);
+  if (bbi >= 0) atomicAdd(&sh_bb[bbi], 1u);
+  if (++t.n == kPkGroups) flush_counters(p, t, sh_c, sh_perf, sh_gain);
 }
 
 __device__ void flush(const RP& p, ThreadAcc& t, uint64_t* sh_c, uint32_t* sh) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
+  if (__any_sync(FULL, t.n != 0)) flush_counters(p, t, sh_c, sh, sh + (p.nb + 1));
 #pragma unroll
   for (int i = 0; i < 4; i++) {
     uint64_t v = t.fx[i];
@@ -267,6 +301,9 @@ __device__ __forceinline__ void init_shared(const RP& p, uint64_t* sh_c, uint32_
   for (int i = 0; i < 4; i++) t.fx[i] = 0;
   t.pmin = t.gmin = ~0ull;
   t.pmax = t.gmax = 0;
+  t.pk = 0;
+  t.rows = t.ok = t.nan = 0;
+  t.n = 0;
   __syncthreads();
 }
 
