@@ -102,26 +102,30 @@ class Clocks:
 # ----------------------------------------------------------------------------------------
 # reference arm: the CPU oracle (tier framing: the oracle is the reference)
 # ----------------------------------------------------------------------------------------
-def oracle_points_per_s(policy, A_by_n=None):
-    """Time the fp64 oracle of euclidean_kernel once per matrix size and scale to the
-    paper policy: a point = (W + K*R) evaluations of the kernel; 32 points per size."""
+def oracle_points_per_s(policy, A_by_n=None, min_s=10.0):
+    """Time the fp64 oracle of euclidean_kernel on a bounded sample and scale to the policy:
+    a point = (W + K*R) evaluations of the kernel at its N; 32 points per size.  The sample
+    evaluates every matrix size once per round, for as many rounds as fit in `min_s` seconds
+    of CPU work (at least one); the per-size time is the mean over rounds."""
     from oracle import kernels as OK
     W, K, R = POLICIES[policy]
     rng = np.random.default_rng(0)
-    total = 0.0
-    work = 0.0
-    for n in SIZES:
-        if A_by_n is not None:
+    if A_by_n is None:
+        A_by_n = {n: (rng.uniform(-1, 1, (n, n)).astype(np.float32),
+                      rng.uniform(-1, 1, n).astype(np.float32)) for n in SIZES}
+    per_n = {n: 0.0 for n in SIZES}
+    rounds, work = 0, 0.0
+    while rounds == 0 or work < min_s:
+        for n in SIZES:
             A, q = A_by_n[n]
-        else:
-            A = rng.uniform(-1, 1, (n, n)).astype(np.float32)
-            q = rng.uniform(-1, 1, n).astype(np.float32)
-        t0 = time.perf_counter()
-        OK.euclid(A, q)
-        dt = time.perf_counter() - t0
-        work += dt
-        total += len(BLOCKS) * (W + K * R) * dt
-    return len(SIZES) * len(BLOCKS) / total, work
+            t0 = time.perf_counter()
+            OK.euclid(A, q)
+            dt = time.perf_counter() - t0
+            per_n[n] += dt
+            work += dt
+        rounds += 1
+    total = sum(len(BLOCKS) * (W + K * R) * per_n[n] / rounds for n in SIZES)
+    return len(SIZES) * len(BLOCKS) / total, work, rounds
 
 
 def run_reference(args):
@@ -129,14 +133,18 @@ def run_reference(args):
     if rank != 0:
         return
     W, K = args.warmup, args.steps
+    rng = np.random.default_rng(0)
+    A_by_n = {n: (rng.uniform(-1, 1, (n, n)).astype(np.float32),
+                  rng.uniform(-1, 1, n).astype(np.float32)) for n in SIZES}
     for _ in range(W):
-        oracle_points_per_s(args.policy)
-    vals, cpu_s = [], 0.0
+        oracle_points_per_s(args.policy, A_by_n, min_s=0.0)
+    vals, cpu_s, rounds = [], 0.0, 0
     t0 = time.perf_counter()
     for _ in range(K):
-        v, w = oracle_points_per_s(args.policy)
+        v, w, r = oracle_points_per_s(args.policy, A_by_n, min_s=5.0)
         vals.append(v)
         cpu_s += w
+        rounds += r
     wall = time.perf_counter() - t0
     value = len(SIZES) * len(BLOCKS) * K / sum(len(SIZES) * len(BLOCKS) / v for v in vals)
     out = {
@@ -147,9 +155,10 @@ def run_reference(args):
                                         "policy": args.policy, "blocks": "32..1024 step 32",
                                         "sizes": SIZES},
         "cpu_baseline": {"value": value, "unit": "points/s", "cores": 1, "kind": "oracle",
-                         "sample": "per step: one fp64 numpy evaluation of euclidean_kernel per "
-                                   "matrix size (8 evals), scaled by 32 blocks x (W+K*R) "
-                                   "launches per point"},
+                         "sample": f"per step: fp64 numpy evaluations of euclidean_kernel, "
+                                   f"every matrix size once per round, rounds for >= 5 s of CPU "
+                                   f"({rounds} rounds, {cpu_s:.1f} s in total), scaled by 32 blocks "
+                                   f"x (W+K*R) launches per point"},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -288,11 +297,11 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         A_by_n = {n: (ctx.suite_tensor(L.K_EUCLID, n, 0).view(n, n).cpu().numpy(),
                       ctx.suite_tensor(L.K_EUCLID, n, 1).cpu().numpy()) for n in SIZES}
-        v, work = oracle_points_per_s(args.policy, A_by_n)
+        v, work, rounds = oracle_points_per_s(args.policy, A_by_n, min_s=10.0)
         cpu = {"value": v, "unit": "points/s", "cores": 1, "kind": "oracle",
-               "sample": f"one fp64 numpy evaluation of euclidean_kernel per matrix size on the "
-                         f"same inputs ({work:.2f} s CPU), scaled by 32 blocks x (W+K*R) launches "
-                         f"per point"}
+               "sample": f"fp64 numpy evaluations of euclidean_kernel on the same inputs, every "
+                         f"matrix size once per round, {rounds} rounds ({work:.1f} s CPU), mean "
+                         f"per-size time scaled by 32 blocks x (W+K*R) launches per point"}
 
     # ---- secondary: table rows/s on the paper-shaped tables, % of peak per suite kernel (N = 1)
     secondary = None
