@@ -43,7 +43,7 @@ def _compile(src, extra):
         [os.path.join(ROOT, "include", "lscat.h")]
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps):
         return obj, None
-    cmd = [NVCC] + flags() + extra + ["-c", src, "-o", obj]
+    cmd = [NVCC] + flags() + extra + os.environ.get("LSCAT_NVCC_EXTRA", "").split() + ["-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         return obj, f"{' '.join(cmd)}\n{r.stdout}\n{r.stderr}"

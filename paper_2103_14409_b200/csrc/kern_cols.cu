@@ -19,7 +19,7 @@ inline int colsum_chunks(int N, int B) {
 }
 
 template <int B, int VEC>
-__global__ void __launch_bounds__(B) colsum_kernel(const float* __restrict__ A,
+__global__ void __launch_bounds__(B, min_blocks_64regs<B>()) colsum_kernel(const float* __restrict__ A,
                                                    float* __restrict__ out,
                                                    float* __restrict__ partials,
                                                    unsigned* __restrict__ tickets, int N,

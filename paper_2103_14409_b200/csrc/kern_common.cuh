@@ -25,6 +25,12 @@ __device__ __forceinline__ float ld_stream(const float* p) {
 __device__ __forceinline__ void st_stream(float4* p, float4 v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(float* p, float v) { __stcs(p, v); }
 
+// Minimum resident CTAs declared in __launch_bounds__ so that ptxas budgets 64 registers per
+// thread (32 warps per SM).  Without it ptxas sizes registers for full occupancy (32 per
+// thread for B >= 64) and serialises independent 128-bit loads (one in flight per thread).
+template <int B>
+constexpr int min_blocks_64regs() { return 1024 / B > 0 ? 1024 / B : 1; }
+
 template <int B>
 __device__ __forceinline__ float block_sum(float v, float* red /* [B/32] smem */) {
 #pragma unroll

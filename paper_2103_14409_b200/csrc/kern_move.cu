@@ -6,39 +6,112 @@ namespace lscat {
 namespace {
 
 // ---------------------------------------------------------------- transpose -------------
-// 32x32 tile through padded shared memory (bank-conflict free), threads (32, B/32): each
-// thread row moves 32/(B/32) tile rows.  Coalesced 128-byte row segments in and out.
+// Each WARP transposes units of TP_TPW 32x32 tiles (stacked vertically by default, so an
+// output row segment is 32 * TP_TPW contiguous floats) through its own padded smem slice
+// (32 x 33 floats); a warp's work does not depend on the block size B (B only groups warps
+// into CTAs):
+//   load: lane (r = l/8, c = 4(l%8)) reads 8 float4 per tile (rows r, r+4, ..., r+28), all
+//         tiles of the unit at once -> 4 KB x TP_TPW of loads in flight per warp; then per tile
+//         scalar stores into the slice (bank = r + c + k: conflict-free);
+//   store: lane writes output rows r + 4i, columns c..c+3 as one float4 gathered from
+//         slice[c..c+3][r + 4i] (bank = c + k + r + 4i: conflict-free), 128 B per output row.
+// Persistent grid (occupancy x SMs), warps stride over the units; edge units (or N % 4 != 0)
+// take a scalar path.  Only __syncwarp: no CTA barrier.
+// B200 calibration (scripts/tp_variants.sh, N = 8192, mean over the 32 blocks): one tile per
+// unit 106.9 us; two horizontal 106.5; two vertical 103.8 (this default); four vertical 114.
+#ifndef TP_TPW
+#define TP_TPW 2  // 32x32 tiles per warp unit (horizontally adjacent): 8 * TP_TPW loads in flight
+#endif
+#ifndef TP_VERT
+#define TP_VERT 1  // 1: the unit's tiles are stacked vertically (longer output row segments)
+#endif
+#ifndef TP_MINB_THREADS
+#define TP_MINB_THREADS 768  // register budget 65536 / TP_MINB_THREADS per thread
+#endif
 template <int B>
-__global__ void __launch_bounds__(B) transpose_kernel(const float* __restrict__ A,
-                                                      float* __restrict__ T, int N) {
-  constexpr int TY = B / 32;
-  __shared__ float tile[32][33];
-  const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
-  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
-  const int x = bx + lx;
-  if (x < N) {
+constexpr int tp_min_blocks() { return TP_MINB_THREADS / B > 0 ? TP_MINB_THREADS / B : 1; }
+
+template <int B>
+__global__ void __launch_bounds__(B, tp_min_blocks<B>()) transpose_kernel(const float* __restrict__ A,
+                                                                         float* __restrict__ T, int N,
+                                                                         int units_x, int nunits) {
+  constexpr int W = B / 32, U = TP_TPW;
+  extern __shared__ float tp_smem[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float(*t)[33] = reinterpret_cast<float(*)[33]>(tp_smem + w * (32 * 33));
+  const bool vec = (N & 3) == 0;
+  const int r = lane >> 3, c = (lane & 7) * 4;
+  constexpr int UX = TP_VERT ? 1 : U, UY = TP_VERT ? U : 1;  // unit = UY x UX tiles
+  for (int id = blockIdx.x * W + w; id < nunits; id += gridDim.x * W) {
+    const int by0 = (id / units_x) * (32 * UY), bx0 = (id % units_x) * (32 * UX);
+    if (vec && by0 + 32 * UY <= N && bx0 + 32 * UX <= N) {
+      float4 v[U][8];
 #pragma unroll
-    for (int i = ly; i < 32; i += TY)
-      if (by + i < N) tile[i][lx] = ld_stream(A + (size_t)(by + i) * N + x);
-  }
-  __syncthreads();
-  const int x2 = by + lx;
-  if (x2 < N) {
+      for (int u = 0; u < U; u++) {
+        const int by = by0 + (TP_VERT ? 32 * u : 0), bx = bx0 + (TP_VERT ? 0 : 32 * u);
 #pragma unroll
-    for (int i = ly; i < 32; i += TY)
-      if (bx + i < N) st_stream(T + (size_t)(bx + i) * N + x2, tile[lx][i]);
+        for (int i = 0; i < 8; i++)
+          v[u][i] = ld_stream(reinterpret_cast<const float4*>(A + (size_t)(by + r + 4 * i) * N + bx + c));
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int by = by0 + (TP_VERT ? 32 * u : 0), bx = bx0 + (TP_VERT ? 0 : 32 * u);
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+          t[r + 4 * i][c + 0] = v[u][i].x; t[r + 4 * i][c + 1] = v[u][i].y;
+          t[r + 4 * i][c + 2] = v[u][i].z; t[r + 4 * i][c + 3] = v[u][i].w;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+          const int o = r + 4 * i;  // output row bx + o = input column bx + o
+          const float4 q = make_float4(t[c + 0][o], t[c + 1][o], t[c + 2][o], t[c + 3][o]);
+          st_stream(reinterpret_cast<float4*>(T + (size_t)(bx + o) * N + by + c), q);
+        }
+        __syncwarp();  // the slice is rewritten by the next tile
+      }
+    } else {
+      for (int u = 0; u < U; u++) {
+        const int by = by0 + (TP_VERT ? 32 * u : 0), bx = bx0 + (TP_VERT ? 0 : 32 * u);
+        if (bx >= N || by >= N) break;
+        for (int rr = 0; rr < 32; rr++)
+          if (by + rr < N && bx + lane < N) t[rr][lane] = ld_stream(A + (size_t)(by + rr) * N + bx + lane);
+        __syncwarp();
+        for (int cc = 0; cc < 32; cc++)
+          if (bx + cc < N && by + lane < N) st_stream(T + (size_t)(bx + cc) * N + by + lane, t[lane][cc]);
+        __syncwarp();
+      }
+    }
   }
 }
 
 template <int B>
 struct TransposeL {
   static constexpr bool kSupported = true;
-  static int occupancy() { return occupancy_warps(transpose_kernel<B>, B); }
+  static constexpr int kSmem = (B / 32) * 32 * 33 * (int)sizeof(float);
+  static int grid_cap() {
+    static int cap = 0;
+    if (!cap) {
+      int dev = 0, sms = 148, per_sm = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (kSmem > 48 * 1024)
+        cudaFuncSetAttribute(transpose_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, transpose_kernel<B>, B, kSmem);
+      cudaGetLastError();
+      cap = (sms > 0 ? sms : 148) * (per_sm > 0 ? per_sm : 1);
+    }
+    return cap;
+  }
+  static int occupancy() { grid_cap(); return occupancy_warps(transpose_kernel<B>, B, kSmem); }
   static cudaError_t launch(const LaunchArgs& a, cudaStream_t s) {
     const SuiteEntry& e = *a.e;
     const int N = (int)e.n;
-    dim3 grid((N + 31) / 32, (N + 31) / 32);
-    transpose_kernel<B><<<grid, B, 0, s>>>((const float*)e.in0, (float*)e.out, N);
+    constexpr int UX = TP_VERT ? 1 : TP_TPW, UY = TP_VERT ? TP_TPW : 1;
+    const int units_x = (N + 32 * UX - 1) / (32 * UX), nunits = units_x * ((N + 32 * UY - 1) / (32 * UY));
+    const int need = (nunits + B / 32 - 1) / (B / 32);
+    const int grid = need < grid_cap() ? need : grid_cap();
+    transpose_kernel<B><<<grid, B, kSmem, s>>>((const float*)e.in0, (float*)e.out, N, units_x, nunits);
     return cudaGetLastError();
   }
 };
@@ -106,9 +179,10 @@ struct AxpyL {
 
 // ---------------------------------------------------------------- stencil5 --------------
 // out = c0 A[i][j] + c1 (A[i-1][j] + A[i+1][j] + A[i][j-1] + A[i][j+1]) inside, border copied.
-// Threads (32, B/32); a warp owns 32*VEC columns and walks a strip of S rows keeping the rows
-// above/at/below in registers (each row loaded once per strip); left/right neighbours come
-// from the adjacent lanes by shuffle, the two warp-edge columns by one scalar load each.
+// A warp owns 32*VEC columns and a strip of S rows: it loads the S + 2
+// rows it needs (strip + halo; the halo rows are L2 hits, shared with the neighbouring
+// strips) into registers up front, then computes; left/right neighbours come from the
+// adjacent lanes by shuffle, the two warp-edge columns by one scalar load per row.
 constexpr int kStencilS = 8;
 constexpr float kC0 = 0.5f, kC1 = 0.125f;
 
@@ -134,51 +208,69 @@ struct Vec<1> {
 };
 
 template <int B, int VEC>
-__global__ void __launch_bounds__(B) stencil_kernel(const float* __restrict__ A,
-                                                    float* __restrict__ out, int N) {
+__global__ void __launch_bounds__(B, min_blocks_64regs<B>()) stencil_kernel(const float* __restrict__ A,
+                                                                          float* __restrict__ out, int N,
+                                                                          int colblocks) {
   using V = Vec<VEC>;
   using T = typename V::T;
-  constexpr int TY = B / 32;
-  const int lane = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int col0 = blockIdx.x * (32 * VEC) + lane * VEC;
-  const bool valid = col0 < N;
-  const int r0 = (blockIdx.y * TY + ty) * kStencilS;
-  if (r0 >= N) return;  // whole warp leaves together (r0 is warp-uniform)
-  const int r1 = min(r0 + kStencilS, N);
-  T up = V::zero(), cur = V::zero(), dn = V::zero();
-  if (valid) {
-    if (r0 > 0) up = V::load(A + (size_t)(r0 - 1) * N + col0);
-    cur = V::load(A + (size_t)r0 * N + col0);
-  }
-  for (int i = r0; i < r1; i++) {
-    if (valid && i + 1 < N) dn = V::load(A + (size_t)(i + 1) * N + col0);
-    // neighbours across lanes
-    float left = __shfl_up_sync(0xffffffffu, V::get(cur, VEC - 1), 1);
-    float right = __shfl_down_sync(0xffffffffu, V::get(cur, 0), 1);
-    if (valid) {
-      if (lane == 0 && col0 > 0) left = ld_stream(A + (size_t)i * N + col0 - 1);
-      if ((lane == 31 || col0 + VEC >= N) && col0 + VEC < N)
-        right = ld_stream(A + (size_t)i * N + col0 + VEC);
-      T o = cur;
-      const bool row_border = (i == 0 || i == N - 1);
+  constexpr int S = kStencilS;
+  const int lane = threadIdx.x & 31;
+  // global warp -> (strip, column block), column block fastest: concurrent warps cover whole
+  // row bands whatever B is.  One strip per warp (a persistent grid-stride version measured
+  // slower on B200: 110 vs 83 us at N = 8192, B = 32).
+  const int item = blockIdx.x * (B / 32) + (threadIdx.x >> 5);
+  {
+    const int cb = item % colblocks, strip = item / colblocks;
+    const int col0 = cb * (32 * VEC) + lane * VEC;
+    const bool valid = col0 < N;
+    const int r0 = strip * S;
+    if (r0 >= N) return;  // warp-uniform
+    // all S + 2 rows of the strip (and the S warp-edge scalars) are loaded before any use:
+    // S + 2 independent 128-bit loads in flight per lane
+    T rows[S + 2];
 #pragma unroll
-      for (int c = 0; c < VEC; c++) {
-        const int j = col0 + c;
-        if (j >= N) break;
-        if (row_border || j == 0 || j == N - 1) continue;  // copy
-        const float l = c == 0 ? left : V::get(cur, c - 1);
-        const float r = c == VEC - 1 ? right : V::get(cur, c + 1);
-        const float nb = (V::get(up, c) + V::get(dn, c)) + (l + r);
-        V::set(o, c, fmaf(kC0, V::get(cur, c), kC1 * nb));
-      }
-      if (col0 + VEC <= N) {
-        V::store(out + (size_t)i * N + col0, o);
-      } else {
-        for (int c = 0; c < VEC && col0 + c < N; c++) out[(size_t)i * N + col0 + c] = V::get(o, c);
+    for (int k = 0; k < S + 2; k++) {
+      const int i = r0 - 1 + k;
+      rows[k] = (valid && i >= 0 && i < N) ? V::load(A + (size_t)i * N + col0) : V::zero();
+    }
+    const bool need_l = valid && lane == 0 && col0 > 0;
+    const bool need_r = valid && lane == 31 && col0 + VEC < N;
+    const int edge_col = need_l ? col0 - 1 : col0 + VEC;
+    float edge[S];
+#pragma unroll
+    for (int k = 0; k < S; k++)
+      edge[k] = ((need_l || need_r) && r0 + k < N) ? ld_stream(A + (size_t)(r0 + k) * N + edge_col) : 0.f;
+#pragma unroll
+    for (int k = 0; k < S; k++) {
+      const int i = r0 + k;
+      if (i >= N) break;  // warp-uniform
+      const T& up = rows[k];
+      const T& cur = rows[k + 1];
+      const T& dn = rows[k + 2];
+      float left = __shfl_up_sync(0xffffffffu, V::get(cur, VEC - 1), 1);
+      float right = __shfl_down_sync(0xffffffffu, V::get(cur, 0), 1);
+      if (need_l) left = edge[k];
+      if (need_r) right = edge[k];
+      if (valid) {
+        T o = cur;
+        const bool row_border = (i == 0 || i == N - 1);
+#pragma unroll
+        for (int c = 0; c < VEC; c++) {
+          const int j = col0 + c;
+          if (j >= N) break;
+          if (row_border || j == 0 || j == N - 1) continue;  // copy
+          const float l = c == 0 ? left : V::get(cur, c - 1);
+          const float r = c == VEC - 1 ? right : V::get(cur, c + 1);
+          const float nb = (V::get(up, c) + V::get(dn, c)) + (l + r);
+          V::set(o, c, fmaf(kC0, V::get(cur, c), kC1 * nb));
+        }
+        if (col0 + VEC <= N) {
+          V::store(out + (size_t)i * N + col0, o);
+        } else {
+          for (int c = 0; c < VEC && col0 + c < N; c++) out[(size_t)i * N + col0 + c] = V::get(o, c);
+        }
       }
     }
-    up = cur;
-    cur = dn;
   }
 }
 
@@ -189,15 +281,13 @@ struct StencilL {
   static cudaError_t launch(const LaunchArgs& a, cudaStream_t s) {
     const SuiteEntry& e = *a.e;
     const int N = (int)e.n;
-    constexpr int TY = B / 32;
-    const int rows_per_cta = TY * kStencilS;
-    if ((N & 3) == 0) {
-      dim3 grid((N + 127) / 128, (N + rows_per_cta - 1) / rows_per_cta);
-      stencil_kernel<B, 4><<<grid, B, 0, s>>>((const float*)e.in0, (float*)e.out, N);
-    } else {
-      dim3 grid((N + 31) / 32, (N + rows_per_cta - 1) / rows_per_cta);
-      stencil_kernel<B, 1><<<grid, B, 0, s>>>((const float*)e.in0, (float*)e.out, N);
-    }
+    const int strips = (N + kStencilS - 1) / kStencilS;
+    const int cbs = (N & 3) == 0 ? (N + 127) / 128 : (N + 31) / 32;
+    const unsigned grid = (unsigned)(((size_t)cbs * strips + B / 32 - 1) / (B / 32));
+    if ((N & 3) == 0)
+      stencil_kernel<B, 4><<<grid, B, 0, s>>>((const float*)e.in0, (float*)e.out, N, cbs);
+    else
+      stencil_kernel<B, 1><<<grid, B, 0, s>>>((const float*)e.in0, (float*)e.out, N, cbs);
     return cudaGetLastError();
   }
 };

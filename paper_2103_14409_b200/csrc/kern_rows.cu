@@ -21,6 +21,15 @@ enum RowOp { kEuclid = 0, kMatvec = 1, kRowsum = 2 };
 #ifndef ROW_U
 #define ROW_U 8  // float4 loads of A in flight per thread (and as many of q/x)
 #endif
+// Register budget: ptxas otherwise sizes registers for full occupancy (32 regs for B >= 64),
+// which serialises the U loads (one 128-bit load in flight per thread).  Declaring at least
+// ROW_MINB_THREADS / B resident CTAs caps registers at 65536 / ROW_MINB_THREADS instead
+// (scripts/row_variants.sh: 1024 -> 64 registers is best on B200).
+#ifndef ROW_MINB_THREADS
+#define ROW_MINB_THREADS 1024
+#endif
+template <int B>
+constexpr int row_min_blocks() { return ROW_MINB_THREADS / B > 0 ? ROW_MINB_THREADS / B : 1; }
 
 template <int OP>
 __device__ __forceinline__ void acc4(float4& s, float4 a, float4 v) {
@@ -44,7 +53,7 @@ __device__ __forceinline__ float acc1(float s, float a, float v) {
 // A CTA of B threads is split into floor(W/TW) teams of TW warps; each team reduces one row
 // (TW from team_warps, calibrated on B200).
 template <int OP, int B>
-__global__ void __launch_bounds__(B) row_kernel(const float* __restrict__ A,
+__global__ void __launch_bounds__(B, row_min_blocks<B>()) row_kernel(const float* __restrict__ A,
                                                 const float* __restrict__ v,
                                                 float* __restrict__ out, int N, int TW) {
   constexpr int W = B / 32;
@@ -99,14 +108,15 @@ __global__ void __launch_bounds__(B) row_kernel(const float* __restrict__ A,
   if (live && tw == 0 && lane == 0) out[row] = (OP == kEuclid) ? sqrtf(r) : r;
 }
 
-// Warps per team d (1..W, W = B/32; floor(W/d) teams per CTA, leftover warps idle), from the
-// B200 calibration in profiles/r01_summary.md (euclid, N = 8192, U = 8): two warps per row is
-// best or within 2 % for every block with W even; one-warp teams run 5-7 % slower, 8+-warp
-// teams up to 20 % slower at large blocks; idle warps cost about their share; a grid that
-// needs just over one (or two) waves of resident CTAs loses most of a wave (B = 352, 416,
-// 544: 70 us instead of 45).  Score = active fraction x preference(d) x tail penalty.
+// Warps per team d (1..W, W = B/32; floor(W/d) teams per CTA, leftover warps idle).
+// B200 calibration (profiles/r01_summary.md, scripts/row_variants.sh; euclid, U = 8, 64
+// registers): at N >= 4096 one warp per row is best at every block (N = 8192: mean over the
+// 32 blocks 44.0 us vs 45.2 for two-warp teams; N = 4096: 10.2 vs 10.7).  Smaller matrices
+// have fewer rows than resident warps, so teams split rows to fill the machine; the score
+// there = active fraction x preference(d) x wave-tail penalty.
 inline int team_warps(int N, int B, int sm_count, int resident) {
   const int W = B / 32;
+  if (N >= 4096) return 1;
   const double slots = (double)sm_count * resident;
   int best = 1;
   double best_score = -1.0;

@@ -4,6 +4,7 @@
     python scripts/profile_kernels.py suite8192          # every suite kernel, blocks 128/256/512/1024
     python scripts/profile_kernels.py reduce [n_rows]    # uniform 32-row table (configs[4] layout)
     python scripts/profile_kernels.py gemm8192 [block]
+    python scripts/profile_kernels.py kernel NAME N BLOCK   # any suite kernel
 """
 import os
 import sys
@@ -36,6 +37,11 @@ def main():
         c.register_suite([L.K_GEMM_BF16], [8192])
         for _ in range(3):
             c.launch(L.K_GEMM_BF16, 8192, b)
+    elif what == "kernel":                 # kernel NAME N BLOCK
+        k, n, b = L.KERNELS[sys.argv[2]], int(sys.argv[3]), int(sys.argv[4])
+        c.register_suite([k], [n])
+        for _ in range(3):
+            c.launch(k, n, b)
     elif what == "reduce":
         n = int(sys.argv[2]) if len(sys.argv) > 2 else 100_000_000
         t = c.gen_table(n, n // 256, preset=L.PRESET_T4, seed=1, offsets=False)

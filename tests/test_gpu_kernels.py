@@ -118,6 +118,44 @@ def test_euclid_full_size_sampled():
         _check_rel(out, ref, ref)
 
 
+@pytest.mark.parametrize("n", [2048, 8192])
+def test_data_movement_full_size_sampled(n):
+    """transpose (bit-exact) and stencil5 at the sizes the sweep times, where the warp-unit
+    loops run several iterations per warp: sampled output rows vs the oracle."""
+    import torch
+    from paper_2103_14409_b200 import K_STENCIL5, K_TRANSPOSE
+    rng = np.random.default_rng(n)
+    rows = np.unique(np.r_[1:5, rng.choice(np.arange(1, n - 1), 40, replace=False), n - 5:n - 1])
+    c = _setup(K_TRANSPOSE, [n])
+    A = c.suite_tensor(K_TRANSPOSE, n, 0).view(n, n)
+    cols = to_np(A[:, torch.as_tensor(rows, device=A.device)])          # A[:, rows]
+    ref_t = OK.transpose(cols)                                          # = T[rows, :]
+    for b in (32, 96, 256, 1024):
+        out = c.suite_tensor(K_TRANSPOSE, n, 2)
+        out.fill_(float("nan"))
+        c.launch(K_TRANSPOSE, n, b)
+        torch.cuda.synchronize()
+        got = to_np(out.view(n, n)[torch.as_tensor(rows, device=A.device)])
+        assert (got.view(np.uint32) == ref_t.view(np.uint32)).all(), (n, b)
+    c2 = _setup(K_STENCIL5, [n])
+    S = c2.suite_tensor(K_STENCIL5, n, 0).view(n, n)
+    Sh = to_np(S)
+    for b in (32, 160, 1024):
+        out = c2.suite_tensor(K_STENCIL5, n, 2)
+        out.fill_(float("nan"))
+        c2.launch(K_STENCIL5, n, b)
+        torch.cuda.synchronize()
+        O = to_np(out.view(n, n))
+        for i in (0, n - 1):                                            # border rows: copies
+            assert (O[i].view(np.uint32) == Sh[i].view(np.uint32)).all(), (n, b, i)
+        for i in rows:                                                  # interior rows
+            band = Sh[i - 1:i + 2]
+            ref = OK.stencil5(band)[1]
+            scale = OK.stencil5_abs_scale(band)[1]
+            assert (O[i, [0, n - 1]].view(np.uint32) == Sh[i, [0, n - 1]].view(np.uint32)).all()
+            _check_rel(O[i, 1:-1], ref[1:-1], scale[1:-1])
+
+
 def test_launch_rejects_illegal_blocks():
     from paper_2103_14409_b200 import K_EUCLID, LscatError
     c = _setup(K_EUCLID, [64])
