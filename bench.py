@@ -175,6 +175,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--policy", choices=list(POLICIES), default="paper")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--launch", choices=["graph", "graph_pdl", "stream"], default="graph_pdl",
+                    help="how a bracket's launches are issued (lscat_launch_mode)")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -209,6 +211,8 @@ def main():
         return t.item()
 
     W, K, R = POLICIES[args.policy]
+    launch_mode = {"graph": L.LAUNCH_GRAPH, "graph_pdl": L.LAUNCH_GRAPH_PDL,
+                   "stream": L.LAUNCH_STREAM}[args.launch]
     ks = [L.K_EUCLID]
     ctx.register_suite(ks, SIZES)
     npts_total = len(ks) * len(SIZES) * len(BLOCKS)
@@ -220,7 +224,7 @@ def main():
 
     def step():
         t = ctx.sweep(ks, SIZES, BLOCKS, warmup=W, brackets=K, launches=R, timeout_s=30.0,
-                      table=table, with_brackets=True)
+                      table=table, with_brackets=True, launch_mode=launch_mode)
         ctx.reduce_table(t, ropts, per_group=False)
         st = ctx.stats(ropts, percentiles=PCTS)
         return t, st
@@ -291,7 +295,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(ctx, L, ks, W, K, R, npts_total, world, barrier, allmax,
-                      steps=min(args.steps, 2))
+                      steps=min(args.steps, 2), launch_mode=launch_mode)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -307,6 +311,23 @@ def main():
     secondary = None
     if not args.no_secondary and world == 1:
         secondary = table_benches(ctx, L, hbm_peak)
+        if args.launch == "graph_pdl":
+            # the same step with plain graph brackets (no programmatic-dependent-launch edges):
+            # the launch gap PDL hides, measured in the same run
+            flush.zero_()
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            tg = ctx.sweep(ks, SIZES, BLOCKS, warmup=W, brackets=K, launches=R, timeout_s=30.0,
+                           table=table, launch_mode=L.LAUNCH_GRAPH)
+            ctx.reduce_table(tg, ropts, per_group=False)
+            ctx.stats(ropts, percentiles=PCTS)
+            e1.record(stream)
+            barrier()
+            gms = e0.elapsed_time(e1)
+            secondary["launch_graph_no_pdl"] = {"value": round(npts_total / (gms / 1e3), 4),
+                                                "unit": "points/s", "ms_per_step": round(gms, 3),
+                                                "steps": 1}
         secondary["suite_roofline_n8192"] = suite_roofline(ctx, L, hbm_peak, load_peaks()[1])
         cpu_rows = secondary.pop("_cpu_rows_per_s", None)
         if cpu:
@@ -321,6 +342,7 @@ def main():
             "config": {"workload": "configs[1] euclid full sweep: euclidean_kernel x blocks "
                                    "32..1024 step 32 x N 64..8192 (powers of 2)",
                        "policy": f"{args.policy}: W={W} K={K} R={R}", "points": npts_total,
+                       "launch": args.launch,
                        "parallelism": f"point-LPT x{world}", "l2": "flushed between steps "
                        "(512 MB write); N=8192 inputs (268 MB) exceed L2 (126 MB)"},
             "clocks": ck, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
@@ -337,7 +359,7 @@ def main():
     del rooflines
 
 
-def run_e2e(ctx, L, ks, W, K, R, npts_total, world, barrier, allmax, steps=2):
+def run_e2e(ctx, L, ks, W, K, R, npts_total, world, barrier, allmax, steps=2, launch_mode=0):
     """Same metric through the C ABI with HOST buffers: each step uploads the suite inputs
     from pinned host memory, sweeps into a pinned host table, reduces that host table and
     reads the stats back."""
@@ -357,7 +379,8 @@ def run_e2e(ctx, L, ks, W, K, R, npts_total, world, barrier, allmax, steps=2):
     def step():
         for (n, slot), t in host_in.items():
             ctx.suite_upload(L.K_EUCLID, n, slot, t)
-        tab = ctx.sweep(ks, SIZES, BLOCKS, warmup=W, brackets=K, launches=R, table=host_tab)
+        tab = ctx.sweep(ks, SIZES, BLOCKS, warmup=W, brackets=K, launches=R, table=host_tab,
+                        launch_mode=launch_mode)
         ctx.reduce_table(tab, ropts, per_group=False)
         return ctx.stats(ropts, percentiles=PCTS), tab.n_rows
 

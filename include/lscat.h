@@ -73,7 +73,14 @@ typedef enum {
 typedef enum { LSCAT_SLOT_IN0 = 0, LSCAT_SLOT_IN1 = 1, LSCAT_SLOT_OUT = 2 } lscat_slot;
 
 typedef enum { LSCAT_MEM_DEVICE = 0, LSCAT_MEM_HOST = 1 } lscat_mem;
-typedef enum { LSCAT_LAUNCH_GRAPH = 0, LSCAT_LAUNCH_STREAM = 1 } lscat_launch_mode;
+/* How a bracket's R launches are issued (the paper's generated main loops on the host):
+   GRAPH      pre-instantiated CUDA graphs of <= 128 launches (no host launch overhead);
+   STREAM     one launch call per launch (the paper's host loop);
+   GRAPH_PDL  graphs whose consecutive launches carry programmatic-dependent-launch edges:
+              launch i+1 is scheduled and reads its (read-only) inputs while launch i drains,
+              and waits for launch i to complete before its first global store.  Results are
+              identical; the bracket time excludes the launch gap (R-3). */
+typedef enum { LSCAT_LAUNCH_GRAPH = 0, LSCAT_LAUNCH_STREAM = 1, LSCAT_LAUNCH_GRAPH_PDL = 2 } lscat_launch_mode;
 typedef enum { LSCAT_SHARD_POINT_LPT = 0, LSCAT_SHARD_GROUP = 1 } lscat_shard;
 typedef enum { LSCAT_SKIPNA = 0, LSCAT_COMPLETE_ONLY = 1 } lscat_nan_policy;
 

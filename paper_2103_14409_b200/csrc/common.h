@@ -33,6 +33,8 @@ struct SuiteEntry {
 struct LaunchArgs {
   const SuiteEntry* e;
   uint64_t spin_ns;
+  bool pdl = false;  // programmatic dependent launch (LSCAT_LAUNCH_GRAPH_PDL); honoured only
+                     // by kernels that call pdl_wait() before their first global store
 };
 
 // One launch of a suite kernel at block index bi (threads = 32*(bi+1)).  Returns the

@@ -28,6 +28,7 @@ __global__ void __launch_bounds__(B, min_blocks_64regs<B>()) colsum_kernel(const
   constexpr int TC = 32 * VEC;  // columns per tile
   __shared__ float red[W][TC];
   __shared__ unsigned is_last;
+  pdl_trigger();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int col = blockIdx.x * TC + lane * VEC;
   const int r0 = blockIdx.y * rows_per_chunk;
@@ -62,6 +63,7 @@ __global__ void __launch_bounds__(B, min_blocks_64regs<B>()) colsum_kernel(const
       }
     }
   }
+  pdl_wait();  // partials / tickets / out are shared with the previous launch
 #pragma unroll
   for (int c = 0; c < VEC; c++) red[w][lane * VEC + c] = acc[c];
   __syncthreads();
@@ -107,14 +109,13 @@ struct ColsumL {
     unsigned* tickets = (unsigned*)((char*)e.scratch + (size_t)kMaxChunks * N * sizeof(float));
     if ((N & 3) == 0) {
       dim3 grid((N + 127) / 128, chunks);
-      colsum_kernel<B, 4><<<grid, B, 0, s>>>((const float*)e.in0, (float*)e.out, partials,
-                                             tickets, N, chunks, rpc);
+      return launch_k(colsum_kernel<B, 4>, grid, dim3(B), 0, s, a.pdl, (const float*)e.in0, (float*)e.out,
+                      partials, tickets, N, chunks, rpc);
     } else {
       dim3 grid((N + 31) / 32, chunks);
-      colsum_kernel<B, 1><<<grid, B, 0, s>>>((const float*)e.in0, (float*)e.out, partials,
-                                             tickets, N, chunks, rpc);
+      return launch_k(colsum_kernel<B, 1>, grid, dim3(B), 0, s, a.pdl, (const float*)e.in0, (float*)e.out,
+                      partials, tickets, N, chunks, rpc);
     }
-    return cudaGetLastError();
   }
 };
 

@@ -31,6 +31,34 @@ __device__ __forceinline__ void st_stream(float* p, float v) { __stcs(p, v); }
 template <int B>
 constexpr int min_blocks_64regs() { return 1024 / B > 0 ? 1024 / B : 1; }
 
+// Programmatic dependent launch (PDL).  A suite kernel triggers its dependents at entry and
+// waits for its predecessor grid (completion + memory flush) before its first global store,
+// so in a back-to-back bracket launch i+1's CTAs are scheduled, and issue their loads of the
+// read-only inputs, while launch i drains.  Both are no-ops for a launch without the
+// programmatic-serialisation attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            bool pdl, Args... args) {
+  if (!pdl) {
+    k<<<grid, block, smem, s>>>(args...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 template <int B>
 __device__ __forceinline__ float block_sum(float v, float* red /* [B/32] smem */) {
 #pragma unroll

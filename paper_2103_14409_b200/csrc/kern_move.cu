@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(B, tp_min_blocks<B>()) transpose_kernel(const 
                                                                          int units_x, int nunits) {
   constexpr int W = B / 32, U = TP_TPW;
   extern __shared__ float tp_smem[];
+  pdl_trigger();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   float(*t)[33] = reinterpret_cast<float(*)[33]>(tp_smem + w * (32 * 33));
   const bool vec = (N & 3) == 0;
@@ -53,6 +54,7 @@ __global__ void __launch_bounds__(B, tp_min_blocks<B>()) transpose_kernel(const 
         for (int i = 0; i < 8; i++)
           v[u][i] = ld_stream(reinterpret_cast<const float4*>(A + (size_t)(by + r + 4 * i) * N + bx + c));
       }
+      pdl_wait();
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const int by = by0 + (TP_VERT ? 32 * u : 0), bx = bx0 + (TP_VERT ? 0 : 32 * u);
@@ -71,6 +73,7 @@ __global__ void __launch_bounds__(B, tp_min_blocks<B>()) transpose_kernel(const 
         __syncwarp();  // the slice is rewritten by the next tile
       }
     } else {
+      pdl_wait();
       for (int u = 0; u < U; u++) {
         const int by = by0 + (TP_VERT ? 32 * u : 0), bx = bx0 + (TP_VERT ? 0 : 32 * u);
         if (bx >= N || by >= N) break;
@@ -111,8 +114,8 @@ struct TransposeL {
     const int units_x = (N + 32 * UX - 1) / (32 * UX), nunits = units_x * ((N + 32 * UY - 1) / (32 * UY));
     const int need = (nunits + B / 32 - 1) / (B / 32);
     const int grid = need < grid_cap() ? need : grid_cap();
-    transpose_kernel<B><<<grid, B, kSmem, s>>>((const float*)e.in0, (float*)e.out, N, units_x, nunits);
-    return cudaGetLastError();
+    return launch_k(transpose_kernel<B>, dim3(grid), dim3(B), (size_t)kSmem, s, a.pdl, (const float*)e.in0,
+                    (float*)e.out, N, units_x, nunits);
   }
 };
 
@@ -125,6 +128,7 @@ template <int B>
 __global__ void __launch_bounds__(B) axpy_kernel4(const float4* __restrict__ x,
                                                   const float4* __restrict__ y,
                                                   float4* __restrict__ z, size_t n4) {
+  pdl_trigger();
   const size_t base = (size_t)blockIdx.x * (B * kAxpyU) + threadIdx.x;
   float4 a[kAxpyU], b[kAxpyU];
 #pragma unroll
@@ -132,6 +136,7 @@ __global__ void __launch_bounds__(B) axpy_kernel4(const float4* __restrict__ x,
     const size_t j = base + (size_t)u * B;
     if (j < n4) { a[u] = ld_stream(x + j); b[u] = ld_stream(y + j); }
   }
+  pdl_wait();
 #pragma unroll
   for (int u = 0; u < kAxpyU; u++) {
     const size_t j = base + (size_t)u * B;
@@ -148,6 +153,8 @@ template <int B>
 __global__ void __launch_bounds__(B) axpy_kernel1(const float* __restrict__ x,
                                                   const float* __restrict__ y,
                                                   float* __restrict__ z, size_t n) {
+  pdl_trigger();
+  pdl_wait();
   const size_t base = (size_t)blockIdx.x * (B * kAxpyU) + threadIdx.x;
 #pragma unroll
   for (int u = 0; u < kAxpyU; u++) {
@@ -166,14 +173,13 @@ struct AxpyL {
     if ((n & 3) == 0) {
       const size_t n4 = n / 4;
       const size_t grid = (n4 + (size_t)B * kAxpyU - 1) / ((size_t)B * kAxpyU);
-      axpy_kernel4<B><<<(unsigned)grid, B, 0, s>>>((const float4*)e.in0, (const float4*)e.in1,
-                                                   (float4*)e.out, n4);
+      return launch_k(axpy_kernel4<B>, dim3((unsigned)grid), dim3(B), 0, s, a.pdl, (const float4*)e.in0,
+                      (const float4*)e.in1, (float4*)e.out, n4);
     } else {
       const size_t grid = (n + (size_t)B * kAxpyU - 1) / ((size_t)B * kAxpyU);
-      axpy_kernel1<B><<<(unsigned)grid, B, 0, s>>>((const float*)e.in0, (const float*)e.in1,
-                                                   (float*)e.out, n);
+      return launch_k(axpy_kernel1<B>, dim3((unsigned)grid), dim3(B), 0, s, a.pdl, (const float*)e.in0,
+                      (const float*)e.in1, (float*)e.out, n);
     }
-    return cudaGetLastError();
   }
 };
 
@@ -214,6 +220,7 @@ __global__ void __launch_bounds__(B, min_blocks_64regs<B>()) stencil_kernel(cons
   using V = Vec<VEC>;
   using T = typename V::T;
   constexpr int S = kStencilS;
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   // global warp -> (strip, column block), column block fastest: concurrent warps cover whole
   // row bands whatever B is.  One strip per warp (a persistent grid-stride version measured
@@ -240,6 +247,7 @@ __global__ void __launch_bounds__(B, min_blocks_64regs<B>()) stencil_kernel(cons
 #pragma unroll
     for (int k = 0; k < S; k++)
       edge[k] = ((need_l || need_r) && r0 + k < N) ? ld_stream(A + (size_t)(r0 + k) * N + edge_col) : 0.f;
+    pdl_wait();
 #pragma unroll
     for (int k = 0; k < S; k++) {
       const int i = r0 + k;
@@ -285,10 +293,8 @@ struct StencilL {
     const int cbs = (N & 3) == 0 ? (N + 127) / 128 : (N + 31) / 32;
     const unsigned grid = (unsigned)(((size_t)cbs * strips + B / 32 - 1) / (B / 32));
     if ((N & 3) == 0)
-      stencil_kernel<B, 4><<<grid, B, 0, s>>>((const float*)e.in0, (float*)e.out, N, cbs);
-    else
-      stencil_kernel<B, 1><<<grid, B, 0, s>>>((const float*)e.in0, (float*)e.out, N, cbs);
-    return cudaGetLastError();
+      return launch_k(stencil_kernel<B, 4>, dim3(grid), dim3(B), 0, s, a.pdl, (const float*)e.in0, (float*)e.out, N, cbs);
+    return launch_k(stencil_kernel<B, 1>, dim3(grid), dim3(B), 0, s, a.pdl, (const float*)e.in0, (float*)e.out, N, cbs);
   }
 };
 

@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(B, row_min_blocks<B>()) row_kernel(const float
                                                 float* __restrict__ out, int N, int TW) {
   constexpr int W = B / 32;
   __shared__ float red[W];
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int team = warp / TW, tw = warp % TW;          // team index, warp within team
   const int T = TW * 32, t = tw * 32 + lane;            // team size, thread within team
@@ -105,6 +106,7 @@ __global__ void __launch_bounds__(B, row_min_blocks<B>()) row_kernel(const float
         for (int k = 0; k < TW; k++) r += red[team * TW + k];
     }
   }
+  pdl_wait();
   if (live && tw == 0 && lane == 0) out[row] = (OP == kEuclid) ? sqrtf(r) : r;
 }
 
@@ -188,9 +190,8 @@ struct RowLauncher {
       const int N = (int)e.n;
       const int tw = (tw_env > 0 && tw_env <= B / 32) ? tw_env : team_warps(N, B, sm_count, resident);
       const int teams = B / 32 / tw;
-      row_kernel<OP, B><<<(N + teams - 1) / teams, B, smem_cap, s>>>((const float*)e.in0, (const float*)e.in1,
-                                                                     (float*)e.out, N, tw);
-      return cudaGetLastError();
+      return launch_k(row_kernel<OP, B>, dim3((N + teams - 1) / teams), dim3(B), (size_t)smem_cap, s, a.pdl,
+                      (const float*)e.in0, (const float*)e.in1, (float*)e.out, N, tw);
     }
   };
 };

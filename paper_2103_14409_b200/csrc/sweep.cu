@@ -5,7 +5,10 @@
 //   warm-up launches bracketed by events -> host waits -> predicted point time = warm * K * R;
 //   over the timeout -> NaN + TIMEOUT without running the brackets;
 //   otherwise K brackets of R launches, each bracket between two CUDA events on `stream`,
-//   launched as pre-instantiated CUDA graphs (LSCAT_LAUNCH_GRAPH, chunks of <= 128 launches)
+//   launched as pre-instantiated CUDA graphs (LSCAT_LAUNCH_GRAPH, chunks of <= 128 launches;
+//   LSCAT_LAUNCH_GRAPH_PDL adds programmatic-dependent-launch edges between the captured
+//   launches, so launch i+1 is scheduled and loads its read-only inputs while launch i
+//   drains; every kernel still waits for its predecessor before its first global store)
 //   or one cudaLaunchKernel per launch (LSCAT_LAUNCH_STREAM, the paper's host loop);
 //   brackets are harvested lazily (one host wait per point, on the warm-up of the next one);
 //   runtime = median over K of bracket/R; measured point time > timeout -> NaN + TIMEOUT.
@@ -48,7 +51,9 @@ lscat_status wait_event(lscat_ctx* ctx, cudaEvent_t ev, double deadline_s) {
 
 cudaError_t get_graph(lscat_ctx* ctx, LaunchFn fn, const LaunchArgs& a, uint32_t kernel,
                       uint32_t n, uint32_t bi, uint32_t count, cudaGraphExec_t* out) {
-  auto key = std::make_tuple(kernel, kernel == LSCAT_K_SPIN ? (uint32_t)a.spin_ns : n, bi, count);
+  // the PDL flag is part of the key: the same point may be captured with and without it
+  auto key = std::make_tuple(kernel, kernel == LSCAT_K_SPIN ? (uint32_t)a.spin_ns : n, bi,
+                             count | (a.pdl ? 0x80000000u : 0u));
   auto it = ctx->graphs.find(key);
   if (it != ctx->graphs.end()) {
     *out = it->second;
@@ -91,7 +96,7 @@ extern "C" lscat_status lscat_sweep(lscat_ctx* ctx, const uint32_t* kernels, uin
                 "sweep: blocks must be unique, ascending, multiples of 32 in [32, 1024] (P:98, P:215)");
   if (o->brackets == 0 || o->launches_per_bracket == 0 || !(o->timeout_s > 0))
     return fail(ctx, LSCAT_ERR_INVALID_ARG, "sweep: brackets, launches_per_bracket, timeout_s must be > 0");
-  if (o->launch_mode > LSCAT_LAUNCH_STREAM || out->mem > LSCAT_MEM_HOST)
+  if (o->launch_mode > LSCAT_LAUNCH_GRAPH_PDL || out->mem > LSCAT_MEM_HOST)
     return fail(ctx, LSCAT_ERR_INVALID_ARG, "sweep: bad launch_mode or table mem");
   if (!out->runtime_ms || !out->block_id || !out->group_offset)
     return fail(ctx, LSCAT_ERR_INVALID_ARG, "sweep: table needs runtime_ms, block_id, group_offset");
@@ -213,9 +218,12 @@ extern "C" lscat_status lscat_sweep(lscat_ctx* ctx, const uint32_t* kernels, uin
     }
     // brackets
     cudaGraphExec_t gx = nullptr, gr = nullptr;
-    if (o->launch_mode == LSCAT_LAUNCH_GRAPH) {
-      le = get_graph(ctx, fn, a, kern, n, bi, chunk, &gx);
-      if (le == cudaSuccess && rem) le = get_graph(ctx, fn, a, kern, n, bi, rem, &gr);
+    const bool graph = o->launch_mode != LSCAT_LAUNCH_STREAM;
+    if (graph) {
+      LaunchArgs ga = a;
+      ga.pdl = o->launch_mode == LSCAT_LAUNCH_GRAPH_PDL;
+      le = get_graph(ctx, fn, ga, kern, n, bi, chunk, &gx);
+      if (le == cudaSuccess && rem) le = get_graph(ctx, fn, ga, kern, n, bi, rem, &gr);
       if (le != cudaSuccess) {
         if (is_sticky(le)) return cuda_fail(ctx, le, "sweep: graph capture");
         cudaGetLastError();
@@ -225,7 +233,7 @@ extern "C" lscat_status lscat_sweep(lscat_ctx* ctx, const uint32_t* kernels, uin
     }
     LSCAT_CUDA(ctx, cudaEventRecord(EV(ps.slot, 0), s));
     for (uint32_t k = 0; k < K; k++) {
-      if (o->launch_mode == LSCAT_LAUNCH_GRAPH) {
+      if (graph) {
         for (uint32_t c = 0; c < full; c++) LSCAT_CUDA(ctx, cudaGraphLaunch(gx, s));
         if (rem) LSCAT_CUDA(ctx, cudaGraphLaunch(gr, s));
       } else {

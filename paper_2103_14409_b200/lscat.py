@@ -25,7 +25,7 @@ KERNELS = {"euclid": K_EUCLID, "matvec": K_MATVEC, "gemm_bf16": K_GEMM_BF16,
            "stencil5": K_STENCIL5, "spin": K_SPIN}
 SLOT_IN0, SLOT_IN1, SLOT_OUT = 0, 1, 2
 MEM_DEVICE, MEM_HOST = 0, 1
-LAUNCH_GRAPH, LAUNCH_STREAM = 0, 1
+LAUNCH_GRAPH, LAUNCH_STREAM, LAUNCH_GRAPH_PDL = 0, 1, 2
 SHARD_POINT_LPT, SHARD_GROUP = 0, 1
 SKIPNA, COMPLETE_ONLY = 0, 1
 PRESET_T4, PRESET_GTX980 = 0, 1

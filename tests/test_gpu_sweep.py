@@ -125,3 +125,49 @@ def test_full_suite_small_sweep_stats():
     c.reduce_table(c.sweep(ks, ns, bs, warmup=1, brackets=3, launches=20), o, per_group=False)
     st = c.stats(o)
     assert st["n_rows"] == t["n_rows"] and st["n_nan"] == 3 * len(ns)
+
+
+@pytest.mark.parametrize("n", [100, 512, 2048])
+def test_pdl_graph_mode_outputs(n):
+    """LAUNCH_GRAPH_PDL: back-to-back launches overlap their prologues/loads with the previous
+    launch's drain; every kernel waits for its predecessor before storing, so after a PDL
+    sweep each output still equals the oracle (colsum's partials/tickets are the sensitive
+    case), and the table is complete."""
+    import torch
+    from oracle import kernels as OK
+    from paper_2103_14409_b200 import KERNELS, LAUNCH_GRAPH_PDL, ROW_OK
+    c = ctx()
+    names = ("euclid", "matvec", "rowsum", "colsum", "transpose", "axpy", "stencil5")
+    ks = [KERNELS[k] for k in names]
+    bs = [32, 96, 256, 1024]
+    c.register_suite(ks, [n])
+    for k in ks:                                       # poison the outputs first
+        c.suite_tensor(k, n, 2).fill_(float("nan"))
+    t = c.sweep(ks, [n], bs, warmup=1, brackets=3, launches=200,
+                launch_mode=LAUNCH_GRAPH_PDL).to_numpy()
+    assert t["n_rows"] == len(ks) * len(bs) and (t["status"] == ROW_OK).all()
+    assert np.isfinite(t["runtime_ms"]).all()
+    torch.cuda.synchronize()
+    f = lambda k, s: c.suite_tensor(KERNELS[k], n, s).cpu().numpy().astype(np.float64)
+    A = f("euclid", 0).reshape(n, n)
+    checks = {
+        "euclid": (OK.euclid(A, f("euclid", 1)), OK.euclid_abs_scale(A, f("euclid", 1))),
+    }
+    for name, (ref, scale) in checks.items():
+        out = f(name, 2)
+        assert (np.abs(out - ref) <= 1e-5 * scale).all(), name
+    Am = f("matvec", 0).reshape(n, n)
+    assert (np.abs(f("matvec", 2) - OK.matvec(Am, f("matvec", 1)))
+            <= 1e-5 * OK.matvec_abs_scale(Am, f("matvec", 1))).all()
+    Ar = f("rowsum", 0).reshape(n, n)
+    assert (np.abs(f("rowsum", 2) - OK.rowsum(Ar)) <= 1e-5 * OK.rowsum_abs_scale(Ar)).all()
+    Ac = f("colsum", 0).reshape(n, n)
+    assert (np.abs(f("colsum", 2) - OK.colsum(Ac)) <= 1e-5 * OK.colsum_abs_scale(Ac)).all()
+    At = c.suite_tensor(KERNELS["transpose"], n, 0).cpu().numpy().reshape(n, n)
+    Tt = c.suite_tensor(KERNELS["transpose"], n, 2).cpu().numpy().reshape(n, n)
+    assert (Tt.view(np.uint32) == OK.transpose(At).view(np.uint32)).all()
+    x, y = f("axpy", 0), f("axpy", 1)
+    assert (np.abs(f("axpy", 2) - OK.axpy(x, y)) <= 1e-5 * OK.axpy_abs_scale(x, y)).all()
+    As = f("stencil5", 0).reshape(n, n)
+    Os = f("stencil5", 2).reshape(n, n)
+    assert (np.abs(Os - OK.stencil5(As)) <= 1e-5 * OK.stencil5_abs_scale(As)).all()
