@@ -2,11 +2,12 @@
 //
 // euclidean_kernel is the one kernel the paper names (Figs. 3/5).  Its source is
 // not given; this build reads it as the distance of every row of A to a query vector q
-// (reading R-14).  Mapping: a CTA of B threads is split into teams of
-// warps, one team per row (one team per CTA for small blocks or long rows), 128-bit streaming
-// loads of A with U independent loads in flight per thread, q/x through the read-only cache
-// (L2/L1 resident), fp32 accumulation, warp shuffles + a fixed-order smem combine.
-// HBM bound: 4N^2 + 8N bytes per launch.
+// (reading R-14).  Mapping: each warp of a CTA of B threads reduces
+// one row (team size 1, calibrated; larger teams remain for calibration), 128-bit streaming
+// loads of A with U = 8 independent loads in flight per thread (64-register budget), q/x
+// through the read-only cache (L2/L1 resident), fp32 accumulation, warp shuffles (+ a
+// fixed-order smem combine for teams > 1); A's loads carry an L2 evict-last policy when A fits
+// in L2 (re-read by every launch of a bracket).  HBM bound: 4N^2 + 8N bytes per launch.
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -55,7 +56,7 @@ __device__ __forceinline__ float acc1(float s, float a, float v) {
 template <int OP, int B>
 __global__ void __launch_bounds__(B, row_min_blocks<B>()) row_kernel(const float* __restrict__ A,
                                                 const float* __restrict__ v,
-                                                float* __restrict__ out, int N, int TW) {
+                                                float* __restrict__ out, int N, int TW, int l2keep) {
   constexpr int W = B / 32;
   __shared__ float red[W];
   pdl_trigger();
@@ -70,6 +71,7 @@ __global__ void __launch_bounds__(B, row_min_blocks<B>()) row_kernel(const float
   if (live) {
     if ((N & 3) == 0) {
       constexpr int U = ROW_U;
+      const uint64_t pol = l2keep ? l2_evict_last_policy() : 0;
       const float4* a4 = reinterpret_cast<const float4*>(a);
       const float4* v4 = reinterpret_cast<const float4*>(v);
       const int n4 = N >> 2;
@@ -78,7 +80,7 @@ __global__ void __launch_bounds__(B, row_min_blocks<B>()) row_kernel(const float
 #pragma unroll
         for (int u = 0; u < U; u++) {
           const int j = base + u * T;
-          x[u] = j < n4 ? ld_stream(a4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+          x[u] = j < n4 ? (l2keep ? ld_keep(a4 + j, pol) : ld_stream(a4 + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
         if constexpr (OP != kRowsum) {
 #pragma unroll
@@ -110,29 +112,13 @@ __global__ void __launch_bounds__(B, row_min_blocks<B>()) row_kernel(const float
   if (live && tw == 0 && lane == 0) out[row] = (OP == kEuclid) ? sqrtf(r) : r;
 }
 
-// Warps per team d (1..W, W = B/32; floor(W/d) teams per CTA, leftover warps idle).
-// B200 calibration (profiles/r01_summary.md, scripts/row_variants.sh; euclid, U = 8, 64
-// registers): at N >= 4096 one warp per row is best at every block (N = 8192: mean over the
-// 32 blocks 44.0 us vs 45.2 for two-warp teams; N = 4096: 10.2 vs 10.7).  Smaller matrices
-// have fewer rows than resident warps, so teams split rows to fill the machine; the score
-// there = active fraction x preference(d) x wave-tail penalty.
-inline int team_warps(int N, int B, int sm_count, int resident) {
-  const int W = B / 32;
-  if (N >= 4096) return 1;
-  const double slots = (double)sm_count * resident;
-  int best = 1;
-  double best_score = -1.0;
-  for (int d = 1; d <= W; d++) {
-    const int teams = W / d;
-    const double pref = d == 2 ? 1.0 : (d == 3 || d == 4) ? 0.99 : d == 1 ? 0.96 : (d <= 8 ? 0.97 : 0.93);
-    const double active = (double)(teams * d) / W;
-    const double waves = std::ceil((double)N / teams) / slots;
-    const double tail = (waves > 1.0 && waves < 1.3) ? 0.5 : (waves > 2.0 && waves < 2.3) ? 0.8 : 1.0;
-    const double score = active * pref * tail;
-    if (score > best_score + 1e-9) { best_score = score; best = d; }
-  }
-  return best;
-}
+// Warps per team (one row per team).  B200 calibration with the 64-register budget and PDL
+// brackets (scripts/row_variants.sh, scripts/tw_probe.sh; euclid, mean per-launch time over
+// the 32 blocks): one warp per row is best at every N -- N = 8192: 44.0 us (two-warp teams
+// 45.2); N = 4096: 10.2 (10.7); N = 2048: 1.94 us (2: 2.75, 4: 4.49, the previous wave-tail
+// heuristic 2.87); N = 1024: 0.83 (1.30, 2.29, heuristic 1.32); N = 512: 0.73 (0.76, 1.20).
+// Larger teams only add the team combine and idle leftover warps.
+inline int team_warps(int /*N*/, int /*B*/) { return 1; }
 
 template <int OP>
 struct RowLauncher {
@@ -142,56 +128,33 @@ struct RowLauncher {
     static int occupancy() { return occupancy_warps(row_kernel<OP, B>, B); }
     static cudaError_t launch(const LaunchArgs& a, cudaStream_t s) {
       const SuiteEntry& e = *a.e;
-      // CTAs resident per SM from threads (2048), CTAs (32) and registers (64K, allocated per
-      // warp in units of 256); shared memory (< 1 KB) never binds
-      static int sm_count = 0, resident = 0;
-      if (!resident) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
-        if (sm_count < 1) sm_count = 148;
-        cudaFuncAttributes fa{};
-        int regs = 32;
-        if (cudaFuncGetAttributes(&fa, row_kernel<OP, B>) == cudaSuccess && fa.numRegs > 0) regs = fa.numRegs;
-        cudaGetLastError();
-        const int per_warp = ((regs * 32 + 255) / 256) * 256;
-        resident = std::max(1, std::min({32, 2048 / B, 65536 / (per_warp * (B / 32))}));
-      }
-      // tuning overrides (profiling only): LSCAT_ROW_TEAM_WARPS, LSCAT_ROW_WARPS_PER_SM
+      const int N = (int)e.n;
+      // calibration overrides (profiling only): LSCAT_ROW_TEAM_WARPS, LSCAT_ROW_L2KEEP=0/1
       static const int tw_env = [] {
         const char* v = getenv("LSCAT_ROW_TEAM_WARPS");
         return v ? atoi(v) : 0;
       }();
-      static const int cap_env = [] {
-        const char* v = getenv("LSCAT_ROW_WARPS_PER_SM");
+      static const int keep_env = [] {
+        const char* v = getenv("LSCAT_ROW_L2KEEP");
         return v ? atoi(v) : -1;
       }();
-      // Optional cap on resident warps per SM by reserving dynamic shared memory (calibration
-      // only, off by default: the reservation also shrinks L1, which holds q/x, and measured
-      // slower on B200 for every cap tried, profiles/r01_summary.md).
-      static int smem_cap = -1;
-      if (smem_cap < 0) {
-        const int cap = cap_env >= 0 ? cap_env : 0;
-        const int W = B / 32;
-        smem_cap = 0;
-        if (cap > 0 && resident * W > cap) {
-          const int ctas = std::max(1, cap / W);
-          smem_cap = (227 * 1024) / ctas - 1024;  // leaves room for the static red[] array
-          smem_cap = std::min(smem_cap, 227 * 1024 - 2048);
-          if (cudaFuncSetAttribute(row_kernel<OP, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap) !=
-              cudaSuccess) {
-            cudaGetLastError();
-            smem_cap = 0;
-          } else {
-            resident = ctas;
-          }
-        }
+      static int l2_bytes = -1;
+      if (l2_bytes < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&l2_bytes, cudaDevAttrL2CacheSize, dev) != cudaSuccess) l2_bytes = 0;
+        cudaGetLastError();
       }
-      const int N = (int)e.n;
-      const int tw = (tw_env > 0 && tw_env <= B / 32) ? tw_env : team_warps(N, B, sm_count, resident);
+      const int tw = (tw_env > 0 && tw_env <= B / 32) ? tw_env : team_warps(N, B);
       const int teams = B / 32 / tw;
-      return launch_k(row_kernel<OP, B>, dim3((N + teams - 1) / teams), dim3(B), (size_t)smem_cap, s, a.pdl,
-                      (const float*)e.in0, (const float*)e.in1, (float*)e.out, N, tw);
+      // L2 residency: every launch of a bracket re-reads A.  When A fits comfortably in L2
+      // (<= 0.6 of it: N <= 4096 on B200) its loads carry an evict-last policy; measured
+      // (scripts/l2keep_probe.sh, PDL brackets, mean over the 32 blocks) N = 4096: 9.16 ->
+      // 6.21 us; at N = 8192 (256 MB, twice L2) the hint only thrashes (37.9 -> 43.6 us), so
+      // it is off there.
+      const int keep = keep_env >= 0 ? keep_env : ((double)N * N * 4.0 <= 0.6 * l2_bytes ? 1 : 0);
+      return launch_k(row_kernel<OP, B>, dim3((N + teams - 1) / teams), dim3(B), 0, s, a.pdl,
+                      (const float*)e.in0, (const float*)e.in1, (float*)e.out, N, tw, keep);
     }
   };
 };
