@@ -23,6 +23,10 @@ ns = [64, 136]
 bs = [32, 96, 128, 256, 1024]
 c.register_suite(ks, ns)
 tab = c.sweep(ks, ns, bs, warmup=1, brackets=2, launches=2)
+# PDL graph brackets (griddepcontrol) and a size where the warp-unit loops iterate
+ks32 = [k for k in ks if k != L.K_GEMM_BF16]
+c.register_suite(ks32, [1040])
+c.sweep(ks32, [1040], [32, 160, 1024], warmup=1, brackets=2, launches=3, launch_mode=L.LAUNCH_GRAPH_PDL)
 o = L.reduce_opts(len(bs), len(ns), block_profile=1)
 c.reduce_table(tab, o)
 st = c.stats(o, percentiles=[0.1, 0.5, 0.9])
