@@ -98,6 +98,9 @@ struct lscat_ctx {
   // graphs: (kernel, n, block_idx, chunk) -> exec
   std::map<std::tuple<uint32_t, uint32_t, uint32_t, uint32_t>, cudaGraphExec_t> graphs;
   cudaStream_t capture_stream = nullptr;
+  // percentile selection: first batch (init + 3 levels + state read-back) as a graph, keyed by
+  // every pointer / size / percentile it bakes in (stats.cu; world == 1)
+  std::vector<std::pair<std::string, cudaGraphExec_t>> sel_graphs;
   std::vector<cudaEvent_t> events;
   // comm
   lscat::Comm* comm = nullptr;  // NCCL, or the local test transport (comm.h)

@@ -170,6 +170,7 @@ void lscat_ctx_destroy(lscat_ctx* c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+  for (auto& kv : c->sel_graphs) cudaGraphExecDestroy(kv.second);
   for (auto ev : c->events) cudaEventDestroy(ev);
   for (auto& kv : c->suite) {
     cudaFree(kv.second.in0);

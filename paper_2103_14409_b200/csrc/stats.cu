@@ -488,59 +488,105 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
   if (err) return cuda_fail(ctx, err, "stats: pinned");
   constexpr int kT0 = 512, kT1 = 256;
   const int pass_smem = kSmemRanges * kBins * 4, res_smem = (int)cap * 8;
-  LSCAT_CUDA(ctx, cudaFuncSetAttribute(sel_pass<true, kT0>, cudaFuncAttributeMaxDynamicSharedMemorySize, pass_smem));
-  LSCAT_CUDA(ctx, cudaFuncSetAttribute(sel_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, res_smem));
+  // kernel attributes and occupancy: once per process (per resolve smem size)
+  static int occ0 = 0, occ1 = 0, res_smem_set = 0;
+  if (!occ0) {
+    LSCAT_CUDA(ctx, cudaFuncSetAttribute(sel_pass<true, kT0>, cudaFuncAttributeMaxDynamicSharedMemorySize, pass_smem));
+    LSCAT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ0, sel_pass<true, kT0>, kT0, pass_smem));
+    LSCAT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, sel_pass<false, kT1>, kT1, 0));
+    occ0 = std::max(occ0, 1);
+    occ1 = std::max(occ1, 1);
+  }
+  if (res_smem_set < res_smem) {
+    LSCAT_CUDA(ctx, cudaFuncSetAttribute(sel_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, res_smem));
+    res_smem_set = res_smem;
+  }
   // grids: every resident CTA once (occupancy API), capped by the work (kU x 32 groups per warp)
   const uint64_t n = rs.own_hi - rs.own_lo;
-  int occ0 = 1, occ1 = 1;
-  LSCAT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ0, sel_pass<true, kT0>, kT0, pass_smem));
-  LSCAT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, sel_pass<false, kT1>, kT1, 0));
   const int grid0 = (int)std::min<uint64_t>(std::max<uint64_t>(1, (n + kT0 * 8 - 1) / (kT0 * 8)),
-                                             (uint64_t)ctx->sm_count * std::max(occ0, 1));
+                                             (uint64_t)ctx->sm_count * occ0);
   const int grid1 = (int)std::min<uint64_t>(std::max<uint64_t>(1, (n + kT1 * 8 - 1) / (kT1 * 8)),
-                                             (uint64_t)ctx->sm_count * std::max(occ1, 1));
+                                             (uint64_t)ctx->sm_count * occ1);
   PctArg pa{};
   for (uint32_t i = 0; i < npct; i++) pa.p[i] = pct[i];
-  LSCAT_CUDA(ctx, cudaMemsetAsync(hist, 0, (size_t)kMaxR * kBins * 4, s));
-  LSCAT_CUDA(ctx, cudaMemsetAsync(cand, 0, (size_t)kMaxR * 8, s));
-  sel_init<<<1, kMaxT, 0, s>>>(st, rs.partials, rs.minmax, pa, npct, cap);
-  ctx->launches++;
-  LSCAT_CUDA(ctx, cudaGetLastError());
-  for (int batch = 0;; batch++) {
-    if (batch == 8) return fail(ctx, LSCAT_ERR_STATE, "stats: percentile selection did not converge");
+  // One batch: kLevelsPerBatch levels of pass -> (merge) -> resolve -> plan, then the state
+  // is read back (one host sync per batch).
+  auto enqueue_levels = [&](cudaStream_t q, bool first) -> lscat_status {
     for (int level = 0; level < kLevelsPerBatch; level++) {
-      if (batch == 0 && level == 0)
-        sel_pass<true, kT0><<<grid0, kT0, pass_smem, s>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, st, hist, cand, cap, cbuf);
+      if (first && level == 0)
+        sel_pass<true, kT0><<<grid0, kT0, pass_smem, q>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, st, hist, cand, cap, cbuf);
       else
-        sel_pass<false, kT1><<<grid1, kT1, 0, s>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, st, hist, cand, cap, cbuf);
-      ctx->launches++;
+        sel_pass<false, kT1><<<grid1, kT1, 0, q>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, st, hist, cand, cap, cbuf);
       LSCAT_CUDA(ctx, cudaGetLastError());
       if (world > 1) {
         lscat_status ns;
-        if ((ns = ctx->comm->allreduce(ctx, {{hist, (size_t)kMaxR * kBins, DT::U32, Op::Sum}}, s))) return ns;
-        if ((ns = ctx->comm->allgather(ctx, cand, cand_all, cand_len, DT::U64, s))) return ns;
+        if ((ns = ctx->comm->allreduce(ctx, {{hist, (size_t)kMaxR * kBins, DT::U32, Op::Sum}}, q))) return ns;
+        if ((ns = ctx->comm->allgather(ctx, cand, cand_all, cand_len, DT::U64, q))) return ns;
       }
-      sel_resolve<<<kMaxR, 1024, res_smem, s>>>(st, hist, cand_all, cand, world, cap);
-      ctx->launches++;
+      sel_resolve<<<kMaxR, 1024, res_smem, q>>>(st, hist, cand_all, cand, world, cap);
       LSCAT_CUDA(ctx, cudaGetLastError());
-      sel_plan<<<1, kMaxT, 0, s>>>(st, cap);
-      ctx->launches++;
+      sel_plan<<<1, kMaxT, 0, q>>>(st, cap);
       LSCAT_CUDA(ctx, cudaGetLastError());
-      if (getenv("LSCAT_SEL_DEBUG")) {
-        LSCAT_CUDA(ctx, cudaMemcpyAsync(hst, st, sizeof(SelState), cudaMemcpyDeviceToHost, s));
-        LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
-        fprintf(stderr, "sel batch %d level %d: nt %u nr %u nw0 %u open %u err %u src %u compact %u nc %llu %llu\n",
-                batch, level, hst->nt, hst->nr, hst->nw0, hst->open, hst->err, hst->src, hst->compact,
-                hst->nc[0], hst->nc[1]);
-        for (uint32_t i = 0; i < hst->nr; i++)
-          fprintf(stderr, "  range %u: which %u lo %016llx hi %016llx base %016llx count %llu shift %u gather %u\n", i,
-                  hst->r[i].which, (unsigned long long)hst->r[i].lo, (unsigned long long)hst->r[i].hi,
-                  (unsigned long long)hst->r[i].base, (unsigned long long)hst->r[i].count, hst->r[i].shift,
-                  hst->r[i].gather);
-      }
     }
-    LSCAT_CUDA(ctx, cudaMemcpyAsync(hst, st, sizeof(SelState), cudaMemcpyDeviceToHost, s));
+    LSCAT_CUDA(ctx, cudaMemcpyAsync(hst, st, sizeof(SelState), cudaMemcpyDeviceToHost, q));
+    return LSCAT_OK;
+  };
+  auto enqueue_first = [&](cudaStream_t q) -> lscat_status {
+    LSCAT_CUDA(ctx, cudaMemsetAsync(hist, 0, (size_t)kMaxR * kBins * 4, q));
+    LSCAT_CUDA(ctx, cudaMemsetAsync(cand, 0, (size_t)kMaxR * 8, q));
+    sel_init<<<1, kMaxT, 0, q>>>(st, rs.partials, rs.minmax, pa, npct, cap);
+    LSCAT_CUDA(ctx, cudaGetLastError());
+    return enqueue_levels(q, true);
+  };
+  const bool debug = getenv("LSCAT_SEL_DEBUG") != nullptr;
+  lscat_status ls;
+  // First batch: launched as a cached CUDA graph when the selection runs on one rank (the
+  // small tables of configs[2]/[3] are launch-latency bound: ~10 dependent launches).
+  if (world == 1 && !debug) {
+    std::string key;
+    auto put = [&](const void* v, size_t n) { key.append(reinterpret_cast<const char*>(v), n); };
+    const void* ptrs[] = {rs.perf, rs.gain, rs.partials, rs.minmax, st, hist, cand, cbuf, hst};
+    put(ptrs, sizeof ptrs);
+    put(&rs.own_lo, 8); put(&rs.own_hi, 8); put(&npct, 4); put(pa.p, npct * 8);
+    put(&grid0, 4); put(&grid1, 4); put(&cap, 4);
+    cudaGraphExec_t gx = nullptr;
+    for (auto& kv : ctx->sel_graphs)
+      if (kv.first == key) gx = kv.second;
+    if (!gx) {
+      cudaStream_t cs = ctx->capture_stream;
+      LSCAT_CUDA(ctx, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+      ls = enqueue_first(cs);
+      cudaGraph_t g = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(cs, &g);
+      if (ls) {
+        if (g) cudaGraphDestroy(g);
+        return ls;
+      }
+      LSCAT_CUDA(ctx, ce);
+      const cudaError_t ie = cudaGraphInstantiate(&gx, g, 0);
+      cudaGraphDestroy(g);
+      LSCAT_CUDA(ctx, ie);
+      if (ctx->sel_graphs.size() >= 8) {  // small LRU-less cache: drop the oldest
+        cudaGraphExecDestroy(ctx->sel_graphs.front().second);
+        ctx->sel_graphs.erase(ctx->sel_graphs.begin());
+      }
+      ctx->sel_graphs.emplace_back(std::move(key), gx);
+    }
+    LSCAT_CUDA(ctx, cudaGraphLaunch(gx, s));
+  } else {
+    if ((ls = enqueue_first(s))) return ls;
+  }
+  ctx->launches += 1 + 3 * kLevelsPerBatch;
+  for (int batch = 0;; batch++) {
+    if (batch == 8) return fail(ctx, LSCAT_ERR_STATE, "stats: percentile selection did not converge");
+    if (batch > 0) {
+      if ((ls = enqueue_levels(s, false))) return ls;
+      ctx->launches += 3 * kLevelsPerBatch;
+    }
     LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
+    if (debug)
+      fprintf(stderr, "sel batch %d: nt %u nr %u nw0 %u open %u err %u src %u compact %u nc %llu %llu\n", batch,
+              hst->nt, hst->nr, hst->nw0, hst->open, hst->err, hst->src, hst->compact, hst->nc[0], hst->nc[1]);
     if (hst->err) return fail(ctx, LSCAT_ERR_STATE, "stats: percentile selection lost keys (code %u)", hst->err);
     if (!hst->open) break;
   }
