@@ -219,11 +219,184 @@ __global__ void __launch_bounds__(B, 1) gemm_kernel(const __grid_constant__ Gemm
   }
 }
 
+// Persistent variant (B >= 192: two role warps + at least four epilogue warps).  One CTA per
+// SM walks the output tiles blockIdx.x, blockIdx.x + gridDim.x, ... (grouped raster order):
+//   warp 0, one lane : TMA producer over the continuous (tile, k-block) sequence;
+//   warp 1, one lane : MMA issuer; tile j accumulates into TMEM buffer j & 1 (2 x 256 of the
+//                      512 columns), waiting on tmem_empty[j & 1] before the first k-block;
+//   warps 2..W-1     : epilogue of tile j from buffer j & 1 while the MMA already runs tile
+//                      j + 1 in the other buffer; each warp arrives on tmem_empty once its
+//                      tcgen05.ld of the tile are done.
+// So the tensor pipe is not idle during the epilogue and the per-tile prologue (barrier init,
+// TMEM allocation) is paid once per CTA.  Measured at N = 8192 in the burst regime
+// (scripts/gemm_ab.py, interleaved short bursts): 738 us = 1489 TFLOP/s (B = 192) vs 767 us =
+// 1433 TFLOP/s for the one-tile-per-CTA kernel (B = 128).
+constexpr uint32_t kTmemColsP = 512;
+
+template <int B>
+__global__ void __launch_bounds__(B, 1) gemm_persistent_kernel(const __grid_constant__ GemmMaps maps,
+                                                               __nv_bfloat16* __restrict__ C, int N) {
+  constexpr int W = B / 32;
+  static_assert(W >= 6, "persistent GEMM needs 2 role warps + 4 epilogue warps");
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kStages * kStageA;
+  uint64_t* full = (uint64_t*)(sB + kStages * kStageB);
+  uint64_t* empty = full + kStages;
+  uint64_t* tmem_full = empty + kStages;  // [2]
+  uint64_t* tmem_empty = tmem_full + 2;   // [2]
+  uint32_t* tmem_slot = (uint32_t*)(tmem_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mt = (N + BM - 1) / BM, nt = (N + BN - 1) / BN, ntiles = mt * nt;
+  const int per_group = kGroupM * nt;
+  const int kblocks = (N + BK - 1) / BK;
+  auto tile_origin = [&](int t, int& m0, int& n0) {
+    const int first_m = (t / per_group) * kGroupM;
+    const int gm = min(mt - first_m, kGroupM);
+    m0 = (first_m + (t % per_group) % gm) * BM;
+    n0 = ((t % per_group) / gm) * BN;
+  };
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.b) : "memory");
+    for (int s = 0; s < kStages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; b++) {
+      mbar_init(&tmem_full[b], 1);
+      mbar_init(&tmem_empty[b], W - 2);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemColsP)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer
+      uint32_t it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int m0, n0;
+        tile_origin(t, m0, n0);
+        for (int kb = 0; kb < kblocks; kb++, it++) {
+          const int s = it % kStages;
+          const uint32_t ph = (it / kStages) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], kStageA + kStageB);
+          tma_load_2d(sA + s * kStageA, &maps.a, &full[s], kb * BK, m0);
+          tma_load_2d(sB + s * kStageB, &maps.b, &full[s], kb * BK, n0);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      uint32_t it = 0, j = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, j++) {
+        const uint32_t buf = j & 1, use = j >> 1;
+        mbar_wait(&tmem_empty[buf], (use & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc = tmem + buf * BN;
+        for (int kb = 0; kb < kblocks; kb++, it++) {
+          const int s = it % kStages;
+          const uint32_t ph = (it / kStages) & 1;
+          mbar_wait(&full[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t ad = sw128_desc(sA + s * kStageA), bd = sw128_desc(sB + s * kStageB);
+#pragma unroll
+          for (int k = 0; k < BK / UK; k++)
+            mma_bf16(acc, ad + (uint64_t)(k * UK * 2 >> 4), bd + (uint64_t)(k * UK * 2 >> 4), (kb | k) != 0);
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&tmem_full[buf]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---- epilogue warps: lane quadrant q = warp % 4 (the TMEM lanes this warp may access);
+    // the warps of one quadrant split the 8 32-column chunks
+    const int q = warp & 3;
+    const int first_w = q >= 2 ? q : q + 4;  // first epilogue warp (>= 2) of quadrant q
+    const int iq = (warp - first_w) >> 2;
+    const int nq = (W - 1 - first_w) / 4 + 1;
+    uint32_t j = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, j++) {
+      int m0, n0;
+      tile_origin(t, m0, n0);
+      const uint32_t buf = j & 1, use = j >> 1;
+      mbar_wait(&tmem_full[buf], use & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int row = m0 + q * 32 + lane;
+      for (int c = iq; c < BN / 32; c += nq) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem + buf * BN + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+              "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+              "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+              "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const int col = n0 + c * 32;
+        if (row < N && col < N) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; i++) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+            pk[i] = *reinterpret_cast<uint32_t*>(&h);
+          }
+          __nv_bfloat16* dst = C + (size_t)row * N + col;
+          if (col + 32 <= N) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+            for (int i = 0; i < 4; i++) d4[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+          } else {
+            for (int i = 0; i < 32 && col + i < N; i++) {
+              uint32_t w = pk[i >> 1];
+              uint16_t h = (i & 1) ? (uint16_t)(w >> 16) : (uint16_t)(w & 0xFFFF);
+              reinterpret_cast<uint16_t*>(dst)[i] = h;
+            }
+          }
+        }
+      }
+      // this warp's reads of buffer `buf` are complete: hand it back to the MMA issuer
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[buf])) : "memory");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemColsP)
+                 : "memory");
+  }
+}
+
 template <int B>
 struct GemmL {
   static constexpr bool kSupported = B >= 128;
   static int occupancy() {
-    if constexpr (B >= 128) {
+    if constexpr (B >= 192) {
+      cudaFuncSetAttribute(gemm_persistent_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+      return occupancy_warps(gemm_persistent_kernel<B>, B, kSmem);
+    } else if constexpr (B >= 128) {
       cudaFuncSetAttribute(gemm_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
       return occupancy_warps(gemm_kernel<B>, B, kSmem);
     } else {
@@ -240,9 +413,24 @@ struct GemmL {
         attr = true;
       }
       const int N = (int)e.n;
-      const int grid = ((N + BM - 1) / BM) * ((N + BN - 1) / BN);
-      gemm_kernel<B><<<grid, B, kSmem, s>>>(*reinterpret_cast<const GemmMaps*>(e.host_blob),
-                                            (__nv_bfloat16*)e.out, N);
+      const int tiles = ((N + BM - 1) / BM) * ((N + BN - 1) / BN);
+      if constexpr (B >= 192) {  // persistent, TMEM double-buffered (one CTA per SM)
+        static int sms = 0;
+        if (!sms) {
+          int dev = 0;
+          cudaGetDevice(&dev);
+          cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+          if (cudaFuncSetAttribute(gemm_persistent_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem) !=
+              cudaSuccess)
+            return cudaGetLastError();
+          if (sms < 1) sms = 148;
+        }
+        gemm_persistent_kernel<B><<<tiles < sms ? tiles : sms, B, kSmem, s>>>(
+            *reinterpret_cast<const GemmMaps*>(e.host_blob), (__nv_bfloat16*)e.out, N);
+        return cudaGetLastError();
+      }
+      gemm_kernel<B><<<tiles, B, kSmem, s>>>(*reinterpret_cast<const GemmMaps*>(e.host_blob),
+                                             (__nv_bfloat16*)e.out, N);
       return cudaGetLastError();
     } else {
       return cudaErrorInvalidConfiguration;

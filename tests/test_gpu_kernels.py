@@ -184,6 +184,20 @@ def test_gemm_bf16_all_blocks():
             _check_rel(out, ref, scale, tol=1e-2)
 
 
+def test_gemm_persistent_multi_tile():
+    """N = 2056: 17 x 9 = 153 output tiles > 148 SMs, so persistent CTAs (B >= 192) run two
+    tiles through both TMEM accumulator buffers; ragged 8-row / 8-column edge tiles."""
+    from paper_2103_14409_b200 import K_GEMM_BF16
+    n = 2056
+    c = _setup(K_GEMM_BF16, [n])
+    A, Bt = _inputs(c, K_GEMM_BF16, n)
+    A, Bt = A.reshape(n, n), Bt.reshape(n, n)
+    ref, scale = OK.gemm(A, Bt), OK.gemm_abs_scale(A, Bt)
+    for b in (128, 192, 224, 256, 1024):
+        out = _run(c, K_GEMM_BF16, n, b).reshape(n, n)
+        _check_rel(out, ref, scale, tol=1e-2)
+
+
 def test_gemm_identity_bit_exact():
     """Bt = I -> C = A exactly (one non-zero product per output, bf16 A exact)."""
     import torch
