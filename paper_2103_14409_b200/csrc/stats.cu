@@ -12,7 +12,7 @@
 //   sel_resolve one CTA per range: scan its histogram (narrow each target to its bin) or sort
 //               its gathered keys (bitonic, shared memory) and pick each target's rank;
 //   sel_plan    merge the open targets into the next level's ranges.
-// The host launches levels in batches of three and reads the state once per batch (one sync
+// The host launches levels in batches of four and reads the state once per batch (one sync
 // for the common case).  `base` skips the empty low binades of a level-0 range whose minimum
 // is far below its maximum (gain = 0 next to gains of order 1).  With world > 1 the histograms
 // are summed and the gathered keys all-gathered between sel_pass and sel_resolve, so every
@@ -34,7 +34,7 @@ constexpr int kMaxT = 128;            // targets: 2 x <= 64 percentiles
 constexpr int kMaxR = kMaxT;          // open ranges per level (<= open targets)
 static_assert(kMaxR <= 128, "sel_pass range search covers 128 ranges");
 constexpr int kSmemRanges = 2;        // histograms privatised in shared memory up to this many
-constexpr int kLevelsPerBatch = 3;
+constexpr int kLevelsPerBatch = 4;
 constexpr uint64_t kGapKeys = 32ull << 52;  // 32 binades: keys below hi - kGapKeys share bin 1
 constexpr uint64_t kNaNKey = 0x7FF8000000000000ull;
 // Once the open ranges hold at most this many keys per quantity (and at most half of them), one
@@ -62,9 +62,10 @@ struct SelState {
   uint32_t open;              // targets still open after the last plan
   uint32_t src;               // 0: passes read perf/gain; 1: the compacted keys
   uint32_t compact;           // 1: the next pass also copies the keys it counts (src 0 only)
-  uint32_t pad;
+  uint32_t r0_valid;          // bit w: r0[w] holds quantity w's level-0 range
   unsigned long long nc[2];   // compacted keys per quantity
   uint64_t n_def;
+  Range r0[2];                // level-0 ranges: later full passes filter keys by level-0 bin
   Range r[kMaxR];
   Tgt t[kMaxT];
 };
@@ -186,6 +187,15 @@ __global__ void __launch_bounds__(kMaxT) sel_init(SelState* st, const uint64_t* 
   }
   __syncthreads();
   plan_ranges(st, cap);
+  __syncthreads();
+  if (i == 0) {  // remember the level-0 range of each quantity (the bin filter of later passes)
+    uint32_t v = 0;
+    for (uint32_t j = 0; j < st->nr; j++) {
+      const uint32_t w = st->r[j].which;
+      if (!st->r[j].gather && !(v & (1u << w))) { st->r0[w] = st->r[j]; v |= 1u << w; }
+    }
+    st->r0_valid = v;
+  }
 }
 
 __global__ void __launch_bounds__(kMaxT) sel_plan(SelState* st, uint32_t cap) {
@@ -203,13 +213,17 @@ __global__ void __launch_bounds__(kMaxT) sel_plan(SelState* st, uint32_t cap) {
 // largest power of two < n (0 for n <= 1): the first step of the range search
 __device__ __forceinline__ uint32_t top_step(uint32_t n) { return n > 1 ? 1u << (31 - __clz(n - 1)) : 0u; }
 
-// Levels >= 1, a warp with at least one key inside an open range (rare): gather, histogram
-// (match.any-aggregated global atomics) and compaction.  Out of line so the unrolled scan loop
+// Levels >= 1, a warp with at least one key inside an open range: gather, histogram
+// (match.any-aggregated global atomics), or -- on the copy-only level that starts compaction --
+// a warp-aggregated copy of the keys.  Out of line so the unrolled scan loop
 // of sel_pass stays small enough for the instruction cache.  Called by all 32 lanes.
+constexpr uint32_t kStageKeys = 1024;  // per quantity and CTA: compaction staged in smem
+
 __device__ __noinline__ void hit_slow(const Range* sr, uint32_t r, uint64_t k, uint64_t d, bool hit, int w,
                                       int lane, uint32_t* __restrict__ hist,
                                       unsigned long long* __restrict__ cand, uint32_t cap, bool compact,
-                                      SelState* __restrict__ st, double* __restrict__ cbuf) {
+                                      SelState* __restrict__ st, double* __restrict__ cbuf,
+                                      uint64_t* __restrict__ stage, uint32_t* __restrict__ s_nc) {
   const unsigned FULL = 0xffffffffu;
   const Range& R = sr[r];
   // lanes may sit in different ranges (gathered or histogrammed): no early exit before the
@@ -219,16 +233,27 @@ __device__ __noinline__ void hit_slow(const Range* sr, uint32_t r, uint64_t k, u
     if (idx < cap) cand[kMaxR + (size_t)r * cap + idx] = k;
   }
   const bool counted = hit && !R.gather;
-  const int key = counted ? (int)(r * kBins) + bin_of_d(R, d) : -1;
-  const unsigned peers = __match_any_sync(FULL, key);
-  if (counted && (__ffs(peers) - 1) == lane) atomicAdd(&hist[key], (uint32_t)__popc(peers));
-  if (compact) {  // copy the counted keys out for the next levels (warp-aggregated)
+  if (!compact) {
+    const int key = counted ? (int)(r * kBins) + bin_of_d(R, d) : -1;
+    const unsigned peers = __match_any_sync(FULL, key);
+    if (counted && (__ffs(peers) - 1) == lane) atomicAdd(&hist[key], (uint32_t)__popc(peers));
+  } else {  // copy-only level: the keys of the open ranges are copied out, not histogrammed
+            // (the next level histograms the copies with the same ranges)
+    // staged in the CTA's shared buffer (one shared atomic per warp); the CTA reserves its
+    // global range once at the end (sel_pass), so the global counter is not a hot spot
     const unsigned m = __ballot_sync(FULL, counted);
-    unsigned long long at = 0;
-    if (m && lane == 0) at = atomicAdd(&st->nc[w], (unsigned long long)__popc(m));
+    uint32_t at = 0;
+    if (m && lane == 0) at = atomicAdd(&s_nc[w], (uint32_t)__popc(m));
     at = __shfl_sync(FULL, at, 0);
-    const unsigned long long pos = at + __popc(m & ((1u << lane) - 1u));
-    if (counted && pos < kCompactCap) reinterpret_cast<uint64_t*>(cbuf)[(size_t)w * kCompactCap + pos] = k;
+    const uint32_t pos = at + __popc(m & ((1u << lane) - 1u));
+    if (counted) {
+      if (pos < kStageKeys) {
+        stage[(size_t)w * kStageKeys + pos] = k;
+      } else {  // stage full: straight to the global buffer
+        const unsigned long long g = atomicAdd(&st->nc[w], 1ull);
+        if (g < kCompactCap) reinterpret_cast<uint64_t*>(cbuf)[(size_t)w * kCompactCap + g] = k;
+      }
+    }
   }
 }
 
@@ -258,7 +283,50 @@ __global__ void __launch_bounds__(kT, kSmem ? 2 : 4) sel_pass(const double* __re
   for (uint32_t i = threadIdx.x; i < nr; i += kT) sr[i] = st->r[i];
   if (kSmem)
     for (uint32_t i = threadIdx.x; i < nr * kBins; i += kT) sh_hist[i] = 0;
+  // Levels >= 1 over the full arrays: a coarse bitmap per quantity over the high key bits,
+  // cell = (k >> S) - (lo0 >> S) with S >= 32 chosen so the level-0 range [lo0, hi0] spans at
+  // most kCells cells; a cell is marked if any open range touches it.  A key whose cell is
+  // unmarked is in no open range, so the range search (and its vote) is skipped for it with a
+  // handful of 32-bit instructions on the key's high word.
+  constexpr uint32_t kCells = 1u << 16;
+  __shared__ uint32_t bm[2][kCells / 32];
+  __shared__ uint32_t s_filt;
+  __shared__ uint64_t stage[kSmem ? 1 : 2 * kStageKeys];
+  __shared__ uint32_t s_nc[2];
+  __shared__ unsigned long long s_base[2];
+  if (threadIdx.x < 2) s_nc[threadIdx.x] = 0;
+  uint32_t filt = (!kSmem && !st->src) ? st->r0_valid : 0u;
+  uint32_t fsh[2] = {0, 0}, fbase[2] = {0, 0};  // S - 32 and (lo0 >> S) per quantity
+  if (filt) {
+#pragma unroll
+    for (int w = 0; w < 2; w++) {
+      if (!(filt & (1u << w))) continue;
+      const uint64_t lo0 = st->r0[w].lo, hi0 = st->r0[w].hi;
+      uint32_t S = 32;
+      while (((hi0 >> S) - (lo0 >> S)) >= kCells) S++;
+      fsh[w] = S - 32;
+      fbase[w] = (uint32_t)(lo0 >> S);
+    }
+    for (uint32_t i = threadIdx.x; i < 2 * (kCells / 32); i += kT) (&bm[0][0])[i] = 0u;
+  }
+  if (threadIdx.x == 0) s_filt = filt;
   __syncthreads();
+  if (filt)
+    for (uint32_t i = threadIdx.x; i < nr; i += kT) {
+      const Range& R = sr[i];
+      const uint32_t w = R.which;
+      if (!(filt & (1u << w))) continue;
+      const uint32_t S = (w ? fsh[1] : fsh[0]) + 32, b0 = w ? fbase[1] : fbase[0];
+      const uint64_t c_lo = (R.lo >> S) - b0, c_hi = (R.hi >> S) - b0;
+      if (c_lo > c_hi || c_hi >= kCells) {  // outside the level-0 range: no filter for w
+        atomicAnd(&s_filt, ~(1u << w));
+        continue;
+      }
+      for (uint32_t cc = (uint32_t)c_lo; cc <= (uint32_t)c_hi; cc++) atomicOr(&bm[w][cc >> 5], 1u << (cc & 31));
+    }
+  __syncthreads();
+  filt = s_filt;
+  const uint32_t* bmp[2] = {bm[0], bm[1]};
   uint32_t c0[2] = {0, 0}, cL[2] = {0, 0};  // level 0: end-bin counts per thread
   Range sr0[2];  // level 0: the range of each quantity, kept in registers
   if (kSmem) {
@@ -285,15 +353,15 @@ __global__ void __launch_bounds__(kT, kSmem ? 2 : 4) sel_pass(const double* __re
       for (int u = 0; u < kU; u++)
         v[w][u] = (full || (rd && (uint64_t)(32 * u + lane) < hw)) ? __ldg(src + 32 * u) : kNaNKey;
     }
+    if (kSmem) {
 #pragma unroll
-    for (int u = 0; u < kU; u++) {
+      for (int u = 0; u < kU; u++) {
 #pragma unroll
-      for (int w = 0; w < 2; w++) {
-        const uint32_t nw = w ? nw1 : nw0;
-        if (!nw) continue;  // uniform
-        const uint64_t k = v[w][u];
-        const uint32_t b0 = w ? nw0 : 0;
-        if (kSmem) {
+        for (int w = 0; w < 2; w++) {
+          const uint32_t nw = w ? nw1 : nw0;
+          if (!nw) continue;  // uniform
+          const uint64_t k = v[w][u];
+          const uint32_t b0 = w ? nw0 : 0;
           // level 0: one range per quantity (registers); end bins counted per thread
           const Range& R = sr0[w];
           const uint64_t d = k - R.lo;
@@ -311,8 +379,37 @@ __global__ void __launch_bounds__(kT, kSmem ? 2 : 4) sel_pass(const double* __re
           c0[w] += is0;
           cL[w] += isL;
           if (hit && !is0 && !isL) atomicAdd(&sh_hist[b0 * kBins + b], 1u);
-          continue;
         }
+      }
+      continue;
+    }
+    // levels >= 1: first a branch-free candidate mask over the 2 x kU keys of each lane (the
+    // coarse cell bitmap, or every key when unfiltered), one vote for the whole batch; the
+    // range search and its per-key vote run only for key slots some lane flagged
+    uint32_t m = 0;
+#pragma unroll
+    for (int u = 0; u < kU; u++)
+#pragma unroll
+      for (int w = 0; w < 2; w++) {
+        const uint32_t nw = w ? nw1 : nw0;
+        uint32_t c = nw != 0;
+        if (filt & (1u << w)) {  // branch-free: clamp the cell, mask the out-of-range case
+          const uint32_t cell = ((uint32_t)(v[w][u] >> 32) >> fsh[w]) - fbase[w];
+          const uint32_t cl = min(cell, kCells - 1);
+          c = (bmp[w][cl >> 5] >> (cl & 31)) & (uint32_t)(cell < kCells);
+        }
+        m |= c << (2 * u + w);
+      }
+    const uint32_t mall = __reduce_or_sync(FULL, m);  // warp-uniform: slots some lane flagged
+    if (!mall) continue;
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+#pragma unroll
+      for (int w = 0; w < 2; w++) {
+        if (!((mall >> (2 * u + w)) & 1u)) continue;
+        const uint32_t nw = w ? nw1 : nw0;
+        const uint64_t k = v[w][u];
+        const uint32_t b0 = w ? nw0 : 0;
         // last range with lo <= k (ranges sorted by lo): binary lifting with a warp-uniform
         // trip count, not unrolled (keeps the 16 unrolled copies small)
         uint32_t r = b0;
@@ -327,7 +424,23 @@ __global__ void __launch_bounds__(kT, kSmem ? 2 : 4) sel_pass(const double* __re
         const uint64_t d = k - R.lo;
         const bool hit = d <= R.span;  // k < lo wraps d past every span (< 2^63)
         if (!__any_sync(FULL, hit)) continue;
-        hit_slow(sr, r, k, d, hit, w, lane, hist, cand, cap, compact, st, cbuf);
+        hit_slow(sr, r, k, d, hit, w, lane, hist, cand, cap, compact, st, cbuf, stage, s_nc);
+      }
+    }
+  }
+  if (!kSmem && compact) {  // flush the staged compaction: one global reservation per quantity
+    __syncthreads();
+    if (threadIdx.x < 2) {
+      const uint32_t n = min(s_nc[threadIdx.x], kStageKeys);
+      s_base[threadIdx.x] = n ? atomicAdd(&st->nc[threadIdx.x], (unsigned long long)n) : 0ull;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < 2; w++) {
+      const uint32_t n = min(s_nc[w], kStageKeys);
+      for (uint32_t i = threadIdx.x; i < n; i += kT) {
+        const unsigned long long g = s_base[w] + i;
+        if (g < kCompactCap) reinterpret_cast<uint64_t*>(cbuf)[(size_t)w * kCompactCap + g] = stage[w * kStageKeys + i];
       }
     }
   }
@@ -364,6 +477,7 @@ __global__ void __launch_bounds__(1024) sel_resolve(SelState* st, uint32_t* __re
   const int nt = (int)st->nt;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (!R.gather) {
+    if (st->compact) return;  // copy-only level: nothing was counted, the ranges stand
     constexpr int kPer = kBins / 1024;
     uint32_t* h = hist + (size_t)r * kBins;
     uint32_t c[kPer];
