@@ -28,6 +28,14 @@ __device__ __forceinline__ uint64_t l2_evict_last_policy() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
+// Fractional policy: a fixed (address-hashed) fraction of the lines accessed is kept with
+// evict-last priority, the rest streams through with evict-first, so a buffer larger than L2
+// leaves a stable resident part instead of thrashing.
+__device__ __forceinline__ uint64_t l2_keep_fraction_policy(float frac) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, %1;" : "=l"(pol) : "f"(frac));
+  return pol;
+}
 __device__ __forceinline__ float4 ld_keep(const float4* p, uint64_t pol) {
   float4 r;
   asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"

@@ -6,8 +6,10 @@
 // one row (team size 1, calibrated; larger teams remain for calibration), 128-bit streaming
 // loads of A with U = 8 independent loads in flight per thread (64-register budget), q/x
 // through the read-only cache (L2/L1 resident), fp32 accumulation, warp shuffles (+ a
-// fixed-order smem combine for teams > 1); A's loads carry an L2 evict-last policy when A fits
-// in L2 (re-read by every launch of a bracket).  HBM bound: 4N^2 + 8N bytes per launch.
+// fixed-order smem combine for teams > 1); A's loads carry a fractional L2 evict-last policy
+// (re-read by every launch of a bracket: all of A stays L2-resident when it fits, a stable
+// fraction of it otherwise).  HBM bound: 4N^2 + 8N bytes per launch (fewer from DRAM in a
+// bracket: the L2-resident part).
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -56,7 +58,7 @@ __device__ __forceinline__ float acc1(float s, float a, float v) {
 template <int OP, int B>
 __global__ void __launch_bounds__(B, row_min_blocks<B>()) row_kernel(const float* __restrict__ A,
                                                 const float* __restrict__ v,
-                                                float* __restrict__ out, int N, int TW, int l2keep) {
+                                                float* __restrict__ out, int N, int TW, float l2keep) {
   constexpr int W = B / 32;
   __shared__ float red[W];
   pdl_trigger();
@@ -71,7 +73,7 @@ __global__ void __launch_bounds__(B, row_min_blocks<B>()) row_kernel(const float
   if (live) {
     if ((N & 3) == 0) {
       constexpr int U = ROW_U;
-      const uint64_t pol = l2keep ? l2_evict_last_policy() : 0;
+      const uint64_t pol = l2keep > 0.f ? l2_keep_fraction_policy(l2keep) : 0;
       const float4* a4 = reinterpret_cast<const float4*>(a);
       const float4* v4 = reinterpret_cast<const float4*>(v);
       const int n4 = N >> 2;
@@ -80,7 +82,7 @@ __global__ void __launch_bounds__(B, row_min_blocks<B>()) row_kernel(const float
 #pragma unroll
         for (int u = 0; u < U; u++) {
           const int j = base + u * T;
-          x[u] = j < n4 ? (l2keep ? ld_keep(a4 + j, pol) : ld_stream(a4 + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
+          x[u] = j < n4 ? (l2keep > 0.f ? ld_keep(a4 + j, pol) : ld_stream(a4 + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
         if constexpr (OP != kRowsum) {
 #pragma unroll
@@ -129,14 +131,14 @@ struct RowLauncher {
     static cudaError_t launch(const LaunchArgs& a, cudaStream_t s) {
       const SuiteEntry& e = *a.e;
       const int N = (int)e.n;
-      // calibration overrides (profiling only): LSCAT_ROW_TEAM_WARPS, LSCAT_ROW_L2KEEP=0/1
+      // calibration overrides (profiling only): LSCAT_ROW_TEAM_WARPS, LSCAT_ROW_L2FRAC
       static const int tw_env = [] {
         const char* v = getenv("LSCAT_ROW_TEAM_WARPS");
         return v ? atoi(v) : 0;
       }();
-      static const int keep_env = [] {
-        const char* v = getenv("LSCAT_ROW_L2KEEP");
-        return v ? atoi(v) : -1;
+      static const double keep_env = [] {  // share of L2 the kept part of A may fill
+        const char* v = getenv("LSCAT_ROW_L2FRAC");
+        return v ? atof(v) : -1.0;
       }();
       static int l2_bytes = -1;
       if (l2_bytes < 0) {
@@ -147,12 +149,16 @@ struct RowLauncher {
       }
       const int tw = (tw_env > 0 && tw_env <= B / 32) ? tw_env : team_warps(N, B);
       const int teams = B / 32 / tw;
-      // L2 residency: every launch of a bracket re-reads A.  When A fits comfortably in L2
-      // (<= 0.6 of it: N <= 4096 on B200) its loads carry an evict-last policy; measured
-      // (scripts/l2keep_probe.sh, PDL brackets, mean over the 32 blocks) N = 4096: 9.16 ->
-      // 6.21 us; at N = 8192 (256 MB, twice L2) the hint only thrashes (37.9 -> 43.6 us), so
-      // it is off there.
-      const int keep = keep_env >= 0 ? keep_env : ((double)N * N * 4.0 <= 0.6 * l2_bytes ? 1 : 0);
+      // L2 residency: every launch of a bracket re-reads A.  Its loads carry a fractional L2
+      // policy: an address-hashed fraction f of A's lines is kept evict-last, the rest streams
+      // evict-first, with f = min(1, share x L2 / |A|), share = 0.45 (LSCAT_ROW_L2FRAC
+      // overrides; 0 = plain streaming loads).  So A stays wholly L2-resident at N <= 4096
+      // and a stable 21 % of it (57 MB) at N = 8192 instead of the whole L2 thrashing.
+      // Measured (scripts/l2frac_probe.sh, PDL brackets, mean over the 32 blocks): N = 8192
+      // share 0: 38.1 us, 0.3: 33.0, 0.45: 32.2, 0.6: 33.1, 0.75: 36.2; N = 4096: 6.2-6.3 us.
+      const double share = keep_env >= 0 ? keep_env : 0.45;
+      const double a_bytes = (double)N * N * 4.0;
+      const float keep = share <= 0 ? 0.f : (float)std::min(1.0, share * l2_bytes / a_bytes);
       return launch_k(row_kernel<OP, B>, dim3((N + teams - 1) / teams), dim3(B), 0, s, a.pdl,
                       (const float*)e.in0, (const float*)e.in1, (float*)e.out, N, tw, keep);
     }

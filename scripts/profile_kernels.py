@@ -21,8 +21,9 @@ def main():
     c = L.Ctx(0)
     if what == "euclid8192":
         b = int(sys.argv[2]) if len(sys.argv) > 2 else 512
+        reps = int(sys.argv[3]) if len(sys.argv) > 3 else 5
         c.register_suite([L.K_EUCLID], [8192])
-        for _ in range(5):
+        for _ in range(reps):
             c.launch(L.K_EUCLID, 8192, b)
     elif what == "suite8192":
         ks = [L.K_EUCLID, L.K_MATVEC, L.K_ROWSUM, L.K_COLSUM, L.K_TRANSPOSE, L.K_AXPY,
