@@ -49,5 +49,9 @@ c.ingest(T(gk.astype(np.uint32), np.int32), T(gm.astype(np.uint32), np.int32),
 c.aggregation_experiment(torch.rand(1000, device="cuda") + 1, k=10, reps=200, seed=1)
 c.occupancy_block(L.K_EUCLID, list(range(32, 1025, 32)))
 c.timeout_curve(tab, [1e-3, 1.0], 1, 2, 2)
+if "--gemm-multi" in sys.argv:  # persistent GEMM with two tiles per CTA (153 tiles)
+    c.register_suite([L.K_GEMM_BF16], [2056])
+    for b in (192, 256):
+        c.launch(L.K_GEMM_BF16, 2056, b)
 torch.cuda.synchronize()
 print("sanitize run ok", st["n_rows"], c.launch_count())
