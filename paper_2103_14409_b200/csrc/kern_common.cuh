@@ -33,7 +33,11 @@ __device__ __forceinline__ uint64_t l2_evict_last_policy() {
 // leaves a stable resident part instead of thrashing.
 __device__ __forceinline__ uint64_t l2_keep_fraction_policy(float frac) {
   uint64_t pol;
+#ifdef L2_SECONDARY_UNCHANGED
+  asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_unchanged.b64 %0, %1;" : "=l"(pol) : "f"(frac));
+#else
   asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, %1;" : "=l"(pol) : "f"(frac));
+#endif
   return pol;
 }
 __device__ __forceinline__ float4 ld_keep(const float4* p, uint64_t pol) {
