@@ -342,6 +342,7 @@ def main():
                                                 "unit": "points/s", "ms_per_step": round(gms, 3),
                                                 "steps": 1}
         secondary["suite_roofline_n8192"] = suite_roofline(ctx, L, hbm_peak, load_peaks()[1])
+        secondary["full_suite_fast_policy"] = full_suite_sweep(ctx, L, launch_mode)
         cpu_rows = secondary.pop("_cpu_rows_per_s", None)
         if cpu:
             cpu["table_rows_per_s"] = cpu_rows
@@ -454,6 +455,44 @@ def suite_roofline(ctx, L, hbm_peak, tc_peak, blocks=(128, 256, 512, 1024), reps
             out[name] = {"bound": "hbm", "block": b, "us": round(ms * 1e3, 2),
                          "achieved": round(ach, 1), "unit": "GB/s", "frac": round(ach / hbm_peak, 4)}
     return out
+
+
+def full_suite_sweep(ctx, L, launch_mode):
+    """The whole suite (8 kernels x 32 blocks x 8 matrix sizes = 2048 points, SURVEY 8(d)
+    scaling workload) swept with the fast policy (1 + 5 x 20 launches), then reduced: sweep
+    points/s and the paper's statistics on this suite."""
+    import torch
+    names = ["euclid", "matvec", "gemm_bf16", "transpose", "axpy", "rowsum", "colsum", "stencil5"]
+    ks = [L.KERNELS[k] for k in names]
+    ctx.register_suite(ks, SIZES)
+    W, K, R = POLICIES["fast"]
+    ctx.sweep(ks, SIZES, BLOCKS, warmup=W, brackets=K, launches=R, launch_mode=launch_mode)  # warm
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    tab = ctx.sweep(ks, SIZES, BLOCKS, warmup=W, brackets=K, launches=R, launch_mode=launch_mode)
+    o = L.reduce_opts(len(BLOCKS), len(SIZES))
+    ctx.reduce_table(tab, o, per_group=False)
+    st = ctx.stats(o, percentiles=[0.5])
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    t = tab.to_numpy()
+    best = {}
+    for gi in range(t["n_groups"]):
+        a, b = t["group_offset"][gi], t["group_offset"][gi + 1]
+        if SIZES[t["group_matrix"][gi]] != 8192 or b <= a:
+            continue
+        rt = t["runtime_ms"][a:b]
+        if np.isfinite(rt).any():
+            j = int(np.nanargmin(rt))
+            best[names[ks.index(int(t["group_kernel"][gi]))]] = [BLOCKS[t["block_id"][a + j]],
+                                                                  round(float(rt[j]) * 1e3, 2)]
+    return {"points": int(t["n_rows"]), "policy": f"fast: W={W} K={K} R={R}",
+            "points_per_s": round(t["n_rows"] / (ms / 1e3), 2), "ms": round(ms, 1),
+            "n_nan_rows": int(st["n_nan"]), "frac_largest_not_best": round(st["frac_largest_not_best"], 4),
+            "mean_perf_largest": round(st["mean_perf"], 4), "frac_gain_gt_20pct": round(st["frac_gain_gt"], 4),
+            "best_block_us_at_n8192": best}
 
 
 def table_benches(ctx, L, hbm_peak):
