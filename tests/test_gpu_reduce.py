@@ -309,3 +309,58 @@ def test_percentiles_dense_bin_compaction():
                group_offset=np.arange(0, 2 * G + 1, 2, dtype=np.int64),
                group_matrix=np.zeros(G, np.uint32))
     _compare(tab, L=2, M=1, ell=1, pcts=[0.01, 0.2, 0.5, 0.7, 0.8, 0.9, 0.95, 0.99])
+
+
+def test_scaled_table_1e9_sampled():
+    """configs[4] at full size, the configuration bench.py times: 10^9 rows = 31.25 M uniform
+    32-row groups (no offset array).  The counters obey every invariant; per-group outputs are
+    bit-exact against the oracle on sampled windows of groups (their rows regenerated by the
+    CPU twin of the generator and compared byte for byte first); every percentile satisfies the
+    nearest-rank property over the device's per-group values (properties that hold at any
+    size, R-13)."""
+    import torch
+    from paper_2103_14409_b200 import reduce_opts, PRESET_T4
+    c = ctx()
+    n, K, L, M = 1_000_000_000, 3_906_250, 32, 8
+    G = n // L
+    tab = c.gen_table(n, K, preset=PRESET_T4, seed=10 ** 9, offsets=False)
+    o = reduce_opts(L, M)
+    out = c.reduce_table(tab, o)
+    st = c.stats(o, percentiles=PCTS)
+    assert st["n_rows"] == n and st["n_groups"] == G
+    assert st["n_ok"] + st["n_nan"] + st["n_invalid"] == n
+    nrd = st["n_ratio_defined"]
+    assert int(st["perf_hist"].sum()) == nrd == int(st["gain_hist"].sum())
+    assert int(st["best_block_hist"].sum()) == st["n_defined"]
+    assert st["n_largest_is_best"] <= nrd and st["n_gain_gt"] <= nrd
+    # sampled windows of 256 groups (first, last and six inside) vs the oracle
+    W = 256
+    rng = np.random.default_rng(1)
+    starts = [0, G - W] + sorted(int(x) for x in rng.integers(1, G - W, 6))
+    for g0 in starts:
+        h = gen_table(n, K, preset="t4", seed=10 ** 9, group_begin=g0, group_end=g0 + W)
+        r0, r1 = g0 * L, (g0 + W) * L
+        dev_rt = tab.runtime_ms[r0:r1].cpu().numpy()
+        dev_id = tab.block_id[r0:r1].cpu().numpy().view(np.uint16)
+        assert (dev_rt.view(np.uint32) == h["runtime_ms"].view(np.uint32)).all()
+        assert (dev_id == h["block_id"]).all()
+        ref = OT.reduce_table(h["runtime_ms"], h["block_id"], rows_per_group=L, first_group=g0,
+                              opts=OT.Opts(n_blocks=L, n_matrices=M))
+        sl = slice(g0, g0 + W)
+        assert (out["best_block_id"][sl].cpu().numpy().view(np.uint16) == ref.best_block).all()
+        assert (out["best_runtime"][sl].cpu().numpy().view(np.uint32) == ref.best_runtime.view(np.uint32)).all()
+        pf, gn = out["perf"][sl].cpu().numpy(), out["gain"][sl].cpu().numpy()
+        assert ((pf == ref.perf) | (np.isnan(pf) & np.isnan(ref.perf))).all()
+        assert ((gn == ref.gain) | (np.isnan(gn) & np.isnan(ref.gain))).all()
+        assert (out["flags"][sl].cpu().numpy().view(np.uint32) == ref.flags).all()
+    # nearest rank: the k-th smallest value v (k = clamp(ceil(p n), 1, n)) has fewer than k
+    # values below it and at least k at or below it
+    for q, vals in (("perf", st["pct_perf"]), ("gain", st["pct_gain"])):
+        x = out[q]
+        for p, v in zip(PCTS, vals):
+            k = min(max(int(np.ceil(p * nrd)), 1), nrd)
+            lt = int((x < v).sum().item())
+            le = int((x <= v).sum().item())
+            assert lt < k <= le, (q, p, v, lt, k, le)
+    del out, tab
+    torch.cuda.empty_cache()

@@ -171,3 +171,33 @@ def test_pdl_graph_mode_outputs(n):
     As = f("stencil5", 0).reshape(n, n)
     Os = f("stencil5", 2).reshape(n, n)
     assert (np.abs(Os - OK.stencil5(As)) <= 1e-5 * OK.stencil5_abs_scale(As)).all()
+
+
+def test_bench_launch_configuration_n8192():
+    """The configuration bench.py times: euclidean_kernel at N = 8192 swept in PDL graph
+    brackets of R = 1000 launches (7 graphs of 128 + one of 104) with the fractional L2 policy
+    on A; afterwards the output equals the oracle on sampled rows (fp32 vs fp64, 1e-5 of the
+    row's distance), and the measured per-launch time is physically plausible (no faster than
+    the non-L2-resident part of A at 10 TB/s)."""
+    import torch
+    from oracle import kernels as OK
+    from paper_2103_14409_b200 import K_EUCLID, LAUNCH_GRAPH_PDL, ROW_OK
+    n = 8192
+    c = ctx()
+    c.register_suite([K_EUCLID], [n])
+    out = c.suite_tensor(K_EUCLID, n, 2)
+    out.fill_(float("nan"))
+    t = c.sweep([K_EUCLID], [n], [32, 352, 1024], warmup=1, brackets=2, launches=1000,
+                launch_mode=LAUNCH_GRAPH_PDL).to_numpy()
+    assert (t["status"] == ROW_OK).all() and np.isfinite(t["runtime_ms"]).all()
+    l2 = torch.cuda.get_device_properties(0).L2_cache_size
+    nbytes = 4 * n * n
+    resident = min(1.0, 0.45 * l2 / nbytes)
+    assert (t["runtime_ms"] * 1e-3 > (1 - resident) * nbytes / 10e12).all()
+    torch.cuda.synchronize()
+    A = c.suite_tensor(K_EUCLID, n, 0).view(n, n)
+    q = c.suite_tensor(K_EUCLID, n, 1).cpu().numpy()
+    rows = np.r_[0:4, np.random.default_rng(3).choice(n, 60, replace=False), n - 4:n]
+    ref = OK.euclid(A[torch.as_tensor(rows, device=A.device)].cpu().numpy(), q)
+    got = out.cpu().numpy()[rows]
+    assert (np.abs(got - ref) <= 1e-5 * ref).all()
