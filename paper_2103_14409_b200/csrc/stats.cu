@@ -11,7 +11,7 @@
 //               when the range holds <= cap keys, gather it;
 //   sel_resolve one CTA per range: scan its histogram (narrow each target to its bin) or sort
 //               its gathered keys (bitonic, shared memory) and pick each target's rank;
-//   sel_plan    merge the open targets into the next level's ranges.
+//   (plan)      the last sel_resolve CTA merges the open targets into the next level's ranges.
 // The host launches levels in batches of four and reads the state once per batch (one sync
 // for the common case).  `base` skips the empty low binades of a level-0 range whose minimum
 // is far below its maximum (gain = 0 next to gains of order 1).  With world > 1 the histograms
@@ -63,6 +63,8 @@ struct SelState {
   uint32_t src;               // 0: passes read perf/gain; 1: the compacted keys
   uint32_t compact;           // 1: the next pass also copies the keys it counts (src 0 only)
   uint32_t r0_valid;          // bit w: r0[w] holds quantity w's level-0 range
+  uint32_t done_ctas;         // sel_resolve CTAs finished (the last one plans; reset to 0)
+  uint32_t pad2;
   unsigned long long nc[2];   // compacted keys per quantity
   uint64_t n_def;
   Range r0[2];                // level-0 ranges: later full passes filter keys by level-0 bin
@@ -105,7 +107,7 @@ __device__ Range make_range(uint64_t lo, uint64_t hi, uint64_t count, uint32_t w
 __device__ __forceinline__ uint64_t t_count(const SelState* st, int i) { return st->t[i].count; }
 
 // Merge the open targets into disjoint ranges sorted by (which, lo).  One CTA; thread i < nt
-// owns target i.  Called by sel_init and sel_plan.
+// owns target i.  Called by sel_init and by the last CTA of sel_resolve.
 __device__ void plan_ranges(SelState* st, uint32_t cap) {
   __shared__ uint64_t slo[kMaxT], shi[kMaxT];
   __shared__ uint32_t sw[kMaxT], sopen[kMaxT], sfirst[kMaxT];
@@ -169,6 +171,7 @@ __global__ void __launch_bounds__(kMaxT) sel_init(SelState* st, const uint64_t* 
   if (i == 0) {
     st->nt = 2 * npct;
     st->err = 0;
+    st->done_ctas = 0;
     st->src = 0;
     st->compact = 0;
     st->n_def = n_def;
@@ -198,10 +201,6 @@ __global__ void __launch_bounds__(kMaxT) sel_init(SelState* st, const uint64_t* 
   }
 }
 
-__global__ void __launch_bounds__(kMaxT) sel_plan(SelState* st, uint32_t cap) {
-  if (st->nr == 0) return;
-  plan_ranges(st, cap);
-}
 
 // One pass over this rank's values (src 0: perf/gain[lo, hi); src 1: the compacted keys).
 // cand = [kMaxR counts][kMaxR x cap keys]; cbuf = [2][kCompactCap] compacted keys.
@@ -463,16 +462,14 @@ __global__ void __launch_bounds__(kT, kSmem ? 2 : 4) sel_pass(const double* __re
 // One CTA per open range.  Histogram ranges: narrow every target of the range to the bin that
 // holds its rank, then zero the histogram for the next level.  Gathered ranges: sort the keys
 // of all ranks and pick.  cand_all = world x [kMaxR counts][kMaxR x cap keys].
-__global__ void __launch_bounds__(1024) sel_resolve(SelState* st, uint32_t* __restrict__ hist,
-                                                    const unsigned long long* __restrict__ cand_all,
-                                                    unsigned long long* __restrict__ cand_own, int world,
-                                                    uint32_t cap) {
+__device__ void resolve_range(SelState* st, uint32_t* __restrict__ hist,
+                              const unsigned long long* __restrict__ cand_all,
+                              unsigned long long* __restrict__ cand_own, int world, uint32_t cap) {
   extern __shared__ unsigned long long sk[];
   __shared__ unsigned long long wsum[32];
   __shared__ unsigned long long s_total;
   __shared__ unsigned long long s_k[kMaxT];
   const uint32_t r = blockIdx.x;
-  if (r >= st->nr) return;
   const Range R = st->r[r];
   const int nt = (int)st->nt;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -578,6 +575,27 @@ __global__ void __launch_bounds__(1024) sel_resolve(SelState* st, uint32_t* __re
   }
 }
 
+// sel_resolve: one CTA per open range (resolve_range); the last CTA to finish then plans the
+// next level's ranges (plan_ranges), so a level is two launches (pass, resolve) instead of three.
+// Every early exit inside resolve_range is CTA-uniform.
+__global__ void __launch_bounds__(1024) sel_resolve(SelState* st, uint32_t* __restrict__ hist,
+                                                    const unsigned long long* __restrict__ cand_all,
+                                                    unsigned long long* __restrict__ cand_own, int world,
+                                                    uint32_t cap) {
+  __shared__ bool s_last;
+  if (blockIdx.x < st->nr) resolve_range(st, hist, cand_all, cand_own, world, cap);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&st->done_ctas, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) st->done_ctas = 0;
+  if (st->nr) plan_ranges(st, cap);
+}
+
 lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct, double* out_perf,
                                 double* out_gain, cudaStream_t s) {
   const ReduceState& rs = ctx->rs;
@@ -639,8 +657,6 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
       }
       sel_resolve<<<kMaxR, 1024, res_smem, q>>>(st, hist, cand_all, cand, world, cap);
       LSCAT_CUDA(ctx, cudaGetLastError());
-      sel_plan<<<1, kMaxT, 0, q>>>(st, cap);
-      LSCAT_CUDA(ctx, cudaGetLastError());
     }
     LSCAT_CUDA(ctx, cudaMemcpyAsync(hst, st, sizeof(SelState), cudaMemcpyDeviceToHost, q));
     return LSCAT_OK;
@@ -690,12 +706,12 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
   } else {
     if ((ls = enqueue_first(s))) return ls;
   }
-  ctx->launches += 1 + 3 * kLevelsPerBatch;
+  ctx->launches += 1 + 2 * kLevelsPerBatch;
   for (int batch = 0;; batch++) {
     if (batch == 8) return fail(ctx, LSCAT_ERR_STATE, "stats: percentile selection did not converge");
     if (batch > 0) {
       if ((ls = enqueue_levels(s, false))) return ls;
-      ctx->launches += 3 * kLevelsPerBatch;
+      ctx->launches += 2 * kLevelsPerBatch;
     }
     LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
     if (debug)
