@@ -278,17 +278,18 @@ def main():
                 "all_blocks_gbs_min_max": [round(min(all_blocks_gbs), 1), round(max(all_blocks_gbs), 1)]}
         # A (268 MB) is twice L2: the row kernel keeps an address-hashed fraction f of its lines
         # L2-resident across the launches of a bracket (fractional evict-last policy, share
-        # 0.45 of L2), so per launch about (1 - f) of the algorithmic bytes come from DRAM
+        # 0.45 of L2); `traffic` is the DRAM bytes per launch in that steady state (committed
+        # ncu capture, application replay, no cache flush), so DRAM GB/s = traffic / time
         l2 = torch.cuda.get_device_properties(lrank).L2_cache_size
         share = float(os.environ.get("LSCAT_ROW_L2FRAC", "0.45"))
-        f = min(1.0, share * l2 / nbytes) if share > 0 else 0.0
-        roof["l2_resident_fraction"] = round(f, 4)
-        roof["dram_gbs_est"] = round((1 - f) * nbytes / (mean_ms * 1e-3) / 1e9, 1)
-        roof["dram_frac_est"] = round((1 - f) * nbytes / (mean_ms * 1e-3) / 1e9 / hbm_peak, 4)
+        roof["l2_resident_fraction"] = round(min(1.0, share * l2 / nbytes) if share > 0 else 0.0, 4)
+        if tr:
+            roof["dram_gbs"] = round(tr / (mean_ms * 1e-3) / 1e9, 1)
+            roof["dram_frac"] = round(tr / (mean_ms * 1e-3) / 1e9 / hbm_peak, 4)
         roof["note"] = ("frac = algorithmic bytes / time (contract); part of A is served from L2 "
-                        "across the bracket's back-to-back launches (l2_resident_fraction), so the "
-                        "DRAM stream is about dram_gbs_est (an estimate: (1 - f) x bytes / time); traffic = ncu --set full "
-                        "capture with L2 flushed (cold launch)")
+                        "across the bracket's back-to-back launches, so DRAM traffic per launch "
+                        "(traffic, ncu steady state) is below the algorithmic bytes and "
+                        "dram_frac = traffic / time / peak is the DRAM-side fraction")
     per_n = {}
     for gi, n in enumerate(SIZES):
         a, b = tab["group_offset"][gi], tab["group_offset"][gi + 1]

@@ -14,6 +14,7 @@ for job in "$@"; do
     ncu_euclid) timeout 600 ncu --set full --clock-control none --import-source on -k regex:row_kernel -c 2 -o gpurun_out/prof_euclid -f python scripts/profile_kernels.py euclid8192 512 > gpurun_out/ncu_euclid.log 2>&1; echo "ncu_euclid rc=$?" ;;
     ncu_euclid32) timeout 600 ncu --set full --clock-control none --import-source on -k regex:row_kernel -c 2 -o gpurun_out/prof_euclid32 -f python scripts/profile_kernels.py euclid8192 32 > gpurun_out/ncu_euclid32.log 2>&1; echo "ncu_euclid32 rc=$?" ;;
     ncu_steady) timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct --cache-control none --clock-control none -k regex:row_kernel --csv --log-file gpurun_out/euclid_steady.csv python scripts/profile_kernels.py euclid8192 32 30 > gpurun_out/ncu_steady.log 2>&1; echo "ncu_steady rc=$?" ;;
+    ncu_euclid_steady_full) timeout 1500 ncu --set full --replay-mode application --cache-control none --clock-control none --import-source on -k regex:row_kernel -s 20 -c 1 -o gpurun_out/prof_euclid32_steady -f python scripts/profile_kernels.py euclid8192 32 24 > gpurun_out/ncu_euclid_steady_full.log 2>&1; echo "ncu_euclid_steady_full rc=$?" ;;
     ncu_transpose) timeout 600 ncu --set full --clock-control none --import-source on -k regex:transpose -c 1 -s 1 -o gpurun_out/prof_transpose -f python scripts/profile_kernels.py kernel transpose 8192 512 > gpurun_out/ncu_tp.log 2>&1; echo "ncu_transpose rc=$?" ;;
     ncu_gemm) timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_kernel -c 1 -o gpurun_out/prof_gemm -f python scripts/profile_kernels.py gemm8192 256 > gpurun_out/ncu_gemm.log 2>&1; echo "ncu_gemm rc=$?" ;;
     launches) timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --policy tiny --steps 1 --warmup 0 --no-e2e --no-secondary --no-cpu > gpurun_out/launches_bench.log 2>&1; echo "launches rc=$?" ;;
