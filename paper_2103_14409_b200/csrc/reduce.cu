@@ -185,7 +185,8 @@ __device__ void finalize_lane(const RP& p, uint64_t g, bool active, const GroupA
   int pbin = -1, gbin = -1, bbi = -1;
   if (defined) {
     flags |= LSCAT_GF_DEFINED;
-    const uint32_t mat = p.gmat ? p.gmat[g] : (uint32_t)((p.first_group + g) % p.M);
+    const uint64_t ag = p.first_group + g;  // implicit matrix index: a mask when M is a power of 2
+    const uint32_t mat = p.gmat ? p.gmat[g] : (uint32_t)((p.M & (p.M - 1)) == 0 ? (ag & (p.M - 1)) : ag % p.M);
     bbi = (int)(mat * p.L + a.min_bid);
     if (a.lcode == 2) {
       flags |= LSCAT_GF_RATIO_DEFINED;
@@ -372,7 +373,7 @@ __device__ __forceinline__ void uniform_fold(const RP& p, uint32_t srt, uint32_t
               y.z == (((w0 + 5) << 16) | (w0 + 4)) && y.w == (((w0 + 7) << 16) | (w0 + 6));
   }
   uint32_t mkey = 0xFFFFFFFFu, mpos = 0xFFFFFFFFu, okm = 0;
-#pragma unroll 2
+#pragma unroll  // fully: the bit positions 4c + q of okm / mpos become constants
   for (int c = 0; c < 8; c++) {
     const uint4 x = lds128(rbase + 16 * (c ^ sw));
     const uint32_t b4[4] = {x.x, x.y, x.z, x.w};
