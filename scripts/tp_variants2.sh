@@ -1,5 +1,6 @@
 #!/bin/bash
-# transpose: store policy and unit-order variants at N = 8192 (calibration)
+# transpose calibration (round 1): the -D variants (TP_STORE_PLAIN, TP_ORDER, TP_COPY, TP_PIPE) were
+# experimental switches measured and then removed from kern_move.cu (results: profiles/r01_summary.md)
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 python __graft_entry__.py build > gpurun_out/build.log 2>&1 || { echo BUILD FAILED; exit 1; }
