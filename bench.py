@@ -300,10 +300,20 @@ def main():
             if n >= 4096:
                 per_n[f"{n}_by_block"] = [round(float(x), 1) for x in v]
     rooflines = None
+    spread = None
     if world > 1:
         objs = [None] * world
         dist.all_gather_object(objs, roof)
         roof = next((r for r in objs if r), None)
+        # SURVEY 8(e) caveat: a group's blocks are timed on different GPUs; the same calibration
+        # point (euclid N = 8192, block 32, one bracket of 200 launches) on every rank gives the
+        # cross-device timing spread
+        cal = ctx.sweep(ks, [8192], [32], warmup=1, brackets=1, launches=200,
+                        launch_mode=launch_mode).to_numpy()
+        times = [None] * world
+        dist.all_gather_object(times, float(cal["runtime_ms"][0]) * 1e3)
+        spread = {"point": "euclid N=8192 block=32, 1 x 200 launches", "us_by_rank": [round(x, 3) for x in times],
+                  "max_over_min": round(max(times) / min(times), 4)}
 
     # ---- e2e through the C ABI with host buffers
     e2e = None
@@ -362,7 +372,7 @@ def main():
                        "(512 MB write); N=8192 inputs (268 MB) exceed L2 (126 MB)"},
             "clocks": ck, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
             "e2e": e2e, "secondary": secondary,
-            "per_n_launch_us": per_n,
+            "per_n_launch_us": per_n, "cross_device_spread": spread,
             "stats_last_step": {k: last[1][k] for k in ("n_rows", "n_ratio_defined",
                                                       "n_largest_is_best", "mean_perf",
                                                       "frac_largest_not_best")},
