@@ -306,13 +306,21 @@ def main():
         dist.all_gather_object(objs, roof)
         roof = next((r for r in objs if r), None)
         # SURVEY 8(e) caveat: a group's blocks are timed on different GPUs; the same calibration
-        # point (euclid N = 8192, block 32, one bracket of 200 launches) on every rank gives the
-        # cross-device timing spread
-        cal = ctx.sweep(ks, [8192], [32], warmup=1, brackets=1, launches=200,
-                        launch_mode=launch_mode).to_numpy()
+        # point (euclid N = 8192, block 32, 200 back-to-back launches, CUDA events) on every
+        # rank gives the cross-device timing spread (the sweep itself shards points, so it is
+        # timed here with direct launches)
+        for _ in range(10):
+            ctx.launch(L.K_EUCLID, 8192, 32)
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        c0.record(stream)
+        for _ in range(200):
+            ctx.launch(L.K_EUCLID, 8192, 32)
+        c1.record(stream)
+        torch.cuda.synchronize()
         times = [None] * world
-        dist.all_gather_object(times, float(cal["runtime_ms"][0]) * 1e3)
-        spread = {"point": "euclid N=8192 block=32, 1 x 200 launches", "us_by_rank": [round(x, 3) for x in times],
+        dist.all_gather_object(times, c0.elapsed_time(c1) / 200 * 1e3)
+        spread = {"point": "euclid N=8192 block=32, 200 stream launches", "us_by_rank": [round(x, 3) for x in times],
                   "max_over_min": round(max(times) / min(times), 4)}
 
     # ---- e2e through the C ABI with host buffers
