@@ -101,6 +101,10 @@ struct lscat_ctx {
   // percentile selection: first batch (init + 3 levels + state read-back) as a graph, keyed by
   // every pointer / size / percentile it bakes in (stats.cu; world == 1)
   std::vector<std::pair<std::string, cudaGraphExec_t>> sel_graphs;
+  // kernel attributes / occupancy already set or queried on this context's device (host calls
+  // kept off the launch path of the small tables)
+  std::map<std::pair<bool, size_t>, int> red_occ;
+  int sel_occ0 = 0, sel_occ1 = 0;
   std::vector<cudaEvent_t> events;
   // comm
   lscat::Comm* comm = nullptr;  // NCCL, or the local test transport (comm.h)
@@ -121,6 +125,9 @@ bool is_sticky(cudaError_t e);
 void* scratch(lscat_ctx* ctx, const char* name, size_t bytes, cudaError_t* err);
 // pinned host staging (grow-only) keyed by name
 void* pinned(lscat_ctx* ctx, const char* name, size_t bytes, cudaError_t* err);
+// Raise a kernel's max-dynamic-shared-memory attribute on the current device to at least
+// `bytes` (device-global state: never lowered, set once per (kernel, device, size increase)).
+cudaError_t ensure_smem_attr(const void* func, size_t bytes);
 // host-side work model
 void kernel_work(uint32_t kernel, uint32_t n, uint64_t* bytes, uint64_t* flops);
 bool block_list_ok(const uint16_t* blocks, uint32_t n);

@@ -5,6 +5,8 @@
 #include <numeric>
 #include <queue>
 
+#include <mutex>
+
 #include "common.h"
 
 namespace lscat {
@@ -125,6 +127,23 @@ const KernelTable* kernel_table(uint32_t kernel) {
 
 using namespace lscat;
 
+namespace lscat {
+cudaError_t ensure_smem_attr(const void* func, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  static std::mutex m;
+  static std::map<std::pair<const void*, int>, size_t> set;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(m);
+  size_t& cur = set[{func, dev}];
+  if (bytes <= cur) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) cur = bytes;
+  return e;
+}
+}  // namespace lscat
+
 extern "C" {
 
 int lscat_abi_version(void) { return LSCAT_ABI_VERSION; }
@@ -186,6 +205,7 @@ void lscat_ctx_destroy(lscat_ctx* c) {
 }
 
 const char* lscat_last_error(const lscat_ctx* c) { return c ? c->err.c_str() : ""; }
+
 
 lscat_status lscat_launch_count(const lscat_ctx* c, uint64_t* out) {
   if (!c || !out) return LSCAT_ERR_INVALID_ARG;

@@ -22,6 +22,7 @@
 // shared-memory histograms and CTA counters, flushed once per CTA with 64-bit atomics.
 // HBM: 6 B/row read (+16 B/group of perf/gain written).
 #include <algorithm>
+#include <map>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -802,20 +803,27 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
   LSCAT_CUDA(ctx, cudaMemsetAsync(p.partials, 0, plen * 8, s));
   init_minmax<<<1, 1, 0, s>>>(p.minmax);
   ctx->launches++;
-  if (smem > 48 * 1024) {
-    LSCAT_CUDA(ctx, cudaFuncSetAttribute(reduce_groups_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    LSCAT_CUDA(ctx, cudaFuncSetAttribute(finalize_merged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fin));
-  }
+  // kernel attributes and occupancy are host calls on the launch path: set/queried once per
+  // shared-memory size (the small tables of configs[2]/[3] are launch-latency bound)
+  LSCAT_CUDA(ctx, ensure_smem_attr((const void*)reduce_groups_kernel, smem));
+  LSCAT_CUDA(ctx, ensure_smem_attr((const void*)finalize_merged_kernel, smem_fin));
   const bool merge = ctx->world > 1 && o->point_sharded;
   const uint64_t warps_needed = (G + 31) / 32;
   const bool uniform = p.vec && p.rpg == 32;
   auto kern = uniform ? reduce_uniform32_kernel : reduce_groups_kernel;
   if (uniform) {
     smem = smem_hist + kUniStageBytes;
-    LSCAT_CUDA(ctx, cudaFuncSetAttribute(reduce_uniform32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    LSCAT_CUDA(ctx, ensure_smem_attr((const void*)reduce_uniform32_kernel, smem));
   }
   int occ = 0;
-  LSCAT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem));
+  const auto ok = std::make_pair(uniform, smem);
+  const auto it = ctx->red_occ.find(ok);
+  if (it != ctx->red_occ.end()) {
+    occ = it->second;
+  } else {
+    LSCAT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem));
+    ctx->red_occ[ok] = occ;
+  }
   const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)ctx->sm_count * std::max(occ, 1), (warps_needed + 7) / 8));
   p.acc_lo = 0;
   p.acc_hi = G;
@@ -858,7 +866,7 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
     uint64_t* prof = p.partials + kNC + sh_words;  // [sum ML][count ML]
     const size_t psm = ML * 12;
     if (psm > 48 * 1024)
-      LSCAT_CUDA(ctx, cudaFuncSetAttribute(profile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
+      LSCAT_CUDA(ctx, ensure_smem_attr((const void*)profile_kernel, psm));
     const int g3 = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)ctx->sm_count * 8, (G + 7) / 8));
     profile_kernel<<<g3, 256, psm, s>>>(p, p.o_bestrt, p.o_flags, prof, prof + ML);
     ctx->launches++;

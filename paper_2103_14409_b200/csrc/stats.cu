@@ -621,17 +621,15 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
   constexpr int kT0 = 512, kT1 = 256;
   const int pass_smem = kSmemRanges * kBins * 4, res_smem = (int)cap * 8;
   // kernel attributes and occupancy: once per process (per resolve smem size)
-  static int occ0 = 0, occ1 = 0, res_smem_set = 0;
+  int& occ0 = ctx->sel_occ0;
+  int& occ1 = ctx->sel_occ1;
+  LSCAT_CUDA(ctx, ensure_smem_attr((const void*)sel_pass<true, kT0>, pass_smem));
+  LSCAT_CUDA(ctx, ensure_smem_attr((const void*)sel_resolve, res_smem));
   if (!occ0) {
-    LSCAT_CUDA(ctx, cudaFuncSetAttribute(sel_pass<true, kT0>, cudaFuncAttributeMaxDynamicSharedMemorySize, pass_smem));
     LSCAT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ0, sel_pass<true, kT0>, kT0, pass_smem));
     LSCAT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, sel_pass<false, kT1>, kT1, 0));
     occ0 = std::max(occ0, 1);
     occ1 = std::max(occ1, 1);
-  }
-  if (res_smem_set < res_smem) {
-    LSCAT_CUDA(ctx, cudaFuncSetAttribute(sel_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, res_smem));
-    res_smem_set = res_smem;
   }
   // grids: every resident CTA once (occupancy API), capped by the work (kU x 32 groups per warp)
   const uint64_t n = rs.own_hi - rs.own_lo;
