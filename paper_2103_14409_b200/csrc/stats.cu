@@ -34,7 +34,10 @@ constexpr int kMaxT = 128;            // targets: 2 x <= 64 percentiles
 constexpr int kMaxR = kMaxT;          // open ranges per level (<= open targets)
 static_assert(kMaxR <= 128, "sel_pass range search covers 128 ranges");
 constexpr int kSmemRanges = 2;        // histograms privatised in shared memory up to this many
-constexpr int kLevelsPerBatch = 4;
+constexpr int kLevelsPerBatch = 4;       // levels per host sync (large inputs)
+constexpr int kLevelsPerBatchSmall = 2;  // up to kSmallKeys keys per quantity: level 0 narrows
+constexpr uint64_t kSmallKeys = 1ull << 20;  // each target to a bin of a few hundred keys at most,
+                                             // level 1 gathers and sorts it
 constexpr uint64_t kGapKeys = 32ull << 52;  // 32 binades: keys below hi - kGapKeys share bin 1
 constexpr uint64_t kNaNKey = 0x7FF8000000000000ull;
 // Once the open ranges hold at most this many keys per quantity (and at most half of them), one
@@ -639,10 +642,11 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
                                              (uint64_t)ctx->sm_count * occ1);
   PctArg pa{};
   for (uint32_t i = 0; i < npct; i++) pa.p[i] = pct[i];
-  // One batch: kLevelsPerBatch levels of pass -> (merge) -> resolve -> plan, then the state
+  const int lpb = n <= kSmallKeys ? kLevelsPerBatchSmall : kLevelsPerBatch;
+  // One batch: lpb levels of pass -> (merge) -> resolve -> plan, then the state
   // is read back (one host sync per batch).
   auto enqueue_levels = [&](cudaStream_t q, bool first) -> lscat_status {
-    for (int level = 0; level < kLevelsPerBatch; level++) {
+    for (int level = 0; level < lpb; level++) {
       if (first && level == 0)
         sel_pass<true, kT0><<<grid0, kT0, pass_smem, q>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, st, hist, cand, cap, cbuf);
       else
@@ -704,12 +708,12 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
   } else {
     if ((ls = enqueue_first(s))) return ls;
   }
-  ctx->launches += 1 + 2 * kLevelsPerBatch;
+  ctx->launches += 1 + 2 * lpb;
   for (int batch = 0;; batch++) {
     if (batch == 8) return fail(ctx, LSCAT_ERR_STATE, "stats: percentile selection did not converge");
     if (batch > 0) {
       if ((ls = enqueue_levels(s, false))) return ls;
-      ctx->launches += 2 * kLevelsPerBatch;
+      ctx->launches += 2 * lpb;
     }
     LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
     if (debug)
