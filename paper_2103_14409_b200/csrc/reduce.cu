@@ -624,8 +624,13 @@ __global__ void __launch_bounds__(kThreads) finalize_merged_kernel(RP p) {
 }
 
 
-__global__ void init_minmax(uint64_t* mm) {
-  mm[0] = ~0ull; mm[1] = 0; mm[2] = ~0ull; mm[3] = 0;
+// Zero the partial vector and reset the key min/max in one launch (was a memset + a kernel).
+__global__ void init_partials(uint64_t* __restrict__ partials, size_t plen, uint64_t* __restrict__ mm) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < plen; i += (size_t)gridDim.x * blockDim.x)
+    partials[i] = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    mm[0] = ~0ull; mm[1] = 0; mm[2] = ~0ull; mm[3] = 0;
+  }
 }
 
 size_t partials_len(const lscat_reduce_opts& o) {
@@ -800,8 +805,7 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
   if (err) return cuda_fail(ctx, err, "reduce_table: scratch");
   p.minmax = (uint64_t*)scratch(ctx, "minmax", 4 * 8, &err);
   if (err) return cuda_fail(ctx, err, "reduce_table: scratch");
-  LSCAT_CUDA(ctx, cudaMemsetAsync(p.partials, 0, plen * 8, s));
-  init_minmax<<<1, 1, 0, s>>>(p.minmax);
+  init_partials<<<(unsigned)std::min<size_t>(64, (plen + 255) / 256), 256, 0, s>>>(p.partials, plen, p.minmax);
   ctx->launches++;
   // kernel attributes and occupancy are host calls on the launch path: set/queried once per
   // shared-memory size (the small tables of configs[2]/[3] are launch-latency bound)
@@ -854,8 +858,8 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
     p.acc_hi = own_hi;
     // reset accumulators written by the partial pass (none: partials untouched by mode 1
     // except zero-valued flushes), then finalize all groups, accumulating the owned range
-    LSCAT_CUDA(ctx, cudaMemsetAsync(p.partials, 0, plen * 8, s));
-    init_minmax<<<1, 1, 0, s>>>(p.minmax);
+    init_partials<<<(unsigned)std::min<size_t>(64, (plen + 255) / 256), 256, 0, s>>>(p.partials, plen, p.minmax);
+    ctx->launches++;
     p.mode = MODE_FINALIZE_MERGED;
     const int g2 = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)ctx->sm_count * 4, (G + 255) / 256));
     if (G) finalize_merged_kernel<<<g2, 256, smem_fin, s>>>(p), ctx->launches++;
