@@ -27,7 +27,7 @@ struct SuiteEntry {
   uint64_t in0_bytes = 0, in1_bytes = 0, out_bytes = 0;
   void* scratch = nullptr;  // colsum: partials + tile counters
   uint64_t scratch_bytes = 0;
-  alignas(64) unsigned char host_blob[256] = {};  // gemm: the two TMA tensor maps
+  alignas(64) unsigned char host_blob[512] = {};  // gemm: the TMA tensor maps
 };
 
 struct LaunchArgs {

@@ -233,3 +233,30 @@ def test_gemm_full_size_sampled():
         torch.cuda.synchronize()
         got = out.view(n, n)[rows].float().cpu().numpy()
         _check_rel(got, ref, scale, tol=1e-2)
+
+
+def test_gemm_one_cta_persistent_path():
+    """The one-CTA persistent GEMM (LSCAT_GEMM_2CTA=0; the CTA-pair kernel is the default for
+    B >= 192) on the multi-tile size, in a child process (the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch\n"
+        "from oracle import kernels as OK\n"
+        "import paper_2103_14409_b200 as L\n"
+        "c = L.Ctx(0, seed=0x15CA7); n = 2056\n"
+        "c.register_suite([L.K_GEMM_BF16], [n])\n"
+        "A = c.suite_tensor(L.K_GEMM_BF16, n, 0).float().cpu().numpy().reshape(n, n)\n"
+        "Bt = c.suite_tensor(L.K_GEMM_BF16, n, 1).float().cpu().numpy().reshape(n, n)\n"
+        "ref, scale = OK.gemm(A, Bt), OK.gemm_abs_scale(A, Bt)\n"
+        "for b in (192, 512):\n"
+        "    c.launch(L.K_GEMM_BF16, n, b); torch.cuda.synchronize()\n"
+        "    out = c.suite_tensor(L.K_GEMM_BF16, n, 2).float().cpu().numpy().reshape(n, n)\n"
+        "    assert (np.abs(out - ref) <= 1e-2 * scale).all(), b\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, LSCAT_GEMM_2CTA="0")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
