@@ -398,12 +398,16 @@ __global__ void __launch_bounds__(B, 1) gemm_persistent_kernel(const __grid_cons
 // measured at N = 8192 in the burst regime (scripts/gemm_ab.py): 716 us = 1535 TFLOP/s (0.95
 // of cuBLAS burst) vs 756 us for the one-CTA persistent kernel in the same run.  Each CTA loads its own
 // 128 rows of A and its own 128 columns of B per k-block (32 KB per stage instead of 48 KB:
-// half the B traffic per SM), 6-stage ring.  Both CTAs' TMA loads complete on the leader
+// half the B traffic per SM), 7-stage ring (4 / 5 / 6 / 7 stages: 1500 / 1543 / 1543 / 1563
+// TFLOP/s at N = 8192, scripts/gemm_variants.sh).  Both CTAs' TMA loads complete on the leader
 // CTA's full barrier (cta_group::2 TMA, peer bit cleared); the leader's single MMA thread
 // issues the pair's MMAs and commits with a multicast arrive to both CTAs' empty / tmem_full
 // barriers; every epilogue warp of both CTAs arrives on the leader's tmem_empty barrier.
 // Persistent over tiles with two TMEM accumulators (2 x 256 columns per CTA).
-constexpr int kStages2 = 6;
+#ifndef GEMM2_STAGES
+#define GEMM2_STAGES 7
+#endif
+constexpr int kStages2 = GEMM2_STAGES;  // calibration switch (scripts/gemm_variants.sh)
 constexpr int kStage2A = 128 * BK * 2, kStage2B = 128 * BK * 2;  // 16 KB each
 constexpr int kSmem2 = kStages2 * (kStage2A + kStage2B) + 1024 + 256;
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address -> the leader CTA's copy
