@@ -28,6 +28,9 @@ enum RowOp { kEuclid = 0, kMatvec = 1, kRowsum = 2 };
 // which serialises the U loads (one 128-bit load in flight per thread).  Declaring at least
 // ROW_MINB_THREADS / B resident CTAs caps registers at 65536 / ROW_MINB_THREADS instead
 // (scripts/row_variants.sh: 1024 -> 64 registers is best on B200).
+#ifndef ROW_PERSIST_BIG
+#define ROW_PERSIST_BIG 1  // persistent grid for B > 512 (calibration switch)
+#endif
 #ifndef ROW_MINB_THREADS
 #define ROW_MINB_THREADS 1024
 #endif
@@ -66,52 +69,60 @@ __global__ void __launch_bounds__(B, row_min_blocks<B>()) row_kernel(const float
   const int team = warp / TW, tw = warp % TW;          // team index, warp within team
   const int T = TW * 32, t = tw * 32 + lane;            // team size, thread within team
   const int teams = W / TW;                            // warps beyond teams*TW idle
-  const int row = blockIdx.x * teams + team;
-  const bool live = team < teams && row < N;
-  const float* a = A + (size_t)(live ? row : 0) * N;
-  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (live) {
-    if ((N & 3) == 0) {
-      constexpr int U = ROW_U;
-      const uint64_t pol = l2keep > 0.f ? l2_keep_fraction_policy(l2keep) : 0;
-      const float4* a4 = reinterpret_cast<const float4*>(a);
-      const float4* v4 = reinterpret_cast<const float4*>(v);
-      const int n4 = N >> 2;
-      for (int base = t; base < n4; base += U * T) {
-        float4 x[U], y[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-          const int j = base + u * T;
-          x[u] = j < n4 ? (l2keep > 0.f ? ld_keep(a4 + j, pol) : ld_stream(a4 + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-        if constexpr (OP != kRowsum) {
+  // grid-stride over row blocks with a CTA-uniform trip count (the team combine's
+  // __syncthreads is reached by every warp); the launcher makes the grid persistent for
+  // B > 512 (one CTA per SM: no CTA retire/launch gaps inside a launch), one pass otherwise.
+  // scripts/row_persist_probe.sh (PDL brackets, blocks 544..1024): N = 8192 34.75 -> 33.42 us,
+  // N = 4096 7.00 -> 6.77 us.
+  for (int row0 = blockIdx.x * teams; row0 < N; row0 += gridDim.x * teams) {
+    const int row = row0 + team;
+    const bool live = team < teams && row < N;
+    const float* a = A + (size_t)(live ? row : 0) * N;
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (live) {
+      if ((N & 3) == 0) {
+        constexpr int U = ROW_U;
+        const uint64_t pol = l2keep > 0.f ? l2_keep_fraction_policy(l2keep) : 0;
+        const float4* a4 = reinterpret_cast<const float4*>(a);
+        const float4* v4 = reinterpret_cast<const float4*>(v);
+        const int n4 = N >> 2;
+        for (int base = t; base < n4; base += U * T) {
+          float4 x[U], y[U];
 #pragma unroll
           for (int u = 0; u < U; u++) {
             const int j = base + u * T;
-            y[u] = j < n4 ? __ldg(v4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+            x[u] = j < n4 ? (l2keep > 0.f ? ld_keep(a4 + j, pol) : ld_stream(a4 + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
           }
+          if constexpr (OP != kRowsum) {
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+              const int j = base + u * T;
+              y[u] = j < n4 ? __ldg(v4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; u++) acc4<OP>(s, x[u], OP != kRowsum ? y[u] : x[u]);
         }
-#pragma unroll
-        for (int u = 0; u < U; u++) acc4<OP>(s, x[u], OP != kRowsum ? y[u] : x[u]);
+      } else {
+        for (int j = t; j < N; j += T) s.x = acc1<OP>(s.x, ld_stream(a + j), OP != kRowsum ? __ldg(v + j) : 0.f);
       }
-    } else {
-      for (int j = t; j < N; j += T) s.x = acc1<OP>(s.x, ld_stream(a + j), OP != kRowsum ? __ldg(v + j) : 0.f);
     }
-  }
-  float r = (s.x + s.y) + (s.z + s.w);
+    float r = (s.x + s.y) + (s.z + s.w);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-  if (TW > 1) {  // combine the team's warps in a fixed order
-    if (lane == 0) red[warp] = r;
-    __syncthreads();
-    if (tw == 0 && lane == 0) {
-      r = 0.f;
-      if (team < teams)
-        for (int k = 0; k < TW; k++) r += red[team * TW + k];
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    if (TW > 1) {  // combine the team's warps in a fixed order
+      if (lane == 0) red[warp] = r;
+      __syncthreads();
+      if (tw == 0 && lane == 0) {
+        r = 0.f;
+        if (team < teams)
+          for (int k = 0; k < TW; k++) r += red[team * TW + k];
+      }
+      __syncthreads();  // red[] is rewritten by the next row block
     }
+    pdl_wait();
+    if (live && tw == 0 && lane == 0) out[row] = (OP == kEuclid) ? sqrtf(r) : r;
   }
-  pdl_wait();
-  if (live && tw == 0 && lane == 0) out[row] = (OP == kEuclid) ? sqrtf(r) : r;
 }
 
 // Warps per team (one row per team).  B200 calibration with the 64-register budget and PDL
@@ -159,7 +170,16 @@ struct RowLauncher {
       const double share = keep_env >= 0 ? keep_env : 0.45;
       const double a_bytes = (double)N * N * 4.0;
       const float keep = share <= 0 ? 0.f : (float)std::min(1.0, share * l2_bytes / a_bytes);
-      return launch_k(row_kernel<OP, B>, dim3((N + teams - 1) / teams), dim3(B), 0, s, a.pdl,
+      static int sms = 0;
+      if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1) sms = 148;
+        cudaGetLastError();
+      }
+      const int need = (N + teams - 1) / teams;
+      const int grid = (ROW_PERSIST_BIG && B > 512 && need > sms) ? sms : need;
+      return launch_k(row_kernel<OP, B>, dim3(grid), dim3(B), 0, s, a.pdl,
                       (const float*)e.in0, (const float*)e.in1, (float*)e.out, N, tw, keep);
     }
   };
