@@ -62,7 +62,7 @@ def _check(results, ref):
         assert st["mean_perf"] == ref.derived["mean_perf"]
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 def test_point_sharded_merge(world):
     require_gpu()
     n, K = 400_000, 1600
@@ -80,7 +80,7 @@ def test_point_sharded_merge(world):
         assert (out["best_block_id"].view(np.uint16) == ref.best_block).all()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 def test_group_aligned_merge(world):
     require_gpu()
     n, K = 32 * 120_000, 15_000
