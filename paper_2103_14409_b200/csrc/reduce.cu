@@ -131,11 +131,6 @@ __device__ __forceinline__ void fold_chunk(GroupAcc& a, bool valid, uint32_t bit
   }
 }
 
-// warp-uniform counter increment: lane 0 adds to the CTA's shared counter slot
-__device__ __forceinline__ void wadd(uint64_t* sh_c, int slot, uint32_t v) {
-  if ((threadIdx.x & 31) == 0 && v) atomicAdd((unsigned long long*)&sh_c[slot], (unsigned long long)v);
-}
-
 __device__ __forceinline__ uint64_t f64_key(double v) { return (uint64_t)__double_as_longlong(v); }
 
 __device__ __forceinline__ uint64_t warp_sum64(uint64_t v) {
@@ -175,7 +170,6 @@ __device__ __forceinline__ void flush_counters(const RP& p, ThreadAcc& t, uint64
 __device__ void finalize_lane(const RP& p, uint64_t g, bool active, const GroupAcc& a,
                               ThreadAcc& t, uint64_t* sh_c, uint32_t* sh_perf, uint32_t* sh_gain,
                               uint32_t* sh_bb) {
-  const unsigned FULL = 0xffffffffu;
   const bool acc = active && g >= p.acc_lo && g < p.acc_hi;
   const bool complete = a.n_rows == p.L && a.n_ok == a.n_rows;
   const bool defined = active && (p.policy ? complete : a.n_ok >= 1);

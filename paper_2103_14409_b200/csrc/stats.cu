@@ -653,9 +653,10 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
         sel_pass<false, kT1><<<grid1, kT1, 0, q>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, st, hist, cand, cap, cbuf);
       LSCAT_CUDA(ctx, cudaGetLastError());
       if (world > 1) {
-        lscat_status ns;
-        if ((ns = ctx->comm->allreduce(ctx, {{hist, (size_t)kMaxR * kBins, DT::U32, Op::Sum}}, q))) return ns;
-        if ((ns = ctx->comm->allgather(ctx, cand, cand_all, cand_len, DT::U64, q))) return ns;
+        lscat_status ns = ctx->comm->allreduce(ctx, {{hist, (size_t)kMaxR * kBins, DT::U32, Op::Sum}}, q);
+        if (ns) return ns;
+        ns = ctx->comm->allgather(ctx, cand, cand_all, cand_len, DT::U64, q);
+        if (ns) return ns;
       }
       sel_resolve<<<kMaxR, 1024, res_smem, q>>>(st, hist, cand_all, cand, world, cap);
       LSCAT_CUDA(ctx, cudaGetLastError());

@@ -147,8 +147,8 @@ lscat_status lscat_suite_buffer(lscat_ctx* ctx, uint32_t kernel, uint32_t n, uin
 lscat_status lscat_suite_upload(lscat_ctx* ctx, uint32_t kernel, uint32_t n, uint32_t slot,
                                 const void* src, uint64_t bytes, uint32_t src_mem, void* stream) {
   LSCAT_CHECK_CTX(ctx);
-  void* dst;
-  uint64_t b;
+  void* dst = nullptr;
+  uint64_t b = 0;
   if (slot > 1) return fail(ctx, LSCAT_ERR_INVALID_ARG, "suite_upload: slot %u is not an input", slot);
   lscat_status st = lscat_suite_buffer(ctx, kernel, n, slot, &dst, &b);
   if (st) return st;
