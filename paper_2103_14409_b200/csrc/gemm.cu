@@ -408,6 +408,11 @@ __global__ void __launch_bounds__(B, 1) gemm_persistent_kernel(const __grid_cons
 #define GEMM2_STAGES 7
 #endif
 constexpr int kStages2 = GEMM2_STAGES;  // calibration switch (scripts/gemm_variants.sh)
+#ifndef GEMM2_GROUPM
+#define GEMM2_GROUPM 8
+#endif
+constexpr int kGroupM2 = GEMM2_GROUPM;  // 256-row tile rows per raster group: 4 / 8 / 16 / 32 ->
+                                        // 1539 / 1584 / 1569 / 1488 TFLOP/s (scripts/gemm_variants2.sh)
 constexpr int kStage2A = 128 * BK * 2, kStage2B = 128 * BK * 2;  // 16 KB each
 constexpr int kSmem2 = kStages2 * (kStage2A + kStage2B) + 1024 + 256;
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address -> the leader CTA's copy
@@ -449,12 +454,12 @@ __global__ void __launch_bounds__(B, 1) gemm_2cta_kernel(const __grid_constant__
   const bool leader = rank == 0;
   constexpr int TM = 256, TN = 256;
   const int mt = (N + TM - 1) / TM, nt = (N + TN - 1) / TN, ntiles = mt * nt;
-  const int per_group = kGroupM * nt;
+  const int per_group = kGroupM2 * nt;
   const int kblocks = (N + BK - 1) / BK;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   auto tile_origin = [&](int t, int& m0, int& n0) {
-    const int first_m = (t / per_group) * kGroupM;
-    const int gm = min(mt - first_m, kGroupM);
+    const int first_m = (t / per_group) * kGroupM2;
+    const int gm = min(mt - first_m, kGroupM2);
     m0 = (first_m + (t % per_group) % gm) * TM;
     n0 = ((t % per_group) / gm) * TN;
   };
