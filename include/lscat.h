@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define LSCAT_ABI_VERSION 1
+#define LSCAT_ABI_VERSION 2
 
 typedef enum {
   LSCAT_OK = 0,
@@ -82,6 +82,22 @@ typedef enum { LSCAT_MEM_DEVICE = 0, LSCAT_MEM_HOST = 1 } lscat_mem;
               identical; the bracket time excludes the launch gap (R-3). */
 typedef enum { LSCAT_LAUNCH_GRAPH = 0, LSCAT_LAUNCH_STREAM = 1, LSCAT_LAUNCH_GRAPH_PDL = 2 } lscat_launch_mode;
 typedef enum { LSCAT_SHARD_POINT_LPT = 0, LSCAT_SHARD_GROUP = 1 } lscat_shard;
+/* Bracket clock (P:201-205 times a loop of 1000 launches):
+   EVENT        a CUDA event pair around the bracket on `stream`;
+   GLOBALTIMER  two one-thread stamp kernels reading %globaltimer (ns) around the bracket,
+                copied back asynchronously.  Events are recorded in both modes (the timeout
+                budget uses them), so the two clocks can be compared on the same brackets. */
+typedef enum { LSCAT_TIMER_EVENT = 0, LSCAT_TIMER_GLOBALTIMER = 1 } lscat_timer;
+/* L2 state of the timed launches:
+   WARM    the paper's loop: every launch of a point reuses the same buffers, so what one launch
+           leaves in the 126 MB L2 serves the next (the suite kernels keep re-read inputs with
+           L2 cache policies).  This is the runtime-table definition (R-3).
+   ROTATE  cold-HBM measurement: c = clamp(ceil(2 x L2 / footprint), 2, 128) copies of the
+           point's buffers (inputs copied from the registered suite before the warm-up, not
+           timed) are cycled launch by launch, and no L2 keep policies are used; a launch's
+           inputs were last touched >= 2 x L2 bytes of traffic earlier (for footprints of at
+           least 2 x L2 / 128, i.e. N >= 512 for the 4N^2-byte kernels). */
+typedef enum { LSCAT_L2_WARM = 0, LSCAT_L2_ROTATE = 1 } lscat_l2_mode;
 typedef enum { LSCAT_SKIPNA = 0, LSCAT_COMPLETE_ONLY = 1 } lscat_nan_policy;
 
 typedef struct lscat_ctx lscat_ctx; /* one per process/rank and device; opaque */
@@ -177,7 +193,20 @@ typedef struct {
   uint32_t shard;                                 /* lscat_shard (world > 1)              */
   double launch_overhead_s;                       /* cost model, as lscat_plan_opts       */
   uint64_t spin_ns;                               /* LSCAT_K_SPIN only                    */
-  float* bracket_ms_host;                         /* optional [cap_rows * brackets] host  */
+  float* bracket_ms_host;                         /* optional [cap_rows * brackets] host:  */
+                                                  /* per-launch ms of every bracket by     */
+                                                  /* `timer` (NaN = bracket not run)       */
+  uint32_t timer;                                 /* lscat_timer (default EVENT)          */
+  uint32_t l2_mode;                               /* lscat_l2_mode (default WARM)         */
+  float* bracket_ms_event_host;                   /* optional [cap_rows * brackets] host:  */
+                                                  /* the CUDA-event clock of the same     */
+                                                  /* brackets (timer agreement check)     */
+  uint32_t verify;                                /* 1: copy every point's output buffer  */
+                                                  /* (the last timed launch's) to host    */
+  void* verify_host;                              /* [verify_cap_bytes] host (pinned for  */
+  uint64_t verify_cap_bytes;                      /* asynchronous copies)                 */
+  uint64_t* verify_offsets;                       /* [cap_rows + 1] host: row i's bytes   */
+                                                  /* at [off[i], off[i+1]) (empty if NaN) */
 } lscat_sweep_opts;
 
 /* Runtime table, structure of arrays (a5; the paper's dataframe rows).
@@ -203,10 +232,14 @@ typedef struct {
 } lscat_table;
 
 /* Run this rank's points: per point `warmup` launches, then `brackets` brackets of
-   `launches_per_bracket` launches each timed with CUDA events on `stream`; runtime = median
-   over brackets of (bracket ms / R) (even count -> midpoint).  A point
-   whose warm-up predicts, or whose measured brackets reach, more than timeout_s gets NaN +
-   TIMEOUT.  Writes ALL groups of the plan (n_groups = n_kernels * n_sizes, canonical order,
+   `launches_per_bracket` launches each timed by `timer` on `stream`; runtime = median over
+   brackets of (bracket ms / R) (even count -> midpoint).  Timeout
+   budget (R-18): a point whose warm-up predicts more than timeout_s gets
+   NaN + TIMEOUT without running its brackets; a point without a warm-up prediction (warmup
+   == 0) or predicted above half the budget runs its brackets one at a time (one queued ahead)
+   and stops as soon as the elapsed time, or the first bracket x K, exceeds timeout_s ("skip
+   the rest" -> NaN + TIMEOUT); any point whose measured total exceeds it is NaN + TIMEOUT.
+   verify requires verify_host / verify_offsets and enough capacity (ERR_INVALID_ARG).  Writes ALL groups of the plan (n_groups = n_kernels * n_sizes, canonical order,
    groups without local rows are empty) and this rank's rows, grouped, ascending block id.
    Synchronous with respect to the host.  Requires lscat_register_suite for every kernel/N. */
 lscat_status lscat_sweep(lscat_ctx* ctx, const uint32_t* kernels, uint32_t n_kernels,
@@ -259,6 +292,10 @@ enum {
   LSCAT_P_LARGEST_IS_BEST, LSCAT_P_LARGEST_SLOWER, LSCAT_P_GAIN_GT, LSCAT_P_PERF_LT,
   LSCAT_P_PERF_BAND, LSCAT_P_PERF_FX_HI, LSCAT_P_PERF_FX_LO, LSCAT_P_GAIN_FX_HI,
   LSCAT_P_GAIN_FX_LO,
+  LSCAT_P_BAD_IDS,   /* defined groups whose best row has block_id >= n_blocks or whose
+                        matrix index >= n_matrices (a table violating the id ranges; such
+                        groups are left out of the best-block histogram and lscat_stats
+                        returns LSCAT_ERR_INVALID_ARG) */
   LSCAT_P_NCOUNTERS = 24 /* padded */
 };
 

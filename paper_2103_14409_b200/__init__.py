@@ -10,5 +10,6 @@ from .lscat import (  # noqa: F401
     K_STENCIL5, K_SPIN, SLOT_IN0, SLOT_IN1, SLOT_OUT, MEM_DEVICE, MEM_HOST, LAUNCH_GRAPH, LAUNCH_GRAPH_PDL,
     LAUNCH_STREAM, SHARD_POINT_LPT, SHARD_GROUP, SKIPNA, COMPLETE_ONLY, PRESET_T4,
     PRESET_GTX980, ROW_OK, ROW_TIMEOUT, ROW_LAUNCH_ERROR, ROW_INVALID_CONFIG, GF, COUNTERS,
-    EXPORTS,
+    EXPORTS, OK, ERR_INVALID_ARG, ERR_CUDA, ERR_STATE, ERR_UNSUPPORTED, TIMER_EVENT,
+    TIMER_GLOBALTIMER, L2_WARM, L2_ROTATE,
 )

@@ -35,6 +35,9 @@ struct LaunchArgs {
   uint64_t spin_ns;
   bool pdl = false;  // programmatic dependent launch (LSCAT_LAUNCH_GRAPH_PDL); honoured only
                      // by kernels that call pdl_wait() before their first global store
+  int sms = 148;     // SMs of the context's device (grid sizing; from lscat_ctx, not a static)
+  size_t l2_bytes = 0;  // L2 size of the context's device (the row kernels' L2 keep share)
+  bool cold = false;  // LSCAT_L2_ROTATE: no L2 keep policies (cold-HBM measurement)
 };
 
 // One launch of a suite kernel at block index bi (threads = 32*(bi+1)).  Returns the
@@ -106,6 +109,10 @@ struct lscat_ctx {
   std::map<std::pair<bool, size_t>, int> red_occ;
   int sel_occ0 = 0, sel_occ1 = 0;
   std::vector<cudaEvent_t> events;
+  // LSCAT_L2_ROTATE (sweep.cu): the (kernel, n) whose input copies the "rot" scratch arena
+  // holds, and the arena base its graphs were captured against
+  std::pair<uint32_t, uint32_t> rot_owner{~0u, ~0u};
+  void* rot_base = nullptr;
   // comm
   lscat::Comm* comm = nullptr;  // NCCL, or the local test transport (comm.h)
   int rank = 0, world = 1;

@@ -637,12 +637,12 @@ struct GemmL {
   static cudaError_t launch(const LaunchArgs& a, cudaStream_t s) {
     if constexpr (B >= 128) {
       const SuiteEntry& e = *a.e;
-      static bool attr = false;
-      if (!attr) {
-        cudaError_t err = cudaFuncSetAttribute(gemm_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-        if (err != cudaSuccess) return err;
-        attr = true;
-      }
+      // kernel attributes: set once per process (thread-safe one-time initialisation; the
+      // value is the same for every sm_100a device)
+      static const cudaError_t attr =
+          cudaFuncSetAttribute(gemm_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+      if (attr != cudaSuccess) return attr;
+      const int sms = a.sms > 0 ? a.sms : 148;
       const int N = (int)e.n;
       const int tiles = ((N + BM - 1) / BM) * ((N + BN - 1) / BN);
       if constexpr (B >= 192) {
@@ -651,16 +651,10 @@ struct GemmL {
           return v ? atoi(v) : 1;
         }();
         if (two_cta && N % 8 == 0) {  // CTA pairs (cluster of 2), persistent
-          static int pairs = 0;
-          if (!pairs) {
-            int dev = 0, sms = 148;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            if (cudaFuncSetAttribute(gemm_2cta_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2) !=
-                cudaSuccess)
-              return cudaGetLastError();
-            pairs = std::max(1, sms / 2);
-          }
+          static const cudaError_t attr2 =
+              cudaFuncSetAttribute(gemm_2cta_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
+          if (attr2 != cudaSuccess) return attr2;
+          const int pairs = std::max(1, sms / 2);
           const int tiles2 = ((N + 255) / 256) * ((N + 255) / 256);
           cudaLaunchConfig_t cfg{};
           cfg.gridDim = dim3(2 * std::min(tiles2, pairs));
@@ -679,16 +673,9 @@ struct GemmL {
         }
       }
       if constexpr (B >= 192) {  // persistent, TMEM double-buffered (one CTA per SM)
-        static int sms = 0;
-        if (!sms) {
-          int dev = 0;
-          cudaGetDevice(&dev);
-          cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-          if (cudaFuncSetAttribute(gemm_persistent_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem) !=
-              cudaSuccess)
-            return cudaGetLastError();
-          if (sms < 1) sms = 148;
-        }
+        static const cudaError_t attrp =
+            cudaFuncSetAttribute(gemm_persistent_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        if (attrp != cudaSuccess) return attrp;
         gemm_persistent_kernel<B><<<tiles < sms ? tiles : sms, B, kSmem, s>>>(
             *reinterpret_cast<const GemmMaps*>(e.host_blob), (__nv_bfloat16*)e.out, N);
         return cudaGetLastError();

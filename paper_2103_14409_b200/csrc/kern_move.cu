@@ -92,28 +92,29 @@ template <int B>
 struct TransposeL {
   static constexpr bool kSupported = true;
   static constexpr int kSmem = (B / 32) * 32 * 33 * (int)sizeof(float);
-  static int grid_cap() {
-    static int cap = 0;
-    if (!cap) {
-      int dev = 0, sms = 148, per_sm = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // resident CTAs per SM (a property of the sm_100a binary, the same on every device of the
+  // process; thread-safe one-time initialisation)
+  static int per_sm() {
+    static const int v = [] {
+      int r = 0;
       if (kSmem > 48 * 1024)
         cudaFuncSetAttribute(transpose_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, transpose_kernel<B>, B, kSmem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, transpose_kernel<B>, B, kSmem);
       cudaGetLastError();
-      cap = (sms > 0 ? sms : 148) * (per_sm > 0 ? per_sm : 1);
-    }
-    return cap;
+      return r > 0 ? r : 1;
+    }();
+    return v;
   }
-  static int occupancy() { grid_cap(); return occupancy_warps(transpose_kernel<B>, B, kSmem); }
+  static int grid_cap(int sms) { return (sms > 0 ? sms : 148) * per_sm(); }
+  static int occupancy() { per_sm(); return occupancy_warps(transpose_kernel<B>, B, kSmem); }
   static cudaError_t launch(const LaunchArgs& a, cudaStream_t s) {
     const SuiteEntry& e = *a.e;
     const int N = (int)e.n;
     constexpr int UX = TP_VERT ? 1 : TP_TPW, UY = TP_VERT ? TP_TPW : 1;
     const int units_x = (N + 32 * UX - 1) / (32 * UX), nunits = units_x * ((N + 32 * UY - 1) / (32 * UY));
     const int need = (nunits + B / 32 - 1) / (B / 32);
-    const int grid = need < grid_cap() ? need : grid_cap();
+    const int cap = grid_cap(a.sms);
+    const int grid = need < cap ? need : cap;
     return launch_k(transpose_kernel<B>, dim3(grid), dim3(B), (size_t)kSmem, s, a.pdl, (const float*)e.in0,
                     (float*)e.out, N, units_x, nunits);
   }

@@ -151,13 +151,6 @@ struct RowLauncher {
         const char* v = getenv("LSCAT_ROW_L2FRAC");
         return v ? atof(v) : -1.0;
       }();
-      static int l2_bytes = -1;
-      if (l2_bytes < 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&l2_bytes, cudaDevAttrL2CacheSize, dev) != cudaSuccess) l2_bytes = 0;
-        cudaGetLastError();
-      }
       const int tw = (tw_env > 0 && tw_env <= B / 32) ? tw_env : team_warps(N, B);
       const int teams = B / 32 / tw;
       // L2 residency: every launch of a bracket re-reads A.  Its loads carry a fractional L2
@@ -169,14 +162,9 @@ struct RowLauncher {
       // share 0: 38.1 us, 0.3: 33.0, 0.45: 32.2, 0.6: 33.1, 0.75: 36.2; N = 4096: 6.2-6.3 us.
       const double share = keep_env >= 0 ? keep_env : 0.45;
       const double a_bytes = (double)N * N * 4.0;
-      const float keep = share <= 0 ? 0.f : (float)std::min(1.0, share * l2_bytes / a_bytes);
-      static int sms = 0;
-      if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1) sms = 148;
-        cudaGetLastError();
-      }
+      // LSCAT_L2_ROTATE (a.cold): plain streaming loads, nothing is kept for the next launch
+      const float keep = (share <= 0 || a.cold) ? 0.f : (float)std::min(1.0, share * (double)a.l2_bytes / a_bytes);
+      const int sms = a.sms > 0 ? a.sms : 148;
       const int need = (N + teams - 1) / teams;
       const int grid = (ROW_PERSIST_BIG && B > 512 && need > sms) ? sms : need;
       return launch_k(row_kernel<OP, B>, dim3(grid), dim3(B), 0, s, a.pdl,

@@ -76,9 +76,9 @@ struct GroupAcc {
 struct ThreadAcc {
   uint64_t fx[4];                  // perf hi, perf lo, gain hi, gain lo
   uint64_t pmin, pmax, gmin, gmax;
-  // Per-lane counters since the last flush_counters (every kPkGroups groups per lane): 14
+  // Per-lane counters since the last flush_counters (every kPkGroups groups per lane): 15
   // packed 4-bit fields (the 12 flag counters LSCAT_P_GROUPS.., the perf == 1 and gain == 0
-  // histogram bins) and the row counts (groups of < 2^28 rows).
+  // histogram bins, LSCAT_P_BAD_IDS) and the row counts (groups of < 2^28 rows).
   uint64_t pk;
   uint32_t rows, ok, nan;
   uint32_t n;                      // groups finalised since the last flush (warp-uniform)
@@ -151,6 +151,8 @@ __device__ __forceinline__ void flush_counters(const RP& p, ThreadAcc& t, uint64
   }
   const uint32_t hp = __reduce_add_sync(FULL, (uint32_t)(t.pk >> 48) & 15u);
   const uint32_t hg = __reduce_add_sync(FULL, (uint32_t)(t.pk >> 52) & 15u);
+  const uint32_t bad = __reduce_add_sync(FULL, (uint32_t)(t.pk >> 56) & 15u);
+  if (l0 && bad) atomicAdd((unsigned long long*)&sh_c[LSCAT_P_BAD_IDS], (unsigned long long)bad);
   if (l0 && hp) atomicAdd(&sh_perf[p.nb], hp);
   if (l0 && hg) atomicAdd(&sh_gain[0], hg);
   const uint64_t r = warp_sum64(t.rows), o = warp_sum64(t.ok), n = warp_sum64(t.nan);
@@ -182,7 +184,8 @@ __device__ void finalize_lane(const RP& p, uint64_t g, bool active, const GroupA
     flags |= LSCAT_GF_DEFINED;
     const uint64_t ag = p.first_group + g;  // implicit matrix index: a mask when M is a power of 2
     const uint32_t mat = p.gmat ? p.gmat[g] : (uint32_t)((p.M & (p.M - 1)) == 0 ? (ag & (p.M - 1)) : ag % p.M);
-    bbi = (int)(mat * p.L + a.min_bid);
+    // ids outside [0, L) x [0, M) violate the table precondition: counted, never indexed
+    bbi = (a.min_bid < p.L && mat < p.M) ? (int)(mat * p.L + a.min_bid) : -2;
     if (a.lcode == 2) {
       flags |= LSCAT_GF_RATIO_DEFINED;
       const double b = (double)__uint_as_float(a.min_bits), tt = (double)__uint_as_float(a.l_bits);
@@ -234,7 +237,9 @@ __device__ void finalize_lane(const RP& p, uint64_t g, bool active, const GroupA
     if (p.o_flags) p.o_flags[g] = flags;
   }
   // per-lane accumulation: packed flag counters and row counts, flushed every kPkGroups groups
-  if (!acc) { flags = 0; bbi = -1; }
+  const bool bad_ids = acc && bbi == -2;
+  if (!acc || bad_ids) bbi = -1;
+  if (!acc) flags = 0;
   {
     uint64_t inc = acc ? 1ull : 0ull;  // field 0: LSCAT_P_GROUPS
     inc |= (uint64_t)((flags & LSCAT_GF_DEFINED) != 0) << 4;
@@ -250,6 +255,7 @@ __device__ void finalize_lane(const RP& p, uint64_t g, bool active, const GroupA
     inc |= (uint64_t)((flags & LSCAT_GF_PERF_BAND) != 0) << 44;
     inc |= (uint64_t)(pbin == (int)p.nb) << 48;  // hot bins: perf == 1, gain == 0
     inc |= (uint64_t)(gbin == 0) << 52;
+    inc |= (uint64_t)bad_ids << 56;
     t.pk += inc;
     if (acc) { t.rows += a.n_rows; t.ok += a.n_ok; t.nan += a.n_nan; }
   }
@@ -456,7 +462,9 @@ __global__ void __launch_bounds__(kThreads, 3) reduce_uniform32_kernel(RP p) {
   auto DI = [&](int b) { return reinterpret_cast<uint4*>(wstage + b * (1024 * 4 + 1024 * 2) + 1024 * 4); };
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  const uint64_t full_batches = p.n_groups / 32;  // batches of 32 complete 32-row groups
+  // batches of 32 complete 32-row groups: a short last group (n_rows < 32 G) always goes to
+  // the tail below, which bounds its rows by n_rows
+  const uint64_t full_batches = (p.n_rows / 32) / 32;
   uint64_t bi = warp;
   if (bi < full_batches) uniform_prefetch(p, bi * 32, D(0), DI(0), lane);
   for (; bi < full_batches; bi += nwarps) {
@@ -665,6 +673,7 @@ __global__ void __launch_bounds__(256) profile_kernel(RP p, const float* __restr
       const float v = __ldcs(p.rt + r);
       if (!ok_bits(__float_as_uint(v))) continue;
       const uint32_t id = __ldcs(p.bid + r);
+      if (id >= p.L || mat >= p.M) continue;  // counted as LSCAT_P_BAD_IDS by the reducer
       const uint64_t q = (uint64_t)__dmul_rn(__ddiv_rn(b, (double)v), 2147483648.0);
       atomicAdd((unsigned long long*)&s_sum[mat * p.L + id], (unsigned long long)q);
       atomicAdd(&s_cnt[mat * p.L + id], 1u);

@@ -770,6 +770,10 @@ extern "C" lscat_status lscat_stats(lscat_ctx* ctx, const lscat_reduce_opts* o, 
   }
   std::vector<uint64_t> P(hP, hP + plen);
   const uint64_t* C = P.data();
+  if (C[LSCAT_P_BAD_IDS])
+    return fail(ctx, LSCAT_ERR_INVALID_ARG,
+                "stats: %llu groups of the reduced table have a block_id >= n_blocks or a matrix "
+                "index >= n_matrices", (unsigned long long)C[LSCAT_P_BAD_IDS]);
   out->n_rows = C[LSCAT_P_ROWS]; out->n_ok = C[LSCAT_P_OK]; out->n_nan = C[LSCAT_P_NAN];
   out->n_invalid = C[LSCAT_P_INVALID]; out->n_groups = C[LSCAT_P_GROUPS];
   out->n_defined = C[LSCAT_P_DEFINED]; out->n_all_nan = C[LSCAT_P_ALL_NAN];

@@ -110,6 +110,7 @@ lscat_status lscat_register_suite(lscat_ctx* ctx, const uint32_t* kernels, uint3
   LSCAT_CUDA(ctx, cudaDeviceSynchronize());
   for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
   ctx->graphs.clear();
+  ctx->rot_owner = {~0u, ~0u};
   for (auto& kv : ctx->suite) free_entry(kv.second);
   ctx->suite.clear();
   for (uint32_t i = 0; i < nk; i++) {
@@ -154,6 +155,7 @@ lscat_status lscat_suite_upload(lscat_ctx* ctx, uint32_t kernel, uint32_t n, uin
   if (st) return st;
   if (!src || bytes != b) return fail(ctx, LSCAT_ERR_INVALID_ARG, "suite_upload: %llu bytes, slot holds %llu",
                                       (unsigned long long)bytes, (unsigned long long)b);
+  ctx->rot_owner = {~0u, ~0u};  // ROTATE copies are stale
   LSCAT_CUDA(ctx, cudaMemcpyAsync(dst, src, b, src_mem == LSCAT_MEM_HOST ? cudaMemcpyHostToDevice
                                                                         : cudaMemcpyDeviceToDevice,
                                   (cudaStream_t)stream));
@@ -177,6 +179,8 @@ lscat_status lscat_launch(lscat_ctx* ctx, uint32_t kernel, uint32_t n, uint32_t 
     e = &it->second;
   }
   LaunchArgs a{e, (uint64_t)n};
+  a.sms = ctx->sm_count;
+  a.l2_bytes = ctx->l2_bytes;
   cudaError_t err = fn(a, (cudaStream_t)stream);
   ctx->launches++;
   if (err != cudaSuccess) return cuda_fail(ctx, err, "launch");

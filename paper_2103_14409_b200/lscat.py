@@ -27,6 +27,8 @@ SLOT_IN0, SLOT_IN1, SLOT_OUT = 0, 1, 2
 MEM_DEVICE, MEM_HOST = 0, 1
 LAUNCH_GRAPH, LAUNCH_STREAM, LAUNCH_GRAPH_PDL = 0, 1, 2
 SHARD_POINT_LPT, SHARD_GROUP = 0, 1
+TIMER_EVENT, TIMER_GLOBALTIMER = 0, 1
+L2_WARM, L2_ROTATE = 0, 1
 SKIPNA, COMPLETE_ONLY = 0, 1
 PRESET_T4, PRESET_GTX980 = 0, 1
 GF = dict(defined=0x1, complete=0x2, all_nan=0x4, ratio_defined=0x8, largest_is_best=0x10,
@@ -66,7 +68,10 @@ class SweepOpts(C.Structure):
                 ("brackets", C.c_uint32), ("launches_per_bracket", C.c_uint32),
                 ("timeout_s", C.c_double), ("launch_mode", C.c_uint32), ("shard", C.c_uint32),
                 ("launch_overhead_s", C.c_double), ("spin_ns", C.c_uint64),
-                ("bracket_ms_host", C.c_void_p)]
+                ("bracket_ms_host", C.c_void_p), ("timer", C.c_uint32), ("l2_mode", C.c_uint32),
+                ("bracket_ms_event_host", C.c_void_p), ("verify", C.c_uint32),
+                ("verify_host", C.c_void_p), ("verify_cap_bytes", C.c_uint64),
+                ("verify_offsets", C.c_void_p)]
 
 
 class TableC(C.Structure):
@@ -165,7 +170,7 @@ def load(path: str = LIB_PATH):
         f = getattr(L, name)
         f.argtypes = args
         f.restype = res
-    if L.lscat_abi_version() != 1:
+    if L.lscat_abi_version() != 2:
         raise ImportError("liblscat ABI version mismatch")
     _lib = L
     return L
@@ -315,6 +320,7 @@ class Ctx:
         self.device = device
 
     def close(self):
+        self._reduce_keep = None
         if getattr(self, "h", None):
             self._lib.lscat_ctx_destroy(self.h)
             self.h = None
@@ -380,7 +386,11 @@ class Ctx:
     # a4/a5
     def sweep(self, kernels, sizes, blocks, warmup=1, brackets=10, launches=1000,
               timeout_s=30.0, launch_mode=LAUNCH_GRAPH, shard=SHARD_POINT_LPT, spin_ns=0,
-              table: Table | None = None, with_brackets=False, stream=None) -> Table:
+              table: Table | None = None, with_brackets=False, stream=None, timer=TIMER_EVENT,
+              l2_mode=L2_WARM, with_event_brackets=False, verify_bytes=0) -> Table:
+        """a2-a5.  with_brackets -> table.brackets [rows, K] (per-launch ms by `timer`);
+        with_event_brackets -> table.brackets_event (the CUDA-event clock of the same brackets);
+        verify_bytes > 0 -> table.verify = list of per-row output byte strings (None if NaN)."""
         k, kp = _arr(kernels, np.uint32)
         s, sp = _arr(sizes, np.uint32)
         b, bp = _arr(blocks, np.uint16)
@@ -388,8 +398,14 @@ class Ctx:
         if table is None:
             table = Table.empty(npts, k.size * s.size)
         brk = np.full(npts * brackets, np.nan, np.float32) if with_brackets else None
+        brk_ev = np.full(npts * brackets, np.nan, np.float32) if with_event_brackets else None
+        vbuf = np.zeros(verify_bytes, np.uint8) if verify_bytes else None
+        voff = np.zeros(npts + 1, np.uint64) if verify_bytes else None
         o = SweepOpts(bp, b.size, warmup, brackets, launches, timeout_s, launch_mode, shard,
-                      0.0, spin_ns, None if brk is None else brk.ctypes.data)
+                      0.0, spin_ns, None if brk is None else brk.ctypes.data, timer, l2_mode,
+                      None if brk_ev is None else brk_ev.ctypes.data, 1 if verify_bytes else 0,
+                      None if vbuf is None else vbuf.ctypes.data, verify_bytes,
+                      None if voff is None else voff.ctypes.data)
         tc = table.c()
         self._ck(self._lib.lscat_sweep(self.h, kp, k.size, sp, s.size, C.byref(o), C.byref(tc),
                                        _stream(stream)), "sweep")
@@ -397,6 +413,10 @@ class Ctx:
         table.rows_per_group, table.first_group = tc.rows_per_group, tc.first_group
         if with_brackets:
             table.brackets = brk[:tc.n_rows * brackets].reshape(tc.n_rows, brackets)
+        if with_event_brackets:
+            table.brackets_event = brk_ev[:tc.n_rows * brackets].reshape(tc.n_rows, brackets)
+        if verify_bytes:
+            table.verify = [bytes(vbuf[int(voff[i]):int(voff[i + 1])]) for i in range(tc.n_rows)]
         return table
 
     # a6-a9
@@ -421,6 +441,9 @@ class Ctx:
         tc = table.c(with_groups=not table.rows_per_group or table.group_offset is not None)
         self._ck(self._lib.lscat_reduce_table(self.h, C.byref(tc), C.byref(opts), C.byref(oc),
                                               _stream(stream)), "reduce_table")
+        # the library reads the per-group perf/gain again in lscat_stats (keep_values): hold
+        # the tensors until the next reduce_table or close, even if the caller drops `out`
+        self._reduce_keep = out
         return out
 
     # a8/a10

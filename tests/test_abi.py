@@ -34,7 +34,7 @@ def test_exports_every_declared_symbol(lib):
     for name in declared:
         assert hasattr(L, name), name
     assert sorted(lib.EXPORTS) == declared
-    assert L.lscat_abi_version() == 1
+    assert L.lscat_abi_version() == 2
     assert L.lscat_status_string(1) == b"invalid argument"
 
 

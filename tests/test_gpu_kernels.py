@@ -215,24 +215,120 @@ def test_gemm_identity_bit_exact():
         assert torch.equal(out.view(n, n), A)
 
 
+def _check_gemm(got, ref, scale):
+    """|C - C^| <= 2^-8 |C^| + 1e-5 sum_k |A_ik Bt_jk| (the bf16 output rounding is
+    <= 2^-9 relative, fp32 accumulation of K products is far below 1e-5 of the absolute sum;
+    a dropped 64-wide k-block (~sqrt(64)/3 ~ 2.7 at |C| ~ 30) fails it)."""
+    err = np.abs(got.astype(np.float64) - ref)
+    bound = 2.0 ** -8 * np.abs(ref) + 1e-5 * scale
+    bad = err > bound
+    assert not bad.any(), f"{bad.sum()} elements off; worst {np.max(err / bound)}"
+
+
+@pytest.mark.parametrize("n", [520, 2056])
+def test_gemm_tight_bound(n):
+    """The tight GEMM bound at the ragged one-tile-row size and the multi-tile size."""
+    from paper_2103_14409_b200 import K_GEMM_BF16
+    c = _setup(K_GEMM_BF16, [n])
+    A, Bt = _inputs(c, K_GEMM_BF16, n)
+    A, Bt = A.reshape(n, n), Bt.reshape(n, n)
+    ref, scale = OK.gemm(A, Bt), OK.gemm_abs_scale(A, Bt)
+    for b in (128, 160, 192, 256, 1024):
+        _check_gemm(_run(c, K_GEMM_BF16, n, b).reshape(n, n), ref, scale)
+
+
 def test_gemm_full_size_sampled():
+    """N = 8192: 32 x 32 tiles of 256 x 256 over 74 CTA pairs, so every pair runs ~14 tiles and
+    each TMEM accumulator buffer is reused (flipped tmem_empty phase).  256 sampled rows (every
+    tile row, each row crossing every tile column) cover every tile, including those a pair
+    processes third or later; checked with the tight bound."""
     import torch
     from paper_2103_14409_b200 import K_GEMM_BF16
     n = 8192
     c = _setup(K_GEMM_BF16, [n])
     A = c.suite_tensor(K_GEMM_BF16, n, 0).view(n, n)
     Bt = c.suite_tensor(K_GEMM_BF16, n, 1).view(n, n)
-    rows = torch.as_tensor(np.r_[0:4, 127:131, 4090:4100, n - 4:n], device="cuda")
+    rng = np.random.default_rng(8192)
+    rows_np = np.unique(np.r_[0:4, 127:131, 4090:4100, n - 4:n,
+                              np.arange(0, n, 256) + rng.integers(0, 256, n // 256),
+                              rng.choice(n, 200, replace=False)])
+    assert len(rows_np) >= 256 and len(np.unique(rows_np // 256)) == n // 256
+    rows = torch.as_tensor(rows_np, device="cuda")
     Ar = A[rows].float().cpu().numpy()
     Bn = Bt.float().cpu().numpy()
     ref, scale = OK.gemm(Ar, Bn), OK.gemm_abs_scale(Ar, Bn)
-    for b in (128, 256):
+    for b in (128, 256, 1024):
         out = c.suite_tensor(K_GEMM_BF16, n, 2)
         out.zero_()
         c.launch(K_GEMM_BF16, n, b)
         torch.cuda.synchronize()
         got = out.view(n, n)[rows].float().cpu().numpy()
-        _check_rel(got, ref, scale, tol=1e-2)
+        _check_gemm(got, ref, scale)
+
+
+@pytest.mark.parametrize("name", ["matvec", "rowsum", "colsum", "euclid"])
+def test_vector_outputs_full_size(name):
+    """N = 8192 (the suite roofline / bench size), every output element: the row kernels'
+    persistent grid for B > 512, colsum's 64 row chunks + last-CTA ticket."""
+    from paper_2103_14409_b200 import KERNELS
+    k = KERNELS[name]
+    n = 8192
+    c = _setup(k, [n])
+    A, v = _inputs(c, k, n)
+    A = A.reshape(n, n)
+    ref, scale = {
+        "euclid": lambda: (OK.euclid(A, v), OK.euclid_abs_scale(A, v)),
+        "matvec": lambda: (OK.matvec(A, v), OK.matvec_abs_scale(A, v)),
+        "rowsum": lambda: (OK.rowsum(A), OK.rowsum_abs_scale(A)),
+        "colsum": lambda: (OK.colsum(A), OK.colsum_abs_scale(A)),
+    }[name]()
+    for b in (32, 128, 256, 512, 544, 1024):
+        out = _run(c, k, n, b)
+        assert np.isfinite(out).all(), (name, b)
+        _check_rel(out, ref, scale)
+
+
+def test_axpy_full_size():
+    from paper_2103_14409_b200 import K_AXPY
+    n = 8192
+    c = _setup(K_AXPY, [n])
+    x, y = _inputs(c, K_AXPY, n)
+    ref, scale = OK.axpy(x, y), OK.axpy_abs_scale(x, y)
+    for b in (32, 256, 1024):
+        _check_rel(_run(c, K_AXPY, n, b), ref, scale)
+
+
+def test_suite_inputs_non_degenerate():
+    """a1 inputs (reading R-15): uniform on [-1, 1) -- range, mean ~ 0, sd ~ 1/sqrt(3), many
+    distinct values, in0 != in1, and different (kernel, N, slot) buffers differ.  A broken
+    generator (all zeros, one constant, a repeated stream) fails here, not silently in the
+    closed-form checks."""
+    import torch
+    from paper_2103_14409_b200 import KERNELS
+    c = ctx()
+    ks = [KERNELS[k] for k in ("euclid", "matvec", "gemm_bf16", "transpose", "axpy", "rowsum",
+                               "colsum", "stencil5")]
+    sizes = [64, 512, 2048]
+    c.register_suite(ks, sizes)
+    seen = {}
+    for k in ks:
+        for n in sizes:
+            for slot in (0, 1):
+                try:
+                    t = c.suite_tensor(k, n, slot)
+                except Exception:
+                    continue
+                x = t.float().cpu().numpy().astype(np.float64)
+                assert x.min() >= -1.0 and x.max() < 1.0, (k, n, slot)
+                assert abs(x.mean()) < 6.0 / np.sqrt(x.size) + 1e-3, (k, n, slot, x.mean())
+                assert abs(x.std() - 1 / np.sqrt(3)) < 6 * np.sqrt(0.8 / (4 * x.size)) / np.sqrt(3) + 1e-3, \
+                    (k, n, slot, x.std())
+                distinct = np.unique(x).size
+                grid = 256 if t.dtype == torch.bfloat16 else 2 ** 24
+                assert distinct >= min(x.size, grid) * 0.5, (k, n, slot, distinct)
+                head = x[:64].tobytes()
+                assert head not in seen, (k, n, slot, seen.get(head))
+                seen[head] = (k, n, slot)
 
 
 def test_gemm_one_cta_persistent_path():

@@ -313,7 +313,7 @@ def test_percentiles_dense_bin_compaction():
 
 def test_scaled_table_1e9_sampled():
     """configs[4] at full size, the configuration bench.py times: 10^9 rows = 31.25 M uniform
-    32-row groups (no offset array).  The counters obey every invariant; per-group outputs are
+    32-row groups (no offset array).  Whole-table oracle comparison at the end.  The counters obey every invariant; per-group outputs are
     bit-exact against the oracle on sampled windows of groups (their rows regenerated by the
     CPU twin of the generator and compared byte for byte first); every percentile satisfies the
     nearest-rank property over the device's per-group values (properties that hold at any
@@ -362,5 +362,111 @@ def test_scaled_table_1e9_sampled():
             lt = int((x < v).sum().item())
             le = int((x <= v).sum().item())
             assert lt < k <= le, (q, p, v, lt, k, le)
+    # the whole table through the oracle: group-aligned chunks of the device table
+    # (the generator twin, bit-exact with synth.gen_table as checked above and in
+    # test_generator_twin_bit_exact) reduced by the C oracle; every counter and histogram is a
+    # sum of integer partials, so the chunked totals equal the whole-table values exactly.  The
+    # percentiles are the nearest-rank values of the concatenated oracle per-group values.
+    CH = 3_906_250
+    tot = {k: 0 for k in OT.COUNTERS}
+    ph = np.zeros(101, np.uint64)
+    gh = np.zeros(1001, np.uint64)
+    bh = np.zeros((M, L), np.uint64)
+    perfs, gains = [], []
+    for g0 in range(0, G, CH):
+        g1 = min(G, g0 + CH)
+        rt = tab.runtime_ms[g0 * L:g1 * L].cpu().numpy()
+        bid = tab.block_id[g0 * L:g1 * L].cpu().numpy().view(np.uint16)
+        ref = OT.reduce_table(rt, bid, rows_per_group=L, first_group=g0,
+                              opts=OT.Opts(n_blocks=L, n_matrices=M))
+        for k, v in ref.counters.items():
+            tot[k] += v
+        ph += ref.perf_hist
+        gh += ref.gain_hist
+        bh += ref.best_block_hist
+        rd = (ref.flags & 0x008) != 0
+        perfs.append(ref.perf[rd])
+        gains.append(ref.gain[rd])
+        del rt, bid, ref
+    for k, v in tot.items():
+        assert st[k] == v, (k, st[k], v)
+    assert (st["perf_hist"] == ph).all() and (st["gain_hist"] == gh).all()
+    assert (st["best_block_hist"] == bh).all()
+    for q, vals, parts in (("perf", st["pct_perf"], perfs), ("gain", st["pct_gain"], gains)):
+        allv = np.sort(np.concatenate(parts))
+        assert allv.size == nrd
+        for p, v in zip(PCTS, vals):
+            k = min(max(int(np.ceil(p * nrd)), 1), nrd)
+            assert v == allv[k - 1], (q, p, v, allv[k - 1])
     del out, tab
     torch.cuda.empty_cache()
+
+
+def _uniform_device_table(rt, bid):
+    import torch
+    from paper_2103_14409_b200 import Table
+    n = rt.size
+    return Table(torch.from_numpy(rt).cuda(), torch.from_numpy(bid.view(np.int16)).cuda(), None,
+                 None, None, None, n_rows=n, n_groups=-(-n // 32), rows_per_group=32)
+
+
+@pytest.mark.parametrize("n_groups,short", [(64, 5), (96, 31), (33, 1), (32, 0)])
+def test_uniform_short_last_group(n_groups, short):
+    """a short last group inside what would be a full 32-group batch of the uniform
+    32-row path (n_groups % 32 == 0, n_rows % 32 != 0) must be bounded by n_rows."""
+    c = ctx()
+    from paper_2103_14409_b200 import reduce_opts
+    rng = np.random.default_rng(n_groups + short)
+    n = 32 * n_groups - short
+    rt = rng.uniform(0.5, 2.0, n).astype(np.float32)
+    rt[rng.random(n) < 0.05] = np.nan
+    bid = np.tile(np.arange(32, dtype=np.uint16), n_groups)[:n].copy()
+    tab = _uniform_device_table(rt, bid)
+    o = reduce_opts(32, 8)
+    c.reduce_table(tab, o, per_group=False)
+    st = c.stats(o, percentiles=PCTS)
+    ref = OT.reduce_table(rt, bid, rows_per_group=32, opts=OT.Opts(), percentiles=PCTS)
+    for k, v in ref.counters.items():
+        assert st[k] == v, (k, st[k], v)
+    assert (st["perf_hist"] == ref.perf_hist).all() and (st["gain_hist"] == ref.gain_hist).all()
+    assert (st["best_block_hist"] == ref.best_block_hist).all()
+    assert st["pct_perf"] == ref.percentiles["perf"] and st["pct_gain"] == ref.percentiles["gain"]
+    assert st["n_rows"] == n
+
+
+def test_out_of_range_ids_rejected():
+    """block ids >= n_blocks or matrix indices >= n_matrices are never used as
+    histogram indices; lscat_stats reports the table as invalid (the oracle rejects it too)."""
+    c = ctx()
+    from paper_2103_14409_b200 import LscatError, ERR_INVALID_ARG
+    for bid_bad, mat_bad in ((40, 0), (3, 9)):
+        t = dict(runtime_ms=np.array([1.0, 0.5, 2.0, 1.0], np.float32),
+                 block_id=np.array([0, bid_bad, 0, 31], np.uint16),
+                 group_offset=np.array([0, 2, 4], np.int64),
+                 group_matrix=np.array([mat_bad, 1], np.uint32))
+        g_opts, _ = _opts_pair()
+        c.reduce_table(_device_table(t), g_opts)
+        with pytest.raises(LscatError) as e:
+            c.stats(g_opts, percentiles=[0.5])
+        assert e.value.status == ERR_INVALID_ARG
+    # the context stays usable
+    t = dict(runtime_ms=np.array([1.0, 0.5], np.float32), block_id=np.array([0, 31], np.uint16),
+             group_offset=np.array([0, 2], np.int64), group_matrix=np.array([0], np.uint32))
+    _compare(t)
+
+
+def test_stats_after_dropping_reduce_outputs():
+    """the per-group perf/gain tensors lscat_stats reads for the percentiles stay
+    alive when the caller drops reduce_table's result (the binding holds them)."""
+    import torch
+    c = ctx()
+    t = gen_table(200_000, 800, preset="t4", seed=5)
+    g_opts, o_opts = _opts_pair()
+    c.reduce_table(_device_table(t), g_opts)          # result dropped immediately
+    junk = [torch.full((1 << 20,), 7.0, dtype=torch.float64, device="cuda") for _ in range(16)]
+    torch.cuda.synchronize()
+    st = c.stats(g_opts, percentiles=PCTS)
+    ref = OT.reduce_table(t["runtime_ms"], t["block_id"], t["group_offset"],
+                          group_matrix=t["group_matrix"], opts=o_opts, percentiles=PCTS)
+    assert st["pct_perf"] == ref.percentiles["perf"] and st["pct_gain"] == ref.percentiles["gain"]
+    del junk

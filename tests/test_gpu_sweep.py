@@ -201,3 +201,148 @@ def test_bench_launch_configuration_n8192():
     ref = OK.euclid(A[torch.as_tensor(rows, device=A.device)].cpu().numpy(), q)
     got = out.cpu().numpy()[rows]
     assert (np.abs(got - ref) <= 1e-5 * ref).all()
+
+
+def test_tiny_sweep_every_point_output_checked():
+    """configs[0] with verify: the output of the last timed launch of all 72 points (3 kernels
+    x 6 blocks x 4 N) is copied back by the sweep and checked against the fp64 oracle."""
+    from oracle import kernels as OK
+    from paper_2103_14409_b200 import K_EUCLID, K_MATVEC, K_AXPY
+    c = ctx()
+    ks, ns, bs = _tiny()
+    c.register_suite(ks, ns)
+    cap = sum(len(bs) * (n * n * 4 if k == K_AXPY else n * 4) for k in ks for n in ns)
+    tab = c.sweep(ks, ns, bs, warmup=1, brackets=10, launches=100, verify_bytes=cap)
+    t = tab.to_numpy()
+    assert t["n_rows"] == 72 and len(tab.verify) == 72
+    row = 0
+    for k in ks:
+        for n in ns:
+            A = c.suite_tensor(k, n, 0).cpu().numpy()
+            v = c.suite_tensor(k, n, 1).cpu().numpy()
+            if k == K_EUCLID:
+                ref, scale = OK.euclid(A.reshape(n, n), v), OK.euclid_abs_scale(A.reshape(n, n), v)
+            elif k == K_MATVEC:
+                ref, scale = OK.matvec(A.reshape(n, n), v), OK.matvec_abs_scale(A.reshape(n, n), v)
+            else:
+                ref, scale = OK.axpy(A, v), OK.axpy_abs_scale(A, v)
+            for _ in bs:
+                out = np.frombuffer(tab.verify[row], np.float32).astype(np.float64)
+                assert out.size == ref.size, (k, n)
+                assert (np.abs(out - ref) <= 1e-5 * scale).all(), (k, n, row)
+                row += 1
+
+
+def test_globaltimer_agrees_with_events():
+    """timer = GLOBALTIMER: the %globaltimer stamp brackets agree with the CUDA-event clock of
+    the same brackets within a few percent."""
+    from paper_2103_14409_b200 import K_EUCLID, TIMER_GLOBALTIMER, ROW_OK
+    c = ctx()
+    c.register_suite([K_EUCLID], [4096, 8192])
+    tab = c.sweep([K_EUCLID], [4096, 8192], [128, 256, 1024], warmup=1, brackets=5, launches=200,
+                  timer=TIMER_GLOBALTIMER, with_brackets=True, with_event_brackets=True)
+    t = tab.to_numpy()
+    assert (t["status"] == ROW_OK).all()
+    gt, ev = tab.brackets.astype(np.float64), tab.brackets_event.astype(np.float64)
+    assert np.isfinite(gt).all() and np.isfinite(ev).all()
+    rel = np.abs(gt - ev) / ev
+    assert rel.max() < 0.03, rel
+    med = np.median(gt, axis=1).astype(np.float32)
+    assert np.allclose(med, t["runtime_ms"], rtol=1e-6)                 # runtime from the stamps
+
+
+def test_rotate_mode_cold_l2():
+    """l2_mode = ROTATE: outputs still exact, the per-launch time at N = 2048 (A = 16.8 MB,
+    L2-resident in WARM mode) does not shrink, and at N = 8192 the cold launch cannot beat HBM: algorithmic
+    bytes / time <= 8 TB/s (nominal B200 HBM3e)."""
+    from oracle import kernels as OK
+    from paper_2103_14409_b200 import K_EUCLID, L2_ROTATE, ROW_OK, kernel_work
+    c = ctx()
+    ns, bs = [2048, 8192], [256, 1024]
+    c.register_suite([K_EUCLID], ns)
+    warm = c.sweep([K_EUCLID], ns, bs, warmup=1, brackets=5, launches=200).to_numpy()
+    cap = sum(len(bs) * n * 4 for n in ns)
+    tab = c.sweep([K_EUCLID], ns, bs, warmup=1, brackets=5, launches=200, l2_mode=L2_ROTATE,
+                  verify_bytes=cap)
+    cold = tab.to_numpy()
+    assert (cold["status"] == ROW_OK).all()
+    assert (cold["runtime_ms"][:2] >= warm["runtime_ms"][:2]).all(), (cold["runtime_ms"], warm["runtime_ms"])
+    nbytes, _ = kernel_work(K_EUCLID, 8192)
+    assert (nbytes / (cold["runtime_ms"][2:] * 1e-3) <= 8.0e12).all()
+    row = 0
+    for n in ns:
+        A = c.suite_tensor(K_EUCLID, n, 0).cpu().numpy().reshape(n, n)
+        q = c.suite_tensor(K_EUCLID, n, 1).cpu().numpy()
+        ref = OK.euclid(A, q)
+        for _ in bs:
+            out = np.frombuffer(tab.verify[row], np.float32).astype(np.float64)
+            assert (np.abs(out - ref) <= 1e-5 * ref).all(), (n, row)
+            row += 1
+
+
+def test_rotate_mode_every_kernel():
+    """ROTATE runs every suite kernel (the GEMM with per-copy tensor maps, colsum sharing its
+    scratch) with outputs equal to the WARM outputs' oracle."""
+    from oracle import kernels as OK
+    from paper_2103_14409_b200 import KERNELS, L2_ROTATE, ROW_OK
+    c = ctx()
+    n = 512
+    names = ["euclid", "matvec", "gemm_bf16", "transpose", "axpy", "rowsum", "colsum", "stencil5"]
+    ks = [KERNELS[k] for k in names]
+    c.register_suite(ks, [n])
+    bs = [128, 1024]
+    tab = c.sweep(ks, [n], bs, warmup=1, brackets=3, launches=20, l2_mode=L2_ROTATE,
+                  verify_bytes=len(ks) * len(bs) * n * n * 4)
+    t = tab.to_numpy()
+    assert (t["status"] == ROW_OK).all()
+    row = 0
+    for name, k in zip(names, ks):
+        A = c.suite_tensor(k, n, 0).float().cpu().numpy()
+        try:
+            v = c.suite_tensor(k, n, 1).float().cpu().numpy()
+        except Exception:
+            v = None
+        for _ in bs:
+            raw = tab.verify[row]
+            row += 1
+            if name == "gemm_bf16":
+                import torch
+                out = torch.frombuffer(bytearray(raw), dtype=torch.bfloat16).float().numpy().reshape(n, n)
+                ref, sc = OK.gemm(A.reshape(n, n), v.reshape(n, n)), OK.gemm_abs_scale(A.reshape(n, n), v.reshape(n, n))
+                assert (np.abs(out - ref) <= 2.0 ** -8 * np.abs(ref) + 1e-5 * sc).all()
+                continue
+            out = np.frombuffer(raw, np.float32)
+            if name == "transpose":
+                assert (out.reshape(n, n) == OK.transpose(A.reshape(n, n))).all()
+                continue
+            ref, sc = {
+                "euclid": lambda: (OK.euclid(A.reshape(n, n), v), OK.euclid_abs_scale(A.reshape(n, n), v)),
+                "matvec": lambda: (OK.matvec(A.reshape(n, n), v), OK.matvec_abs_scale(A.reshape(n, n), v)),
+                "rowsum": lambda: (OK.rowsum(A.reshape(n, n)), OK.rowsum_abs_scale(A.reshape(n, n))),
+                "colsum": lambda: (OK.colsum(A.reshape(n, n)), OK.colsum_abs_scale(A.reshape(n, n))),
+                "axpy": lambda: (OK.axpy(A, v), OK.axpy_abs_scale(A, v)),
+                "stencil5": lambda: (OK.stencil5(A.reshape(n, n)).ravel(), OK.stencil5_abs_scale(A.reshape(n, n)).ravel()),
+            }[name]()
+            assert (np.abs(out.astype(np.float64) - ref) <= 1e-5 * sc).all(), name
+
+
+def test_budget_checked_after_every_bracket():
+    """A-18 / P:228: without a warm-up prediction (warmup = 0) the brackets run one at a time
+    and the point stops as soon as the budget is exceeded: 10 brackets of 0.4 s against a 1 s
+    budget stop after 2 (the second was already queued), not after 4 s."""
+    from paper_2103_14409_b200 import K_SPIN, ROW_TIMEOUT, ROW_OK
+    c = ctx()
+    t0 = time.time()
+    tab = c.sweep([K_SPIN], [1], [32], warmup=0, brackets=10, launches=2, timeout_s=1.0,
+                  spin_ns=200_000_000, with_brackets=True)
+    wall = time.time() - t0
+    t = tab.to_numpy()
+    assert t["status"][0] == ROW_TIMEOUT and np.isnan(t["runtime_ms"][0])
+    ran = np.isfinite(tab.brackets[0]).sum()
+    assert ran == 2, tab.brackets[0]
+    assert wall < 2.0, wall
+    # the same point with a budget that fits runs all brackets one at a time
+    tab = c.sweep([K_SPIN], [1], [32], warmup=0, brackets=4, launches=1, timeout_s=1.0,
+                  spin_ns=100_000_000, with_brackets=True)
+    t = tab.to_numpy()
+    assert t["status"][0] == ROW_OK and np.isfinite(tab.brackets[0]).all()

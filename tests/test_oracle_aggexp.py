@@ -49,3 +49,30 @@ def test_median_is_most_stable(seed):
     sp = dict(zip(A.METHODS, spread))
     assert sp["median"] < sp["mean"] and sp["median"] < sp["max"]
     assert sp["median"] < 0.02
+
+
+@pytest.mark.parametrize("reps", [2, 3, 50])
+def test_spread_is_population_sd_over_mean(reps):
+    """R-23 / S:324-332: variation = population standard deviation (ddof = 0) of the reps
+    aggregates divided by their mean, recomputed here with numpy from the oracle's own
+    per-repetition aggregates.  Small reps make ddof = 1 differ by sqrt(reps / (reps - 1))."""
+    pool = runtime_pool(2000, seed=4)
+    agg, spread, means = A.experiment(pool, k=10, reps=reps, seed=9)
+    for m in range(5):
+        a = np.array(agg[m], np.float64)
+        assert math.isclose(means[m], a.mean(), rel_tol=1e-12)
+        ref = np.std(a, ddof=0) / np.mean(a)
+        assert math.isclose(spread[m], ref, rel_tol=1e-9, abs_tol=1e-15), (m, spread[m], ref)
+        if np.std(a) > 0:
+            assert not math.isclose(spread[m], np.std(a, ddof=1) / np.mean(a), rel_tol=1e-6)
+
+
+def test_whole_pool_sample_has_no_spread():
+    """k = n: every repetition samples the whole pool (a permutation), so every aggregate is
+    the pool's own statistic and each variation is exactly 0."""
+    pool = [3.0, 1.0, 4.0, 1.5, 9.0, 2.5, 6.0, 5.0, 3.5, 8.0]
+    agg, spread, means = A.experiment(pool, k=10, reps=20, seed=1)
+    s = sorted(pool)
+    assert spread == [0.0] * 5
+    assert means[1] == (s[4] + s[5]) / 2 and means[2] == 1.0 and means[3] == 9.0
+    assert math.isclose(means[0], sum(pool) / 10) and math.isclose(means[4], sum(s[1:9]) / 8)

@@ -186,6 +186,50 @@ def test_brute_force(oracle_lib, seed, policy):
     if res["n_ratio_defined"]:
         exact = sum(Fraction(p) for p in perfs) / len(perfs)
         assert abs(Fraction(r.derived["mean_perf"]) - exact) <= Fraction(1, 2 ** 50)
+    _check_finalize(r.derived, res, fxp, fxg)
+
+
+def _ulp(x):
+    return math.ulp(x) if x else 2.0 ** -1074
+
+
+def _check_finalize(D, res, fxp, fxg):
+    """a10 / oracle_finalize pinned by exact rationals: every fraction is the
+    correctly rounded count / denominator with the denominators of O3 step 11 -- n_rows for
+    frac_nonnan, n_ratio_defined for every other share (groups
+    whose largest-block row is missing or NaN are excluded, R-7/R-9) -- and each mean is the
+    brute-force fixed-point total / (2^s n_ratio_defined) within one ulp (O3 step 9)."""
+    nrd = res["n_ratio_defined"]
+    assert D["frac_nonnan"] == float(Fraction(res["n_ok"], res["n_rows"]))
+    if nrd == 0:
+        for k in ("frac_largest_not_best", "frac_gain_gt", "frac_perf_lt", "frac_perf_band",
+                  "mean_perf", "mean_gain"):
+            assert math.isnan(D[k]), k
+        return
+    assert D["frac_largest_not_best"] == float(Fraction(nrd - res["n_largest_is_best"], nrd))
+    assert D["frac_gain_gt"] == float(Fraction(res["n_gain_gt"], nrd))
+    assert D["frac_perf_lt"] == float(Fraction(res["n_perf_lt"], nrd))
+    assert D["frac_perf_band"] == float(Fraction(res["n_perf_band"], nrd))
+    mp = Fraction(fxp, 2 ** 52 * nrd)
+    mg = Fraction(fxg, 2 ** 32 * nrd)
+    assert abs(Fraction(D["mean_perf"]) - mp) <= Fraction(_ulp(float(mp)))
+    assert abs(Fraction(D["mean_gain"]) - mg) <= Fraction(_ulp(float(mg)))
+
+
+def test_finalize_denominators_distinguishable(oracle_lib):
+    """The random tables of test_brute_force make every denominator choice observable: groups
+    that are defined but lack a usable largest-block row (n_defined > n_ratio_defined), and
+    largest-is-best groups, so a wrong denominator or numerator changes a fraction."""
+    rng = np.random.default_rng(0)
+    rt, bid, off, gm = _random_table(rng, 300, 4, dup_vals=True)
+    r = oracle_lib.reduce_table(rt, bid, off, group_matrix=gm,
+                                opts=oracle_lib.Opts(n_blocks=4, largest_block_id=3))
+    C, D = r.counters, r.derived
+    assert C["n_defined"] > C["n_ratio_defined"] > C["n_largest_is_best"] > 0
+    assert C["n_ratio_defined"] > C["n_perf_lt"] > 0 and C["n_perf_band"] > 0
+    wrong = float(Fraction(C["n_defined"] - C["n_largest_is_best"], C["n_defined"]))
+    assert D["frac_largest_not_best"] != wrong
+    assert D["frac_perf_lt"] != float(Fraction(C["n_perf_lt"], C["n_defined"]))
 
 
 def test_invariants_generator_table(oracle_lib):
