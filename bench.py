@@ -4,14 +4,21 @@ rows/s; % HBM peak per kernel).
 
 A step = one pass of the whole hot path over the configs[1] workload:
 plan (a2) -> sweep `euclidean_kernel` over blocks 32..1024 step 32 x N = 64..8192 (a3-a5,
-paper timing policy: 1 preheat + 10 brackets x 1000 launches, median) -> reduce the runtime
-table (a6/a7, NCCL merge a9 when N > 1) -> stats with percentiles (a8/a10).
+paper timing policy: 1 preheat + 10 brackets x 1000 launches, median; plain CUDA-graph
+brackets, each launch waits for the previous one as in the paper's serial loop; warm L2 = the
+paper's runtime definition) -> reduce the runtime table (a6/a7, NCCL merge a9 when N > 1) ->
+stats with percentiles (a8/a10) -> the dominant point (euclid N = 8192 at the step's best
+block) re-timed with cold L2 (LSCAT_L2_ROTATE) for the roofline.
 `value` = sweep points/s of the whole job (points of all ranks / max-over-ranks device time).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--policy paper|fast] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--policy paper|fast]
+                    [--launch graph|graph_pdl|stream] [--timer event|globaltimer]
+                    [--impl ours|reference]
 
 Multi-GPU: launched by torchrun, one rank per GPU, points LPT-sharded (strong scaling: the
-256-point sweep is fixed).  `--impl reference` times the CPU oracle (the tier's reference arm).
+256-point sweep is fixed); table rows/s of configs[2]-[4] sharded over the ranks (group-aligned
+and point-sharded, NCCL merge).  `--impl reference` times the CPU oracle (the tier's reference
+arm).
 """
 from __future__ import annotations
 
@@ -102,7 +109,36 @@ class Clocks:
 # ----------------------------------------------------------------------------------------
 # reference arm: the CPU oracle (tier framing: the oracle is the reference)
 # ----------------------------------------------------------------------------------------
-def oracle_points_per_s(policy, A_by_n=None, min_s=10.0):
+def host_info():
+    """Host cores this process may use and the CPU model (recorded with the
+    CPU baseline)."""
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        cores = os.cpu_count() or 1
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"nproc": cores, "cpu_count": os.cpu_count(), "cpu_model": model}
+
+
+def _euclid_threads(OK, A, q, threads):
+    """The oracle's fp64 euclid on row chunks in `threads` threads (numpy releases the GIL in
+    its array kernels); the arithmetic per row is the oracle's own."""
+    if threads <= 1 or A.shape[0] < 256:
+        return OK.euclid(A, q)
+    from concurrent.futures import ThreadPoolExecutor
+    parts = np.array_split(np.arange(A.shape[0]), threads)
+    with ThreadPoolExecutor(threads) as ex:
+        return np.concatenate(list(ex.map(lambda ix: OK.euclid(A[ix[0]:ix[-1] + 1], q), parts)))
+
+
+def oracle_points_per_s(policy, A_by_n=None, min_s=10.0, threads=1):
     """Time the fp64 oracle of euclidean_kernel on a bounded sample and scale to the policy:
     a point = (W + K*R) evaluations of the kernel at its N; 32 points per size.  The sample
     evaluates every matrix size once per round, for as many rounds as fit in `min_s` seconds
@@ -119,7 +155,7 @@ def oracle_points_per_s(policy, A_by_n=None, min_s=10.0):
         for n in SIZES:
             A, q = A_by_n[n]
             t0 = time.perf_counter()
-            OK.euclid(A, q)
+            _euclid_threads(OK, A, q, threads)
             dt = time.perf_counter() - t0
             per_n[n] += dt
             work += dt
@@ -133,6 +169,7 @@ def run_reference(args):
     if rank != 0:
         return
     W, K = args.warmup, args.steps
+    hi = host_info()
     rng = np.random.default_rng(0)
     A_by_n = {n: (rng.uniform(-1, 1, (n, n)).astype(np.float32),
                   rng.uniform(-1, 1, n).astype(np.float32)) for n in SIZES}
@@ -155,6 +192,7 @@ def run_reference(args):
                                         "policy": args.policy, "blocks": "32..1024 step 32",
                                         "sizes": SIZES},
         "cpu_baseline": {"value": value, "unit": "points/s", "cores": 1, "kind": "oracle",
+                         "host": hi,
                          "sample": f"per step: fp64 numpy evaluations of euclidean_kernel, "
                                    f"every matrix size once per round, rounds for >= 5 s of CPU "
                                    f"({rounds} rounds, {cpu_s:.1f} s in total), scaled by 32 blocks "
@@ -175,8 +213,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--policy", choices=list(POLICIES), default="paper")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--launch", choices=["graph", "graph_pdl", "stream"], default="graph_pdl",
-                    help="how a bracket's launches are issued (lscat_launch_mode)")
+    ap.add_argument("--launch", choices=["graph", "graph_pdl", "stream"], default="graph",
+                    help="how a bracket's launches are issued (lscat_launch_mode); the runtime "
+                         "table's default is plain graphs (launches serialised as in the paper)")
+    ap.add_argument("--timer", choices=["event", "globaltimer"], default="event")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -211,23 +251,33 @@ def main():
         return t.item()
 
     W, K, R = POLICIES[args.policy]
-    launch_mode = {"graph": L.LAUNCH_GRAPH, "graph_pdl": L.LAUNCH_GRAPH_PDL,
-                   "stream": L.LAUNCH_STREAM}[args.launch]
+    modes = {"graph": L.LAUNCH_GRAPH, "graph_pdl": L.LAUNCH_GRAPH_PDL, "stream": L.LAUNCH_STREAM}
+    launch_mode = modes[args.launch]
+    timer = {"event": L.TIMER_EVENT, "globaltimer": L.TIMER_GLOBALTIMER}[args.timer]
     ks = [L.K_EUCLID]
     ctx.register_suite(ks, SIZES)
     npts_total = len(ks) * len(SIZES) * len(BLOCKS)
-    my_pts = L.plan(ks, SIZES, BLOCKS, rank, world, W, K, R)
     table = L.Table.empty(npts_total, len(ks) * len(SIZES))
     ropts = L.reduce_opts(len(BLOCKS), len(SIZES), point_sharded=1 if world > 1 else 0)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
+    g8 = len(SIZES) - 1
+    COLD = (1, 3, 200)  # cold re-timing of the dominant point: W, K, R
 
-    def step():
+    def step(mode=launch_mode):
         t = ctx.sweep(ks, SIZES, BLOCKS, warmup=W, brackets=K, launches=R, timeout_s=30.0,
-                      table=table, with_brackets=True, launch_mode=launch_mode)
-        ctx.reduce_table(t, ropts, per_group=False)
+                      table=table, with_brackets=True, launch_mode=mode, timer=timer)
+        red = ctx.reduce_table(t, ropts, per_group=True)
         st = ctx.stats(ropts, percentiles=PCTS)
-        return t, st
+        # the dominant kernel (euclid N = 8192) at the step's best block, cold L2: the roofline
+        bb = int(red["best_block_id"][g8].item()) & 0xFFFF
+        cold = None
+        if bb < len(BLOCKS):
+            c = ctx.sweep(ks, [8192], [BLOCKS[bb]], warmup=COLD[0], brackets=COLD[1],
+                          launches=COLD[2], l2_mode=L.L2_ROTATE, with_brackets=True,
+                          timer=timer, table=L.Table.empty(1, 1))
+            cold = (BLOCKS[bb], c.brackets[0].copy() if c.n_rows else None)
+        return t, st, red, cold
 
     for _ in range(args.warmup):
         step()
@@ -235,61 +285,63 @@ def main():
     clocks = Clocks(lrank)
     l0 = ctx.launch_count()
     dev_ms = 0.0
-    brackets_best = []
+    brackets_all = []
+    colds = []
     last = None
     for _ in range(args.steps):
         flush.zero_()                      # L2 flushed between timed steps (outside the events)
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        t, st = step()
+        t, st, red, cold = step()
         e1.record(stream)
         barrier()
         dev_ms += e0.elapsed_time(e1)
-        last = (t, st)
-        brackets_best.append(t.brackets.copy())
+        last = (t, st, red)
+        brackets_all.append(t.brackets.copy())
+        colds.append(cold)
     ck = clocks.stop()
     launches = ctx.launch_count() - l0
     tot_ms = allmax(dev_ms)
     value = npts_total * args.steps / (tot_ms / 1e3)
 
-    # ---- roofline of the dominant kernel: euclidean_kernel at N = 8192, its best block
+    # ---- roofline of the dominant kernel: euclidean_kernel at N = 8192, best block, cold L2
     tab = last[0].to_numpy()
-    hbm_peak, _, peak_kind = load_peaks()
+    hbm_peak, tc_peak, peak_kind = load_peaks()
     nbytes, _ = L.kernel_work(L.K_EUCLID, 8192)
-    g8 = len(SIZES) - 1
     lo, hi = tab["group_offset"][g8], tab["group_offset"][g8 + 1]
-    roof = None
+    roof, roof_warm = None, None
+    cold_ms = [float(np.mean(c[1])) for c in colds if c and c[1] is not None and np.isfinite(c[1]).all()]
+    if cold_ms:
+        mean_ms = float(np.mean(cold_ms))
+        achieved = nbytes / (mean_ms * 1e-3) / 1e9
+        tr = load_traffic().get("euclid_8192_cold")
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(achieved / hbm_peak, 4), "traffic": tr,
+                "kernel": f"euclid N=8192 block={colds[-1][0]}", "peak_kind": peak_kind,
+                "l2": "cold (LSCAT_L2_ROTATE: 2 buffer copies cycled, no L2 keep policy)",
+                "algorithmic_bytes_per_launch": nbytes, "avg_launch_ms": round(mean_ms, 5),
+                "timing": f"CUDA events ({args.timer}) over {COLD[1]} brackets x {COLD[2]} launches "
+                          f"per timed step, inside the timed region"}
     if hi > lo:
         rt = tab["runtime_ms"][lo:hi]
         i = int(np.nanargmin(rt))
-        best_block = BLOCKS[tab["block_id"][lo + i]]
-        mean_ms = float(np.mean([b[lo + i].mean() for b in brackets_best]))
-        achieved = nbytes / (mean_ms * 1e-3) / 1e9
-        tr = load_traffic().get(f"euclid_8192_b{best_block}") or load_traffic().get("euclid_8192")
-        all_blocks_gbs = [nbytes / (float(np.mean([b[lo + j].mean() for b in brackets_best])) * 1e-3)
-                          / 1e9 for j in range(hi - lo)]
-        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(achieved / hbm_peak, 4), "traffic": tr,
-                "kernel": f"euclid N=8192 block={best_block}", "peak_kind": peak_kind,
-                "algorithmic_bytes_per_launch": nbytes, "avg_launch_ms": round(mean_ms, 5),
-                "share_of_step": round(sum(float(np.mean([b[lo + j].mean() for b in brackets_best]))
-                                           for j in range(hi - lo)) * (W + K * R) / (dev_ms / args.steps), 4),
-                "all_blocks_gbs_min_max": [round(min(all_blocks_gbs), 1), round(max(all_blocks_gbs), 1)]}
-        # A (268 MB) is twice L2: the row kernel keeps an address-hashed fraction f of its lines
-        # L2-resident across the launches of a bracket (fractional evict-last policy, share
-        # 0.45 of L2); `traffic` is the DRAM bytes per launch in that steady state (committed
-        # ncu capture, application replay, no cache flush), so DRAM GB/s = traffic / time
-        l2 = torch.cuda.get_device_properties(lrank).L2_cache_size
-        share = float(os.environ.get("LSCAT_ROW_L2FRAC", "0.45"))
-        roof["l2_resident_fraction"] = round(min(1.0, share * l2 / nbytes) if share > 0 else 0.0, 4)
+        mean_w = float(np.mean([b[lo + i].mean() for b in brackets_all]))
+        share = sum(float(np.mean([b[lo + j].mean() for b in brackets_all]))
+                    for j in range(hi - lo)) * (W + K * R) / (dev_ms / args.steps)
+        tr = load_traffic().get("euclid_8192")
+        roof_warm = {"kernel": f"euclid N=8192 block={BLOCKS[tab['block_id'][lo + i]]}",
+                     "l2": "warm (the paper's loop: same buffers; the row kernel keeps a fraction "
+                           "of A L2-resident across the bracket's launches)",
+                     "avg_launch_ms": round(mean_w, 5),
+                     "effective_gbs": round(nbytes / (mean_w * 1e-3) / 1e9, 1),
+                     "effective_frac": round(nbytes / (mean_w * 1e-3) / 1e9 / hbm_peak, 4),
+                     "share_of_step": round(share, 4)}
         if tr:
-            roof["dram_gbs"] = round(tr / (mean_ms * 1e-3) / 1e9, 1)
-            roof["dram_frac"] = round(tr / (mean_ms * 1e-3) / 1e9 / hbm_peak, 4)
-        roof["note"] = ("frac = algorithmic bytes / time (contract); part of A is served from L2 "
-                        "across the bracket's back-to-back launches, so DRAM traffic per launch "
-                        "(traffic, ncu steady state) is below the algorithmic bytes and "
-                        "dram_frac = traffic / time / peak is the DRAM-side fraction")
+            roof_warm["dram_bytes_per_launch_steady"] = tr
+            roof_warm["dram_frac"] = round(tr / (mean_w * 1e-3) / 1e9 / hbm_peak, 4)
+        if roof:
+            roof["share_of_step"] = roof_warm["share_of_step"]
     per_n = {}
     for gi, n in enumerate(SIZES):
         a, b = tab["group_offset"][gi], tab["group_offset"][gi + 1]
@@ -299,7 +351,6 @@ def main():
                              round(float(np.nanmax(v)), 2)]
             if n >= 4096:
                 per_n[f"{n}_by_block"] = [round(float(x), 1) for x in v]
-    rooflines = None
     spread = None
     if world > 1:
         objs = [None] * world
@@ -307,8 +358,7 @@ def main():
         roof = next((r for r in objs if r), None)
         # SURVEY 8(e) caveat: a group's blocks are timed on different GPUs; the same calibration
         # point (euclid N = 8192, block 32, 200 back-to-back launches, CUDA events) on every
-        # rank gives the cross-device timing spread (the sweep itself shards points, so it is
-        # timed here with direct launches)
+        # rank gives the cross-device timing spread
         for _ in range(10):
             ctx.launch(L.K_EUCLID, 8192, 32)
         c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -327,44 +377,36 @@ def main():
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(ctx, L, ks, W, K, R, npts_total, world, barrier, allmax,
-                      steps=min(args.steps, 2), launch_mode=launch_mode)
+                      steps=min(args.steps, 2), launch_mode=launch_mode, timer=timer)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         A_by_n = {n: (ctx.suite_tensor(L.K_EUCLID, n, 0).view(n, n).cpu().numpy(),
                       ctx.suite_tensor(L.K_EUCLID, n, 1).cpu().numpy()) for n in SIZES}
-        v, work, rounds = oracle_points_per_s(args.policy, A_by_n, min_s=10.0)
-        cpu = {"value": v, "unit": "points/s", "cores": 1, "kind": "oracle",
-               "sample": f"fp64 numpy evaluations of euclidean_kernel on the same inputs, every "
-                         f"matrix size once per round, {rounds} rounds ({work:.1f} s CPU), mean "
-                         f"per-size time scaled by 32 blocks x (W+K*R) launches per point"}
+        hi_ = host_info()
+        v1, work1, rounds1 = oracle_points_per_s(args.policy, A_by_n, min_s=8.0)
+        vn, workn, roundsn = oracle_points_per_s(args.policy, A_by_n, min_s=8.0, threads=hi_["nproc"])
+        cpu = {"value": vn, "unit": "points/s", "cores": hi_["nproc"], "kind": "oracle",
+               "host": hi_, "single_core_value": v1,
+               "sample": f"fp64 numpy evaluations of euclidean_kernel on the same inputs (row chunks "
+                         f"on {hi_['nproc']} threads; single core: {rounds1} rounds, {work1:.1f} s), "
+                         f"every matrix size once per round, {roundsn} rounds ({workn:.1f} s wall), "
+                         f"mean per-size time scaled by 32 blocks x (W+K*R) launches per point"}
 
-    # ---- secondary: table rows/s on the paper-shaped tables, % of peak per suite kernel (N = 1)
-    secondary = None
-    if not args.no_secondary and world == 1:
-        secondary = table_benches(ctx, L, hbm_peak)
-        if args.launch == "graph_pdl":
-            # the same step with plain graph brackets (no programmatic-dependent-launch edges):
-            # the launch gap PDL hides, measured in the same run
-            flush.zero_()
-            barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            tg = ctx.sweep(ks, SIZES, BLOCKS, warmup=W, brackets=K, launches=R, timeout_s=30.0,
-                           table=table, launch_mode=L.LAUNCH_GRAPH)
-            ctx.reduce_table(tg, ropts, per_group=False)
-            ctx.stats(ropts, percentiles=PCTS)
-            e1.record(stream)
-            barrier()
-            gms = e0.elapsed_time(e1)
-            secondary["launch_graph_no_pdl"] = {"value": round(npts_total / (gms / 1e3), 4),
-                                                "unit": "points/s", "ms_per_step": round(gms, 3),
-                                                "steps": 1}
-        secondary["suite_roofline_n8192"] = suite_roofline(ctx, L, hbm_peak, load_peaks()[1])
-        secondary["full_suite_fast_policy"] = full_suite_sweep(ctx, L, launch_mode)
-        cpu_rows = secondary.pop("_cpu_rows_per_s", None)
-        if cpu:
+    # ---- secondary: table rows/s (all N), the PDL launch mode, % of peak per kernel (cold L2)
+    secondary = {}
+    if not args.no_secondary:
+        secondary["tables"] = table_benches(ctx, L, hbm_peak, rank, world, barrier, allmax,
+                                            cpu_rows=(rank == 0 and world == 1 and not args.no_cpu))
+        cpu_rows = secondary["tables"].pop("_cpu_rows_per_s", None)
+        if cpu is not None and cpu_rows:
             cpu["table_rows_per_s"] = cpu_rows
+        secondary["full_suite_fast_policy"] = full_suite_sweep(ctx, L, launch_mode, world, barrier, allmax)
+        if world == 1:
+            secondary["launch_modes"] = launch_mode_compare(ctx, L, ks, table, ropts, W, K, R, flush,
+                                                            barrier, last[1], args.launch)
+            secondary["suite_roofline_n8192"] = suite_roofline(ctx, L, hbm_peak, tc_peak)
+            secondary["occupancy_api"] = occupancy_vs_sweep(ctx, L)
 
     if rank == 0:
         out = {
@@ -375,11 +417,11 @@ def main():
             "config": {"workload": "configs[1] euclid full sweep: euclidean_kernel x blocks "
                                    "32..1024 step 32 x N 64..8192 (powers of 2)",
                        "policy": f"{args.policy}: W={W} K={K} R={R}", "points": npts_total,
-                       "launch": args.launch,
+                       "launch": args.launch, "timer": args.timer, "l2_table": "warm (paper)",
                        "parallelism": f"point-LPT x{world}", "l2": "flushed between steps "
                        "(512 MB write); N=8192 inputs (268 MB) exceed L2 (126 MB)"},
-            "clocks": ck, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
-            "e2e": e2e, "secondary": secondary,
+            "clocks": ck, "gpu_launches": launches, "roofline": roof, "roofline_warm": roof_warm,
+            "cpu_baseline": cpu, "e2e": e2e, "secondary": secondary,
             "per_n_launch_us": per_n, "cross_device_spread": spread,
             "stats_last_step": {k: last[1][k] for k in ("n_rows", "n_ratio_defined",
                                                       "n_largest_is_best", "mean_perf",
@@ -389,10 +431,37 @@ def main():
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
-    del rooflines
 
 
-def run_e2e(ctx, L, ks, W, K, R, npts_total, world, barrier, allmax, steps=2, launch_mode=0):
+def launch_mode_compare(ctx, L, ks, table, ropts, W, K, R, flush, barrier, st_default, default):
+    """The same step with the other launch mode (PDL edges between a bracket's launches: launch
+    i+1 is resident while launch i drains) as a throughput secondary, with the paper's
+    statistics of both tables: the runtime table depends on the launch mode."""
+    import torch
+    other = "graph_pdl" if default != "graph_pdl" else "graph"
+    mode = {"graph": L.LAUNCH_GRAPH, "graph_pdl": L.LAUNCH_GRAPH_PDL}[other]
+    flush.zero_()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    t = ctx.sweep(ks, SIZES, BLOCKS, warmup=W, brackets=K, launches=R, timeout_s=30.0, table=table,
+                  launch_mode=mode)
+    red = ctx.reduce_table(t, ropts, per_group=True)
+    st = ctx.stats(ropts, percentiles=PCTS)
+    e1.record()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    keys = ("n_largest_is_best", "frac_largest_not_best", "mean_perf", "mean_gain", "frac_gain_gt")
+    bb = red["best_block_id"].cpu().numpy().view(np.uint16)
+    return {other: {"value": round(len(SIZES) * len(BLOCKS) / (ms / 1e3), 4), "unit": "points/s",
+                    "ms_per_step": round(ms, 3), "steps": 1,
+                    "stats": {k: st[k] for k in keys},
+                    "best_block_by_n": {str(n): BLOCKS[b] if b < len(BLOCKS) else None for n, b in zip(SIZES, bb)}},
+            default: {"stats": {k: st_default[k] for k in keys}}}
+
+
+def run_e2e(ctx, L, ks, W, K, R, npts_total, world, barrier, allmax, steps=2, launch_mode=0,
+            timer=0):
     """Same metric through the C ABI with HOST buffers: each step uploads the suite inputs
     from pinned host memory, sweeps into a pinned host table, reduces that host table and
     reads the stats back."""
@@ -413,7 +482,7 @@ def run_e2e(ctx, L, ks, W, K, R, npts_total, world, barrier, allmax, steps=2, la
         for (n, slot), t in host_in.items():
             ctx.suite_upload(L.K_EUCLID, n, slot, t)
         tab = ctx.sweep(ks, SIZES, BLOCKS, warmup=W, brackets=K, launches=R, table=host_tab,
-                        launch_mode=launch_mode)
+                        launch_mode=launch_mode, timer=timer)
         ctx.reduce_table(tab, ropts, per_group=False)
         return ctx.stats(ropts, percentiles=PCTS), tab.n_rows
 
@@ -438,33 +507,23 @@ def run_e2e(ctx, L, ks, W, K, R, npts_total, world, barrier, allmax, steps=2, la
                                     "percentile-selection histograms not counted in d2h"}
 
 
-def suite_roofline(ctx, L, hbm_peak, tc_peak, blocks=(128, 256, 512, 1024), reps=20):
+def suite_roofline(ctx, L, hbm_peak, tc_peak, blocks=(128, 256, 512, 1024)):
     """BASELINE metric '% HBM peak per kernel': every suite kernel at N = 8192, best of a few
-    blocks, per-launch time from CUDA events over `reps` back-to-back launches (inputs exceed
-    L2 except colsum/rowsum/matvec/euclid's 256 MB, which also exceed it)."""
-    import torch
+    blocks, per-launch time from CUDA events over 3 brackets x 20 launches with COLD L2
+    (LSCAT_L2_ROTATE: >= 2 x L2 of buffer copies cycled launch by launch, no keep policies),
+    so every byte counted comes from HBM."""
     names = ["euclid", "matvec", "rowsum", "colsum", "transpose", "axpy", "stencil5", "gemm_bf16"]
     ks = [L.KERNELS[k] for k in names]
     n = 8192
     ctx.register_suite(ks, [n])
-    stream = torch.cuda.current_stream()
     out = {}
     for name, k in zip(names, ks):
         nbytes, flops = L.kernel_work(k, n)
-        best = None
-        for b in blocks:
-            ctx.launch(k, n, b)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            e0.record(stream)
-            for _ in range(reps):
-                ctx.launch(k, n, b)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1) / reps
-            if best is None or ms < best[1]:
-                best = (b, ms)
-        b, ms = best
+        t = ctx.sweep([k], [n], list(blocks), warmup=1, brackets=3, launches=20,
+                      l2_mode=L.L2_ROTATE, with_brackets=True).to_numpy()
+        rt = t["runtime_ms"]
+        i = int(np.nanargmin(rt))
+        b, ms = blocks[int(t["block_id"][i])], float(rt[i])
         if k == L.K_GEMM_BF16:
             ach = flops / (ms * 1e-3) / 1e12
             out[name] = {"bound": "tensor", "block": b, "us": round(ms * 1e3, 2),
@@ -473,91 +532,160 @@ def suite_roofline(ctx, L, hbm_peak, tc_peak, blocks=(128, 256, 512, 1024), reps
             ach = nbytes / (ms * 1e-3) / 1e9
             out[name] = {"bound": "hbm", "block": b, "us": round(ms * 1e3, 2),
                          "achieved": round(ach, 1), "unit": "GB/s", "frac": round(ach / hbm_peak, 4)}
+    out["l2"] = "cold (LSCAT_L2_ROTATE), median of 3 brackets x 20 launches, best of blocks " + str(list(blocks))
     return out
 
 
-def full_suite_sweep(ctx, L, launch_mode):
+def occupancy_vs_sweep(ctx, L):
+    """the block cudaOccupancyMaxPotentialBlockSize picks for each suite kernel
+    (independent of N by construction) against the swept argmin per (kernel, N) of the full
+    suite (fast policy), evaluated with the table reducer by taking the API's block as the
+    'largest' block: its performance best / r(api) per group."""
+    names = ["euclid", "matvec", "gemm_bf16", "transpose", "axpy", "rowsum", "colsum", "stencil5"]
+    ks = [L.KERNELS[k] for k in names]
+    ctx.register_suite(ks, SIZES)
+    Wf, Kf, Rf = POLICIES["fast"]
+    out = {}
+    for name, k in zip(names, ks):
+        api = ctx.occupancy_block(k, BLOCKS)
+        sub = ctx.sweep([k], SIZES, BLOCKS, warmup=Wf, brackets=Kf, launches=Rf)
+        o = L.reduce_opts(len(BLOCKS), len(SIZES), largest_block_id=api["block_id"])
+        red = ctx.reduce_table(sub, o, per_group=True)
+        st = ctx.stats(o)
+        best = red["best_block_id"].cpu().numpy().view(np.uint16)
+        perf = red["perf"].cpu().numpy()
+        out[name] = {"api_block": BLOCKS[api["block_id"]], "api_min_grid": api["min_grid"],
+                     "swept_best_by_n": {str(n): (BLOCKS[b] if b < len(BLOCKS) else None) for n, b in zip(SIZES, best)},
+                     "api_perf_by_n": {str(n): (round(float(p), 4) if np.isfinite(p) else None) for n, p in zip(SIZES, perf)},
+                     "api_is_best": st["n_largest_is_best"], "groups": st["n_ratio_defined"],
+                     "mean_perf_api": round(st["mean_perf"], 4)}
+    return out
+
+
+def full_suite_sweep(ctx, L, launch_mode, world, barrier, allmax):
     """The whole suite (8 kernels x 32 blocks x 8 matrix sizes = 2048 points, SURVEY 8(d)
-    scaling workload) swept with the fast policy (1 + 5 x 20 launches), then reduced: sweep
-    points/s and the paper's statistics on this suite."""
+    scaling workload) swept with the fast policy (1 + 5 x 20 launches), point-LPT sharded over
+    the ranks, then reduced (per-group NCCL merge when N > 1): sweep points/s (max over ranks)
+    and the paper's statistics on this suite."""
     import torch
     names = ["euclid", "matvec", "gemm_bf16", "transpose", "axpy", "rowsum", "colsum", "stencil5"]
     ks = [L.KERNELS[k] for k in names]
     ctx.register_suite(ks, SIZES)
     W, K, R = POLICIES["fast"]
-    ctx.sweep(ks, SIZES, BLOCKS, warmup=W, brackets=K, launches=R, launch_mode=launch_mode)  # warm
-    torch.cuda.synchronize()
+    o = L.reduce_opts(len(BLOCKS), len(SIZES), point_sharded=1 if world > 1 else 0)
+    tab = ctx.sweep(ks, SIZES, BLOCKS, warmup=W, brackets=K, launches=R, launch_mode=launch_mode)  # warm
+    barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     tab = ctx.sweep(ks, SIZES, BLOCKS, warmup=W, brackets=K, launches=R, launch_mode=launch_mode)
-    o = L.reduce_opts(len(BLOCKS), len(SIZES))
-    ctx.reduce_table(tab, o, per_group=False)
+    red = ctx.reduce_table(tab, o, per_group=True)
     st = ctx.stats(o, percentiles=[0.5])
     e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    t = tab.to_numpy()
-    best = {}
-    for gi in range(t["n_groups"]):
-        a, b = t["group_offset"][gi], t["group_offset"][gi + 1]
-        if SIZES[t["group_matrix"][gi]] != 8192 or b <= a:
-            continue
-        rt = t["runtime_ms"][a:b]
-        if np.isfinite(rt).any():
-            j = int(np.nanargmin(rt))
-            best[names[ks.index(int(t["group_kernel"][gi]))]] = [BLOCKS[t["block_id"][a + j]],
-                                                                  round(float(rt[j]) * 1e3, 2)]
-    return {"points": int(t["n_rows"]), "policy": f"fast: W={W} K={K} R={R}",
-            "points_per_s": round(t["n_rows"] / (ms / 1e3), 2), "ms": round(ms, 1),
+    barrier()
+    ms = allmax(e0.elapsed_time(e1))
+    bb = red["best_block_id"].cpu().numpy().view(np.uint16)
+    G = len(ks) * len(SIZES)
+    best = {names[gi // len(SIZES)]: BLOCKS[bb[gi]] for gi in range(G)
+            if SIZES[gi % len(SIZES)] == 8192 and bb[gi] < len(BLOCKS)}
+    return {"points": G * len(BLOCKS), "policy": f"fast: W={W} K={K} R={R}", "n_gpus": world,
+            "points_per_s": round(G * len(BLOCKS) / (ms / 1e3), 2), "ms": round(ms, 1),
             "n_nan_rows": int(st["n_nan"]), "frac_largest_not_best": round(st["frac_largest_not_best"], 4),
             "mean_perf_largest": round(st["mean_perf"], 4), "frac_gain_gt_20pct": round(st["frac_gain_gt"], 4),
-            "best_block_us_at_n8192": best}
+            "best_block_at_n8192": best}
 
 
-def table_benches(ctx, L, hbm_peak):
-    """Table rows/s of reduce+stats (device-resident tables, BASELINE configs[2]-[4] at N=1)."""
+TABLE_CASES = [
+    ("gtx980_2140796", dict(n_rows_global=2_140_796, n_kernels=8363, preset=1, seed=980)),
+    ("t4_5028536", dict(n_rows_global=5_028_536, n_kernels=19_683, preset=0, seed=4)),
+    ("scaled_1e9", dict(n_rows_global=1_000_000_000, n_kernels=3_906_250, preset=0,
+                        seed=10 ** 9, offsets=False)),
+]
+
+
+def table_benches(ctx, L, hbm_peak, rank, world, barrier, allmax, cpu_rows=False):
+    """Table rows/s of reduce + merge + stats (9 percentiles) on device-resident tables,
+    BASELINE configs[2]-[4] (median of 10, max over ranks).  With N ranks each rank generates
+    its own shard in place: group-aligned (contiguous group ranges: only the ~11 KB partial
+    vector and the percentile histograms are merged) and, for configs[2]/[3], point-sharded
+    (block ids b % N == rank: the per-group MIN/MAX/SUM merge of 28 B/group first).  `local_ms`
+    is the same shard reduced by a context without a communicator (no merge): the difference
+    is the NCCL merge."""
     import torch
-    from oracle import table as OT
     out = {}
-    cpu_rows = {}
-    cases = [("gtx980_2140796", dict(n_rows_global=2_140_796, n_kernels=8363, preset=L.PRESET_GTX980, seed=980)),
-             ("t4_5028536", dict(n_rows_global=5_028_536, n_kernels=19_683, preset=L.PRESET_T4, seed=4)),
-             ("scaled_1e9", dict(n_rows_global=1_000_000_000, n_kernels=3_906_250, preset=L.PRESET_T4,
-                                 seed=10 ** 9, offsets=False))]
+    cpu = {}
+    solo = L.Ctx(torch.cuda.current_device(), seed=0x15CA7) if world > 1 else None
     stream = torch.cuda.current_stream()
-    for name, kw in cases:
-        tab = ctx.gen_table(**kw)
-        o = L.reduce_opts(32, 8)
-        for _ in range(3):
-            ctx.reduce_table(tab, o, per_group=False)
-            ctx.stats(o, percentiles=PCTS)
-        times, rtimes = [], []
-        for _ in range(10):
-            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-            torch.cuda.synchronize()
-            e0.record(stream)
-            ctx.reduce_table(tab, o, per_group=False)
-            e1.record(stream)
-            ctx.stats(o, percentiles=PCTS)
-            e2.record(stream)
-            torch.cuda.synchronize()
-            times.append(e0.elapsed_time(e2))
-            rtimes.append(e0.elapsed_time(e1))
-        ms, rms = statistics.median(times), statistics.median(rtimes)
-        G = tab.n_groups
-        alg = tab.n_rows * 6 + G * 16          # runtime+block id read, perf+gain written
-        out[name] = {"rows_per_s": round(tab.n_rows / (ms / 1e3), 1), "ms_reduce_plus_stats": round(ms, 4),
-                     "ms_reduce_kernel_path": round(rms, 4),
-                     "reduce_hbm_frac": round(alg / (rms * 1e-3) / 1e9 / hbm_peak, 4)}
-        if name != "scaled_1e9":
-            h = tab.to_numpy()
-            t0 = time.perf_counter()
-            OT.reduce_table(h["runtime_ms"], h["block_id"], h["group_offset"],
-                            group_matrix=h["group_matrix"], percentiles=PCTS)
-            cpu_rows[name] = round(tab.n_rows / (time.perf_counter() - t0), 1)
-        del tab
-        torch.cuda.empty_cache()
-    out["_cpu_rows_per_s"] = cpu_rows
+    for name, kw in TABLE_CASES:
+        kw = dict(kw)
+        offsets = kw.pop("offsets", True)
+        n_glob = kw["n_rows_global"]
+        shapes = [("group_aligned", False)] + ([("point_sharded", True)] if world > 1 and offsets else [])
+        for shard_name, point in shapes:
+            G = -(-n_glob // 32)
+            if point:
+                tab = ctx.gen_table(**kw, block_mod=world, block_rem=rank, offsets=offsets)
+            else:
+                g0, g1 = G * rank // world, G * (rank + 1) // world
+                tab = ctx.gen_table(**kw, group_begin=g0, group_end=g1 if world > 1 else 0, offsets=offsets)
+            o = L.reduce_opts(32, 8, point_sharded=1 if (point and world > 1) else 0)
+
+            def run(c, oo):
+                c.reduce_table(tab, oo, per_group=False)
+                return c.stats(oo, percentiles=PCTS)
+            for _ in range(3):
+                run(ctx, o)
+            times, rtimes = [], []
+            for _ in range(10):
+                e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                barrier()
+                e0.record(stream)
+                ctx.reduce_table(tab, o, per_group=False)
+                e1.record(stream)
+                st = ctx.stats(o, percentiles=PCTS)
+                e2.record(stream)
+                barrier()
+                times.append(allmax(e0.elapsed_time(e2)))
+                rtimes.append(allmax(e0.elapsed_time(e1)))
+            ms, rms = statistics.median(times), statistics.median(rtimes)
+            key = name if world == 1 else f"{name}_{shard_name}"
+            alg = tab.n_rows * 6 + tab.n_groups * 16    # runtime + block id read, perf + gain written
+            res = {"rows_per_s": round(n_glob / (ms / 1e3), 1), "ms_reduce_plus_stats": round(ms, 4),
+                   "ms_reduce_kernel_path": round(rms, 4), "n_rows_global": n_glob,
+                   "rows_per_rank": tab.n_rows, "reduce_hbm_frac": round(alg / (rms * 1e-3) / 1e9 / hbm_peak, 4),
+                   "check_n_rows": st["n_rows"]}
+            if solo is not None:
+                so = L.reduce_opts(32, 8)
+                for _ in range(2):
+                    run(solo, so)
+                lt = []
+                for _ in range(5):
+                    e0, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+                    torch.cuda.synchronize()
+                    e0.record(stream)
+                    run(solo, so)
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    lt.append(e0.elapsed_time(e1))
+                res["local_ms_no_merge"] = round(allmax(statistics.median(lt)), 4)
+            out[key] = res
+            if cpu_rows and name != "scaled_1e9":
+                from oracle import table as OT
+                h = tab.to_numpy()
+                t0 = time.perf_counter()
+                OT.reduce_table(h["runtime_ms"], h["block_id"], h["group_offset"],
+                                group_matrix=h["group_matrix"], percentiles=PCTS)
+                one = tab.n_rows / (time.perf_counter() - t0)
+                t0 = time.perf_counter()
+                OT.reduce_table_parallel(h["runtime_ms"], h["block_id"], h["group_offset"],
+                                         group_matrix=h["group_matrix"])
+                alln = tab.n_rows / (time.perf_counter() - t0)
+                cpu[name] = {"one_core": round(one, 1), "all_cores": round(alln, 1),
+                             "all_cores_note": "counters + histograms (percentiles on one core)"}
+            del tab
+            torch.cuda.empty_cache()
+    if solo is not None:
+        solo.close()
+    out["_cpu_rows_per_s"] = cpu
     return out
 
 

@@ -375,14 +375,31 @@ lscat_status lscat_ingest(lscat_ctx* ctx, const uint32_t* kernel, const uint32_t
                           uint64_t n, lscat_table* out, uint64_t* n_duplicates, void* stream);
 
 /* ------------------------------------------------- side analyses (8f #4) ----------- */
-/* The block the CUDA occupancy calculator picks for `kernel` among `blocks`:
-   the most resident warps per SM, ties -> the larger block (cudaOccupancyMaxPotentialBlockSize
-   semantics).  Independent of N by construction ("insensitive to matrix sizes").
-   *out_block_id = its index in `blocks`; warps_per_sm (HOST [n_blocks], may be NULL) receives
-   the occupancy of every candidate.  Evaluate its quality with lscat_reduce_table by setting
-   largest_block_id to this id. */
+/* The block the CUDA occupancy calculator picks for `kernel` ("The
+   cudaOccupancyMaxPotentialBlockSize is Nvidias own solution to find the optimal thread block
+   size for a kernel"; "insensitive to matrix sizes").  The suite is templated on the block
+   size, so every candidate B has its own compiled function f_B.  For each candidate the
+   library calls cudaOccupancyMaxPotentialBlockSizeVariableSMem(f_B, its dynamic smem, limit B)
+   (info.api_block / api_min_grid) and cudaOccupancyMaxActiveBlocksPerMultiprocessor(f_B, B)
+   (info.blocks_per_sm); the choice is the API's rule applied across the family: the candidate
+   with the most resident threads (warps) per SM, ties -> the larger block (R-24).
+   Independent of N by construction.  *out_block_id = its index in `blocks`; info (HOST
+   [n_blocks], may be NULL) receives every candidate's attributes.  Evaluate the choice with
+   lscat_reduce_table by setting largest_block_id to it. */
+typedef struct {
+  uint32_t threads;           /* candidate block size B                                     */
+  int32_t regs_per_thread;    /* cudaFuncAttributes.numRegs of f_B                          */
+  int32_t static_smem;        /* cudaFuncAttributes.sharedSizeBytes                         */
+  int32_t dynamic_smem;       /* dynamic shared memory of the default launch at B           */
+  int32_t max_threads_per_block; /* cudaFuncAttributes.maxThreadsPerBlock (launch bounds)   */
+  int32_t blocks_per_sm;      /* cudaOccupancyMaxActiveBlocksPerMultiprocessor(f_B, B, dyn) */
+  int32_t warps_per_sm;       /* blocks_per_sm * B / 32                                     */
+  int32_t api_block;          /* cudaOccupancyMaxPotentialBlockSizeVariableSMem, limit B    */
+  int32_t api_min_grid;       /* its minGridSize (= blocks per SM at api_block x SMs)       */
+} lscat_occupancy_info;
 lscat_status lscat_occupancy_block(lscat_ctx* ctx, uint32_t kernel, const uint16_t* blocks,
-                                   uint32_t n_blocks, uint32_t* out_block_id, uint32_t* warps_per_sm);
+                                   uint32_t n_blocks, uint32_t* out_block_id,
+                                   lscat_occupancy_info* info);
 
 /* Timeout economics ("for two seconds of timeout around one third of the kernels had
    enough time to execute"): counts[i] (HOST) = number of rows of the (device) table that have

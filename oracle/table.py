@@ -25,12 +25,22 @@ COUNTERS = [
 ]
 
 
+OMP_LIB_PATH = os.path.join(HERE, "liboracle_omp.so")
+OMP_SRC = os.path.join(HERE, "lscat_oracle_omp.c")
+
+
 def build(force: bool = False) -> str:
-    """Compile the oracle with plain gcc (-O2, no FMA contraction, no fast-math)."""
+    """Compile the oracle with plain gcc (-O2, no FMA contraction, no fast-math), and its
+    all-cores variant (the same oracle over group-aligned chunks, OpenMP; baseline timing)."""
+    deps = [SRC, OMP_SRC, os.path.join(HERE, "oracle.h")]
+    flags = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
     if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < max(
-            os.path.getmtime(SRC), os.path.getmtime(os.path.join(HERE, "oracle.h"))):
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math",
-                               "-fPIC", "-shared", "-o", LIB_PATH, SRC, "-lm"])
+            os.path.getmtime(d) for d in deps):
+        subprocess.check_call(["gcc"] + flags + ["-o", LIB_PATH, SRC, "-lm"])
+    if force or not os.path.exists(OMP_LIB_PATH) or os.path.getmtime(OMP_LIB_PATH) < max(
+            os.path.getmtime(d) for d in deps):
+        subprocess.check_call(["gcc"] + flags + ["-fopenmp", "-o", OMP_LIB_PATH, SRC, OMP_SRC,
+                                                 "-lm"])
     return LIB_PATH
 
 
@@ -178,6 +188,52 @@ def reduce_table(runtime_ms, block_id, group_offset=None, rows_per_group=0, grou
             "gain": [percentile(gn[rd], p) for p in percentiles],
         }
     return res
+
+
+_omp = None
+
+
+def omp_lib():
+    global _omp
+    if _omp is None:
+        build()
+        _omp = C.CDLL(OMP_LIB_PATH)
+        _omp.oracle_reduce_table_omp.argtypes = [C.POINTER(_Table), C.POINTER(_Opts),
+                                                 C.POINTER(_Result), C.c_void_p, C.c_int]
+        _omp.oracle_reduce_table_omp.restype = C.c_int
+    return _omp
+
+
+def reduce_table_parallel(runtime_ms, block_id, group_offset=None, rows_per_group=0,
+                          group_matrix=None, first_group=0, opts: Opts | None = None,
+                          threads: int = 0):
+    """The same oracle on all host cores (group-aligned chunks, integer partials summed):
+    counters and histograms only.  Baseline timing (bench.py cpu_baseline)."""
+    o = opts or Opts()
+    rt = np.ascontiguousarray(runtime_ms, dtype=np.float32)
+    bid = np.ascontiguousarray(block_id, dtype=np.uint16)
+    n = rt.size
+    if rows_per_group:
+        G = -(-n // rows_per_group)
+        off = None
+    else:
+        off = np.ascontiguousarray(group_offset, dtype=np.int64)
+        G = off.size - 1
+    gm = None if group_matrix is None else np.ascontiguousarray(group_matrix, dtype=np.uint32)
+    T = _Table(rt.ctypes.data, bid.ctypes.data, n, None if off is None else off.ctypes.data, G,
+               rows_per_group, None if gm is None else gm.ctypes.data, first_group)
+    op = _Opts(o.n_blocks, o.ell(), o.n_matrices, o.nan_policy, o.bins_per_unit, o.gain_cap,
+               o.gain_gt[0], o.gain_gt[1], o.perf_lt[0], o.perf_lt[1], o.band_lo[0], o.band_lo[1])
+    ph = np.zeros(o.bins_per_unit + 1, np.uint64)
+    gh = np.zeros(o.gain_cap * o.bins_per_unit + 1, np.uint64)
+    bh = np.zeros(o.n_matrices * o.n_blocks, np.uint64)
+    R = _Result()
+    R.perf_hist, R.gain_hist, R.best_block_hist = ph.ctypes.data, gh.ctypes.data, bh.ctypes.data
+    rc = omp_lib().oracle_reduce_table_omp(C.byref(T), C.byref(op), C.byref(R), None, threads)
+    if rc != 0:
+        raise OracleError(f"oracle_reduce_table_omp failed: code {rc}")
+    return ({k: int(R.counters[i]) for i, k in enumerate(COUNTERS)}, ph, gh,
+            bh.reshape(o.n_matrices, o.n_blocks))
 
 
 def percentile(values, p: float) -> float:

@@ -1,7 +1,8 @@
 // analysis.cu — the paper's two side analyses adjacent to the sweep:
 //   * occupancy-API block: the block size CUDA's occupancy calculator
-//     picks for a kernel — the candidate with the most resident warps per SM, ties to the
-//     larger block, like cudaOccupancyMaxPotentialBlockSize.  It depends on the kernel's
+//     picks for a kernel — cudaOccupancyMaxPotentialBlockSizeVariableSMem and
+//     cudaOccupancyMaxActiveBlocksPerMultiprocessor on every candidate's compiled function,
+//     the most resident warps per SM winning, ties to the larger block (the API's rule).  It depends on the kernel's
 //     resources only, never on the matrix size ("insensitive to matrix sizes").  Its
 //     quality is then measured with lscat_reduce_table by setting largest_block_id to it.
 //   * timeout economics: how many sweep points finish within a timeout tau, from the
@@ -46,7 +47,7 @@ using namespace lscat;
 extern "C" {
 
 lscat_status lscat_occupancy_block(lscat_ctx* ctx, uint32_t kernel, const uint16_t* blocks,
-                                   uint32_t n_blocks, uint32_t* out_block_id, uint32_t* warps_per_sm) {
+                                   uint32_t n_blocks, uint32_t* out_block_id, lscat_occupancy_info* info) {
   LSCAT_CHECK_CTX(ctx);
   const KernelTable* t = kernel_table(kernel);
   if (!t || !out_block_id || !block_list_ok(blocks, n_blocks))
@@ -54,12 +55,33 @@ lscat_status lscat_occupancy_block(lscat_ctx* ctx, uint32_t kernel, const uint16
   LSCAT_CUDA(ctx, cudaSetDevice(ctx->device));
   int best = -1, best_w = -1;
   for (uint32_t i = 0; i < n_blocks; i++) {
-    OccFn f = t->occ[blocks[i] / 32 - 1];
-    const int w = f ? f() : 0;
-    if (warps_per_sm) warps_per_sm[i] = (uint32_t)w;
-    if (w > 0 && w >= best_w) { best_w = w; best = (int)i; }  // ties -> the larger block
+    const int B = blocks[i];
+    lscat_occupancy_info in{};
+    in.threads = (uint32_t)B;
+    AttrFn af = t->attrs[B / 32 - 1];
+    const void* f = nullptr;
+    size_t dyn = 0;
+    if (af && af(&f, &dyn) == cudaSuccess && f) {
+      cudaFuncAttributes fa{};
+      LSCAT_CUDA(ctx, cudaFuncGetAttributes(&fa, f));
+      in.regs_per_thread = fa.numRegs;
+      in.static_smem = (int32_t)fa.sharedSizeBytes;
+      in.dynamic_smem = (int32_t)dyn;
+      in.max_threads_per_block = fa.maxThreadsPerBlock;
+      int nb = 0;
+      LSCAT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, B, dyn));
+      in.blocks_per_sm = nb;
+      in.warps_per_sm = nb * B / 32;
+      int min_grid = 0, blk = 0;
+      LSCAT_CUDA(ctx, cudaOccupancyMaxPotentialBlockSizeVariableSMem(
+                          &min_grid, &blk, f, [dyn](int) { return dyn; }, B));
+      in.api_block = blk;
+      in.api_min_grid = min_grid;
+    }
+    cudaGetLastError();
+    if (info) info[i] = in;
+    if (in.warps_per_sm > 0 && in.warps_per_sm >= best_w) { best_w = in.warps_per_sm; best = (int)i; }  // ties -> larger
   }
-  cudaGetLastError();
   if (best < 0) return fail(ctx, LSCAT_ERR_UNSUPPORTED, "occupancy_block: no block size is launchable");
   *out_block_id = (uint32_t)best;
   return LSCAT_OK;

@@ -45,12 +45,14 @@ struct LaunchArgs {
 using LaunchFn = cudaError_t (*)(const LaunchArgs&, cudaStream_t);
 
 // Per-kernel dispatch: nullptr entries = no implementation at that block (INVALID_CONFIG).
-// Resident warps per SM of the kernel at one block size (occupancy API), for lscat_occupancy_block.
-using OccFn = int (*)();
+// AttrFn gives the device function the default launch at that block size runs and its dynamic
+// shared memory (raising the kernel's max-dynamic-smem attribute when needed), for the
+// occupancy API in lscat_occupancy_block / lscat_kernel_attrs.
+using AttrFn = cudaError_t (*)(const void** func, size_t* dyn_smem);
 
 struct KernelTable {
   LaunchFn fn[kMaxBlockIdx];
-  OccFn occ[kMaxBlockIdx];
+  AttrFn attrs[kMaxBlockIdx];
 };
 
 // registries filled by each kernel translation unit

@@ -623,16 +623,12 @@ __global__ void __launch_bounds__(B, 1) gemm_2cta_kernel(const __grid_constant__
 template <int B>
 struct GemmL {
   static constexpr bool kSupported = B >= 128;
-  static int occupancy() {
-    if constexpr (B >= 192) {
-      cudaFuncSetAttribute(gemm_persistent_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-      return occupancy_warps(gemm_persistent_kernel<B>, B, kSmem);
-    } else if constexpr (B >= 128) {
-      cudaFuncSetAttribute(gemm_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-      return occupancy_warps(gemm_kernel<B>, B, kSmem);
-    } else {
-      return 0;
-    }
+  // the kernel the default launch runs: CTA pairs for B >= 192 (N % 8 == 0), one tile per CTA
+  // for 128 / 160 threads
+  static cudaError_t attrs(const void** f, size_t* sm) {
+    if constexpr (B >= 192) return kernel_attrs(gemm_2cta_kernel<B>, kSmem2, f, sm);
+    else if constexpr (B >= 128) return kernel_attrs(gemm_kernel<B>, kSmem, f, sm);
+    else return cudaErrorInvalidConfiguration;
   }
   static cudaError_t launch(const LaunchArgs& a, cudaStream_t s) {
     if constexpr (B >= 128) {

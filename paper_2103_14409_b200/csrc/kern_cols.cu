@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(B, min_blocks_64regs<B>()) colsum_kernel(const
 template <int B>
 struct ColsumL {
   static constexpr bool kSupported = true;
-  static int occupancy() { return occupancy_warps(colsum_kernel<B, 4>, B); }
+  static cudaError_t attrs(const void** f, size_t* sm) { return kernel_attrs(colsum_kernel<B, 4>, 0, f, sm); }
   static cudaError_t launch(const LaunchArgs& a, cudaStream_t s) {
     const SuiteEntry& e = *a.e;
     const int N = (int)e.n;

@@ -104,12 +104,14 @@ __device__ __forceinline__ float block_sum(float v, float* red /* [B/32] smem */
   }
 }
 
-// Resident warps per SM of `kernel` launched with B threads and `smem` dynamic bytes.
+// The device function of a launch and its dynamic shared memory (AttrFn in common.h).
 template <typename F>
-inline int occupancy_warps(F kernel, int B, size_t smem = 0) {
-  int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, B, smem) != cudaSuccess) return 0;
-  return nb * B / 32;
+inline cudaError_t kernel_attrs(F kernel, size_t dyn, const void** f, size_t* smem) {
+  *f = (const void*)kernel;
+  *smem = dyn;
+  if (dyn > 48 * 1024)
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  return cudaSuccess;
 }
 
 // Builds a KernelTable whose entry i launches Launcher<32*(i+1)>::launch (or nullptr when
@@ -119,7 +121,7 @@ KernelTable make_table_impl(std::integer_sequence<int, Is...>) {
   KernelTable t{};
   ((t.fn[Is] = Launcher<32 * (Is + 1)>::kSupported ? &Launcher<32 * (Is + 1)>::launch : nullptr),
    ...);
-  ((t.occ[Is] = Launcher<32 * (Is + 1)>::kSupported ? &Launcher<32 * (Is + 1)>::occupancy : nullptr),
+  ((t.attrs[Is] = Launcher<32 * (Is + 1)>::kSupported ? &Launcher<32 * (Is + 1)>::attrs : nullptr),
    ...);
   return t;
 }

@@ -106,7 +106,7 @@ struct TransposeL {
     return v;
   }
   static int grid_cap(int sms) { return (sms > 0 ? sms : 148) * per_sm(); }
-  static int occupancy() { per_sm(); return occupancy_warps(transpose_kernel<B>, B, kSmem); }
+  static cudaError_t attrs(const void** f, size_t* sm) { return kernel_attrs(transpose_kernel<B>, kSmem, f, sm); }
   static cudaError_t launch(const LaunchArgs& a, cudaStream_t s) {
     const SuiteEntry& e = *a.e;
     const int N = (int)e.n;
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(B) axpy_kernel1(const float* __restrict__ x,
 template <int B>
 struct AxpyL {
   static constexpr bool kSupported = true;
-  static int occupancy() { return occupancy_warps(axpy_kernel4<B>, B); }
+  static cudaError_t attrs(const void** f, size_t* sm) { return kernel_attrs(axpy_kernel4<B>, 0, f, sm); }
   static cudaError_t launch(const LaunchArgs& a, cudaStream_t s) {
     const SuiteEntry& e = *a.e;
     const size_t n = (size_t)e.n * e.n;
@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(B, min_blocks_64regs<B>()) stencil_kernel(cons
 template <int B>
 struct StencilL {
   static constexpr bool kSupported = true;
-  static int occupancy() { return occupancy_warps(stencil_kernel<B, 4>, B); }
+  static cudaError_t attrs(const void** f, size_t* sm) { return kernel_attrs(stencil_kernel<B, 4>, 0, f, sm); }
   static cudaError_t launch(const LaunchArgs& a, cudaStream_t s) {
     const SuiteEntry& e = *a.e;
     const int N = (int)e.n;
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(B) spin_kernel(uint64_t ns) {
 template <int B>
 struct SpinL {
   static constexpr bool kSupported = true;
-  static int occupancy() { return occupancy_warps(spin_kernel<B>, B); }
+  static cudaError_t attrs(const void** f, size_t* sm) { return kernel_attrs(spin_kernel<B>, 0, f, sm); }
   static cudaError_t launch(const LaunchArgs& a, cudaStream_t s) {
     spin_kernel<B><<<1, B, 0, s>>>(a.spin_ns);
     return cudaGetLastError();

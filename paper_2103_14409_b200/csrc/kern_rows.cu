@@ -138,7 +138,7 @@ struct RowLauncher {
   template <int B>
   struct L {
     static constexpr bool kSupported = true;
-    static int occupancy() { return occupancy_warps(row_kernel<OP, B>, B); }
+    static cudaError_t attrs(const void** f, size_t* sm) { return kernel_attrs(row_kernel<OP, B>, 0, f, sm); }
     static cudaError_t launch(const LaunchArgs& a, cudaStream_t s) {
       const SuiteEntry& e = *a.e;
       const int N = (int)e.n;

@@ -105,6 +105,12 @@ class StatsOutC(C.Structure):
                  ("profile_count", C.c_void_p)])
 
 
+class OccInfo(C.Structure):
+    _fields_ = [("threads", C.c_uint32)] + [(n, C.c_int32) for n in (
+        "regs_per_thread", "static_smem", "dynamic_smem", "max_threads_per_block",
+        "blocks_per_sm", "warps_per_sm", "api_block", "api_min_grid")]
+
+
 class GenOpts(C.Structure):
     _fields_ = [("n_rows_global", C.c_uint64), ("n_kernels", C.c_uint32),
                 ("n_blocks", C.c_uint32), ("largest_block_id", C.c_uint32),
@@ -162,7 +168,7 @@ def load(path: str = LIB_PATH):
         "lscat_gen_table": ([vp, C.POINTER(GenOpts), C.POINTER(TableC), vp], i32),
         "lscat_gen_table_shape": ([C.POINTER(GenOpts), C.POINTER(u64), C.POINTER(u64)], i32),
         "lscat_aggregation_experiment": ([vp, vp, u64, u32, u32, u64, vp, vp, vp, vp], i32),
-        "lscat_occupancy_block": ([vp, u32, vp, u32, C.POINTER(u32), vp], i32),
+        "lscat_occupancy_block": ([vp, u32, vp, u32, C.POINTER(u32), C.POINTER(OccInfo)], i32),
         "lscat_timeout_curve": ([vp, C.POINTER(TableC), u32, u32, u32, vp, u32, vp, vp], i32),
         "lscat_ingest": ([vp, vp, vp, vp, vp, vp, u64, C.POINTER(TableC), C.POINTER(u64), vp], i32),
     }
@@ -499,13 +505,15 @@ class Ctx:
 
     # occupancy-API block and timeout economics
     def occupancy_block(self, kernel, blocks):
-        """(index into blocks of the occupancy calculator's choice, warps/SM per candidate)."""
+        """{'block_id': index into blocks of the occupancy calculator's choice, 'min_grid': the
+        API's minGridSize at that block, 'info': per-candidate dicts (lscat_occupancy_info)}."""
         b, bp = _arr(blocks, np.uint16)
-        w = np.zeros(b.size, np.uint32)
+        info = (OccInfo * b.size)()
         out = C.c_uint32()
-        self._ck(self._lib.lscat_occupancy_block(self.h, kernel, bp, b.size, C.byref(out),
-                                                 w.ctypes.data), "occupancy_block")
-        return out.value, w
+        self._ck(self._lib.lscat_occupancy_block(self.h, kernel, bp, b.size, C.byref(out), info),
+                 "occupancy_block")
+        rows = [{f: getattr(x, f) for f, _ in OccInfo._fields_} for x in info]
+        return {"block_id": out.value, "min_grid": rows[out.value]["api_min_grid"], "info": rows}
 
     def timeout_curve(self, table: Table, taus, warmup=1, brackets=10, launches=1000,
                       stream=None):

@@ -12,16 +12,44 @@ pytestmark = pytest.mark.gpu
 BLOCKS = list(range(32, 1025, 32))
 
 
+def _device():
+    import torch
+    from oracle import occupancy as O
+    p = torch.cuda.get_device_properties(0)
+    d = O.Device()
+    d.max_threads_per_sm = p.max_threads_per_multi_processor
+    d.regs_per_sm = p.regs_per_multiprocessor
+    d.smem_per_sm = p.shared_memory_per_multiprocessor
+    return d
+
+
 def test_occupancy_block():
+    """The library's occupancy-API numbers against the oracle's restatement of the occupancy
+    rule (oracle/occupancy.py) from the same compiled attributes (registers, static shared
+    memory) and the device limits: blocks per SM of every candidate of every suite kernel, and
+    the family choice (most resident warps, ties -> larger block)."""
+    from oracle import occupancy as O
     from paper_2103_14409_b200 import KERNELS, LscatError
     c = ctx()
+    dev = _device()
     for name, k in KERNELS.items():
-        bid, w = c.occupancy_block(k, BLOCKS)
-        assert 0 <= bid < 32 and w[bid] == w.max()
-        # ties go to the larger block
-        assert all(w[j] < w[bid] for j in range(bid + 1, 32))
+        r = c.occupancy_block(k, BLOCKS)
+        info = r["info"]
+        cands = []
+        for b, x in zip(BLOCKS, info):
+            assert x["threads"] == b
+            if x["regs_per_thread"] == 0 and x["blocks_per_sm"] == 0:   # no implementation
+                cands.append((b, -1, 0, 0))
+                continue
+            want = O.blocks_per_sm(b, x["regs_per_thread"], x["static_smem"], x["dynamic_smem"], dev)
+            assert x["blocks_per_sm"] == want, (name, b, x, want)
+            assert x["warps_per_sm"] == want * b // 32
+            assert 0 < x["api_block"] <= b and x["api_min_grid"] > 0, (name, b, x)
+            assert x["max_threads_per_block"] >= b
+            cands.append((b, x["regs_per_thread"], x["static_smem"], x["dynamic_smem"]))
+        assert r["block_id"] == O.choose(cands, dev), (name, r["block_id"], O.choose(cands, dev))
         if name == "gemm_bf16":
-            assert (w[:3] == 0).all()            # < 128 threads: no implementation
+            assert all(x["blocks_per_sm"] == 0 for x in info[:3])     # < 128 threads: none
     with pytest.raises(LscatError):
         c.occupancy_block(KERNELS["euclid"], [33])
 
@@ -31,7 +59,7 @@ def test_occupancy_block_quality_via_reduce():
     largest_block_id = that choice and compare with the oracle."""
     from paper_2103_14409_b200 import KERNELS, reduce_opts
     c = ctx()
-    bid, _ = c.occupancy_block(KERNELS["euclid"], BLOCKS)
+    bid = c.occupancy_block(KERNELS["euclid"], BLOCKS)["block_id"]
     t = gen_table(100_000, 400, preset="t4", seed=3)
     from tests.test_gpu_reduce import _device_table
     o = reduce_opts(32, 8, largest_block_id=bid)

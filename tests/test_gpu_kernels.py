@@ -251,7 +251,7 @@ def test_gemm_full_size_sampled():
     rng = np.random.default_rng(8192)
     rows_np = np.unique(np.r_[0:4, 127:131, 4090:4100, n - 4:n,
                               np.arange(0, n, 256) + rng.integers(0, 256, n // 256),
-                              rng.choice(n, 200, replace=False)])
+                              rng.choice(n, 240, replace=False)])
     assert len(rows_np) >= 256 and len(np.unique(rows_np // 256)) == n // 256
     rows = torch.as_tensor(rows_np, device="cuda")
     Ar = A[rows].float().cpu().numpy()
@@ -320,7 +320,9 @@ def test_suite_inputs_non_degenerate():
                     continue
                 x = t.float().cpu().numpy().astype(np.float64)
                 assert x.min() >= -1.0 and x.max() < 1.0, (k, n, slot)
-                assert abs(x.mean()) < 6.0 / np.sqrt(x.size) + 1e-3, (k, n, slot, x.mean())
+                # the grid's own mean: -2^-8 on the bf16 grid (256 points), -2^-24 on fp32's
+                mu = -2.0 ** -8 if t.dtype == torch.bfloat16 else -2.0 ** -24
+                assert abs(x.mean() - mu) < 6.0 / np.sqrt(3 * x.size), (k, n, slot, x.mean())
                 assert abs(x.std() - 1 / np.sqrt(3)) < 6 * np.sqrt(0.8 / (4 * x.size)) / np.sqrt(3) + 1e-3, \
                     (k, n, slot, x.std())
                 distinct = np.unique(x).size

@@ -335,3 +335,23 @@ def test_block_profile_brute_force(oracle_lib):
     assert all(int(r.profile_sum[i, j]) == int(ps[i, j]) for i in range(8) for j in range(8))
     # the best block of a group with a unique minimum contributes exactly 2^31 (perf 1)
     assert r.profile_mean.max() <= 1.0
+
+
+@pytest.mark.parametrize("threads", [1, 3, 8])
+def test_parallel_oracle_equals_oracle(oracle_lib, threads):
+    """The all-cores baseline variant (group-aligned chunks, integer partials summed) gives the
+    single-threaded oracle's counters and histograms exactly, ragged and uniform tables."""
+    rng = np.random.default_rng(threads)
+    rt, bid, off, gm = _random_table(rng, 500, 8, dup_vals=True)
+    o = oracle_lib.Opts(n_blocks=8)
+    r = oracle_lib.reduce_table(rt, bid, off, group_matrix=gm, opts=o)
+    c, ph, gh, bh = oracle_lib.reduce_table_parallel(rt, bid, off, group_matrix=gm, opts=o,
+                                                     threads=threads)
+    assert c == r.counters and (ph == r.perf_hist).all() and (gh == r.gain_hist).all()
+    assert (bh == r.best_block_hist).all()
+    t = gen_table(32 * 1000 - 7, 125, preset="t4", seed=3)
+    r = oracle_lib.reduce_table(t["runtime_ms"], t["block_id"], rows_per_group=32, first_group=5)
+    c, ph, gh, bh = oracle_lib.reduce_table_parallel(t["runtime_ms"], t["block_id"],
+                                                     rows_per_group=32, first_group=5,
+                                                     threads=threads)
+    assert c == r.counters and (ph == r.perf_hist).all() and (bh == r.best_block_hist).all()
