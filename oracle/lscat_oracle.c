@@ -236,3 +236,78 @@ void oracle_finalize(const oracle_result* R, oracle_derived* D) {
   D->mean_perf = nrd > 0 ? ((double)tp * 0x1p-52) / nrd : NAN;
   D->mean_gain = nrd > 0 ? ((double)tg * 0x1p-32) / nrd : NAN;
 }
+
+/* ---- per-kernel roll-up (R-26) ----------------------------------------- */
+typedef struct { uint64_t kernel, group; } kg_pair;
+
+static int cmp_kg(const void* a, const void* b) {
+  const kg_pair *x = (const kg_pair*)a, *y = (const kg_pair*)b;
+  if (x->kernel != y->kernel) return x->kernel < y->kernel ? -1 : 1;
+  return (x->group > y->group) - (x->group < y->group);
+}
+
+int oracle_kernel_rollup(const oracle_table* T, const uint32_t* group_kernel, const oracle_opts* o,
+                         const oracle_group_out* G, oracle_rollup* K) {
+  /* The paper states two results over kernels: the share of kernels for which "the
+     best performing thread block was not the largest one", and the share whose largest-block
+     performance "ranges from 40 to 85%".  For each kernel k, over its ratio-defined groups
+     (the matrix sizes where perf = best / t_l is defined, R-5/R-6):
+       c_k     = their number (a kernel with c_k = 0 is not counted);
+       S_k     = sum of floor(perf * 2^52) (the exact fixed-point values of O3 step 9);
+       not_best(k)  <=> some such group's best block != l;
+       mean perf    P_k = S_k / (c_k 2^52), compared exactly:
+       perf_lt(k)   <=> P_k < perf_lt_num / perf_lt_den;
+       band(k)      <=> band_lo <= P_k < perf_lt  (half-open, as R-10);
+       histogram bin = the largest j in [0, nb] with j c_k 2^52 <= nb S_k;
+       mean over kernels = sum_k floor(S_k / c_k) / (2^52 n_kernels), kept as two limbs.
+     Groups are collected per kernel id by sorting (kernel, group) pairs, so the roll-up does
+     not depend on the table's group order. */
+  if (!G || !G->perf || !G->flags || !G->best_block || o->bins_per_unit == 0 || o->n_matrices == 0)
+    return ORACLE_EINVAL;
+  const uint32_t nb = o->bins_per_unit;
+  memset(K->counters, 0, sizeof(K->counters));
+  memset(K->perf_hist, 0, sizeof(uint64_t) * (nb + 1));
+  uint64_t n = T->n_groups;
+  kg_pair* pr = (kg_pair*)malloc((n ? n : 1) * sizeof(kg_pair));
+  if (!pr) return ORACLE_ENOMEM;
+  for (uint64_t g = 0; g < n; g++) {
+    pr[g].kernel = group_kernel ? group_kernel[g] : (T->first_group + g) / o->n_matrices;
+    pr[g].group = g;
+  }
+  qsort(pr, n, sizeof(kg_pair), cmp_kg);
+  const unsigned __int128 one = (unsigned __int128)1 << 52;
+  uint64_t i = 0;
+  while (i < n) {
+    uint64_t j = i, c = 0;
+    unsigned __int128 S = 0;
+    int not_best = 0;
+    while (j < n && pr[j].kernel == pr[i].kernel) {
+      uint64_t g = pr[j].group;
+      if (G->flags[g] & 0x008u) {            /* ratio-defined */
+        c++;
+        S += (uint64_t)floor(G->perf[g] * 4503599627370496.0);
+        if (G->best_block[g] != o->largest_block_id) not_best = 1;
+      }
+      j++;
+    }
+    if (c > 0) {
+      uint64_t* C = K->counters;
+      C[OK_N_KERNELS]++;
+      if (not_best) C[OK_N_NOT_BEST]++;
+      unsigned __int128 cd = (unsigned __int128)c * one;  /* P_k = S / cd */
+      int lt = (unsigned __int128)o->perf_lt_den * S < (unsigned __int128)o->perf_lt_num * cd;
+      if (lt) C[OK_N_PERF_LT]++;
+      if (lt && (unsigned __int128)o->band_lo_den * S >= (unsigned __int128)o->band_lo_num * cd)
+        C[OK_N_PERF_BAND]++;
+      uint32_t bin = nb;
+      while (bin > 0 && (unsigned __int128)bin * cd > (unsigned __int128)nb * S) bin--;
+      K->perf_hist[bin]++;
+      uint64_t kfx = (uint64_t)(S / c);
+      C[OK_MEAN_FX_HI] += kfx >> 21;
+      C[OK_MEAN_FX_LO] += kfx & ((1ull << 21) - 1);
+    }
+    i = j;
+  }
+  free(pr);
+  return ORACLE_OK;
+}

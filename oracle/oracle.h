@@ -55,6 +55,25 @@ typedef struct {
 
 int oracle_reduce_table(const oracle_table* T, const oracle_opts* o, oracle_result* R,
                         oracle_group_out* G);
+
+/* Per-kernel roll-up (P:258 counts *kernels*: "this was also true for 83% of the kernels",
+   "in around 1% of the kernels this ranges from 40 to 85%"; R-26). */
+enum {
+  OK_N_KERNELS = 0,          /* kernels with >= 1 ratio-defined group                       */
+  OK_N_NOT_BEST,             /* ... in which some ratio-defined group's best block != l     */
+  OK_N_PERF_LT,              /* ... whose mean performance is < perf_lt (17/20)            */
+  OK_N_PERF_BAND,            /* ... whose mean performance is in [band_lo, perf_lt)        */
+  OK_MEAN_FX_HI, OK_MEAN_FX_LO,  /* sum over kernels of floor(S_k / c_k), two 21-bit limbs   */
+  ORACLE_NKCOUNTERS
+};
+typedef struct {
+  uint64_t counters[ORACLE_NKCOUNTERS];
+  uint64_t* perf_hist;       /* [bins+1] caller-owned: bin j = largest j with j c 2^52 <= nb S */
+} oracle_rollup;
+/* group_kernel[g] (NULL -> (first_group + g) / n_matrices) names each group's kernel; G holds
+   oracle_reduce_table's per-group outputs of the same table. */
+int oracle_kernel_rollup(const oracle_table* T, const uint32_t* group_kernel, const oracle_opts* o,
+                         const oracle_group_out* G, oracle_rollup* K);
 void oracle_finalize(const oracle_result* R, oracle_derived* D);
 double oracle_percentile(const double* values, uint64_t n, double p);
 size_t oracle_partials_len(uint32_t bins_per_unit, uint32_t gain_cap, uint32_t n_matrices,

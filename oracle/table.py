@@ -69,6 +69,14 @@ class _GroupOut(C.Structure):
                 ("gain", C.c_void_p), ("flags", C.c_void_p)]
 
 
+ROLLUP = ["n_kernels", "n_kernels_not_best", "n_kernels_perf_lt", "n_kernels_perf_band",
+          "kernel_mean_fx_hi", "kernel_mean_fx_lo"]
+
+
+class _Rollup(C.Structure):
+    _fields_ = [("counters", C.c_uint64 * len(ROLLUP)), ("perf_hist", C.c_void_p)]
+
+
 class _Derived(C.Structure):
     _fields_ = [(n, C.c_double) for n in (
         "frac_nonnan", "frac_largest_not_best", "frac_gain_gt", "frac_perf_lt",
@@ -87,6 +95,9 @@ def lib():
         _lib.oracle_reduce_table.restype = C.c_int
         _lib.oracle_finalize.argtypes = [C.POINTER(_Result), C.POINTER(_Derived)]
         _lib.oracle_finalize.restype = None
+        _lib.oracle_kernel_rollup.argtypes = [C.POINTER(_Table), C.c_void_p, C.POINTER(_Opts),
+                                              C.POINTER(_GroupOut), C.POINTER(_Rollup)]
+        _lib.oracle_kernel_rollup.restype = C.c_int
         _lib.oracle_percentile.argtypes = [C.c_void_p, C.c_uint64, C.c_double]
         _lib.oracle_percentile.restype = C.c_double
     return _lib
@@ -123,6 +134,7 @@ class Result:
     gain: np.ndarray
     flags: np.ndarray
     percentiles: dict = field(default_factory=dict)
+    rollup: dict | None = None
     profile_sum: np.ndarray | None = None
     profile_count: np.ndarray | None = None
     profile_mean: np.ndarray | None = None
@@ -133,8 +145,10 @@ class OracleError(RuntimeError):
 
 
 def reduce_table(runtime_ms, block_id, group_offset=None, rows_per_group=0, group_matrix=None,
-                 first_group=0, opts: Opts | None = None, percentiles=()) -> Result:
-    """Run the oracle on one table (host numpy arrays)."""
+                 first_group=0, opts: Opts | None = None, percentiles=(), group_kernel=None,
+                 kernel_rollup=False) -> Result:
+    """Run the oracle on one table (host numpy arrays).  kernel_rollup: also the per-kernel
+    roll-up (P:258, R-26) with group_kernel (None -> (first_group + g) // n_matrices)."""
     o = opts or Opts()
     rt = np.ascontiguousarray(runtime_ms, dtype=np.float32)
     bid = np.ascontiguousarray(block_id, dtype=np.uint16)
@@ -181,6 +195,23 @@ def reduce_table(runtime_ms, block_id, group_offset=None, rows_per_group=0, grou
         with np.errstate(invalid="ignore", divide="ignore"):
             res.profile_mean = (psum.astype(np.float64) * 2.0 ** -31 / pcnt).reshape(
                 o.n_matrices, o.n_blocks)
+    if kernel_rollup:
+        gk = None if group_kernel is None else np.ascontiguousarray(group_kernel, dtype=np.uint32)
+        kh = np.zeros(o.bins_per_unit + 1, np.uint64)
+        K = _Rollup()
+        K.perf_hist = kh.ctypes.data
+        rc = lib().oracle_kernel_rollup(C.byref(T), None if gk is None else gk.ctypes.data,
+                                        C.byref(op), C.byref(GO), C.byref(K))
+        if rc != 0:
+            raise OracleError(f"oracle_kernel_rollup failed: code {rc}")
+        kc = {k: int(K.counters[i]) for i, k in enumerate(ROLLUP)}
+        nk = kc["n_kernels"]
+        tot = (kc["kernel_mean_fx_hi"] << 21) + kc["kernel_mean_fx_lo"]
+        res.rollup = dict(kc, perf_hist=kh,
+                          frac_kernels_not_best=kc["n_kernels_not_best"] / nk if nk else float("nan"),
+                          frac_kernels_perf_lt=kc["n_kernels_perf_lt"] / nk if nk else float("nan"),
+                          frac_kernels_perf_band=kc["n_kernels_perf_band"] / nk if nk else float("nan"),
+                          mean_kernel_perf=(float(tot) * 2.0 ** -52) / nk if nk else float("nan"))
     if percentiles:
         rd = (fl & 0x008) != 0
         res.percentiles = {

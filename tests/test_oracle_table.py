@@ -355,3 +355,81 @@ def test_parallel_oracle_equals_oracle(oracle_lib, threads):
                                                      rows_per_group=32, first_group=5,
                                                      threads=threads)
     assert c == r.counters and (ph == r.perf_hist).all() and (bh == r.best_block_hist).all()
+
+
+# ----------------------------------------------------------------------------------------
+# Per-kernel roll-up (R-26)
+# ----------------------------------------------------------------------------------------
+def test_kernel_rollup_golden(oracle_lib):
+    g = json.load(open(os.path.join(GOLDEN, "kernel_rollup.json")))
+    rt, bid, off, gm = _table_from_groups(g["groups"])
+    gk = np.array([x["kernel"] for x in g["groups"]], np.uint32)
+    o = oracle_lib.Opts(n_blocks=g["n_blocks"], n_matrices=g["n_matrices"])
+    r = oracle_lib.reduce_table(rt, bid, off, group_matrix=gm, opts=o, group_kernel=gk,
+                                kernel_rollup=True)
+    e = g["expected"]
+    for k in ("n_kernels", "n_kernels_not_best", "n_kernels_perf_lt", "n_kernels_perf_band"):
+        assert r.rollup[k] == e[k], k
+    # sum over kernels of floor(S_k / c_k) = the four per-kernel values listed in the golden
+    assert sum(e["kernel_mean_fx"].values()) == e["kernel_mean_fx_total"]
+    assert (r.rollup["kernel_mean_fx_hi"] << 21) + r.rollup["kernel_mean_fx_lo"] == e["kernel_mean_fx_total"]
+    want = np.zeros(101, np.uint64)
+    for b, v in e["perf_hist_nonzero"].items():
+        want[int(b)] = v
+    assert (r.rollup["perf_hist"] == want).all()
+    assert r.rollup["frac_kernels_not_best"] == 3 / 4
+    assert r.rollup["frac_kernels_perf_band"] == 2 / 4
+    # the roll-up does not depend on the order of the groups (the oracle sorts by kernel id)
+    perm = np.random.default_rng(0).permutation(len(g["groups"]))
+    rt2, bid2, off2, gm2 = _table_from_groups([g["groups"][i] for i in perm])
+    r2 = oracle_lib.reduce_table(rt2, bid2, off2, group_matrix=gm2, opts=o, group_kernel=gk[perm],
+                                 kernel_rollup=True)
+    assert {k: r2.rollup[k] for k in e if k in r2.rollup} == {k: r.rollup[k] for k in e if k in r.rollup}
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_kernel_rollup_brute_force(oracle_lib, seed):
+    """Fraction brute force of every roll-up quantity from the brute-force per-group values
+    (pandas argmin, Fraction-free RN(b/t) doubles) on random ragged tables with contiguous
+    kernels of 1..10 groups."""
+    rng = np.random.default_rng(100 + seed)
+    L = [4, 8, 32][seed % 3]
+    ell = L - 1
+    G = 400
+    rt, bid, off, gm = _random_table(rng, G, L, dup_vals=seed < 2)
+    sizes = rng.integers(1, 11, G)
+    gk = np.repeat(np.arange(G), sizes)[:G].astype(np.uint32) * 7 + 3
+    o = oracle_lib.Opts(n_blocks=L, largest_block_id=ell)
+    r = oracle_lib.reduce_table(rt, bid, off, group_matrix=gm, opts=o, group_kernel=gk,
+                                kernel_rollup=True)
+    res, ph, gh, bbh, fxp, fxg, best, perfs, gains = brute_force(rt, bid, off, gm, L, ell)
+    # per-group ratio-defined flag and perf, recomputed independently
+    df_ok = np.isfinite(rt) & (rt > 0)
+    per = {}
+    for g in range(G):
+        rows = range(off[g], off[g + 1])
+        okr = [i for i in rows if df_ok[i]]
+        lrow = [i for i in rows if bid[i] == ell]
+        if not okr or not lrow or not df_ok[lrow[0]]:
+            continue
+        b = min(float(rt[i]) for i in okr)
+        t = float(rt[lrow[0]])
+        per.setdefault(int(gk[g]), []).append((math.floor(Fraction(b / t) * 2 ** 52), best[g] != ell))
+    n_k = len(per)
+    nb_ = sum(any(x[1] for x in v) for v in per.values())
+    lt = band = 0
+    hist = [0] * 101
+    mean_fx = 0
+    for v in per.values():
+        S, c = sum(x[0] for x in v), len(v)
+        P = Fraction(S, c * 2 ** 52)
+        lt += P < Fraction(17, 20)
+        band += Fraction(2, 5) <= P < Fraction(17, 20)
+        hist[math.floor(P * 100)] += 1
+        mean_fx += S // c
+    R = r.rollup
+    assert R["n_kernels"] == n_k and R["n_kernels_not_best"] == nb_
+    assert R["n_kernels_perf_lt"] == lt and R["n_kernels_perf_band"] == band
+    assert R["perf_hist"].tolist() == hist
+    assert (R["kernel_mean_fx_hi"] << 21) + R["kernel_mean_fx_lo"] == mean_fx
+    assert n_k >= nb_ > 0
