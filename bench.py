@@ -667,6 +667,24 @@ def table_benches(ctx, L, hbm_peak, rank, world, barrier, allmax, cpu_rows=False
                     torch.cuda.synchronize()
                     lt.append(e0.elapsed_time(e1))
                 res["local_ms_no_merge"] = round(allmax(statistics.median(lt)), 4)
+            # the per-kernel roll-up of P:258 (R-26) on the same shard: its extra time and values
+            ok_ = L.reduce_opts(32, 8, point_sharded=1 if (point and world > 1) else 0, kernel_rollup=1)
+            run(ctx, ok_)
+            kt = []
+            for _ in range(5):
+                e0, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+                barrier()
+                e0.record(stream)
+                kst = run(ctx, ok_)
+                e1.record(stream)
+                barrier()
+                kt.append(allmax(e0.elapsed_time(e1)))
+            res["with_kernel_rollup"] = {
+                "ms_reduce_plus_stats": round(statistics.median(kt), 4),
+                "n_kernels": kst["n_kernels"],
+                "frac_kernels_largest_not_best": round(kst["frac_kernels_largest_not_best"], 4),
+                "frac_kernels_perf_band": round(kst["frac_kernels_perf_band"], 5),
+                "mean_kernel_perf": round(kst["mean_kernel_perf"], 5)}
             out[key] = res
             if cpu_rows and name != "scaled_1e9":
                 from oracle import table as OT

@@ -265,6 +265,15 @@ typedef struct {
                               /*      of floor(RN(best / r_b) * 2^31) over the ok rows of   */
                               /*      defined groups, and their count (R-22); one */
                               /*      extra read of the table                               */
+  uint32_t kernel_rollup;     /* 1 -> also the per-kernel roll-up of P:258 ("83 % of the    */
+                              /*      kernels", "1 % of the kernels ... from 40 to 85 %",  */
+                              /*      DESIGN.md R-26): per kernel id (group_kernel, or      */
+                              /*      (first_group + g) / n_matrices when NULL) over its    */
+                              /*      ratio-defined groups: some best block != l, and the  */
+                              /*      exact kernel-mean perf S_k / (c_k 2^52) against the  */
+                              /*      thresholds and in 1 % bins.  Precondition: a kernel's */
+                              /*      groups are contiguous in table order (sweep, generator */
+                              /*      and ingest tables are); 8 extra bytes per group       */
 } lscat_reduce_opts;
 
 /* Fills `opts` with the defaults above for a block list of n_blocks with largest id l. */
@@ -284,7 +293,9 @@ typedef struct {
 /* Layout of the packed partial vector (uint64 words), LSCAT_P_* counter slots first, then
    perf_hist [bins_per_unit+1], gain_hist [gain_cap*bins_per_unit+1], best_block_hist
    [n_matrices*n_blocks], and with block_profile: profile_sum [n_matrices*n_blocks],
-   profile_count [n_matrices*n_blocks]. */
+   profile_count [n_matrices*n_blocks], and with kernel_rollup: 8 words (n_kernels,
+   n_kernels_largest_not_best, n_kernels_perf_lt, n_kernels_perf_band, kernel_mean_fx_hi,
+   kernel_mean_fx_lo, 0, 0) and kernel_perf_hist [bins_per_unit+1]. */
 enum {
   LSCAT_P_ROWS = 0, LSCAT_P_OK, LSCAT_P_NAN, LSCAT_P_INVALID,
   LSCAT_P_GROUPS, LSCAT_P_DEFINED, LSCAT_P_ALL_NAN, LSCAT_P_COMPLETE, LSCAT_P_INCOMPLETE,
@@ -353,6 +364,17 @@ typedef struct {
   double* profile_mean;         /* mean of best / r_b ((double)sum * 2^-31 / count); NaN  */
                                 /* where count == 0                                        */
   uint64_t* profile_count;      /* number of rows averaged                                 */
+  /* with opts->kernel_rollup (else untouched): the per-kernel roll-up (R-26) */
+  uint64_t n_kernels;                    /* kernels with >= 1 ratio-defined group        */
+  uint64_t n_kernels_largest_not_best;   /* ... some such group's best block != l        */
+  uint64_t n_kernels_perf_lt;            /* ... kernel-mean perf < perf_lt               */
+  uint64_t n_kernels_perf_band;          /* ... kernel-mean perf in [band_lo, perf_lt)   */
+  uint64_t kernel_mean_fx_hi, kernel_mean_fx_lo;  /* sum_k floor(S_k / c_k), 21-bit limbs */
+  double frac_kernels_largest_not_best;  /* P:258 "83 % of the kernels"                   */
+  double frac_kernels_perf_lt;
+  double frac_kernels_perf_band;         /* P:258 "around 1 % of the kernels"             */
+  double mean_kernel_perf;               /* mean over kernels of the kernel-mean perf      */
+  uint64_t* kernel_perf_hist;            /* optional HOST [bins_per_unit + 1]             */
 } lscat_stats_out;
 
 /* Finalize the statistics of the last lscat_reduce_table on ctx (a10) and, when

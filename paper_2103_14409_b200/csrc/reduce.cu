@@ -60,6 +60,8 @@ struct RP {
   uint64_t* g_lcode;
   uint32_t* g_cnt;  // [3*G]: n_ok, n_nan, n_rows
   int mode;
+  // per-kernel roll-up (R-26): per-group record fx_perf | rd << 53 | not_best << 54
+  uint64_t* krec;
   uint32_t smem_words;  // perf + gain + best-block histogram words in smem
   uint32_t vec;         // runtime / block-id arrays are 16-byte aligned (vector path allowed)
 };
@@ -228,6 +230,13 @@ __device__ void finalize_lane(const RP& p, uint64_t g, bool active, const GroupA
     } else {
       flags |= LSCAT_GF_LARGEST_MISSING;
     }
+  }
+  if (active && p.krec) {  // roll-up record of an accumulated, ratio-defined group
+    uint64_t r = 0;
+    if (acc && (flags & LSCAT_GF_RATIO_DEFINED))
+      r = (uint64_t)__dmul_rn(perf, 4503599627370496.0) | (1ull << 53) |
+          ((uint64_t)((flags & LSCAT_GF_LARGEST_IS_BEST) == 0) << 54);
+    p.krec[g] = r;
   }
   if (active) {
     if (p.o_best) p.o_best[g] = defined ? (uint16_t)a.min_bid : (uint16_t)0xFFFF;
@@ -637,7 +646,8 @@ __global__ void init_partials(uint64_t* __restrict__ partials, size_t plen, uint
 
 size_t partials_len(const lscat_reduce_opts& o) {
   return (size_t)kNC + (o.bins_per_unit + 1) + ((size_t)o.gain_cap * o.bins_per_unit + 1) +
-         (size_t)o.n_matrices * o.n_blocks * (o.block_profile ? 3 : 1);
+         (size_t)o.n_matrices * o.n_blocks * (o.block_profile ? 3 : 1) +
+         (o.kernel_rollup ? (size_t)8 + o.bins_per_unit + 1 : 0);
 }
 
 // Block profile (Figs. 2/4; reading R-22): a second pass over this rank's rows once
@@ -688,6 +698,115 @@ __global__ void __launch_bounds__(256) profile_kernel(RP p, const float* __restr
   }
 }
 
+// ---- per-kernel roll-up (R-26) ------------------------------------------
+// Over the groups [lo, hi) this rank accumulated, a thread at each kernel's first group folds
+// the kernel's records (c = ratio-defined groups, S = sum of floor(perf 2^52) as a 128-bit
+// integer, any best block != l).  Kernels wholly inside (lo, hi) are finalised here; the
+// segment touching lo and the one touching hi may continue on another rank, so they go to two
+// boundary records (kernel id + partial sums) that rank 0 merges after an all-gather.
+constexpr int kRollupWords = 8;   // counters region of the roll-up partials
+constexpr int kBndWords = 5;      // boundary record: kid | 1 << 32, c, S lo64, S hi64, not_best
+
+struct RollupArgs {
+  const uint64_t* krec;
+  const uint32_t* gkern;  // NULL -> (first_group + g) / M
+  uint64_t first_group, lo, hi;
+  uint32_t M, nb, pln, pld, bln, bld;
+  uint64_t* part;         // roll-up region of the partial vector: [8] counters, [nb+1] hist
+  uint64_t* bnd;          // [2 * kBndWords] this rank's boundary records
+};
+
+__device__ __forceinline__ uint32_t kid_of(const RollupArgs& q, uint64_t g) {
+  return q.gkern ? q.gkern[g] : (uint32_t)((q.first_group + g) / q.M);
+}
+
+// One kernel's roll-up (exact: 128-bit products of the fixed-point sum, R-26).
+__device__ void kernel_fin(const RollupArgs& q, uint64_t c, unsigned __int128 S, bool not_best,
+                           unsigned long long* cnt, uint32_t* hist32, unsigned long long* hist64) {
+  if (c == 0) return;
+  const unsigned __int128 cd = (unsigned __int128)c << 52;  // kernel-mean perf = S / cd
+  const bool lt = (unsigned __int128)q.pld * S < (unsigned __int128)q.pln * cd;
+  const bool band = lt && (unsigned __int128)q.bld * S >= (unsigned __int128)q.bln * cd;
+  uint32_t bin = (uint32_t)(((unsigned __int128)q.nb * S) / cd);  // largest j: j cd <= nb S
+  if (bin > q.nb) bin = q.nb;
+  const uint64_t kfx = (uint64_t)(S / c);
+  atomicAdd(&cnt[0], 1ull);
+  if (not_best) atomicAdd(&cnt[1], 1ull);
+  if (lt) atomicAdd(&cnt[2], 1ull);
+  if (band) atomicAdd(&cnt[3], 1ull);
+  atomicAdd(&cnt[4], (unsigned long long)(kfx >> 21));
+  atomicAdd(&cnt[5], (unsigned long long)(kfx & ((1ull << 21) - 1)));
+  if (hist32) atomicAdd(&hist32[bin], 1u);
+  else atomicAdd(&hist64[bin], 1ull);
+}
+
+__global__ void __launch_bounds__(256) rollup_kernel(RollupArgs q) {
+  extern __shared__ unsigned long long rs[];
+  unsigned long long* cnt = rs;                                  // [kRollupWords]
+  uint32_t* hist = reinterpret_cast<uint32_t*>(rs + kRollupWords);  // [nb + 1]
+  for (uint32_t i = threadIdx.x; i < kRollupWords; i += blockDim.x) cnt[i] = 0;
+  for (uint32_t i = threadIdx.x; i <= q.nb; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  for (uint64_t g = q.lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < q.hi;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = kid_of(q, g);
+    if (g > q.lo && kid_of(q, g - 1) == k) continue;  // not the kernel's first group here
+    uint64_t c = 0, e = g;
+    unsigned __int128 S = 0;
+    bool nbst = false;
+    for (; e < q.hi && kid_of(q, e) == k; e++) {
+      const uint64_t r = q.krec[e];
+      if (r >> 53 & 1) {
+        c++;
+        S += r & ((1ull << 53) - 1);
+        nbst |= (r >> 54) & 1;
+      }
+    }
+    if (g == q.lo || e == q.hi) {  // may continue on a neighbouring rank: boundary record
+      uint64_t* b = q.bnd + (g == q.lo ? 0 : kBndWords);
+      b[0] = (uint64_t)k | (1ull << 32);
+      b[1] = c;
+      b[2] = (uint64_t)S;
+      b[3] = (uint64_t)(S >> 64);
+      b[4] = nbst;
+    } else {
+      kernel_fin(q, c, S, nbst, cnt, hist, nullptr);
+    }
+  }
+  __syncthreads();
+  unsigned long long* gc = reinterpret_cast<unsigned long long*>(q.part);
+  for (uint32_t i = threadIdx.x; i < kRollupWords; i += blockDim.x)
+    if (cnt[i]) atomicAdd(&gc[i], cnt[i]);
+  for (uint32_t i = threadIdx.x; i <= q.nb; i += blockDim.x)
+    if (hist[i]) atomicAdd(&gc[kRollupWords + i], (unsigned long long)hist[i]);
+}
+
+// Rank 0 merges every rank's two boundary records in rank order (equal kernel ids are adjacent
+// because a kernel's groups are contiguous) and finalises the merged kernels.
+__global__ void rollup_boundary_kernel(RollupArgs q, const uint64_t* __restrict__ all, int nrec) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  unsigned long long* gc = reinterpret_cast<unsigned long long*>(q.part);
+  bool have = false;
+  uint32_t kid = 0;
+  uint64_t c = 0;
+  unsigned __int128 S = 0;
+  bool nbst = false;
+  for (int i = 0; i < nrec; i++) {
+    const uint64_t* b = all + (size_t)i * kBndWords;
+    if (!(b[0] >> 32)) continue;
+    const uint32_t k = (uint32_t)b[0];
+    if (have && k != kid) {
+      kernel_fin(q, c, S, nbst, gc, nullptr, gc + kRollupWords);
+      have = false;
+    }
+    if (!have) { have = true; kid = k; c = 0; S = 0; nbst = false; }
+    c += b[1];
+    S += ((unsigned __int128)b[3] << 64) | b[2];
+    nbst |= b[4] != 0;
+  }
+  if (have) kernel_fin(q, c, S, nbst, gc, nullptr, gc + kRollupWords);
+}
+
 bool opts_ok(const lscat_reduce_opts* o) {
   if (!o) return false;
   if (o->n_blocks == 0 || o->n_blocks > 65535 || o->largest_block_id >= o->n_blocks) return false;
@@ -699,6 +818,7 @@ bool opts_ok(const lscat_reduce_opts* o) {
   if (o->band_lo_num >= (1u << 29) || o->band_lo_den >= (1u << 29)) return false;
   if (o->nan_policy > LSCAT_COMPLETE_ONLY) return false;
   if (o->block_profile && (uint64_t)o->n_matrices * o->n_blocks * 12 > 200 * 1024) return false;
+  if (o->kernel_rollup > 1 || o->block_profile > 1) return false;
   return true;
 }
 
@@ -752,6 +872,7 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
   cudaError_t err;
 
   RP p{};
+  const uint32_t* gkern = T->group_kernel;
   // stage host tables through device scratch (e2e path)
   if (T->mem == LSCAT_MEM_HOST) {
     float* rt = (float*)scratch(ctx, "h_rt", n * 4, &err);
@@ -773,6 +894,12 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
       if (err) return cuda_fail(ctx, err, "reduce_table: scratch");
       LSCAT_CUDA(ctx, cudaMemcpyAsync(gm, T->group_matrix, G * 4, cudaMemcpyHostToDevice, s));
       p.gmat = gm;
+    }
+    if (T->group_kernel && o->kernel_rollup) {
+      uint32_t* gk = (uint32_t*)scratch(ctx, "h_gk", G * 4, &err);
+      if (err) return cuda_fail(ctx, err, "reduce_table: scratch");
+      LSCAT_CUDA(ctx, cudaMemcpyAsync(gk, T->group_kernel, G * 4, cudaMemcpyHostToDevice, s));
+      gkern = gk;
     }
   } else {
     p.rt = T->runtime_ms;
@@ -802,6 +929,10 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
   if (o->keep_values) {
     if (!p.o_perf) { p.o_perf = (double*)scratch(ctx, "perf", G * 8, &err); if (err) return cuda_fail(ctx, err, "scratch"); }
     if (!p.o_gain) { p.o_gain = (double*)scratch(ctx, "gain", G * 8, &err); if (err) return cuda_fail(ctx, err, "scratch"); }
+  }
+  if (o->kernel_rollup) {
+    p.krec = (uint64_t*)scratch(ctx, "krec", std::max<uint64_t>(G, 1) * 8, &err);
+    if (err) return cuda_fail(ctx, err, "reduce_table: scratch");
   }
   const size_t plen = partials_len(*o);
   p.partials = (uint64_t*)scratch(ctx, "partials", plen * 8, &err);
@@ -878,6 +1009,43 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
     profile_kernel<<<g3, 256, psm, s>>>(p, p.o_bestrt, p.o_flags, prof, prof + ML);
     ctx->launches++;
     LSCAT_CUDA(ctx, cudaGetLastError());
+  }
+  if (o->kernel_rollup) {  // R-26, over the groups this rank accumulated
+    RollupArgs q{};
+    q.krec = p.krec;
+    q.gkern = gkern;
+    q.first_group = T->first_group;
+    q.lo = p.acc_lo;
+    q.hi = p.acc_hi;
+    q.M = o->n_matrices;
+    q.nb = o->bins_per_unit;
+    q.pln = o->perf_lt_num; q.pld = o->perf_lt_den; q.bln = o->band_lo_num; q.bld = o->band_lo_den;
+    q.part = p.partials + plen - (8 + o->bins_per_unit + 1);
+    const int W = ctx->world;
+    uint64_t* bnd = (uint64_t*)scratch(ctx, "kbnd", (size_t)2 * kBndWords * 8 * (1 + W), &err);
+    if (err) return cuda_fail(ctx, err, "reduce_table: scratch");
+    q.bnd = bnd;
+    LSCAT_CUDA(ctx, cudaMemsetAsync(bnd, 0, 2 * kBndWords * 8, s));
+    const size_t rsm = kRollupWords * 8 + (o->bins_per_unit + 1) * 4;
+    if (rsm > 48 * 1024) LSCAT_CUDA(ctx, ensure_smem_attr((const void*)rollup_kernel, rsm));
+    const uint64_t ng = q.hi - q.lo;
+    if (ng) {
+      const int g4 = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)ctx->sm_count * 8, (ng + 255) / 256));
+      rollup_kernel<<<g4, 256, rsm, s>>>(q);
+      ctx->launches++;
+      LSCAT_CUDA(ctx, cudaGetLastError());
+    }
+    uint64_t* all = bnd;
+    if (W > 1) {
+      all = bnd + 2 * kBndWords;
+      lscat_status ns = ctx->comm->allgather(ctx, bnd, all, 2 * kBndWords, DT::U64, s);
+      if (ns) return ns;
+    }
+    if (ctx->rank == 0) {
+      rollup_boundary_kernel<<<1, 32, 0, s>>>(q, all, 2 * W);
+      ctx->launches++;
+      LSCAT_CUDA(ctx, cudaGetLastError());
+    }
   }
   if (ctx->world > 1) {
     lscat_status ns = ctx->comm->allreduce(

@@ -755,7 +755,8 @@ extern "C" lscat_status lscat_stats(lscat_ctx* ctx, const lscat_reduce_opts* o, 
   cudaStream_t s = (cudaStream_t)stream;
   LSCAT_CUDA(ctx, cudaSetDevice(ctx->device));
   const size_t nb = o->bins_per_unit, ng = (size_t)o->gain_cap * nb, nbb = (size_t)o->n_matrices * o->n_blocks;
-  const size_t plen = LSCAT_P_NCOUNTERS + (nb + 1) + (ng + 1) + nbb * (o->block_profile ? 3 : 1);
+  const size_t plen = LSCAT_P_NCOUNTERS + (nb + 1) + (ng + 1) + nbb * (o->block_profile ? 3 : 1) +
+                      (o->kernel_rollup ? 8 + nb + 1 : 0);
   cudaError_t err;
   uint64_t* hP = (uint64_t*)pinned(ctx, "stats_partials", plen * 8, &err);
   if (err) return cuda_fail(ctx, err, "stats: pinned");
@@ -799,6 +800,22 @@ extern "C" lscat_status lscat_stats(lscat_ctx* ctx, const lscat_reduce_opts* o, 
   if (out->perf_hist) memcpy(out->perf_hist, H, (nb + 1) * 8);
   if (out->gain_hist) memcpy(out->gain_hist, H + nb + 1, (ng + 1) * 8);
   if (out->best_block_hist) memcpy(out->best_block_hist, H + nb + 1 + ng + 1, nbb * 8);
+  if (o->kernel_rollup) {  // R-26: the per-kernel roll-up
+    const uint64_t* K = C + plen - (8 + nb + 1);
+    out->n_kernels = K[0];
+    out->n_kernels_largest_not_best = K[1];
+    out->n_kernels_perf_lt = K[2];
+    out->n_kernels_perf_band = K[3];
+    out->kernel_mean_fx_hi = K[4];
+    out->kernel_mean_fx_lo = K[5];
+    const double nk = (double)K[0];
+    out->frac_kernels_largest_not_best = K[0] ? (double)K[1] / nk : NAN;
+    out->frac_kernels_perf_lt = K[0] ? (double)K[2] / nk : NAN;
+    out->frac_kernels_perf_band = K[0] ? (double)K[3] / nk : NAN;
+    const unsigned __int128 tk = ((unsigned __int128)K[4] << 21) + K[5];
+    out->mean_kernel_perf = K[0] ? ((double)tk * 0x1p-52) / nk : NAN;
+    if (out->kernel_perf_hist) memcpy(out->kernel_perf_hist, K + 8, (nb + 1) * 8);
+  }
   if (o->block_profile) {  // R-22: mean of best / r_b per (matrix, block)
     const uint64_t* ps = H + nb + 1 + ng + 1 + nbb;
     const uint64_t* pc = ps + nbb;

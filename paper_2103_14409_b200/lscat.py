@@ -39,6 +39,10 @@ COUNTERS = ["n_rows", "n_ok", "n_nan", "n_invalid", "n_groups", "n_defined", "n_
             "n_complete", "n_incomplete", "n_largest_missing", "n_ratio_defined",
             "n_largest_is_best", "n_largest_strictly_slower", "n_gain_gt", "n_perf_lt",
             "n_perf_band", "perf_fx_hi", "perf_fx_lo", "gain_fx_hi", "gain_fx_lo"]
+ROLLUP = ["n_kernels", "n_kernels_largest_not_best", "n_kernels_perf_lt", "n_kernels_perf_band",
+          "kernel_mean_fx_hi", "kernel_mean_fx_lo"]
+ROLLUP_DERIVED = ["frac_kernels_largest_not_best", "frac_kernels_perf_lt", "frac_kernels_perf_band",
+                  "mean_kernel_perf"]
 DERIVED = ["frac_nonnan", "frac_largest_not_best", "frac_gain_gt", "frac_perf_lt",
            "frac_perf_band", "mean_perf", "mean_gain"]
 
@@ -87,7 +91,7 @@ class ReduceOpts(C.Structure):
     _fields_ = [(n, C.c_uint32) for n in (
         "n_blocks", "largest_block_id", "n_matrices", "nan_policy", "bins_per_unit", "gain_cap",
         "gain_gt_num", "gain_gt_den", "perf_lt_num", "perf_lt_den", "band_lo_num",
-        "band_lo_den", "point_sharded", "keep_values", "block_profile")]
+        "band_lo_den", "point_sharded", "keep_values", "block_profile", "kernel_rollup")]
 
 
 class ReduceOutC(C.Structure):
@@ -102,7 +106,9 @@ class StatsOutC(C.Structure):
                  ("best_block_hist", C.c_void_p), ("percentiles", C.c_void_p),
                  ("n_percentiles", C.c_uint32), ("pct_perf", C.c_void_p),
                  ("pct_gain", C.c_void_p), ("profile_mean", C.c_void_p),
-                 ("profile_count", C.c_void_p)])
+                 ("profile_count", C.c_void_p)] +
+                [(n, C.c_uint64) for n in ROLLUP] + [(n, C.c_double) for n in ROLLUP_DERIVED] +
+                [("kernel_perf_hist", C.c_void_p)])
 
 
 class OccInfo(C.Structure):
@@ -472,6 +478,9 @@ class Ctx:
         pn = np.zeros(opts.n_matrices * opts.n_blocks, np.uint64)
         if opts.block_profile:
             so.profile_mean, so.profile_count = pm.ctypes.data, pn.ctypes.data
+        kh = np.zeros(nb + 1, np.uint64)
+        if opts.kernel_rollup:
+            so.kernel_perf_hist = kh.ctypes.data
         self._ck(self._lib.lscat_stats(self.h, C.byref(opts), C.byref(so), _stream(stream)),
                  "stats")
         res = {k: int(getattr(so, k)) for k in COUNTERS}
@@ -481,6 +490,10 @@ class Ctx:
             res["best_block_hist"] = bh.reshape(opts.n_matrices, opts.n_blocks)
         if pc.size:
             res["pct_perf"], res["pct_gain"] = pp.tolist(), pg.tolist()
+        if opts.kernel_rollup:
+            res.update({k: int(getattr(so, k)) for k in ROLLUP})
+            res.update({k: float(getattr(so, k)) for k in ROLLUP_DERIVED})
+            res["kernel_perf_hist"] = kh
         if opts.block_profile:
             res["profile_mean"] = pm.reshape(opts.n_matrices, opts.n_blocks)
             res["profile_count"] = pn.reshape(opts.n_matrices, opts.n_blocks)

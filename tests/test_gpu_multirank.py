@@ -51,7 +51,10 @@ def _run_ranks(world, make_table, opts_kw, name):
 
 
 def _check(results, ref):
+    from tests.test_gpu_reduce import _check_rollup
     for st, _ in results:
+        if ref.rollup is not None:
+            _check_rollup(st, ref.rollup)
         for k, v in ref.counters.items():
             assert st[k] == v, k
         assert (st["perf_hist"] == ref.perf_hist).all()
@@ -65,15 +68,16 @@ def _check(results, ref):
 @pytest.mark.parametrize("world", [2, 3, 4, 8])
 def test_point_sharded_merge(world):
     require_gpu()
-    n, K = 400_000, 1600
+    n, K = 400_000, 1601                 # 7 or 8 groups per kernel: rank ranges split kernels
     full = gen_table(n, K, preset="t4", seed=31)
     ref = OT.reduce_table(full["runtime_ms"], full["block_id"], full["group_offset"],
-                          group_matrix=full["group_matrix"], percentiles=PCTS)
+                          group_matrix=full["group_matrix"], percentiles=PCTS,
+                          group_kernel=full["group_kernel"], kernel_rollup=True)
 
     def make(ctx, r):
         return ctx.gen_table(n, K, preset=0, seed=31, block_mod=world, block_rem=r)
 
-    res = _run_ranks(world, make, dict(point_sharded=1), f"ps{world}")
+    res = _run_ranks(world, make, dict(point_sharded=1, kernel_rollup=1), f"ps{world}")
     _check(res, ref)
     # every rank holds the merged per-group argmin for all groups
     for _, out in res:
@@ -83,15 +87,16 @@ def test_point_sharded_merge(world):
 @pytest.mark.parametrize("world", [2, 3, 8])
 def test_group_aligned_merge(world):
     require_gpu()
-    n, K = 32 * 120_000, 15_000
+    n, K = 32 * 120_000, 15_001
     full = gen_table(n, K, preset="gtx980", seed=41)
     ref = OT.reduce_table(full["runtime_ms"], full["block_id"], full["group_offset"],
-                          group_matrix=full["group_matrix"], percentiles=PCTS)
+                          group_matrix=full["group_matrix"], percentiles=PCTS,
+                          group_kernel=full["group_kernel"], kernel_rollup=True)
     G = full["n_groups"]
 
     def make(ctx, r):
         return ctx.gen_table(n, K, preset=1, seed=41, group_begin=G * r // world,
                              group_end=G * (r + 1) // world)
 
-    res = _run_ranks(world, make, {}, f"ga{world}")
+    res = _run_ranks(world, make, dict(kernel_rollup=1), f"ga{world}")
     _check(res, ref)

@@ -28,7 +28,8 @@ def _device_table(t, host=False):
         x = torch.from_numpy(np.ascontiguousarray(a).view(dt))
         return x.pin_memory() if host else x.to(dev)
     tab = Table(T(t["runtime_ms"], np.float32), T(t["block_id"].astype(np.uint16), np.int16),
-                None, T(t["group_offset"].astype(np.int64), np.int64), None,
+                None, T(t["group_offset"].astype(np.int64), np.int64),
+                T(t["group_kernel"].astype(np.uint32), np.int32) if t.get("group_kernel") is not None else None,
                 T(t["group_matrix"].astype(np.uint32), np.int32) if t.get("group_matrix") is not None else None,
                 n_rows=len(t["runtime_ms"]), n_groups=len(t["group_offset"]) - 1,
                 first_group=t.get("first_group", 0))
@@ -38,23 +39,37 @@ def _device_table(t, host=False):
     return tab
 
 
-def _opts_pair(L=32, M=8, ell=None, policy=0):
+def _opts_pair(L=32, M=8, ell=None, policy=0, rollup=0):
     from paper_2103_14409_b200 import reduce_opts
     ell = L - 1 if ell is None else ell
-    g = reduce_opts(L, M, largest_block_id=ell, nan_policy=policy)
+    g = reduce_opts(L, M, largest_block_id=ell, nan_policy=policy, kernel_rollup=rollup)
     o = OT.Opts(n_blocks=L, largest_block_id=ell, n_matrices=M, nan_policy=policy)
     return g, o
 
 
-def _compare(t, L=32, M=8, ell=None, policy=0, host=False, pcts=PCTS):
+def _check_rollup(st, R):
+    """Per-kernel roll-up (R-26) against the oracle: counters, histogram, fractions, mean."""
+    for k_gpu, k_or in (("n_kernels", "n_kernels"), ("n_kernels_largest_not_best", "n_kernels_not_best"),
+                        ("n_kernels_perf_lt", "n_kernels_perf_lt"), ("n_kernels_perf_band", "n_kernels_perf_band"),
+                        ("kernel_mean_fx_hi", "kernel_mean_fx_hi"), ("kernel_mean_fx_lo", "kernel_mean_fx_lo")):
+        assert st[k_gpu] == R[k_or], (k_gpu, st[k_gpu], R[k_or])
+    assert (st["kernel_perf_hist"] == R["perf_hist"]).all()
+    assert st["frac_kernels_largest_not_best"] == R["frac_kernels_not_best"] or R["n_kernels"] == 0
+    assert st["frac_kernels_perf_band"] == R["frac_kernels_perf_band"] or R["n_kernels"] == 0
+
+
+def _compare(t, L=32, M=8, ell=None, policy=0, host=False, pcts=PCTS, rollup=0):
     c = ctx()
-    g_opts, o_opts = _opts_pair(L, M, ell, policy)
+    g_opts, o_opts = _opts_pair(L, M, ell, policy, rollup)
     tab = _device_table(t, host=host)
     out = c.reduce_table(tab, g_opts)
     st = c.stats(g_opts, percentiles=pcts)
     ref = OT.reduce_table(t["runtime_ms"], t["block_id"], t["group_offset"],
                           group_matrix=t.get("group_matrix"), first_group=t.get("first_group", 0),
-                          opts=o_opts, percentiles=pcts)
+                          opts=o_opts, percentiles=pcts, group_kernel=t.get("group_kernel"),
+                          kernel_rollup=bool(rollup))
+    if rollup:
+        _check_rollup(st, ref.rollup)
     for k, v in ref.counters.items():
         assert st[k] == v, (k, st[k], v)
     assert (st["perf_hist"] == ref.perf_hist).all()
@@ -80,7 +95,7 @@ def _compare(t, L=32, M=8, ell=None, policy=0, host=False, pcts=PCTS):
 def test_gtx980_scale_table():
     """BASELINE configs[2]: 2 140 796 rows, ~3 % NaN."""
     t = gen_table(2_140_796, 8363, preset="gtx980", nan_rate=0.03, seed=980)
-    st = _compare(t)
+    st = _compare(t, rollup=1)
     assert st["n_rows"] == 2_140_796 and st["n_groups"] == 66_900
 
 
@@ -88,13 +103,13 @@ def test_gtx980_scale_table():
 def test_t4_scale_table(policy):
     """BASELINE configs[3]: 5 028 536 runtimes over 19 683 kernel ids."""
     t = gen_table(5_028_536, 19_683, preset="t4", nan_rate=0.03, seed=4)
-    _compare(t, policy=policy)
+    _compare(t, policy=policy, rollup=1)
 
 
 def test_point_sharded_shape_and_host_table():
     t = gen_table(200_000, 800, preset="t4", nan_rate=0.05, seed=5, block_mod=3, block_rem=1)
     _compare(t)
-    _compare(t, host=True)
+    _compare(t, host=True, rollup=1)
 
 
 @pytest.mark.parametrize("seed", range(4))
@@ -324,7 +339,7 @@ def test_scaled_table_1e9_sampled():
     n, K, L, M = 1_000_000_000, 3_906_250, 32, 8
     G = n // L
     tab = c.gen_table(n, K, preset=PRESET_T4, seed=10 ** 9, offsets=False)
-    o = reduce_opts(L, M)
+    o = reduce_opts(L, M, kernel_rollup=1)
     out = c.reduce_table(tab, o)
     st = c.stats(o, percentiles=PCTS)
     assert st["n_rows"] == n and st["n_groups"] == G
@@ -367,8 +382,10 @@ def test_scaled_table_1e9_sampled():
     # test_generator_twin_bit_exact) reduced by the C oracle; every counter and histogram is a
     # sum of integer partials, so the chunked totals equal the whole-table values exactly.  The
     # percentiles are the nearest-rank values of the concatenated oracle per-group values.
-    CH = 3_906_250
+    CH = 3_906_256                     # a multiple of M: chunks hold whole kernels (g // 8)
     tot = {k: 0 for k in OT.COUNTERS}
+    rtot = {k: 0 for k in OT.ROLLUP}
+    rh = np.zeros(101, np.uint64)
     ph = np.zeros(101, np.uint64)
     gh = np.zeros(1001, np.uint64)
     bh = np.zeros((M, L), np.uint64)
@@ -378,9 +395,12 @@ def test_scaled_table_1e9_sampled():
         rt = tab.runtime_ms[g0 * L:g1 * L].cpu().numpy()
         bid = tab.block_id[g0 * L:g1 * L].cpu().numpy().view(np.uint16)
         ref = OT.reduce_table(rt, bid, rows_per_group=L, first_group=g0,
-                              opts=OT.Opts(n_blocks=L, n_matrices=M))
+                              opts=OT.Opts(n_blocks=L, n_matrices=M), kernel_rollup=True)
         for k, v in ref.counters.items():
             tot[k] += v
+        for k in OT.ROLLUP:
+            rtot[k] += ref.rollup[k]
+        rh += ref.rollup["perf_hist"]
         ph += ref.perf_hist
         gh += ref.gain_hist
         bh += ref.best_block_hist
@@ -392,6 +412,11 @@ def test_scaled_table_1e9_sampled():
         assert st[k] == v, (k, st[k], v)
     assert (st["perf_hist"] == ph).all() and (st["gain_hist"] == gh).all()
     assert (st["best_block_hist"] == bh).all()
+    rtot["perf_hist"] = rh
+    nk = rtot["n_kernels"]
+    rtot["frac_kernels_not_best"] = rtot["n_kernels_not_best"] / nk
+    rtot["frac_kernels_perf_band"] = rtot["n_kernels_perf_band"] / nk
+    _check_rollup(st, rtot)
     for q, vals, parts in (("perf", st["pct_perf"], perfs), ("gain", st["pct_gain"], gains)):
         allv = np.sort(np.concatenate(parts))
         assert allv.size == nrd
