@@ -262,7 +262,9 @@ def main():
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
     g8 = len(SIZES) - 1
-    COLD = (1, 3, 200)  # cold re-timing of the dominant point: W, K, R
+    # cold re-timing of the dominant point: W, K, R (scaled down with the policy so a tiny-policy
+    # launch list under ncu keeps the sweep's proportions)
+    COLD = {"paper": (1, 3, 200), "fast": (1, 3, 20), "tiny": (1, 1, 2)}[args.policy]
 
     def step(mode=launch_mode):
         t = ctx.sweep(ks, SIZES, BLOCKS, warmup=W, brackets=K, launches=R, timeout_s=30.0,

@@ -288,6 +288,32 @@ def test_vector_outputs_full_size(name):
         _check_rel(out, ref, scale)
 
 
+@pytest.mark.parametrize("name", ["euclid", "matvec", "rowsum"])
+def test_row_kernels_split_rows(name):
+    """The row kernels' balanced work split: rows of S segments of 256 float4
+    shared by several warps and combined by the completing warp.  Sizes with a ragged last
+    segment (N = 1028: S = 2 with one float4 in the second; 4100: S = 5), exactly two segments
+    (2048) and a scalar row (N % 4 != 0), at every block size; every launch twice (the tickets
+    are reset by the completing warp)."""
+    from paper_2103_14409_b200 import KERNELS
+    k = KERNELS[name]
+    sizes = [1028, 2048, 2050, 4100]
+    c = _setup(k, sizes)
+    for n in sizes:
+        A, v = _inputs(c, k, n)
+        A = A.reshape(n, n)
+        ref, scale = {
+            "euclid": lambda: (OK.euclid(A, v), OK.euclid_abs_scale(A, v)),
+            "matvec": lambda: (OK.matvec(A, v), OK.matvec_abs_scale(A, v)),
+            "rowsum": lambda: (OK.rowsum(A), OK.rowsum_abs_scale(A)),
+        }[name]()
+        for b in BLOCKS:
+            for _ in range(2):
+                out = _run(c, k, n, b)
+                assert np.isfinite(out).all(), (name, n, b)
+                _check_rel(out, ref, scale)
+
+
 def test_axpy_full_size():
     from paper_2103_14409_b200 import K_AXPY
     n = 8192
