@@ -60,21 +60,32 @@ __device__ __forceinline__ float acc1(float s, float a, float v) {
   else return s + a;
 }
 
-// Work split: a row of N floats is S = ceil(N/4 / 256) segments of 256 float4
-// (one pass of 8 float4 per lane of a warp; S = 1 for N % 4 != 0 or N <= 1024), the work units
-// are the U = N S (row, segment) pairs, and warp w of the grid's Wt warps takes the contiguous
-// units [w U / Wt, (w+1) U / Wt) -- every warp gets the same number of units to within one,
-// whatever the block size, so no partial last wave of rows (measured on the one-row-per-warp
-// layout, round 1: N = 8192 at 33.6-40.7 us across the blocks; 8192 rows over 4736 warps is
-// 1.73 rows per warp, so most warps idled through a second row's time).  A row a warp covers
-// whole is reduced in registers and stored; a row split between warps leaves one partial sum
-// per piece in `part[row][first segment]` and adds (segments | 1 << (32 + first segment)) to the
-// row's 64-bit ticket: the warp whose add completes the S segments sums the pieces in segment
-// order, applies the finish (sqrt for euclid), stores the row and resets the ticket.
+// Work split.  With at least one warp per row (N <= Wt warps in the grid) warp
+// w reduces the whole rows [w N / Wt, (w+1) N / Wt).  With fewer warps than rows, rows are cut
+// into S = ceil(N/4 / 256) segments of 256 float4 (one pass of 8 float4 per lane), the work
+// units are the U = N S (row, segment) pairs, and warp w takes the contiguous units
+// [w U / Wt, (w+1) U / Wt): every warp gets the same work to within one segment, whatever the
+// block size (one row per warp left most warps idle through a second row's time: N = 8192 is
+// 1.73 rows per warp at 4736 resident warps; measured 33.6-40.7 us across the blocks).
+// A row a warp covers whole is reduced in registers and stored.  A row split between warps
+// leaves one partial sum per piece in part[row][first segment] and adds (segments |
+// 1 << (32 + first segment)) to the row's 64-bit ticket with an acq_rel atomic; the warp whose
+// add completes the S segments sums the pieces in segment order, applies the finish (sqrt for
+// euclid), stores the row and resets the ticket.  The atomic's result is only inspected after
+// the warp's next piece has been loaded, so its round trip overlaps the streaming.
+__device__ __forceinline__ unsigned long long atom_add_acq_rel(unsigned long long* p, unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
+
+template <int OP>
+__device__ __forceinline__ float row_finish(float s) { return OP == kEuclid ? sqrtf(s) : s; }
+
 template <int OP, int B>
 __global__ void __launch_bounds__(B, row_min_blocks<B>()) row_kernel(const float* __restrict__ A,
                                                 const float* __restrict__ v,
-                                                float* __restrict__ out, int N, int S,
+                                                float* __restrict__ out, int N, int S, int split,
                                                 float* __restrict__ part,
                                                 unsigned long long* __restrict__ tick,
                                                 float l2keep) {
@@ -83,7 +94,9 @@ __global__ void __launch_bounds__(B, row_min_blocks<B>()) row_kernel(const float
   const int lane = threadIdx.x & 31;
   const uint64_t Wt = (uint64_t)gridDim.x * W;
   const uint64_t w = (uint64_t)blockIdx.x * W + (threadIdx.x >> 5);
-  const uint64_t U = (uint64_t)N * S;
+  // unit = a segment when split, else a whole row
+  const uint64_t U = split ? (uint64_t)N * S : (uint64_t)N;
+  const int upr = split ? S : 1;  // units per row
   uint64_t u = w * U / Wt;
   const uint64_t u1 = (w + 1) * U / Wt;
   const bool vec = (N & 3) == 0;
@@ -91,9 +104,12 @@ __global__ void __launch_bounds__(B, row_min_blocks<B>()) row_kernel(const float
   const uint64_t pol = (vec && l2keep > 0.f) ? l2_keep_fraction_policy(l2keep) : 0;
   const float4* A4 = reinterpret_cast<const float4*>(A);
   const float4* v4 = reinterpret_cast<const float4*>(v);
+  int pend_r = -1;                 // split row whose ticket result is not yet inspected
+  unsigned long long pend_now = 0;
   while (u < u1) {
-    const int r = (int)(u / S), s0 = (int)(u % S);
-    const int s1 = (int)min((uint64_t)S, (uint64_t)s0 + (u1 - u));  // this piece: [s0, s1)
+    const int r = (int)(u / upr), p0 = (int)(u % upr);
+    const int p1 = (int)min((uint64_t)upr, (uint64_t)p0 + (u1 - u));  // this piece: units [p0, p1)
+    const int s0 = split ? p0 : 0, s1 = split ? p1 : S;                // segments [s0, s1)
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     if (vec) {
       constexpr int UL = ROW_U;  // 8 float4 per lane in flight = one 256-float4 segment
@@ -116,7 +132,7 @@ __global__ void __launch_bounds__(B, row_min_blocks<B>()) row_kernel(const float
 #pragma unroll
         for (int k = 0; k < UL; k++) acc4<OP>(acc, x[k], OP != kRowsum ? y[k] : x[k]);
       }
-    } else {  // scalar rows (S == 1)
+    } else {  // scalar rows (S == 1, never split)
       const float* a = A + (size_t)r * N;
       for (int j = lane; j < N; j += 32) acc.x = acc1<OP>(acc.x, ld_stream(a + j), OP != kRowsum ? __ldg(v + j) : 0.f);
     }
@@ -125,24 +141,31 @@ __global__ void __launch_bounds__(B, row_min_blocks<B>()) row_kernel(const float
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     pdl_wait();  // the predecessor launch is complete before this launch's first store
     if (lane == 0) {
+      if (pend_r >= 0 && (uint32_t)pend_now == (uint32_t)S) {  // the previous piece completed its row
+        float tot = 0.f;
+        for (uint32_t m = (uint32_t)(pend_now >> 32); m; m &= m - 1)
+          tot += __ldcg(&part[(size_t)pend_r * S + (__ffs(m) - 1)]);
+        out[pend_r] = row_finish<OP>(tot);
+        tick[pend_r] = 0;
+      }
+      pend_r = -1;
       if (s0 == 0 && s1 == S) {
-        out[r] = (OP == kEuclid) ? sqrtf(sum) : sum;
+        out[r] = row_finish<OP>(sum);
       } else {
         part[(size_t)r * S + s0] = sum;
-        __threadfence();
         const unsigned long long add = (unsigned long long)(s1 - s0) | (1ull << (32 + s0));
-        const unsigned long long now = atomicAdd(&tick[r], add) + add;
-        if ((uint32_t)now == (uint32_t)S) {  // all segments are in: combine in segment order
-          __threadfence();
-          float tot = 0.f;
-          for (uint32_t m = (uint32_t)(now >> 32); m; m &= m - 1)
-            tot += __ldcg(&part[(size_t)r * S + (__ffs(m) - 1)]);
-          out[r] = (OP == kEuclid) ? sqrtf(tot) : tot;
-          tick[r] = 0;
-        }
+        pend_now = atom_add_acq_rel(&tick[r], add) + add;
+        pend_r = r;
       }
     }
-    u += s1 - s0;
+    u += p1 - p0;
+  }
+  if (lane == 0 && pend_r >= 0 && (uint32_t)pend_now == (uint32_t)S) {
+    float tot = 0.f;
+    for (uint32_t m = (uint32_t)(pend_now >> 32); m; m &= m - 1)
+      tot += __ldcg(&part[(size_t)pend_r * S + (__ffs(m) - 1)]);
+    out[pend_r] = row_finish<OP>(tot);
+    tick[pend_r] = 0;
   }
 }
 
@@ -187,8 +210,9 @@ struct RowLauncher {
       // warps of the device, with the units spread evenly over them
       const long need = (N + B / 32 - 1) / (B / 32);
       const int grid = (int)std::min<long>(need, (long)per_sm() * sms);
+      const int split = (long)grid * (B / 32) < N && S > 1;  // fewer warps than rows
       return launch_k(row_kernel<OP, B>, dim3(grid), dim3(B), 0, s, a.pdl,
-                      (const float*)e.in0, (const float*)e.in1, (float*)e.out, N, S,
+                      (const float*)e.in0, (const float*)e.in1, (float*)e.out, N, S, split,
                       (float*)e.scratch, row_tickets(e), keep);
     }
   };

@@ -293,11 +293,12 @@ def test_row_kernels_split_rows(name):
     """The row kernels' balanced work split: rows of S segments of 256 float4
     shared by several warps and combined by the completing warp.  Sizes with a ragged last
     segment (N = 1028: S = 2 with one float4 in the second; 4100: S = 5), exactly two segments
-    (2048) and a scalar row (N % 4 != 0), at every block size; every launch twice (the tickets
+    (2048), a scalar row (N % 4 != 0) and N = 6000 (S = 6, ragged, split at every block size with
+    fewer than 6000 resident warps), at every block size; every launch twice (the tickets
     are reset by the completing warp)."""
     from paper_2103_14409_b200 import KERNELS
     k = KERNELS[name]
-    sizes = [1028, 2048, 2050, 4100]
+    sizes = [1028, 2048, 2050, 4100, 6000]
     c = _setup(k, sizes)
     for n in sizes:
         A, v = _inputs(c, k, n)
