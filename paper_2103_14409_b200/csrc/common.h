@@ -25,7 +25,7 @@ struct SuiteEntry {
   void* in1 = nullptr;
   void* out = nullptr;
   uint64_t in0_bytes = 0, in1_bytes = 0, out_bytes = 0;
-  void* scratch = nullptr;  // colsum: partials + tile counters; row kernels: split-row partials + tickets
+  void* scratch = nullptr;  // colsum: partials + tile counters
   uint64_t scratch_bytes = 0;
   alignas(64) unsigned char host_blob[512] = {};  // gemm: the TMA tensor maps
 };
@@ -69,7 +69,6 @@ const KernelTable* kernel_table(uint32_t kernel);
 
 // suite buffer preparation that needs kernel-specific knowledge
 cudaError_t colsum_prepare(SuiteEntry& e);
-cudaError_t row_prepare(SuiteEntry& e);  // euclid, matvec, rowsum: split-row partials + tickets
 cudaError_t gemm_prepare(SuiteEntry& e);
 
 // reducer scratch kept between lscat_reduce_table and lscat_stats

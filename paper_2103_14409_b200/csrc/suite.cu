@@ -83,8 +83,6 @@ cudaError_t alloc_entry(lscat_ctx* ctx, SuiteEntry& e, cudaStream_t s) {
   if ((err = cudaGetLastError()) != cudaSuccess) return err;
   if ((err = cudaMemsetAsync(e.out, 0, bo, s)) != cudaSuccess) return err;
   if (e.kernel == LSCAT_K_COLSUM) return colsum_prepare(e);
-  if (e.kernel == LSCAT_K_EUCLID || e.kernel == LSCAT_K_MATVEC || e.kernel == LSCAT_K_ROWSUM)
-    return row_prepare(e);
   if (e.kernel == LSCAT_K_GEMM_BF16) return gemm_prepare(e);
   return cudaSuccess;
 }

@@ -289,16 +289,13 @@ def test_vector_outputs_full_size(name):
 
 
 @pytest.mark.parametrize("name", ["euclid", "matvec", "rowsum"])
-def test_row_kernels_split_rows(name):
-    """The row kernels' balanced work split: rows of S segments of 256 float4
-    shared by several warps and combined by the completing warp.  Sizes with a ragged last
-    segment (N = 1028: S = 2 with one float4 in the second; 4100: S = 5), exactly two segments
-    (2048), a scalar row (N % 4 != 0) and N = 6000 (S = 6, ragged, split at every block size with
-    fewer than 6000 resident warps), at every block size; every launch twice (the tickets
-    are reset by the completing warp)."""
+def test_row_kernels_mid_sizes(name):
+    """The row kernels between the parity sizes and N = 8192, at every block size, each launch
+    twice: a ragged float4 tail (N = 1028, 4100, 6000: 257, 1025, 1500 float4 per row), a scalar
+    row (N % 4 != 0), grids above one wave (one row per warp) and the persistent grid (B > 512)."""
     from paper_2103_14409_b200 import KERNELS
     k = KERNELS[name]
-    sizes = [1028, 2048, 2050, 4100, 6000]
+    sizes = [1028, 2050, 4100, 6000]
     c = _setup(k, sizes)
     for n in sizes:
         A, v = _inputs(c, k, n)
