@@ -292,8 +292,7 @@ typedef struct {
 
 /* Layout of the packed partial vector (uint64 words), LSCAT_P_* counter slots first, then
    perf_hist [bins_per_unit+1], gain_hist [gain_cap*bins_per_unit+1], best_block_hist
-   [n_matrices*n_blocks], with keep_values: the fixed level-0 bins of the percentile selection
-   [2 x 2051] (perf, gain; csrc/selbins.h), with block_profile: profile_sum [n_matrices*n_blocks],
+   [n_matrices*n_blocks], and with block_profile: profile_sum [n_matrices*n_blocks],
    profile_count [n_matrices*n_blocks], and with kernel_rollup: 8 words (n_kernels,
    n_kernels_largest_not_best, n_kernels_perf_lt, n_kernels_perf_band, kernel_mean_fx_hi,
    kernel_mean_fx_lo, 0, 0) and kernel_perf_hist [bins_per_unit+1]. */

@@ -13,7 +13,6 @@
 
 #include "comm.h"
 #include "lscat.h"
-#include "selbins.h"
 
 namespace lscat {
 
@@ -81,7 +80,6 @@ struct ReduceState {
   double* perf = nullptr;      // device [n_groups] (caller's or scratch)
   double* gain = nullptr;
   uint64_t* partials = nullptr;  // device, len = partials_len (SUM-merged)
-  size_t fx_off = 0;             // offset of the fixed level-0 selection bins in partials
   uint64_t* minmax = nullptr;    // device [4]: perf min, perf max, gain min, gain max keys
 };
 
@@ -139,9 +137,6 @@ void* pinned(lscat_ctx* ctx, const char* name, size_t bytes, cudaError_t* err);
 // Raise a kernel's max-dynamic-shared-memory attribute on the current device to at least
 // `bytes` (device-global state: never lowered, set once per (kernel, device, size increase)).
 cudaError_t ensure_smem_attr(const void* func, size_t bytes);
-// words of the fixed level-0 selection histogram in the partial vector (selbins.h): counted by
-// the reducer whenever it keeps the per-group values for the percentiles
-inline size_t fx_words(const lscat_reduce_opts& o) { return o.keep_values ? 2 * (size_t)kFxBins : 0; }
 // host-side work model
 void kernel_work(uint32_t kernel, uint32_t n, uint64_t* bytes, uint64_t* flops);
 bool block_list_ok(const uint16_t* blocks, uint32_t n);

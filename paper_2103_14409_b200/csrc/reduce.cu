@@ -28,7 +28,6 @@
 #include <vector>
 
 #include "common.h"
-#include "selbins.h"
 
 namespace lscat {
 namespace {
@@ -63,8 +62,7 @@ struct RP {
   int mode;
   // per-kernel roll-up (R-26): per-group record fx_perf | rd << 53 | not_best << 54
   uint64_t* krec;
-  uint32_t smem_words;  // perf + gain + best-block (+ fixed level-0 selection) histogram words in smem
-  uint32_t fxbins;      // 1: count the fixed level-0 selection bins (selbins.h) after sh_bb
+  uint32_t smem_words;  // perf + gain + best-block histogram words in smem
   uint32_t vec;         // runtime / block-id arrays are 16-byte aligned (vector path allowed)
 };
 
@@ -270,14 +268,7 @@ __device__ void finalize_lane(const RP& p, uint64_t g, bool active, const GroupA
     t.pk += inc;
     if (acc) { t.rows += a.n_rows; t.ok += a.n_ok; t.nan += a.n_nan; }
   }
-  if (pbin >= 0 && pbin != (int)p.nb) {
-    atomicAdd(&sh_perf[pbin], 1u);
-    if (p.fxbins) {  // perf < 1 <=> gain > 0: the counted (non-virtual) level-0 selection bins
-      uint32_t* sh_fx = sh_bb + p.M * p.L;
-      atomicAdd(&sh_fx[fx_perf_bin(f64_key(perf))], 1u);
-      atomicAdd(&sh_fx[kFxBins + fx_gain_bin(f64_key(gain))], 1u);
-    }
-  }
+  if (pbin >= 0 && pbin != (int)p.nb) atomicAdd(&sh_perf[pbin], 1u);
   if (gbin > 0) atomicAdd(&sh_gain[gbin], 1u);
   if (bbi >= 0) atomicAdd(&sh_bb[bbi], 1u);
   if (++t.n == kPkGroups) flush_counters(p, t, sh_c, sh_perf, sh_gain);
@@ -655,7 +646,7 @@ __global__ void init_partials(uint64_t* __restrict__ partials, size_t plen, uint
 
 size_t partials_len(const lscat_reduce_opts& o) {
   return (size_t)kNC + (o.bins_per_unit + 1) + ((size_t)o.gain_cap * o.bins_per_unit + 1) +
-         (size_t)o.n_matrices * o.n_blocks * (o.block_profile ? 3 : 1) + fx_words(o) +
+         (size_t)o.n_matrices * o.n_blocks * (o.block_profile ? 3 : 1) +
          (o.kernel_rollup ? (size_t)8 + o.bins_per_unit + 1 : 0);
 }
 
@@ -867,7 +858,7 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
   if (T->rows_per_group && (T->n_groups != (T->n_rows + T->rows_per_group - 1) / T->rows_per_group))
     return fail(ctx, LSCAT_ERR_INVALID_ARG, "reduce_table: n_groups != ceil(n_rows / rows_per_group)");
   const size_t sh_words = (o->bins_per_unit + 1) + ((size_t)o->gain_cap * o->bins_per_unit + 1) +
-                          (size_t)o->n_matrices * o->n_blocks + fx_words(*o);
+                          (size_t)o->n_matrices * o->n_blocks;
   const size_t smem_fin = kNC * 8 + sh_words * 4;
   const size_t smem_hist = kNC * 8 + ((sh_words * 4 + 15) & ~(size_t)15);
   size_t smem = smem_hist + kStageBytes;
@@ -926,7 +917,6 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
   p.ggn = o->gain_gt_num; p.ggd = o->gain_gt_den; p.pln = o->perf_lt_num; p.pld = o->perf_lt_den;
   p.bln = o->band_lo_num; p.bld = o->band_lo_den;
   p.smem_words = (uint32_t)sh_words;
-  p.fxbins = o->keep_values ? 1u : 0u;
   p.o_best = out->best_block_id;
   p.o_bestrt = out->best_runtime;
   p.o_perf = out->perf;
@@ -1074,7 +1064,6 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
   rs.perf = o->keep_values ? p.o_perf : out->perf;
   rs.gain = o->keep_values ? p.o_gain : out->gain;
   rs.partials = p.partials;
-  rs.fx_off = kNC + sh_words - fx_words(*o);
   rs.minmax = p.minmax;
   if (T->mem == LSCAT_MEM_HOST) LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
   return LSCAT_OK;

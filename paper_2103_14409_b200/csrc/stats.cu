@@ -166,6 +166,43 @@ __device__ void plan_ranges(SelState* st, uint32_t cap) {
   }
 }
 
+__global__ void __launch_bounds__(kMaxT) sel_init(SelState* st, const uint64_t* __restrict__ partials,
+                                                  const uint64_t* __restrict__ mm, PctArg pct, uint32_t npct,
+                                                  uint32_t cap) {
+  const int i = threadIdx.x;
+  const uint64_t n_def = partials[LSCAT_P_RATIO_DEFINED];
+  if (i == 0) {
+    st->nt = 2 * npct;
+    st->err = 0;
+    st->done_ctas = 0;
+    st->src = 0;
+    st->compact = 0;
+    st->n_def = n_def;
+  }
+  if (i < (int)(2 * npct)) {
+    Tgt t{};
+    t.which = i >= (int)npct;
+    const double r = ceil(pct.p[i % npct] * (double)n_def);  // nearest rank (R-13)
+    t.k = r < 1.0 ? 1 : (r > (double)n_def ? n_def : (uint64_t)r);
+    t.lo = mm[2 * t.which];
+    t.hi = mm[2 * t.which + 1];
+    t.count = n_def;
+    t.done = n_def == 0;
+    t.key = kNaNKey;
+    st->t[i] = t;
+  }
+  __syncthreads();
+  plan_ranges(st, cap);
+  __syncthreads();
+  if (i == 0) {  // remember the level-0 range of each quantity (the bin filter of later passes)
+    uint32_t v = 0;
+    for (uint32_t j = 0; j < st->nr; j++) {
+      const uint32_t w = st->r[j].which;
+      if (!st->r[j].gather && !(v & (1u << w))) { st->r0[w] = st->r[j]; v |= 1u << w; }
+    }
+    st->r0_valid = v;
+  }
+}
 
 
 // One pass over this rank's values (src 0: perf/gain[lo, hi); src 1: the compacted keys).
@@ -562,102 +599,6 @@ __global__ void __launch_bounds__(1024) sel_resolve(SelState* st, uint32_t* __re
   if (st->nr) plan_ranges(st, cap);
 }
 
-// Level 0 from the reducer's fixed bins (selbins.h): every target is narrowed to the bin that
-// holds its rank -- an inclusive scan of each quantity's kFxBins counts (the two virtual bins
-// take the exact perf == 1 / gain == 0 count perf_hist[nb]) and a binary search per target --
-// and the bin's key range is clipped to the quantity's [min, max] key.  Then the open targets are
-// planned into ranges, and the level-0 bitmap filter of the later full passes is set to
-// [min, max].  One CTA of 1024 threads.
-__global__ void __launch_bounds__(1024) sel_init_fixed(SelState* st, const uint64_t* __restrict__ partials,
-                                                       const uint64_t* __restrict__ fx, uint32_t nb,
-                                                       const uint64_t* __restrict__ mm, PctArg pct,
-                                                       uint32_t npct, uint32_t cap) {
-  __shared__ unsigned long long pre[2][kFxBins];
-  __shared__ unsigned long long part_sum[1024];
-  const int tid = threadIdx.x;
-  const uint64_t n_def = partials[LSCAT_P_RATIO_DEFINED];
-  const uint64_t n_one = partials[LSCAT_P_NCOUNTERS + nb];  // perf == 1 <=> gain == 0
-  constexpr int kPer = (kFxBins + 1023) / 1024;
-  for (int w = 0; w < 2; w++) {
-    unsigned long long c[kPer], sum = 0;
-#pragma unroll
-    for (int j = 0; j < kPer; j++) {
-      const uint32_t b = (uint32_t)tid * kPer + j;
-      unsigned long long v = 0;
-      if (b < kFxBins) {
-        const bool virt = (w == 0 && b == kFxBins - 2) || (w == 1 && b == 0);
-        v = virt ? n_one : fx[(size_t)w * kFxBins + b];
-      }
-      c[j] = v;
-      sum += v;
-    }
-    part_sum[tid] = sum;
-    __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {  // Hillis-Steele scan of the 1024 chunk sums
-      const unsigned long long y = tid >= o ? part_sum[tid - o] : 0ull;
-      __syncthreads();
-      part_sum[tid] += y;
-      __syncthreads();
-    }
-    unsigned long long run = part_sum[tid] - sum;
-#pragma unroll
-    for (int j = 0; j < kPer; j++) {
-      const uint32_t b = (uint32_t)tid * kPer + j;
-      run += c[j];
-      if (b < kFxBins) pre[w][b] = run;
-    }
-    __syncthreads();
-  }
-  if (tid == 0) {
-    st->nt = 2 * npct;
-    st->err = (pre[0][kFxBins - 1] != n_def || pre[1][kFxBins - 1] != n_def) ? 16u : 0u;
-    st->done_ctas = 0;
-    st->src = 0;
-    st->compact = 0;
-    st->n_def = n_def;
-  }
-  if (tid < (int)(2 * npct)) {
-    Tgt t{};
-    t.which = tid >= (int)npct;
-    const double r = ceil(pct.p[tid % npct] * (double)n_def);  // nearest rank (R-13)
-    t.k = r < 1.0 ? 1 : (r > (double)n_def ? n_def : (uint64_t)r);
-    t.done = n_def == 0;
-    t.key = kNaNKey;
-    t.lo = mm[2 * t.which];
-    t.hi = mm[2 * t.which + 1];
-    t.count = n_def;
-    if (!t.done) {
-      const unsigned long long* P = pre[t.which];
-      uint32_t lo = 0, hi = kFxBins - 1;  // smallest b with P[b] >= k
-      while (lo < hi) {
-        const uint32_t m = (lo + hi) / 2;
-        if (P[m] >= t.k) hi = m; else lo = m + 1;
-      }
-      const unsigned long long below = lo ? P[lo - 1] : 0ull;
-      uint64_t blo, bhi;
-      fx_bin_range(t.which, lo, &blo, &bhi);
-      t.lo = blo > t.lo ? blo : t.lo;  // clip to the quantity's [min, max] key
-      t.hi = bhi < t.hi ? bhi : t.hi;
-      t.k -= below;
-      t.count = P[lo] - below;
-    }
-    st->t[tid] = t;
-  }
-  __syncthreads();
-  plan_ranges(st, cap);
-  __syncthreads();
-  if (tid == 0) {  // the bitmap filter of later full passes: the quantity's whole [min, max]
-    uint32_t v = 0;
-    for (uint32_t w = 0; w < 2; w++) {
-      if (n_def > cap && mm[2 * w] <= mm[2 * w + 1]) {
-        st->r0[w] = make_range(mm[2 * w], mm[2 * w + 1], n_def, w, cap);
-        v |= 1u << w;
-      }
-    }
-    st->r0_valid = v;
-  }
-}
-
 lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct, double* out_perf,
                                 double* out_gain, cudaStream_t s) {
   const ReduceState& rs = ctx->rs;
@@ -726,10 +667,9 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
   auto enqueue_first = [&](cudaStream_t q) -> lscat_status {
     LSCAT_CUDA(ctx, cudaMemsetAsync(hist, 0, (size_t)kMaxR * kBins * 4, q));
     LSCAT_CUDA(ctx, cudaMemsetAsync(cand, 0, (size_t)kMaxR * 8, q));
-    sel_init_fixed<<<1, 1024, 0, q>>>(st, rs.partials, rs.partials + rs.fx_off, rs.opts.bins_per_unit,
-                                      rs.minmax, pa, npct, cap);
+    sel_init<<<1, kMaxT, 0, q>>>(st, rs.partials, rs.minmax, pa, npct, cap);
     LSCAT_CUDA(ctx, cudaGetLastError());
-    return enqueue_levels(q, false);
+    return enqueue_levels(q, true);
   };
   const bool debug = getenv("LSCAT_SEL_DEBUG") != nullptr;
   lscat_status ls;
@@ -816,7 +756,7 @@ extern "C" lscat_status lscat_stats(lscat_ctx* ctx, const lscat_reduce_opts* o, 
   LSCAT_CUDA(ctx, cudaSetDevice(ctx->device));
   const size_t nb = o->bins_per_unit, ng = (size_t)o->gain_cap * nb, nbb = (size_t)o->n_matrices * o->n_blocks;
   const size_t plen = LSCAT_P_NCOUNTERS + (nb + 1) + (ng + 1) + nbb * (o->block_profile ? 3 : 1) +
-                      fx_words(*o) + (o->kernel_rollup ? 8 + nb + 1 : 0);
+                      (o->kernel_rollup ? 8 + nb + 1 : 0);
   cudaError_t err;
   uint64_t* hP = (uint64_t*)pinned(ctx, "stats_partials", plen * 8, &err);
   if (err) return cuda_fail(ctx, err, "stats: pinned");
@@ -877,7 +817,7 @@ extern "C" lscat_status lscat_stats(lscat_ctx* ctx, const lscat_reduce_opts* o, 
     if (out->kernel_perf_hist) memcpy(out->kernel_perf_hist, K + 8, (nb + 1) * 8);
   }
   if (o->block_profile) {  // R-22: mean of best / r_b per (matrix, block)
-    const uint64_t* ps = H + nb + 1 + ng + 1 + nbb + fx_words(*o);
+    const uint64_t* ps = H + nb + 1 + ng + 1 + nbb;
     const uint64_t* pc = ps + nbb;
     for (size_t i = 0; i < nbb; i++) {
       if (out->profile_count) out->profile_count[i] = pc[i];
