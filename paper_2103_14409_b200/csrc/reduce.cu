@@ -717,12 +717,20 @@ struct RollupArgs {
 };
 
 __device__ __forceinline__ uint32_t kid_of(const RollupArgs& q, uint64_t g) {
-  return q.gkern ? q.gkern[g] : (uint32_t)((q.first_group + g) / q.M);
+  if (q.gkern) return q.gkern[g];
+  const uint64_t ag = q.first_group + g;  // implicit: a shift when M is a power of two
+  return (uint32_t)((q.M & (q.M - 1)) == 0 ? ag >> (__ffs(q.M) - 1) : ag / q.M);
 }
+
+// Per-thread roll-up counters (flushed once per warp: the per-kernel increments all go to the
+// same six words, so per-kernel atomics would serialise).
+struct KAcc {
+  unsigned long long v[6];  // n_kernels, not_best, perf_lt, band, mean fx hi, mean fx lo
+};
 
 // One kernel's roll-up (exact: 128-bit products of the fixed-point sum, R-26).
 __device__ void kernel_fin(const RollupArgs& q, uint64_t c, unsigned __int128 S, bool not_best,
-                           unsigned long long* cnt, uint32_t* hist32, unsigned long long* hist64) {
+                           KAcc& a, uint32_t* hist32, unsigned long long* hist64) {
   if (c == 0) return;
   const unsigned __int128 cd = (unsigned __int128)c << 52;  // kernel-mean perf = S / cd
   const bool lt = (unsigned __int128)q.pld * S < (unsigned __int128)q.pln * cd;
@@ -730,12 +738,12 @@ __device__ void kernel_fin(const RollupArgs& q, uint64_t c, unsigned __int128 S,
   uint32_t bin = (uint32_t)(((unsigned __int128)q.nb * S) / cd);  // largest j: j cd <= nb S
   if (bin > q.nb) bin = q.nb;
   const uint64_t kfx = (uint64_t)(S / c);
-  atomicAdd(&cnt[0], 1ull);
-  if (not_best) atomicAdd(&cnt[1], 1ull);
-  if (lt) atomicAdd(&cnt[2], 1ull);
-  if (band) atomicAdd(&cnt[3], 1ull);
-  atomicAdd(&cnt[4], (unsigned long long)(kfx >> 21));
-  atomicAdd(&cnt[5], (unsigned long long)(kfx & ((1ull << 21) - 1)));
+  a.v[0] += 1;
+  a.v[1] += not_best;
+  a.v[2] += lt;
+  a.v[3] += band;
+  a.v[4] += kfx >> 21;
+  a.v[5] += kfx & ((1ull << 21) - 1);
   if (hist32) atomicAdd(&hist32[bin], 1u);
   else atomicAdd(&hist64[bin], 1ull);
 }
@@ -747,6 +755,7 @@ __global__ void __launch_bounds__(256) rollup_kernel(RollupArgs q) {
   for (uint32_t i = threadIdx.x; i < kRollupWords; i += blockDim.x) cnt[i] = 0;
   for (uint32_t i = threadIdx.x; i <= q.nb; i += blockDim.x) hist[i] = 0;
   __syncthreads();
+  KAcc acc{};
   for (uint64_t g = q.lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < q.hi;
        g += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t k = kid_of(q, g);
@@ -770,8 +779,15 @@ __global__ void __launch_bounds__(256) rollup_kernel(RollupArgs q) {
       b[3] = (uint64_t)(S >> 64);
       b[4] = nbst;
     } else {
-      kernel_fin(q, c, S, nbst, cnt, hist, nullptr);
+      kernel_fin(q, c, S, nbst, acc, hist, nullptr);
     }
+  }
+#pragma unroll
+  for (int i = 0; i < 6; i++) {
+    unsigned long long x = acc.v[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0 && x) atomicAdd(&cnt[i], x);
   }
   __syncthreads();
   unsigned long long* gc = reinterpret_cast<unsigned long long*>(q.part);
@@ -786,6 +802,7 @@ __global__ void __launch_bounds__(256) rollup_kernel(RollupArgs q) {
 __global__ void rollup_boundary_kernel(RollupArgs q, const uint64_t* __restrict__ all, int nrec) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   unsigned long long* gc = reinterpret_cast<unsigned long long*>(q.part);
+  KAcc acc{};
   bool have = false;
   uint32_t kid = 0;
   uint64_t c = 0;
@@ -796,7 +813,7 @@ __global__ void rollup_boundary_kernel(RollupArgs q, const uint64_t* __restrict_
     if (!(b[0] >> 32)) continue;
     const uint32_t k = (uint32_t)b[0];
     if (have && k != kid) {
-      kernel_fin(q, c, S, nbst, gc, nullptr, gc + kRollupWords);
+      kernel_fin(q, c, S, nbst, acc, nullptr, gc + kRollupWords);
       have = false;
     }
     if (!have) { have = true; kid = k; c = 0; S = 0; nbst = false; }
@@ -804,7 +821,8 @@ __global__ void rollup_boundary_kernel(RollupArgs q, const uint64_t* __restrict_
     S += ((unsigned __int128)b[3] << 64) | b[2];
     nbst |= b[4] != 0;
   }
-  if (have) kernel_fin(q, c, S, nbst, gc, nullptr, gc + kRollupWords);
+  if (have) kernel_fin(q, c, S, nbst, acc, nullptr, gc + kRollupWords);
+  for (int i = 0; i < 6; i++) gc[i] += acc.v[i];
 }
 
 bool opts_ok(const lscat_reduce_opts* o) {
