@@ -763,12 +763,26 @@ __global__ void __launch_bounds__(256) rollup_kernel(RollupArgs q) {
     uint64_t c = 0, e = g;
     unsigned __int128 S = 0;
     bool nbst = false;
-    for (; e < q.hi && kid_of(q, e) == k; e++) {
-      const uint64_t r = q.krec[e];
-      if (r >> 53 & 1) {
-        c++;
-        S += r & ((1ull << 53) - 1);
-        nbst |= (r >> 54) & 1;
+    for (bool more = true; more;) {  // 8 records per round trip (independent loads in flight)
+      uint64_t rr[8];
+      uint32_t kk[8];
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        const bool in = e + j < q.hi;
+        rr[j] = in ? q.krec[e + j] : 0;
+        kk[j] = in ? kid_of(q, e + j) : ~k;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        if (!more) break;
+        if (kk[j] != k) { more = false; break; }
+        const uint64_t r = rr[j];
+        if (r >> 53 & 1) {
+          c++;
+          S += r & ((1ull << 53) - 1);
+          nbst |= (r >> 54) & 1;
+        }
+        e++;
       }
     }
     if (g == q.lo || e == q.hi) {  // may continue on a neighbouring rank: boundary record

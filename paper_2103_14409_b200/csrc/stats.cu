@@ -230,9 +230,17 @@ __device__ __noinline__ void hit_slow(const Range* sr, uint32_t r, uint64_t k, u
   const Range& R = sr[r];
   // lanes may sit in different ranges (gathered or histogrammed): no early exit before the
   // warp collectives below
-  if (hit && R.gather) {  // <= cap keys in the whole range
-    const unsigned long long idx = atomicAdd(&cand[r], 1ull);
-    if (idx < cap) cand[kMaxR + (size_t)r * cap + idx] = k;
+  {  // gather (<= cap keys in the whole range): one counter atomic per range and warp
+    const bool g = hit && R.gather;
+    const unsigned peers = __match_any_sync(FULL, g ? r : 0xFFFFFFFFu);
+    const int leader = __ffs(peers) - 1;
+    unsigned long long base = 0;
+    if (g && lane == leader) base = atomicAdd(&cand[r], (unsigned long long)__popc(peers));
+    base = __shfl_sync(FULL, base, leader);
+    if (g) {
+      const unsigned long long idx = base + __popc(peers & ((1u << lane) - 1u));
+      if (idx < cap) cand[kMaxR + (size_t)r * cap + idx] = k;
+    }
   }
   const bool counted = hit && !R.gather;
   if (!compact) {
@@ -368,10 +376,17 @@ __global__ void __launch_bounds__(kT, kSmem ? 2 : 4) sel_pass(const double* __re
           const Range& R = sr0[w];
           const uint64_t d = k - R.lo;
           const bool hit = d <= R.span;  // k < lo wraps d past every span (< 2^63)
-          if (R.gather) {                // uniform
-            if (hit) {
-              const unsigned long long idx = atomicAdd(&cand[b0], 1ull);
-              if (idx < cap) cand[kMaxR + (size_t)b0 * cap + idx] = k;
+          if (R.gather) {                // uniform: one counter atomic per warp
+            const unsigned m = __ballot_sync(FULL, hit);
+            if (m) {
+              const int leader = __ffs(m) - 1;
+              unsigned long long base = 0;
+              if (lane == leader) base = atomicAdd(&cand[b0], (unsigned long long)__popc(m));
+              base = __shfl_sync(FULL, base, leader);
+              if (hit) {
+                const unsigned long long idx = base + __popc(m & ((1u << lane) - 1u));
+                if (idx < cap) cand[kMaxR + (size_t)b0 * cap + idx] = k;
+              }
             }
             continue;
           }
@@ -658,7 +673,8 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
         ns = ctx->comm->allgather(ctx, cand, cand_all, cand_len, DT::U64, q);
         if (ns) return ns;
       }
-      sel_resolve<<<kMaxR, 1024, res_smem, q>>>(st, hist, cand_all, cand, world, cap);
+      // one CTA per open range: at most one range per open target
+      sel_resolve<<<std::min<int>(kMaxR, 2 * (int)npct), 1024, res_smem, q>>>(st, hist, cand_all, cand, world, cap);
       LSCAT_CUDA(ctx, cudaGetLastError());
     }
     LSCAT_CUDA(ctx, cudaMemcpyAsync(hst, st, sizeof(SelState), cudaMemcpyDeviceToHost, q));
