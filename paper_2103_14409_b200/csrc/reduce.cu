@@ -987,6 +987,12 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
   }
   int occ = 0;
   const auto ok = std::make_pair(uniform, smem);
+  if (ctx->red_occ.empty()) {  // the selection chain's carve-out (stats.cu): no reconfiguration
+    for (const void* f : {(const void*)reduce_groups_kernel, (const void*)reduce_uniform32_kernel,
+                          (const void*)finalize_merged_kernel, (const void*)init_partials})
+      LSCAT_CUDA(ctx, cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                           (int)cudaSharedmemCarveoutMaxShared));
+  }
   const auto it = ctx->red_occ.find(ok);
   if (it != ctx->red_occ.end()) {
     occ = it->second;

@@ -267,7 +267,7 @@ __device__ __noinline__ void hit_slow(const Range* sr, uint32_t r, uint64_t k, u
   }
 }
 
-template <bool kSmem, int kT>
+template <bool kSmem, int kT, int kU = 8>
 __global__ void __launch_bounds__(kT, kSmem ? 2 : 4) sel_pass(const double* __restrict__ perf, const double* __restrict__ gain,
                                                uint64_t lo, uint64_t hi, SelState* __restrict__ st,
                                                uint32_t* __restrict__ hist, unsigned long long* __restrict__ cand,
@@ -347,8 +347,8 @@ __global__ void __launch_bounds__(kT, kSmem ? 2 : 4) sel_pass(const double* __re
   const int lane = threadIdx.x & 31;
   const uint64_t end = hi0 > hi1 ? hi0 : hi1;
   // A warp takes kU chunks of 32 consecutive keys per iteration and issues all loads before
-  // using them; arrays with no open range are not read.
-  constexpr int kU = 8;
+  // using them; arrays with no open range are not read.  (kU = 1 for small inputs: more warps,
+  // each with a shorter latency-bound critical path.)
   const uint64_t wstride = (uint64_t)gridDim.x * kT * kU;
   for (uint64_t base = lo + (blockIdx.x * (uint64_t)kT + (threadIdx.x & ~31u)) * kU; base < end;
        base += wstride) {
@@ -648,16 +648,28 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
     LSCAT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, sel_pass<false, kT1>, kT1, 0));
     occ0 = std::max(occ0, 1);
     occ1 = std::max(occ1, 1);
+    // one shared-memory carve-out for the whole chain: a kernel whose carve-out differs from
+    // its predecessor's waits for the SMs to be reconfigured (measured: ~18 us of a 20 us
+    // sel_resolve on a small table was launch, not work)
+    const void* chain[] = {(const void*)sel_init, (const void*)sel_pass<true, kT0>,
+                           (const void*)sel_pass<false, kT1>, (const void*)sel_pass<false, kT1, 1>,
+                           (const void*)sel_resolve};
+    for (const void* f : chain)
+      LSCAT_CUDA(ctx, cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                           (int)cudaSharedmemCarveoutMaxShared));
   }
   // grids: every resident CTA once (occupancy API), capped by the work (kU x 32 groups per warp)
   const uint64_t n = rs.own_hi - rs.own_lo;
   const int grid0 = (int)std::min<uint64_t>(std::max<uint64_t>(1, (n + kT0 * 8 - 1) / (kT0 * 8)),
                                              (uint64_t)ctx->sm_count * occ0);
-  const int grid1 = (int)std::min<uint64_t>(std::max<uint64_t>(1, (n + kT1 * 8 - 1) / (kT1 * 8)),
-                                             (uint64_t)ctx->sm_count * occ1);
+  const bool small = n <= kSmallKeys;
+  const int grid1 = small ? (int)std::min<uint64_t>(std::max<uint64_t>(1, (n + kT1 - 1) / kT1),
+                                                    (uint64_t)ctx->sm_count * occ1)
+                          : (int)std::min<uint64_t>(std::max<uint64_t>(1, (n + kT1 * 8 - 1) / (kT1 * 8)),
+                                                    (uint64_t)ctx->sm_count * occ1);
   PctArg pa{};
   for (uint32_t i = 0; i < npct; i++) pa.p[i] = pct[i];
-  const int lpb = n <= kSmallKeys ? kLevelsPerBatchSmall : kLevelsPerBatch;
+  const int lpb = small ? kLevelsPerBatchSmall : kLevelsPerBatch;
   // One batch: lpb levels of pass -> (merge) -> resolve -> plan, then the state
   // is read back (one host sync per batch).
   auto enqueue_levels = [&](cudaStream_t q, bool first) -> lscat_status {
@@ -665,7 +677,10 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
       if (first && level == 0)
         sel_pass<true, kT0><<<grid0, kT0, pass_smem, q>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, st, hist, cand, cap, cbuf);
       else
-        sel_pass<false, kT1><<<grid1, kT1, 0, q>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, st, hist, cand, cap, cbuf);
+        if (small)
+          sel_pass<false, kT1, 1><<<grid1, kT1, 0, q>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, st, hist, cand, cap, cbuf);
+        else
+          sel_pass<false, kT1><<<grid1, kT1, 0, q>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, st, hist, cand, cap, cbuf);
       LSCAT_CUDA(ctx, cudaGetLastError());
       if (world > 1) {
         lscat_status ns = ctx->comm->allreduce(ctx, {{hist, (size_t)kMaxR * kBins, DT::U32, Op::Sum}}, q);
