@@ -735,9 +735,17 @@ __device__ void kernel_fin(const RollupArgs& q, uint64_t c, unsigned __int128 S,
   const unsigned __int128 cd = (unsigned __int128)c << 52;  // kernel-mean perf = S / cd
   const bool lt = (unsigned __int128)q.pld * S < (unsigned __int128)q.pln * cd;
   const bool band = lt && (unsigned __int128)q.bld * S >= (unsigned __int128)q.bln * cd;
-  uint32_t bin = (uint32_t)(((unsigned __int128)q.nb * S) / cd);  // largest j: j cd <= nb S
-  if (bin > q.nb) bin = q.nb;
-  const uint64_t kfx = (uint64_t)(S / c);
+  // 128-bit divisions are long software sequences: estimate in double, then fix up exactly
+  // with 128-bit products (the same integers as a division would give)
+  const unsigned __int128 nbS = (unsigned __int128)q.nb * S;
+  const double sd = (double)(uint64_t)S + (double)(uint64_t)(S >> 64) * 0x1p64;
+  int64_t bin = (int64_t)(sd / (double)c * (double)q.nb * 0x1p-52);  // largest j: j cd <= nb S
+  if (bin < 0) bin = 0;
+  while (bin < (int64_t)q.nb && (unsigned __int128)(bin + 1) * cd <= nbS) bin++;
+  while (bin > 0 && (unsigned __int128)bin * cd > nbS) bin--;
+  uint64_t kfx = (uint64_t)(sd / (double)c);  // floor(S / c) <= 2^52
+  while ((unsigned __int128)(kfx + 1) * c <= S) kfx++;
+  while (kfx > 0 && (unsigned __int128)kfx * c > S) kfx--;
   a.v[0] += 1;
   a.v[1] += not_best;
   a.v[2] += lt;
