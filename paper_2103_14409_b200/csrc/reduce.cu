@@ -756,6 +756,22 @@ __device__ void kernel_fin(const RollupArgs& q, uint64_t c, unsigned __int128 S,
   else atomicAdd(&hist64[bin], 1ull);
 }
 
+__device__ __forceinline__ void write_bnd(const RollupArgs& q, int slot, uint32_t k, uint64_t c,
+                                          unsigned __int128 S, bool nbst) {
+  uint64_t* b = q.bnd + slot * kBndWords;
+  b[0] = (uint64_t)k | (1ull << 32);
+  b[1] = c;
+  b[2] = (uint64_t)S;
+  b[3] = (uint64_t)(S >> 64);
+  b[4] = nbst;
+}
+
+// Warp-cooperative: a warp takes a contiguous range of 32-group chunks, lane j holds group
+// base + j; kernels are the runs of equal kernel ids (segments), summed with a segmented scan
+// (plain inclusive scans minus the value before each segment's head).  A segment ending
+// inside the chunk is finalised by its last lane; the one reaching lane 31 is carried to the
+// next chunk.  A warp skips the leading groups of a kernel that began before its range (the
+// previous warp finishes it) and reads past its range end to finish its last kernel.
 __global__ void __launch_bounds__(256) rollup_kernel(RollupArgs q) {
   extern __shared__ unsigned long long rs[];
   unsigned long long* cnt = rs;                                  // [kRollupWords]
@@ -764,44 +780,79 @@ __global__ void __launch_bounds__(256) rollup_kernel(RollupArgs q) {
   for (uint32_t i = threadIdx.x; i <= q.nb; i += blockDim.x) hist[i] = 0;
   __syncthreads();
   KAcc acc{};
-  for (uint64_t g = q.lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < q.hi;
-       g += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t k = kid_of(q, g);
-    if (g > q.lo && kid_of(q, g - 1) == k) continue;  // not the kernel's first group here
-    uint64_t c = 0, e = g;
-    unsigned __int128 S = 0;
-    bool nbst = false;
-    for (bool more = true; more;) {  // 8 records per round trip (independent loads in flight)
-      uint64_t rr[8];
-      uint32_t kk[8];
-#pragma unroll
-      for (int j = 0; j < 8; j++) {
-        const bool in = e + j < q.hi;
-        rr[j] = in ? q.krec[e + j] : 0;
-        kk[j] = in ? kid_of(q, e + j) : ~k;
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const uint64_t nch = (q.hi - q.lo + 31) / 32;
+  const uint64_t Wt = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t ch0 = w * nch / Wt, ch1 = (w + 1) * nch / Wt;
+  if (ch0 < ch1) {
+    const uint64_t g_begin = q.lo + ch0 * 32, g_end = min(q.lo + ch1 * 32, q.hi);
+    bool skipping = g_begin > q.lo;
+    const uint32_t skip_k = skipping ? kid_of(q, g_begin - 1) : 0u;
+    bool cv = false, cfirst = false;  // carried kernel (warp-uniform)
+    uint32_t ck = 0;
+    uint64_t cc = 0, cn = 0;
+    unsigned __int128 cS = 0;
+    for (uint64_t base = g_begin; base < q.hi; base += 32) {
+      const bool beyond = base >= g_end;
+      if (beyond && !cv) break;
+      const uint64_t g = base + lane;
+      const bool in = g < q.hi;
+      const uint32_t k = in ? kid_of(q, g) : 0u;
+      const uint64_t r = in ? q.krec[g] : 0ull;
+      bool inc = in;
+      if (skipping) {
+        const bool sk = in && k == skip_k;
+        inc = inc && !sk;
+        skipping = __all_sync(FULL, sk || !in) && __any_sync(FULL, in) && base + 32 < q.hi;
       }
+      if (beyond) inc = inc && k == ck;  // only the carried kernel's continuation
+      const uint64_t vc = (inc && ((r >> 53) & 1)) ? 1ull : 0ull;
+      const uint64_t vs = vc ? (r & ((1ull << 53) - 1)) : 0ull;
+      const uint64_t vn = vc ? ((r >> 54) & 1) : 0ull;
+      const uint32_t pk = __shfl_up_sync(FULL, k, 1);
+      const bool pin = __shfl_up_sync(FULL, inc, 1);
+      const bool head = lane == 0 || k != pk || inc != pin;
+      const unsigned hm = __ballot_sync(FULL, head);
+      uint64_t ic = vc, is = vs, in_ = vn;
 #pragma unroll
-      for (int j = 0; j < 8; j++) {
-        if (!more) break;
-        if (kk[j] != k) { more = false; break; }
-        const uint64_t r = rr[j];
-        if (r >> 53 & 1) {
-          c++;
-          S += r & ((1ull << 53) - 1);
-          nbst |= (r >> 54) & 1;
-        }
-        e++;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t yc = __shfl_up_sync(FULL, ic, o), ys = __shfl_up_sync(FULL, is, o),
+                       yn = __shfl_up_sync(FULL, in_, o);
+        if (lane >= o) { ic += yc; is += ys; in_ += yn; }
       }
+      const int start = 31 - __clz(hm & (FULL >> (31 - lane)));
+      const int src = start ? start - 1 : 0;
+      uint64_t bc = __shfl_sync(FULL, ic, src), bs = __shfl_sync(FULL, is, src), bn = __shfl_sync(FULL, in_, src);
+      if (start == 0) bc = bs = bn = 0;
+      const bool tail = lane == 31 || ((hm >> (lane + 1)) & 1);
+      const bool l0_in = __shfl_sync(FULL, inc, 0);
+      const uint32_t l0_k = __shfl_sync(FULL, k, 0);
+      const bool cont = cv && l0_in && l0_k == ck;  // the carried kernel continues at lane 0
+      if (cv && !cont && lane == 0) {               // it ended exactly at the chunk boundary
+        if (cfirst) write_bnd(q, 0, ck, cc, cS, cn != 0);
+        else kernel_fin(q, cc, cS, cn != 0, acc, hist, nullptr);
+      }
+      uint64_t tc = ic - bc, tn = in_ - bn;
+      unsigned __int128 tS = is - bs;
+      bool tfirst = base + start == q.lo;
+      if (start == 0 && cont) { tc += cc; tS += cS; tn += cn; tfirst = cfirst; }
+      if (tail && inc && lane != 31) {               // a kernel that ends inside this chunk
+        if (tfirst || g + 1 == q.hi) write_bnd(q, tfirst ? 0 : 1, k, tc, tS, tn != 0);  // rank edges
+        else kernel_fin(q, tc, tS, tn != 0, acc, hist, nullptr);
+      }
+      // carry = lane 31's segment when it is included (it may continue in the next chunk)
+      cv = __shfl_sync(FULL, inc, 31);
+      ck = __shfl_sync(FULL, k, 31);
+      cc = __shfl_sync(FULL, tc, 31);
+      cn = __shfl_sync(FULL, tn, 31);
+      const uint64_t slo = __shfl_sync(FULL, (uint64_t)tS, 31), shi = __shfl_sync(FULL, (uint64_t)(tS >> 64), 31);
+      cS = ((unsigned __int128)shi << 64) | slo;
+      cfirst = __shfl_sync(FULL, tfirst, 31);
     }
-    if (g == q.lo || e == q.hi) {  // may continue on a neighbouring rank: boundary record
-      uint64_t* b = q.bnd + (g == q.lo ? 0 : kBndWords);
-      b[0] = (uint64_t)k | (1ull << 32);
-      b[1] = c;
-      b[2] = (uint64_t)S;
-      b[3] = (uint64_t)(S >> 64);
-      b[4] = nbst;
-    } else {
-      kernel_fin(q, c, S, nbst, acc, hist, nullptr);
+    if (cv && lane == 0) {  // the last kernel reaches hi: it may continue on the next rank
+      write_bnd(q, cfirst ? 0 : 1, ck, cc, cS, cn != 0);
     }
   }
 #pragma unroll

@@ -495,3 +495,21 @@ def test_stats_after_dropping_reduce_outputs():
                           group_matrix=t["group_matrix"], opts=o_opts, percentiles=PCTS)
     assert st["pct_perf"] == ref.percentiles["perf"] and st["pct_gain"] == ref.percentiles["gain"]
     del junk
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_kernel_rollup_kernel_lengths(seed):
+    """The roll-up's warp-segmented pass on kernels of 1 to ~3000 groups (within a 32-group
+    chunk, across chunks, across warps' ranges, across the whole table), ragged groups with
+    NaN / missing largest rows, explicit non-monotone kernel ids."""
+    from tests.test_oracle_table import _random_table
+    rng = np.random.default_rng(700 + seed)
+    G = 40_000
+    rt, bid, off, gm = _random_table(rng, G, 32, nan_p=0.1, dup_vals=False)
+    lens = []
+    while sum(lens) < G:
+        lens.append(int(rng.choice([1, 2, 3, 7, 8, 31, 32, 33, 64, 100, 1000, 3000])))
+    ids = rng.permutation(len(lens)).astype(np.uint32) * 13 + 5
+    gk = np.repeat(ids, lens)[:G]
+    t = dict(runtime_ms=rt, block_id=bid, group_offset=off, group_matrix=gm, group_kernel=gk)
+    _compare(t, rollup=1)
