@@ -712,6 +712,7 @@ struct RollupArgs {
   const uint32_t* gkern;  // NULL -> (first_group + g) / M
   uint64_t first_group, lo, hi;
   uint32_t M, nb, pln, pld, bln, bld;
+  int mshift;             // log2(M) when M is a power of two, else -1
   uint64_t* part;         // roll-up region of the partial vector: [8] counters, [nb+1] hist
   uint64_t* bnd;          // [2 * kBndWords] this rank's boundary records
 };
@@ -719,7 +720,9 @@ struct RollupArgs {
 __device__ __forceinline__ uint32_t kid_of(const RollupArgs& q, uint64_t g) {
   if (q.gkern) return q.gkern[g];
   const uint64_t ag = q.first_group + g;  // implicit: a shift when M is a power of two
-  return (uint32_t)((q.M & (q.M - 1)) == 0 ? ag >> (__ffs(q.M) - 1) : ag / q.M);
+  if (q.mshift >= 0) return (uint32_t)(ag >> q.mshift);
+  if (ag < (1ull << 32)) return (uint32_t)ag / q.M;
+  return (uint32_t)(ag / q.M);
 }
 
 // Per-thread roll-up counters (flushed once per warp: the per-kernel increments all go to the
@@ -1115,6 +1118,7 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
     q.lo = p.acc_lo;
     q.hi = p.acc_hi;
     q.M = o->n_matrices;
+    q.mshift = (q.M & (q.M - 1)) == 0 ? __builtin_ctz(q.M) : -1;
     q.nb = o->bins_per_unit;
     q.pln = o->perf_lt_num; q.pld = o->perf_lt_den; q.bln = o->band_lo_num; q.bld = o->band_lo_den;
     q.part = p.partials + plen - (8 + o->bins_per_unit + 1);
