@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 
 #include "kern_common.cuh"
 
@@ -133,12 +134,30 @@ __global__ void __launch_bounds__(B, row_min_blocks<B>()) row_kernel(const float
 // Larger teams only add the team combine and idle leftover warps.
 inline int team_warps(int /*N*/, int /*B*/) { return 1; }
 
+inline bool legacy_grid() {
+  static const bool v = [] {
+    const char* e = getenv("LSCAT_ROW_GRID");
+    return e && strcmp(e, "legacy") == 0;
+  }();
+  return v;
+}
+
 template <int OP>
 struct RowLauncher {
   template <int B>
   struct L {
     static constexpr bool kSupported = true;
     static cudaError_t attrs(const void** f, size_t* sm) { return kernel_attrs(row_kernel<OP, B>, 0, f, sm); }
+    // resident CTAs per SM (a property of the sm_100a binary; thread-safe one-time query)
+    static int per_sm() {
+      static const int v = [] {
+        int r = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, row_kernel<OP, B>, B, 0);
+        cudaGetLastError();
+        return r > 0 ? r : 1;
+      }();
+      return v;
+    }
     static cudaError_t launch(const LaunchArgs& a, cudaStream_t s) {
       const SuiteEntry& e = *a.e;
       const int N = (int)e.n;
@@ -165,8 +184,21 @@ struct RowLauncher {
       // LSCAT_L2_ROTATE (a.cold): plain streaming loads, nothing is kept for the next launch
       const float keep = (share <= 0 || a.cold) ? 0.f : (float)std::min(1.0, share * (double)a.l2_bytes / a_bytes);
       const int sms = a.sms > 0 ? a.sms : 148;
-      const int need = (N + teams - 1) / teams;
-      const int grid = (ROW_PERSIST_BIG && B > 512 && need > sms) ? sms : need;
+      // Grid: one row block per CTA while they all fit in one wave; otherwise r = ceil(row
+      // blocks / resident CTAs) row blocks per CTA over the fewest CTAs that need no more than
+      // r -- every CTA (and warp) streams the same number of rows and none idles through a
+      // partial last round (LSCAT_ROW_GRID=legacy: the round-1 grid, for A/B runs).
+      const long need = (N + teams - 1) / teams;
+      const long slots = (long)sms * per_sm();
+      int grid;
+      if (legacy_grid()) {
+        grid = (int)((ROW_PERSIST_BIG && B > 512 && need > sms) ? sms : need);
+      } else if (need <= slots) {
+        grid = (int)need;
+      } else {
+        const long r = (need + slots - 1) / slots;
+        grid = (int)((need + r - 1) / r);
+      }
       return launch_k(row_kernel<OP, B>, dim3(grid), dim3(B), 0, s, a.pdl,
                       (const float*)e.in0, (const float*)e.in1, (float*)e.out, N, tw, keep);
     }
