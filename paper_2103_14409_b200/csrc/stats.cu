@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "common.h"
+#include "selbins.h"
 
 namespace lscat {
 namespace {
@@ -70,6 +71,8 @@ struct SelState {
   uint32_t pad2;
   unsigned long long nc[2];   // compacted keys per quantity
   uint64_t n_def;
+  uint32_t sampled_fail;      // the sampled first level missed a target (host falls back)
+  uint32_t pad3;
   Range r0[2];                // level-0 ranges: later full passes filter keys by level-0 bin
   Range r[kMaxR];
   Tgt t[kMaxT];
@@ -614,6 +617,298 @@ __global__ void __launch_bounds__(1024) sel_resolve(SelState* st, uint32_t* __re
   if (st->nr) plan_ranges(st, cap);
 }
 
+// ---- sampled first level (large inputs) -----------------------------------------------
+// Instead of a histogram pass and then a compaction pass over perf/gain, one pass copies out
+// the keys of narrow intervals that hold the targets and counts, exactly, the keys below each
+// interval.  The intervals come from a systematic sample (every s-th key, s odd) binned into
+// the fixed bins of selbins.h: a target of global rank k has sample rank ~ k ns / n; the
+// interval spans the bins of sample ranks k ns / n -/+ (6 sqrt(.) + 64).  If a target's rank
+// is not inside its interval after the exact counts (a sampling miss) or the copies overflow,
+// the selection restarts on the histogram path, so the result never depends on the sample.
+constexpr int kIvQ = 9;                  // intervals per quantity (<= percentiles)
+constexpr uint64_t kSampleKeys = 1 << 20;  // about this many samples per quantity
+
+struct SampState {
+  uint32_t niv[2];                       // intervals per quantity
+  uint32_t fail;
+  uint32_t pad;
+  uint64_t lo[2][kIvQ], hi[2][kIvQ];     // sorted, disjoint, per quantity
+  unsigned long long cge[2][kIvQ];       // keys >= lo  (over all ranks)
+  unsigned long long cin[2][kIvQ];       // keys inside [lo, hi]
+  unsigned long long scanned[2];         // keys read (NaN keys of undefined groups included)
+  unsigned long long ncopy_all[2];       // keys copied (summed over ranks: the overflow check)
+  unsigned long long ncopy[2];           // keys copied (this rank)
+  uint32_t tiv[kMaxT];                   // target -> interval
+};
+
+__device__ __forceinline__ bool valid_key(uint64_t k) { return k < 0x7FF0000000000000ull; }
+
+__global__ void __launch_bounds__(256) sel_sample_hist(const double* __restrict__ perf,
+                                                       const double* __restrict__ gain, uint64_t lo,
+                                                       uint64_t hi, uint64_t stride,
+                                                       uint32_t* __restrict__ shist) {
+  __shared__ uint32_t h[2 * kFxBins];
+  for (uint32_t i = threadIdx.x; i < 2 * kFxBins; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = lo + j * stride;
+    if (i >= hi) break;
+    const uint64_t kp = (uint64_t)__double_as_longlong(perf[i]);
+    const uint64_t kg = (uint64_t)__double_as_longlong(gain[i]);
+    if (valid_key(kp)) atomicAdd(&h[fx_perf_bin(kp)], 1u);
+    if (valid_key(kg)) atomicAdd(&h[kFxBins + fx_gain_bin(kg)], 1u);
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < 2 * kFxBins; i += blockDim.x)
+    if (h[i]) atomicAdd(&shist[i], h[i]);
+}
+
+// One CTA: targets, their sample intervals, merged per quantity.
+__global__ void __launch_bounds__(1024) sel_plan_sampled(SelState* st, SampState* ss,
+                                                         const uint64_t* __restrict__ partials,
+                                                         const uint32_t* __restrict__ shist,
+                                                         const uint64_t* __restrict__ mm, PctArg pct,
+                                                         uint32_t npct, double dmul, double dadd) {
+  __shared__ unsigned long long pre[2][kFxBins];
+  __shared__ unsigned long long part_sum[1024];
+  __shared__ uint64_t tlo[kMaxT], thi[kMaxT], tk[kMaxT];
+  const int tid = threadIdx.x;
+  const uint64_t n_def = partials[LSCAT_P_RATIO_DEFINED];
+  constexpr int kPer = (kFxBins + 1023) / 1024;
+  for (int w = 0; w < 2; w++) {  // inclusive scan of the sample histogram
+    unsigned long long c[kPer], sum = 0;
+#pragma unroll
+    for (int j = 0; j < kPer; j++) {
+      const uint32_t b = (uint32_t)tid * kPer + j;
+      c[j] = b < kFxBins ? shist[(size_t)w * kFxBins + b] : 0ull;
+      sum += c[j];
+    }
+    part_sum[tid] = sum;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+      const unsigned long long y = tid >= o ? part_sum[tid - o] : 0ull;
+      __syncthreads();
+      part_sum[tid] += y;
+      __syncthreads();
+    }
+    unsigned long long run = part_sum[tid] - sum;
+#pragma unroll
+    for (int j = 0; j < kPer; j++) {
+      const uint32_t b = (uint32_t)tid * kPer + j;
+      run += c[j];
+      if (b < kFxBins) pre[w][b] = run;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    st->nt = 2 * npct;
+    st->err = 0;
+    st->done_ctas = 0;
+    st->src = 0;
+    st->compact = 0;
+    st->n_def = n_def;
+    st->sampled_fail = 0;
+    st->r0_valid = 0;
+    st->nr = 0;
+    ss->fail = 0;
+  }
+  if (tid < (int)(2 * npct)) {
+    Tgt t{};
+    t.which = tid >= (int)npct;
+    const double r = ceil(pct.p[tid % npct] * (double)n_def);  // nearest rank (R-13)
+    t.k = r < 1.0 ? 1 : (r > (double)n_def ? n_def : (uint64_t)r);
+    t.done = n_def == 0;
+    t.key = kNaNKey;
+    t.lo = mm[2 * t.which];
+    t.hi = mm[2 * t.which + 1];
+    t.count = n_def;
+    st->t[tid] = t;
+    tk[tid] = t.k;
+    const unsigned long long* P = pre[t.which];
+    const double ns = (double)P[kFxBins - 1];
+    uint64_t lo = t.lo, hi = t.hi;
+    if (!t.done && ns > 0) {
+      const double ks = (double)t.k * ns / (double)n_def;
+      const double d = dmul * sqrt(ks > 1.0 ? ks : 1.0) + dadd;
+      const unsigned long long s_lo = (unsigned long long)fmax(1.0, floor(ks - d));
+      const unsigned long long s_hi = (unsigned long long)fmin(ns, ceil(ks + d));
+      auto first_reaching = [&](unsigned long long x) {  // smallest b with P[b] >= x
+        uint32_t a = 0, b = kFxBins - 1;
+        while (a < b) {
+          const uint32_t m = (a + b) / 2;
+          if (P[m] >= x) b = m; else a = m + 1;
+        }
+        return a;
+      };
+      const uint32_t b1 = first_reaching(s_lo), b2 = first_reaching(s_hi);
+      uint64_t l1, h1, l2, h2;
+      fx_bin_range(t.which, b1, &l1, &h1);
+      fx_bin_range(t.which, b2, &l2, &h2);
+      lo = l1 > lo ? l1 : lo;
+      hi = h2 < hi ? h2 : hi;
+    }
+    tlo[tid] = lo;
+    thi[tid] = hi;
+  }
+  __syncthreads();
+  if (tid == 0) {  // per quantity: sort the targets' intervals by lo, merge overlapping ones
+    bool fail = false;
+    for (uint32_t w = 0; w < 2; w++) {
+      uint32_t idx[kMaxT / 2], n = 0;
+      for (uint32_t i = 0; i < npct; i++) idx[n++] = w * npct + i;
+      for (uint32_t a = 1; a < n; a++)
+        for (uint32_t b = a; b > 0 && tlo[idx[b]] < tlo[idx[b - 1]]; b--) {
+          const uint32_t x = idx[b]; idx[b] = idx[b - 1]; idx[b - 1] = x;
+        }
+      uint32_t m = 0;
+      for (uint32_t a = 0; a < n; a++) {
+        const uint32_t i = idx[a];
+        if (m > 0 && tlo[i] <= ss->hi[w][m - 1] + 1) {
+          if (thi[i] > ss->hi[w][m - 1]) ss->hi[w][m - 1] = thi[i];
+        } else {
+          if (m == kIvQ) { fail = true; break; }
+          ss->lo[w][m] = tlo[i];
+          ss->hi[w][m] = thi[i];
+          m++;
+        }
+        ss->tiv[i] = m - 1;
+      }
+      ss->niv[w] = m;
+      for (uint32_t r = 0; r < kIvQ; r++) { ss->cge[w][r] = 0; ss->cin[w][r] = 0; }
+      ss->scanned[w] = 0;
+      ss->ncopy_all[w] = 0;
+      ss->ncopy[w] = 0;
+    }
+    if (fail) ss->fail = 1;
+  }
+  (void)tk;
+}
+
+// One pass over this rank's keys: count keys >= lo and inside [lo, hi] of every interval of
+// their quantity, copy the keys inside multi-valued intervals to cbuf (warp-aggregated).
+template <int kT>
+__global__ void __launch_bounds__(kT, 2) sel_pass_sampled(const double* __restrict__ perf,
+                                                          const double* __restrict__ gain, uint64_t lo,
+                                                          uint64_t hi, SampState* __restrict__ ss,
+                                                          double* __restrict__ cbuf) {
+  __shared__ uint64_t s_lo[2][kIvQ], s_hi[2][kIvQ];
+  __shared__ uint32_t s_n[2];
+  if (threadIdx.x < 2) s_n[threadIdx.x] = ss->fail ? 0u : ss->niv[threadIdx.x];
+  if (threadIdx.x < 2 * kIvQ) {
+    const int w = threadIdx.x / kIvQ, r = threadIdx.x % kIvQ;
+    s_lo[w][r] = ss->lo[w][r];
+    s_hi[w][r] = ss->hi[w][r];
+  }
+  __syncthreads();
+  const uint32_t n0 = s_n[0], n1 = s_n[1];
+  if (n0 == 0 && n1 == 0) return;
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  uint32_t cge[2][kIvQ] = {}, cin[2][kIvQ] = {};
+  uint32_t scanned = 0;
+  constexpr int kU = 4;
+  const uint64_t wstride = (uint64_t)gridDim.x * kT * kU;
+  for (uint64_t base = lo + (blockIdx.x * (uint64_t)kT + (threadIdx.x & ~31u)) * kU; base < hi; base += wstride) {
+    uint64_t v[2][kU];
+#pragma unroll
+    for (int w = 0; w < 2; w++) {
+      const uint64_t* src = reinterpret_cast<const uint64_t*>(w ? gain : perf) + base + lane;
+#pragma unroll
+      for (int u = 0; u < kU; u++) {
+        const uint64_t i = base + lane + 32 * u;
+        v[w][u] = i < hi ? __ldg(src + 32 * u) : kNaNKey;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+      const bool ok = base + lane + 32 * u < hi;  // lanes past the end count nowhere
+      scanned += ok;
+#pragma unroll
+      for (int w = 0; w < 2; w++) {
+        const uint64_t k = v[w][u];
+        const uint32_t nw = w ? n1 : n0;
+        bool copy = false;
+#pragma unroll
+        for (int r = 0; r < kIvQ; r++) {
+          if (r >= (int)nw) break;
+          const bool ge = ok && k >= s_lo[w][r];
+          const bool in = ge && k <= s_hi[w][r];
+          cge[w][r] += ge;
+          cin[w][r] += in;
+          copy |= in && s_lo[w][r] != s_hi[w][r];
+        }
+        const unsigned m = __ballot_sync(FULL, copy);
+        if (m) {
+          const int leader = __ffs(m) - 1;
+          unsigned long long at = 0;
+          if (lane == leader) {
+            at = atomicAdd(&ss->ncopy[w], (unsigned long long)__popc(m));
+            atomicAdd(&ss->ncopy_all[w], (unsigned long long)__popc(m));
+          }
+          at = __shfl_sync(FULL, at, leader) + __popc(m & ((1u << lane) - 1u));
+          if (copy && at < kCompactCap) reinterpret_cast<uint64_t*>(cbuf)[(size_t)w * kCompactCap + at] = k;
+        }
+      }
+    }
+  }
+  // the counters: warp sums, one atomic per warp and counter
+#pragma unroll
+  for (int w = 0; w < 2; w++)
+#pragma unroll
+    for (int r = 0; r < kIvQ; r++) {
+      const uint32_t a = __reduce_add_sync(FULL, cge[w][r]), b = __reduce_add_sync(FULL, cin[w][r]);
+      if (lane == 0 && a) atomicAdd(&ss->cge[w][r], (unsigned long long)a);
+      if (lane == 0 && b) atomicAdd(&ss->cin[w][r], (unsigned long long)b);
+    }
+  const uint32_t sc = __reduce_add_sync(FULL, scanned);
+  if (lane == 0 && sc) {
+    atomicAdd(&ss->scanned[0], (unsigned long long)sc);
+    atomicAdd(&ss->scanned[1], (unsigned long long)sc);
+  }
+}
+
+// One CTA: exact ranks inside the intervals.  A target whose rank is not inside its interval
+// (a sampling miss) or copies beyond the buffer -> sampled_fail (the host restarts on the
+// histogram path).  Otherwise every target gets its interval, rank and count, the passes read
+// the copies from now on, and the open targets are planned into ranges.
+__global__ void __launch_bounds__(kMaxT) sel_check_sampled(SelState* st, SampState* ss, uint32_t cap) {
+  const int i = threadIdx.x;
+  __shared__ uint32_t s_fail;
+  if (i == 0) s_fail = ss->fail || ss->ncopy_all[0] > kCompactCap || ss->ncopy_all[1] > kCompactCap;
+  __syncthreads();
+  if (i < (int)st->nt && !s_fail) {
+    Tgt& t = st->t[i];
+    if (!t.done) {
+      const uint32_t w = t.which, r = ss->tiv[i];
+      const unsigned long long below = ss->scanned[w] - ss->cge[w][r], in = ss->cin[w][r];
+      if (!(below < t.k && t.k <= below + in)) {
+        atomicOr(&s_fail, 1u);
+      } else {
+        t.lo = ss->lo[w][r];
+        t.hi = ss->hi[w][r];
+        t.k -= below;
+        t.count = in;
+      }
+    }
+  }
+  __syncthreads();
+  if (s_fail) {
+    if (i == 0) {  // no open ranges: the levels queued behind this are no-ops
+      st->sampled_fail = 1;
+      st->nr = 0;
+      st->open = 0;
+    }
+    return;
+  }
+  if (i == 0) {
+    st->src = 1;  // the later passes read the copies
+    st->nc[0] = ss->ncopy[0];
+    st->nc[1] = ss->ncopy[1];
+  }
+  __syncthreads();
+  plan_ranges(st, cap);
+}
+
 lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct, double* out_perf,
                                 double* out_gain, cudaStream_t s) {
   const ReduceState& rs = ctx->rs;
@@ -695,6 +990,44 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
     LSCAT_CUDA(ctx, cudaMemcpyAsync(hst, st, sizeof(SelState), cudaMemcpyDeviceToHost, q));
     return LSCAT_OK;
   };
+  // sampled first level (large inputs, <= kIvQ percentiles; LSCAT_SEL_NOSAMPLE=1 disables it)
+  SampState* ss = (SampState*)scratch(ctx, "sel_samp", sizeof(SampState), &err);
+  if (err) return cuda_fail(ctx, err, "stats: scratch");
+  uint32_t* shist = (uint32_t*)scratch(ctx, "sel_shist", 2 * kFxBins * 4, &err);
+  if (err) return cuda_fail(ctx, err, "stats: scratch");
+  static const bool no_sample = getenv("LSCAT_SEL_NOSAMPLE") != nullptr;
+  // interval half-width in sample ranks: dmul sqrt(rank) + dadd (LSCAT_SEL_SAMPLE_DELTA=0 makes
+  // it 0: single bins, sampling misses -- the tests use it to exercise the fallback)
+  static const bool zero_delta = getenv("LSCAT_SEL_SAMPLE_DELTA") && atof(getenv("LSCAT_SEL_SAMPLE_DELTA")) == 0.0;
+  const double dmul = zero_delta ? 0.0 : 6.0, dadd = zero_delta ? 0.0 : 64.0;
+  bool sampled = !small && npct <= (uint32_t)kIvQ && !no_sample;
+  const uint64_t stride = std::max<uint64_t>(1, n / kSampleKeys) | 1;  // odd: no period-2^k alias
+  const int grid_s = (int)std::min<uint64_t>(std::max<uint64_t>(1, (n / stride + 255) / 256),
+                                             (uint64_t)ctx->sm_count * 4);
+  const int grid_p = (int)std::min<uint64_t>(std::max<uint64_t>(1, (n + 256 * 4 - 1) / (256 * 4)),
+                                             (uint64_t)ctx->sm_count * 2);
+  auto enqueue_first_sampled = [&](cudaStream_t q) -> lscat_status {
+    LSCAT_CUDA(ctx, cudaMemsetAsync(hist, 0, (size_t)kMaxR * kBins * 4, q));
+    LSCAT_CUDA(ctx, cudaMemsetAsync(cand, 0, (size_t)kMaxR * 8, q));
+    LSCAT_CUDA(ctx, cudaMemsetAsync(shist, 0, 2 * kFxBins * 4, q));
+    sel_sample_hist<<<grid_s, 256, 0, q>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, stride, shist);
+    LSCAT_CUDA(ctx, cudaGetLastError());
+    if (world > 1) {
+      lscat_status ns = ctx->comm->allreduce(ctx, {{shist, 2 * (size_t)kFxBins, DT::U32, Op::Sum}}, q);
+      if (ns) return ns;
+    }
+    sel_plan_sampled<<<1, 1024, 0, q>>>(st, ss, rs.partials, shist, rs.minmax, pa, npct, dmul, dadd);
+    LSCAT_CUDA(ctx, cudaGetLastError());
+    sel_pass_sampled<256><<<grid_p, 256, 0, q>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, ss, cbuf);
+    LSCAT_CUDA(ctx, cudaGetLastError());
+    if (world > 1) {  // cge, cin, scanned, ncopy_all: contiguous u64 counters
+      lscat_status ns = ctx->comm->allreduce(ctx, {{&ss->cge[0][0], 4 * kIvQ + 4, DT::U64, Op::Sum}}, q);
+      if (ns) return ns;
+    }
+    sel_check_sampled<<<1, kMaxT, 0, q>>>(st, ss, cap);
+    LSCAT_CUDA(ctx, cudaGetLastError());
+    return enqueue_levels(q, false);
+  };
   auto enqueue_first = [&](cudaStream_t q) -> lscat_status {
     LSCAT_CUDA(ctx, cudaMemsetAsync(hist, 0, (size_t)kMaxR * kBins * 4, q));
     LSCAT_CUDA(ctx, cudaMemsetAsync(cand, 0, (size_t)kMaxR * 8, q));
@@ -706,41 +1039,47 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
   lscat_status ls;
   // First batch: launched as a cached CUDA graph when the selection runs on one rank (the
   // small tables of configs[2]/[3] are launch-latency bound: ~10 dependent launches).
-  if (world == 1 && !debug) {
-    std::string key;
-    auto put = [&](const void* v, size_t n) { key.append(reinterpret_cast<const char*>(v), n); };
-    const void* ptrs[] = {rs.perf, rs.gain, rs.partials, rs.minmax, st, hist, cand, cbuf, hst};
-    put(ptrs, sizeof ptrs);
-    put(&rs.own_lo, 8); put(&rs.own_hi, 8); put(&npct, 4); put(pa.p, npct * 8);
-    put(&grid0, 4); put(&grid1, 4); put(&cap, 4);
-    cudaGraphExec_t gx = nullptr;
-    for (auto& kv : ctx->sel_graphs)
-      if (kv.first == key) gx = kv.second;
-    if (!gx) {
-      cudaStream_t cs = ctx->capture_stream;
-      LSCAT_CUDA(ctx, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-      ls = enqueue_first(cs);
-      cudaGraph_t g = nullptr;
-      const cudaError_t ce = cudaStreamEndCapture(cs, &g);
-      if (ls) {
-        if (g) cudaGraphDestroy(g);
-        return ls;
+  auto launch_first = [&](bool samp) -> lscat_status {
+    auto enq = [&](cudaStream_t q) { return samp ? enqueue_first_sampled(q) : enqueue_first(q); };
+    if (world == 1 && !debug) {
+      std::string key;
+      auto put = [&](const void* v, size_t n_) { key.append(reinterpret_cast<const char*>(v), n_); };
+      const void* ptrs[] = {rs.perf, rs.gain, rs.partials, rs.minmax, st, hist, cand, cbuf, hst, ss, shist};
+      put(ptrs, sizeof ptrs);
+      put(&rs.own_lo, 8); put(&rs.own_hi, 8); put(&npct, 4); put(pa.p, npct * 8);
+      put(&grid0, 4); put(&grid1, 4); put(&cap, 4); put(&samp, sizeof samp);
+      cudaGraphExec_t gx = nullptr;
+      for (auto& kv : ctx->sel_graphs)
+        if (kv.first == key) gx = kv.second;
+      if (!gx) {
+        cudaStream_t cs = ctx->capture_stream;
+        LSCAT_CUDA(ctx, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        lscat_status e = enq(cs);
+        cudaGraph_t g = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(cs, &g);
+        if (e) {
+          if (g) cudaGraphDestroy(g);
+          return e;
+        }
+        LSCAT_CUDA(ctx, ce);
+        const cudaError_t ie = cudaGraphInstantiate(&gx, g, 0);
+        cudaGraphDestroy(g);
+        LSCAT_CUDA(ctx, ie);
+        if (ctx->sel_graphs.size() >= 8) {  // small LRU-less cache: drop the oldest
+          cudaGraphExecDestroy(ctx->sel_graphs.front().second);
+          ctx->sel_graphs.erase(ctx->sel_graphs.begin());
+        }
+        ctx->sel_graphs.emplace_back(std::move(key), gx);
       }
-      LSCAT_CUDA(ctx, ce);
-      const cudaError_t ie = cudaGraphInstantiate(&gx, g, 0);
-      cudaGraphDestroy(g);
-      LSCAT_CUDA(ctx, ie);
-      if (ctx->sel_graphs.size() >= 8) {  // small LRU-less cache: drop the oldest
-        cudaGraphExecDestroy(ctx->sel_graphs.front().second);
-        ctx->sel_graphs.erase(ctx->sel_graphs.begin());
-      }
-      ctx->sel_graphs.emplace_back(std::move(key), gx);
+      LSCAT_CUDA(ctx, cudaGraphLaunch(gx, s));
+    } else {
+      lscat_status e = enq(s);
+      if (e) return e;
     }
-    LSCAT_CUDA(ctx, cudaGraphLaunch(gx, s));
-  } else {
-    if ((ls = enqueue_first(s))) return ls;
-  }
-  ctx->launches += 1 + 2 * lpb;
+    ctx->launches += (samp ? 4 : 1) + 2 * lpb;
+    return LSCAT_OK;
+  };
+  if ((ls = launch_first(sampled))) return ls;
   for (int batch = 0;; batch++) {
     if (batch == 8) return fail(ctx, LSCAT_ERR_STATE, "stats: percentile selection did not converge");
     if (batch > 0) {
@@ -749,8 +1088,16 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
     }
     LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
     if (debug)
-      fprintf(stderr, "sel batch %d: nt %u nr %u nw0 %u open %u err %u src %u compact %u nc %llu %llu\n", batch,
-              hst->nt, hst->nr, hst->nw0, hst->open, hst->err, hst->src, hst->compact, hst->nc[0], hst->nc[1]);
+      fprintf(stderr, "sel batch %d: nt %u nr %u nw0 %u open %u err %u src %u compact %u nc %llu %llu sampled %d fail %u\n",
+              batch, hst->nt, hst->nr, hst->nw0, hst->open, hst->err, hst->src, hst->compact, hst->nc[0],
+              hst->nc[1], (int)sampled, hst->sampled_fail);
+    if (batch == 0 && sampled && hst->sampled_fail) {  // a sampling miss: the histogram path
+      sampled = false;
+      ctx->sel_fallbacks++;
+      if ((ls = launch_first(false))) return ls;
+      batch = -1;
+      continue;
+    }
     if (hst->err) return fail(ctx, LSCAT_ERR_STATE, "stats: percentile selection lost keys (code %u)", hst->err);
     if (!hst->open) break;
   }

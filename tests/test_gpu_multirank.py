@@ -100,3 +100,24 @@ def test_group_aligned_merge(world):
 
     res = _run_ranks(world, make, dict(kernel_rollup=1), f"ga{world}")
     _check(res, ref)
+
+
+@pytest.mark.parametrize("world,point", [(2, True), (3, False)])
+def test_sampled_selection_multirank(world, point):
+    """The sampled first level of the percentile selection (> 2^20 keys per rank) over the local
+    transport: sample histograms and interval counts summed over ranks, copies per rank."""
+    require_gpu()
+    n, K = 36 * 2 ** 21 if point else 3 * 36 * 2 ** 20, 300_000
+    full = gen_table(n, K, preset="t4", seed=91)
+    ref = OT.reduce_table(full["runtime_ms"], full["block_id"], full["group_offset"],
+                          group_matrix=full["group_matrix"], percentiles=PCTS)
+    G = full["n_groups"]
+
+    def make(ctx, r):
+        if point:
+            return ctx.gen_table(n, K, preset=0, seed=91, block_mod=world, block_rem=r)
+        return ctx.gen_table(n, K, preset=0, seed=91, group_begin=G * r // world,
+                             group_end=G * (r + 1) // world)
+
+    res = _run_ranks(world, make, dict(point_sharded=1) if point else {}, f"smp{world}{int(point)}")
+    _check(res, ref)

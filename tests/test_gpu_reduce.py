@@ -513,3 +513,33 @@ def test_kernel_rollup_kernel_lengths(seed):
     gk = np.repeat(ids, lens)[:G]
     t = dict(runtime_ms=rt, block_id=bid, group_offset=off, group_matrix=gm, group_kernel=gk)
     _compare(t, rollup=1)
+
+
+def test_percentiles_sampled_first_level():
+    """More than 2^20 ratio-defined groups with <= 9 percentiles take the sampled first level
+    (one pass copying the keys of sample-derived intervals, exact counts below each interval):
+    values exact against the oracle, ragged table, NaN groups."""
+    t = gen_table(40_000_000, 150_000, preset="t4", nan_rate=0.03, seed=2024)
+    _compare(t, pcts=[0.01, 0.05, 0.1, 0.25, 0.5, 0.75, 0.9, 0.95, 0.99])
+
+
+def test_percentiles_sampled_fallback():
+    """A zero-width sample interval (LSCAT_SEL_SAMPLE_DELTA=0) makes targets miss their
+    interval: the selection restarts on the histogram path and stays exact (child process: the
+    switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np\n"
+        "from tests.test_gpu_reduce import _compare\n"
+        "from synth import gen_table\n"
+        "t = gen_table(36_000_000, 140_000, preset='gtx980', nan_rate=0.03, seed=7)\n"
+        "_compare(t, pcts=[0.01, 0.1, 0.5, 0.9, 0.99])\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, LSCAT_SEL_SAMPLE_DELTA="0", LSCAT_SEL_DEBUG="1")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+    assert "sampled 1 fail 1" in r.stderr, r.stderr[-2000:]
