@@ -618,30 +618,32 @@ __global__ void __launch_bounds__(1024) sel_resolve(SelState* st, uint32_t* __re
 }
 
 // ---- sampled first level (large inputs) -----------------------------------------------
-// Instead of a histogram pass and then a compaction pass over perf/gain, one pass copies out
-// the keys of narrow intervals that hold the targets and counts, exactly, the keys below each
-// interval.  The intervals come from a systematic sample (every s-th key, s odd) binned into
-// the fixed bins of selbins.h: a target of global rank k has sample rank ~ k ns / n; the
-// interval spans the bins of sample ranks k ns / n -/+ (6 sqrt(.) + 64).  If a target's rank
-// is not inside its interval after the exact counts (a sampling miss) or the copies overflow,
-// the selection restarts on the histogram path, so the result never depends on the sample.
-constexpr int kIvQ = 9;                  // intervals per quantity (<= percentiles)
+// Instead of a histogram pass followed by a compaction pass over perf/gain, one pass both
+// counts every key into the fixed bins of selbins.h (exact) and copies out the keys of the
+// bins that, by a sample, hold the targets.  The sample is systematic (every s-th key, s odd)
+// and binned the same way: a target of global rank k has sample rank ~ k ns / n, and the bins
+// of sample ranks k ns / n -/+ (4.5 sqrt(.) + 32) are copied.  After the pass the exact
+// histogram narrows every target to one bin (like a histogram level); if that bin was not
+// copied (a sampling miss) or the copies overflow, the selection restarts on the histogram
+// path, so the result never depends on the sample.  The single-valued bins (perf == 1, gain
+// == 0) are neither counted nor copied: their count is the reducer's perf_hist[nb].
+constexpr int kIvQ = 9;                    // copied bin intervals per quantity (<= percentiles)
 constexpr uint64_t kSampleKeys = 1 << 20;  // about this many samples per quantity
+constexpr uint32_t kCopyStage = 1536;      // per quantity and CTA: copies staged in smem
 
 struct SampState {
   uint32_t niv[2];                       // intervals per quantity
   uint32_t fail;
   uint32_t pad;
-  uint64_t lo[2][kIvQ], hi[2][kIvQ];     // sorted, disjoint, per quantity
-  unsigned long long cge[2][kIvQ];       // keys >= lo  (over all ranks)
-  unsigned long long cin[2][kIvQ];       // keys inside [lo, hi]
-  unsigned long long scanned[2];         // keys read (NaN keys of undefined groups included)
-  unsigned long long ncopy_all[2];       // keys copied (summed over ranks: the overflow check)
+  uint32_t b1[2][kIvQ], b2[2][kIvQ];     // copied bin intervals (inclusive), sorted, disjoint
+  unsigned long long ncopy_all[2];       // keys copied, summed over ranks (overflow check)
   unsigned long long ncopy[2];           // keys copied (this rank)
-  uint32_t tiv[kMaxT];                   // target -> interval
+  uint32_t fh[2][kFxBins];               // exact counts of the counted bins (summed over ranks)
 };
 
 __device__ __forceinline__ bool valid_key(uint64_t k) { return k < 0x7FF0000000000000ull; }
+__device__ __forceinline__ bool virtual_bin(uint32_t w, uint32_t b) { return w == 0 ? b == kFxBins - 2 : b == 0; }
+__device__ __forceinline__ uint32_t fx_bin(uint32_t w, uint64_t k) { return w == 0 ? fx_perf_bin(k) : fx_gain_bin(k); }
 
 __global__ void __launch_bounds__(256) sel_sample_hist(const double* __restrict__ perf,
                                                        const double* __restrict__ gain, uint64_t lo,
@@ -653,8 +655,8 @@ __global__ void __launch_bounds__(256) sel_sample_hist(const double* __restrict_
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;; j += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t i = lo + j * stride;
     if (i >= hi) break;
-    const uint64_t kp = (uint64_t)__double_as_longlong(perf[i]);
-    const uint64_t kg = (uint64_t)__double_as_longlong(gain[i]);
+    const uint64_t kp = (uint64_t)__double_as_longlong(__ldcs(perf + i));
+    const uint64_t kg = (uint64_t)__double_as_longlong(__ldcs(gain + i));
     if (valid_key(kp)) atomicAdd(&h[fx_perf_bin(kp)], 1u);
     if (valid_key(kg)) atomicAdd(&h[kFxBins + fx_gain_bin(kg)], 1u);
   }
@@ -663,43 +665,59 @@ __global__ void __launch_bounds__(256) sel_sample_hist(const double* __restrict_
     if (h[i]) atomicAdd(&shist[i], h[i]);
 }
 
-// One CTA: targets, their sample intervals, merged per quantity.
+// Inclusive scan of a quantity's kFxBins counts into pre[] (1024 threads; part is scratch).
+__device__ void scan_bins(const uint32_t* __restrict__ c_in, unsigned long long virt, uint32_t w,
+                          unsigned long long* pre, unsigned long long* part) {
+  constexpr int kPer = (kFxBins + 1023) / 1024;
+  const int tid = threadIdx.x;
+  unsigned long long c[kPer], sum = 0;
+#pragma unroll
+  for (int j = 0; j < kPer; j++) {
+    const uint32_t b = (uint32_t)tid * kPer + j;
+    c[j] = b < kFxBins ? (virtual_bin(w, b) ? virt : (unsigned long long)c_in[b]) : 0ull;
+    sum += c[j];
+  }
+  part[tid] = sum;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const unsigned long long y = tid >= o ? part[tid - o] : 0ull;
+    __syncthreads();
+    part[tid] += y;
+    __syncthreads();
+  }
+  unsigned long long run = part[tid] - sum;
+#pragma unroll
+  for (int j = 0; j < kPer; j++) {
+    const uint32_t b = (uint32_t)tid * kPer + j;
+    run += c[j];
+    if (b < kFxBins) pre[b] = run;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ uint32_t first_reaching(const unsigned long long* P, unsigned long long x) {
+  uint32_t a = 0, b = kFxBins - 1;  // smallest b with P[b] >= x
+  while (a < b) {
+    const uint32_t m = (a + b) / 2;
+    if (P[m] >= x) b = m; else a = m + 1;
+  }
+  return a;
+}
+
+// One CTA: targets, and per quantity the merged bin intervals the sample points at.
 __global__ void __launch_bounds__(1024) sel_plan_sampled(SelState* st, SampState* ss,
-                                                         const uint64_t* __restrict__ partials,
+                                                         const uint64_t* __restrict__ partials, uint32_t nb,
                                                          const uint32_t* __restrict__ shist,
                                                          const uint64_t* __restrict__ mm, PctArg pct,
                                                          uint32_t npct, double dmul, double dadd) {
   __shared__ unsigned long long pre[2][kFxBins];
-  __shared__ unsigned long long part_sum[1024];
-  __shared__ uint64_t tlo[kMaxT], thi[kMaxT], tk[kMaxT];
+  __shared__ unsigned long long part[1024];
+  __shared__ uint32_t tb1[kMaxT], tb2[kMaxT];
   const int tid = threadIdx.x;
   const uint64_t n_def = partials[LSCAT_P_RATIO_DEFINED];
-  constexpr int kPer = (kFxBins + 1023) / 1024;
-  for (int w = 0; w < 2; w++) {  // inclusive scan of the sample histogram
-    unsigned long long c[kPer], sum = 0;
-#pragma unroll
-    for (int j = 0; j < kPer; j++) {
-      const uint32_t b = (uint32_t)tid * kPer + j;
-      c[j] = b < kFxBins ? shist[(size_t)w * kFxBins + b] : 0ull;
-      sum += c[j];
-    }
-    part_sum[tid] = sum;
-    __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {
-      const unsigned long long y = tid >= o ? part_sum[tid - o] : 0ull;
-      __syncthreads();
-      part_sum[tid] += y;
-      __syncthreads();
-    }
-    unsigned long long run = part_sum[tid] - sum;
-#pragma unroll
-    for (int j = 0; j < kPer; j++) {
-      const uint32_t b = (uint32_t)tid * kPer + j;
-      run += c[j];
-      if (b < kFxBins) pre[w][b] = run;
-    }
-    __syncthreads();
-  }
+  // the single-valued bins are left out of the scan (0): the targets' sample ranks are shifted
+  // past them below
+  for (uint32_t w = 0; w < 2; w++) scan_bins(shist + w * kFxBins, 0ull, w, pre[w], part);
   if (tid == 0) {
     st->nt = 2 * npct;
     st->err = 0;
@@ -723,184 +741,203 @@ __global__ void __launch_bounds__(1024) sel_plan_sampled(SelState* st, SampState
     t.hi = mm[2 * t.which + 1];
     t.count = n_def;
     st->t[tid] = t;
-    tk[tid] = t.k;
+    // sample bins of the target's sample-rank window (sample counts of the single-valued bins
+    // included: they sit in shist like any bin)
+    uint32_t b1 = 1, b2 = 0;  // empty
     const unsigned long long* P = pre[t.which];
-    const double ns = (double)P[kFxBins - 1];
-    uint64_t lo = t.lo, hi = t.hi;
+    const uint32_t w = t.which;
+    const unsigned long long ns = P[kFxBins - 1] + shist[w * kFxBins + (w == 0 ? kFxBins - 2 : 0)];
     if (!t.done && ns > 0) {
-      const double ks = (double)t.k * ns / (double)n_def;
+      const unsigned long long vs = shist[w * kFxBins + (w == 0 ? kFxBins - 2 : 0)];
+      const double ks = (double)t.k * (double)ns / (double)n_def;
       const double d = dmul * sqrt(ks > 1.0 ? ks : 1.0) + dadd;
-      const unsigned long long s_lo = (unsigned long long)fmax(1.0, floor(ks - d));
-      const unsigned long long s_hi = (unsigned long long)fmin(ns, ceil(ks + d));
-      auto first_reaching = [&](unsigned long long x) {  // smallest b with P[b] >= x
-        uint32_t a = 0, b = kFxBins - 1;
-        while (a < b) {
-          const uint32_t m = (a + b) / 2;
-          if (P[m] >= x) b = m; else a = m + 1;
-        }
-        return a;
-      };
-      const uint32_t b1 = first_reaching(s_lo), b2 = first_reaching(s_hi);
-      uint64_t l1, h1, l2, h2;
-      fx_bin_range(t.which, b1, &l1, &h1);
-      fx_bin_range(t.which, b2, &l2, &h2);
-      lo = l1 > lo ? l1 : lo;
-      hi = h2 < hi ? h2 : hi;
+      // sample ranks among the counted keys: the single-valued bin sits first (gain == 0) or
+      // last (perf == 1) in key order
+      const double off = w == 1 ? (double)vs : 0.0;
+      const double s_lo = fmax(1.0, floor(ks - d - off)), s_hi = fmax(1.0, ceil(ks + d - off));
+      const unsigned long long total = P[kFxBins - 1];
+      if (total > 0) {
+        b1 = first_reaching(P, (unsigned long long)fmin(s_lo, (double)total));
+        b2 = first_reaching(P, (unsigned long long)fmin(s_hi, (double)total));
+      }
     }
-    tlo[tid] = lo;
-    thi[tid] = hi;
+    tb1[tid] = b1;
+    tb2[tid] = b2;
   }
   __syncthreads();
-  if (tid == 0) {  // per quantity: sort the targets' intervals by lo, merge overlapping ones
+  if (tid == 0) {  // per quantity: sort the targets' bin intervals, merge overlapping ones
     bool fail = false;
     for (uint32_t w = 0; w < 2; w++) {
       uint32_t idx[kMaxT / 2], n = 0;
-      for (uint32_t i = 0; i < npct; i++) idx[n++] = w * npct + i;
+      for (uint32_t i = 0; i < npct; i++)
+        if (tb1[w * npct + i] <= tb2[w * npct + i]) idx[n++] = w * npct + i;
       for (uint32_t a = 1; a < n; a++)
-        for (uint32_t b = a; b > 0 && tlo[idx[b]] < tlo[idx[b - 1]]; b--) {
+        for (uint32_t b = a; b > 0 && tb1[idx[b]] < tb1[idx[b - 1]]; b--) {
           const uint32_t x = idx[b]; idx[b] = idx[b - 1]; idx[b - 1] = x;
         }
       uint32_t m = 0;
       for (uint32_t a = 0; a < n; a++) {
         const uint32_t i = idx[a];
-        if (m > 0 && tlo[i] <= ss->hi[w][m - 1] + 1) {
-          if (thi[i] > ss->hi[w][m - 1]) ss->hi[w][m - 1] = thi[i];
+        if (m > 0 && tb1[i] <= ss->b2[w][m - 1] + 1) {
+          if (tb2[i] > ss->b2[w][m - 1]) ss->b2[w][m - 1] = tb2[i];
         } else {
           if (m == kIvQ) { fail = true; break; }
-          ss->lo[w][m] = tlo[i];
-          ss->hi[w][m] = thi[i];
+          ss->b1[w][m] = tb1[i];
+          ss->b2[w][m] = tb2[i];
           m++;
         }
-        ss->tiv[i] = m - 1;
       }
       ss->niv[w] = m;
-      for (uint32_t r = 0; r < kIvQ; r++) { ss->cge[w][r] = 0; ss->cin[w][r] = 0; }
-      ss->scanned[w] = 0;
       ss->ncopy_all[w] = 0;
       ss->ncopy[w] = 0;
     }
     if (fail) ss->fail = 1;
   }
-  (void)tk;
+  for (uint32_t i = tid; i < 2 * kFxBins; i += blockDim.x) (&ss->fh[0][0])[i] = 0;
+  (void)nb;
 }
 
-// One pass over this rank's keys: count keys >= lo and inside [lo, hi] of every interval of
-// their quantity, copy the keys inside multi-valued intervals to cbuf (warp-aggregated).
+// One pass over this rank's keys: exact counts of the counted bins (privatised in shared
+// memory) and copies of the keys in the sample's bin intervals (staged per CTA in shared
+// memory, flushed with one global reservation per CTA and quantity whenever a stage fills).
 template <int kT>
-__global__ void __launch_bounds__(kT, 2) sel_pass_sampled(const double* __restrict__ perf,
-                                                          const double* __restrict__ gain, uint64_t lo,
-                                                          uint64_t hi, SampState* __restrict__ ss,
-                                                          double* __restrict__ cbuf) {
-  __shared__ uint64_t s_lo[2][kIvQ], s_hi[2][kIvQ];
-  __shared__ uint32_t s_n[2];
-  if (threadIdx.x < 2) s_n[threadIdx.x] = ss->fail ? 0u : ss->niv[threadIdx.x];
-  if (threadIdx.x < 2 * kIvQ) {
-    const int w = threadIdx.x / kIvQ, r = threadIdx.x % kIvQ;
-    s_lo[w][r] = ss->lo[w][r];
-    s_hi[w][r] = ss->hi[w][r];
-  }
+__global__ void __launch_bounds__(kT) sel_pass_sampled(const double* __restrict__ perf,
+                                                       const double* __restrict__ gain, uint64_t lo,
+                                                       uint64_t hi, SampState* __restrict__ ss,
+                                                       double* __restrict__ cbuf) {
+  constexpr int kU = 4;
+  __shared__ uint32_t h[2 * kFxBins];
+  __shared__ uint8_t cmap[2 * kFxBins];
+  __shared__ uint64_t stage[2][kCopyStage];
+  __shared__ uint32_t s_nc[2];
+  __shared__ unsigned long long s_base[2];
+  const bool on = !ss->fail;
+  for (uint32_t i = threadIdx.x; i < 2 * kFxBins; i += kT) { h[i] = 0; cmap[i] = 0; }
+  if (threadIdx.x < 2) s_nc[threadIdx.x] = 0;
   __syncthreads();
-  const uint32_t n0 = s_n[0], n1 = s_n[1];
-  if (n0 == 0 && n1 == 0) return;
+  if (on)
+    for (uint32_t w = 0; w < 2; w++)
+      for (uint32_t r = 0; r < ss->niv[w]; r++)
+        for (uint32_t b = ss->b1[w][r] + threadIdx.x; b <= ss->b2[w][r]; b += kT)
+          cmap[w * kFxBins + b] = !virtual_bin(w, b);
+  __syncthreads();
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
-  uint32_t cge[2][kIvQ] = {}, cin[2][kIvQ] = {};
-  uint32_t scanned = 0;
-  constexpr int kU = 4;
-  const uint64_t wstride = (uint64_t)gridDim.x * kT * kU;
-  for (uint64_t base = lo + (blockIdx.x * (uint64_t)kT + (threadIdx.x & ~31u)) * kU; base < hi; base += wstride) {
+  auto flush = [&]() {  // CTA-wide: reserve once per quantity, copy the stage out
+    __syncthreads();
+    if (threadIdx.x < 2 && s_nc[threadIdx.x]) {
+      s_base[threadIdx.x] = atomicAdd(&ss->ncopy[threadIdx.x], (unsigned long long)s_nc[threadIdx.x]);
+      atomicAdd(&ss->ncopy_all[threadIdx.x], (unsigned long long)s_nc[threadIdx.x]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < 2; w++)
+      for (uint32_t i = threadIdx.x; i < s_nc[w]; i += kT) {
+        const unsigned long long g = s_base[w] + i;
+        if (g < kCompactCap) reinterpret_cast<uint64_t*>(cbuf)[(size_t)w * kCompactCap + g] = stage[w][i];
+      }
+    __syncthreads();
+    if (threadIdx.x < 2) s_nc[threadIdx.x] = 0;
+    __syncthreads();
+  };
+  const uint64_t cstride = (uint64_t)gridDim.x * kT * kU;
+  for (uint64_t base = lo + blockIdx.x * (uint64_t)kT * kU; base < hi; base += cstride) {
     uint64_t v[2][kU];
 #pragma unroll
     for (int w = 0; w < 2; w++) {
-      const uint64_t* src = reinterpret_cast<const uint64_t*>(w ? gain : perf) + base + lane;
+      const uint64_t* src = reinterpret_cast<const uint64_t*>(w ? gain : perf);
 #pragma unroll
       for (int u = 0; u < kU; u++) {
-        const uint64_t i = base + lane + 32 * u;
-        v[w][u] = i < hi ? __ldg(src + 32 * u) : kNaNKey;
+        const uint64_t i = base + threadIdx.x + (uint64_t)kT * u;
+        v[w][u] = i < hi ? __ldcs(src + i) : kNaNKey;
       }
     }
 #pragma unroll
     for (int u = 0; u < kU; u++) {
-      const bool ok = base + lane + 32 * u < hi;  // lanes past the end count nowhere
-      scanned += ok;
 #pragma unroll
       for (int w = 0; w < 2; w++) {
         const uint64_t k = v[w][u];
-        const uint32_t nw = w ? n1 : n0;
-        bool copy = false;
-#pragma unroll
-        for (int r = 0; r < kIvQ; r++) {
-          if (r >= (int)nw) break;
-          const bool ge = ok && k >= s_lo[w][r];
-          const bool in = ge && k <= s_hi[w][r];
-          cge[w][r] += ge;
-          cin[w][r] += in;
-          copy |= in && s_lo[w][r] != s_hi[w][r];
-        }
+        const bool counted = valid_key(k) && (w == 0 ? k < kPerfOne : k != 0);
+        const uint32_t b = counted ? fx_bin(w, k) : 0u;
+        if (counted) atomicAdd(&h[w * kFxBins + b], 1u);
+        const bool copy = on && counted && cmap[w * kFxBins + b];
         const unsigned m = __ballot_sync(FULL, copy);
         if (m) {
           const int leader = __ffs(m) - 1;
-          unsigned long long at = 0;
-          if (lane == leader) {
-            at = atomicAdd(&ss->ncopy[w], (unsigned long long)__popc(m));
-            atomicAdd(&ss->ncopy_all[w], (unsigned long long)__popc(m));
-          }
+          uint32_t at = 0;
+          if (lane == leader) at = atomicAdd(&s_nc[w], (uint32_t)__popc(m));
           at = __shfl_sync(FULL, at, leader) + __popc(m & ((1u << lane) - 1u));
-          if (copy && at < kCompactCap) reinterpret_cast<uint64_t*>(cbuf)[(size_t)w * kCompactCap + at] = k;
+          if (copy) {
+            if (at < kCopyStage) {
+              stage[w][at] = k;
+            } else {  // stage full (cannot happen: flushed below before a tile can overfill it)
+              const unsigned long long g = atomicAdd(&ss->ncopy[w], 1ull);
+              atomicAdd(&ss->ncopy_all[w], 1ull);
+              if (g < kCompactCap) reinterpret_cast<uint64_t*>(cbuf)[(size_t)w * kCompactCap + g] = k;
+            }
+          }
         }
       }
     }
+    __syncthreads();
+    const bool full = s_nc[0] > kCopyStage - kT * kU || s_nc[1] > kCopyStage - kT * kU;
+    if (full) flush();  // CTA-uniform
   }
-  // the counters: warp sums, one atomic per warp and counter
-#pragma unroll
-  for (int w = 0; w < 2; w++)
-#pragma unroll
-    for (int r = 0; r < kIvQ; r++) {
-      const uint32_t a = __reduce_add_sync(FULL, cge[w][r]), b = __reduce_add_sync(FULL, cin[w][r]);
-      if (lane == 0 && a) atomicAdd(&ss->cge[w][r], (unsigned long long)a);
-      if (lane == 0 && b) atomicAdd(&ss->cin[w][r], (unsigned long long)b);
-    }
-  const uint32_t sc = __reduce_add_sync(FULL, scanned);
-  if (lane == 0 && sc) {
-    atomicAdd(&ss->scanned[0], (unsigned long long)sc);
-    atomicAdd(&ss->scanned[1], (unsigned long long)sc);
-  }
+  flush();
+  for (uint32_t i = threadIdx.x; i < 2 * kFxBins; i += kT)
+    if (h[i]) atomicAdd(&ss->fh[0][0] + i, h[i]);
 }
 
-// One CTA: exact ranks inside the intervals.  A target whose rank is not inside its interval
-// (a sampling miss) or copies beyond the buffer -> sampled_fail (the host restarts on the
-// histogram path).  Otherwise every target gets its interval, rank and count, the passes read
-// the copies from now on, and the open targets are planned into ranges.
-__global__ void __launch_bounds__(kMaxT) sel_check_sampled(SelState* st, SampState* ss, uint32_t cap) {
-  const int i = threadIdx.x;
+// One CTA of 1024: the exact histogram narrows every target to one bin; a bin that was not
+// copied (a sampling miss) or copies beyond the buffer -> sampled_fail (the host restarts on
+// the histogram path).  Otherwise the passes read the copies from now on and the open
+// targets are planned into ranges.
+__global__ void __launch_bounds__(1024) sel_check_sampled(SelState* st, SampState* ss,
+                                                          const uint64_t* __restrict__ partials,
+                                                          uint32_t nb, const uint64_t* __restrict__ mm,
+                                                          uint32_t cap, uint32_t force_miss) {
+  __shared__ unsigned long long pre[2][kFxBins];
+  __shared__ unsigned long long part[1024];
   __shared__ uint32_t s_fail;
-  if (i == 0) s_fail = ss->fail || ss->ncopy_all[0] > kCompactCap || ss->ncopy_all[1] > kCompactCap;
+  const int tid = threadIdx.x;
+  const unsigned long long n_one = partials[LSCAT_P_NCOUNTERS + nb];  // perf == 1 <=> gain == 0
+  for (uint32_t w = 0; w < 2; w++) scan_bins(ss->fh[w], n_one, w, pre[w], part);
+  if (tid == 0)
+    s_fail = force_miss || ss->fail || ss->ncopy_all[0] > kCompactCap || ss->ncopy_all[1] > kCompactCap ||
+             pre[0][kFxBins - 1] != st->n_def || pre[1][kFxBins - 1] != st->n_def;
   __syncthreads();
-  if (i < (int)st->nt && !s_fail) {
-    Tgt& t = st->t[i];
+  if (tid < (int)st->nt && !s_fail) {
+    Tgt& t = st->t[tid];
     if (!t.done) {
-      const uint32_t w = t.which, r = ss->tiv[i];
-      const unsigned long long below = ss->scanned[w] - ss->cge[w][r], in = ss->cin[w][r];
-      if (!(below < t.k && t.k <= below + in)) {
+      const uint32_t w = t.which;
+      const unsigned long long* P = pre[w];
+      const uint32_t b = first_reaching(P, t.k);
+      const unsigned long long below = b ? P[b - 1] : 0ull;
+      uint64_t blo, bhi;
+      fx_bin_range(w, b, &blo, &bhi);
+      const uint64_t lo = blo > mm[2 * w] ? blo : mm[2 * w], hi = bhi < mm[2 * w + 1] ? bhi : mm[2 * w + 1];
+      bool copied = virtual_bin(w, b);  // single-valued: decided without copies
+      for (uint32_t r = 0; r < ss->niv[w]; r++) copied |= ss->b1[w][r] <= b && b <= ss->b2[w][r];
+      if (!copied) {
         atomicOr(&s_fail, 1u);
       } else {
-        t.lo = ss->lo[w][r];
-        t.hi = ss->hi[w][r];
+        t.lo = lo;
+        t.hi = hi;
         t.k -= below;
-        t.count = in;
+        t.count = P[b] - below;
       }
     }
   }
   __syncthreads();
   if (s_fail) {
-    if (i == 0) {  // no open ranges: the levels queued behind this are no-ops
+    if (tid == 0) {  // no open ranges: the levels queued behind this are no-ops
       st->sampled_fail = 1;
       st->nr = 0;
       st->open = 0;
     }
     return;
   }
-  if (i == 0) {
+  if (tid == 0) {
     st->src = 1;  // the later passes read the copies
     st->nc[0] = ss->ncopy[0];
     st->nc[1] = ss->ncopy[1];
@@ -996,16 +1033,22 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
   uint32_t* shist = (uint32_t*)scratch(ctx, "sel_shist", 2 * kFxBins * 4, &err);
   if (err) return cuda_fail(ctx, err, "stats: scratch");
   static const bool no_sample = getenv("LSCAT_SEL_NOSAMPLE") != nullptr;
-  // interval half-width in sample ranks: dmul sqrt(rank) + dadd (LSCAT_SEL_SAMPLE_DELTA=0 makes
-  // it 0: single bins, sampling misses -- the tests use it to exercise the fallback)
-  static const bool zero_delta = getenv("LSCAT_SEL_SAMPLE_DELTA") && atof(getenv("LSCAT_SEL_SAMPLE_DELTA")) == 0.0;
-  const double dmul = zero_delta ? 0.0 : 6.0, dadd = zero_delta ? 0.0 : 64.0;
+  // interval half-width in sample ranks: dmul sqrt(rank) + dadd
+  // LSCAT_SEL_FORCE_MISS=1 (tests): every sampled first level reports a miss, exercising the
+  // restart on the histogram path
+  static const bool force_miss = getenv("LSCAT_SEL_FORCE_MISS") != nullptr;
+  const double dmul = 4.5, dadd = 32.0;
   bool sampled = !small && npct <= (uint32_t)kIvQ && !no_sample;
   const uint64_t stride = std::max<uint64_t>(1, n / kSampleKeys) | 1;  // odd: no period-2^k alias
   const int grid_s = (int)std::min<uint64_t>(std::max<uint64_t>(1, (n / stride + 255) / 256),
                                              (uint64_t)ctx->sm_count * 4);
+  static int occ_p = 0;  // resident CTAs per SM of the sampled pass (binary property)
+  if (!occ_p) {
+    LSCAT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, sel_pass_sampled<256>, 256, 0));
+    occ_p = std::max(occ_p, 1);
+  }
   const int grid_p = (int)std::min<uint64_t>(std::max<uint64_t>(1, (n + 256 * 4 - 1) / (256 * 4)),
-                                             (uint64_t)ctx->sm_count * 2);
+                                             (uint64_t)ctx->sm_count * occ_p);
   auto enqueue_first_sampled = [&](cudaStream_t q) -> lscat_status {
     LSCAT_CUDA(ctx, cudaMemsetAsync(hist, 0, (size_t)kMaxR * kBins * 4, q));
     LSCAT_CUDA(ctx, cudaMemsetAsync(cand, 0, (size_t)kMaxR * 8, q));
@@ -1016,15 +1059,18 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
       lscat_status ns = ctx->comm->allreduce(ctx, {{shist, 2 * (size_t)kFxBins, DT::U32, Op::Sum}}, q);
       if (ns) return ns;
     }
-    sel_plan_sampled<<<1, 1024, 0, q>>>(st, ss, rs.partials, shist, rs.minmax, pa, npct, dmul, dadd);
+    sel_plan_sampled<<<1, 1024, 0, q>>>(st, ss, rs.partials, rs.opts.bins_per_unit, shist, rs.minmax, pa,
+                                        npct, dmul, dadd);
     LSCAT_CUDA(ctx, cudaGetLastError());
     sel_pass_sampled<256><<<grid_p, 256, 0, q>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, ss, cbuf);
     LSCAT_CUDA(ctx, cudaGetLastError());
-    if (world > 1) {  // cge, cin, scanned, ncopy_all: contiguous u64 counters
-      lscat_status ns = ctx->comm->allreduce(ctx, {{&ss->cge[0][0], 4 * kIvQ + 4, DT::U64, Op::Sum}}, q);
+    if (world > 1) {  // the exact bin counts and the copy totals over all ranks
+      lscat_status ns = ctx->comm->allreduce(ctx, {{&ss->fh[0][0], 2 * (size_t)kFxBins, DT::U32, Op::Sum},
+                                                   {&ss->ncopy_all[0], 2, DT::U64, Op::Sum}}, q);
       if (ns) return ns;
     }
-    sel_check_sampled<<<1, kMaxT, 0, q>>>(st, ss, cap);
+    sel_check_sampled<<<1, 1024, 0, q>>>(st, ss, rs.partials, rs.opts.bins_per_unit, rs.minmax, cap,
+                                         force_miss ? 1u : 0u);
     LSCAT_CUDA(ctx, cudaGetLastError());
     return enqueue_levels(q, false);
   };

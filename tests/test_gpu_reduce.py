@@ -524,9 +524,8 @@ def test_percentiles_sampled_first_level():
 
 
 def test_percentiles_sampled_fallback():
-    """A zero-width sample interval (LSCAT_SEL_SAMPLE_DELTA=0) makes targets miss their
-    interval: the selection restarts on the histogram path and stays exact (child process: the
-    switch is read once)."""
+    """A sampling miss (forced: LSCAT_SEL_FORCE_MISS=1) restarts the selection on the histogram
+    path, which stays exact (child process: the switch is read once)."""
     import os
     import subprocess
     import sys
@@ -538,7 +537,7 @@ def test_percentiles_sampled_fallback():
         "_compare(t, pcts=[0.01, 0.1, 0.5, 0.9, 0.99])\n"
         "print('ok')\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, LSCAT_SEL_SAMPLE_DELTA="0", LSCAT_SEL_DEBUG="1")
+    env = dict(os.environ, LSCAT_SEL_FORCE_MISS="1", LSCAT_SEL_DEBUG="1")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
