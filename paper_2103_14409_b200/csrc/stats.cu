@@ -652,13 +652,20 @@ __global__ void __launch_bounds__(256) sel_sample_hist(const double* __restrict_
   __shared__ uint32_t h[2 * kFxBins];
   for (uint32_t i = threadIdx.x; i < 2 * kFxBins; i += blockDim.x) h[i] = 0;
   __syncthreads();
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;; j += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t i = lo + j * stride;
-    if (i >= hi) break;
-    const uint64_t kp = (uint64_t)__double_as_longlong(__ldcs(perf + i));
-    const uint64_t kg = (uint64_t)__double_as_longlong(__ldcs(gain + i));
-    if (valid_key(kp)) atomicAdd(&h[fx_perf_bin(kp)], 1u);
-    if (valid_key(kg)) atomicAdd(&h[kFxBins + fx_gain_bin(kg)], 1u);
+  const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; lo + j * stride < hi; j += 4 * T) {
+    uint64_t kp[4], kg[4];  // four independent samples in flight per thread
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const uint64_t i = lo + (j + u * T) * stride;
+      kp[u] = i < hi ? (uint64_t)__double_as_longlong(__ldcs(perf + i)) : kNaNKey;
+      kg[u] = i < hi ? (uint64_t)__double_as_longlong(__ldcs(gain + i)) : kNaNKey;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      if (valid_key(kp[u])) atomicAdd(&h[fx_perf_bin(kp[u])], 1u);
+      if (valid_key(kg[u])) atomicAdd(&h[kFxBins + fx_gain_bin(kg[u])], 1u);
+    }
   }
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < 2 * kFxBins; i += blockDim.x)
@@ -805,7 +812,9 @@ __global__ void __launch_bounds__(kT) sel_pass_sampled(const double* __restrict_
                                                        const double* __restrict__ gain, uint64_t lo,
                                                        uint64_t hi, SampState* __restrict__ ss,
                                                        double* __restrict__ cbuf) {
-  constexpr int kU = 4;
+  constexpr int kU = 8;
+  constexpr int kTilesPerCheck = 4;  // stage checked every 4 tiles (copies are ~5 % of keys;
+                                     // a stage that fills in between spills to global atomics)
   __shared__ uint32_t h[2 * kFxBins];
   __shared__ uint8_t cmap[2 * kFxBins];
   __shared__ uint64_t stage[2][kCopyStage];
@@ -841,7 +850,8 @@ __global__ void __launch_bounds__(kT) sel_pass_sampled(const double* __restrict_
     __syncthreads();
   };
   const uint64_t cstride = (uint64_t)gridDim.x * kT * kU;
-  for (uint64_t base = lo + blockIdx.x * (uint64_t)kT * kU; base < hi; base += cstride) {
+  int tile = 0;
+  for (uint64_t base = lo + blockIdx.x * (uint64_t)kT * kU; base < hi; base += cstride, tile++) {
     uint64_t v[2][kU];
 #pragma unroll
     for (int w = 0; w < 2; w++) {
@@ -870,7 +880,7 @@ __global__ void __launch_bounds__(kT) sel_pass_sampled(const double* __restrict_
           if (copy) {
             if (at < kCopyStage) {
               stage[w][at] = k;
-            } else {  // stage full (cannot happen: flushed below before a tile can overfill it)
+            } else {  // stage full between two checks: straight to the global buffer
               const unsigned long long g = atomicAdd(&ss->ncopy[w], 1ull);
               atomicAdd(&ss->ncopy_all[w], 1ull);
               if (g < kCompactCap) reinterpret_cast<uint64_t*>(cbuf)[(size_t)w * kCompactCap + g] = k;
@@ -879,9 +889,11 @@ __global__ void __launch_bounds__(kT) sel_pass_sampled(const double* __restrict_
         }
       }
     }
-    __syncthreads();
-    const bool full = s_nc[0] > kCopyStage - kT * kU || s_nc[1] > kCopyStage - kT * kU;
-    if (full) flush();  // CTA-uniform
+    if (tile % kTilesPerCheck == kTilesPerCheck - 1) {
+      __syncthreads();
+      const bool full = s_nc[0] > kCopyStage / 2 || s_nc[1] > kCopyStage / 2;
+      if (full) flush();  // CTA-uniform
+    }
   }
   flush();
   for (uint32_t i = threadIdx.x; i < 2 * kFxBins; i += kT)
@@ -1040,14 +1052,14 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
   const double dmul = 4.5, dadd = 32.0;
   bool sampled = !small && npct <= (uint32_t)kIvQ && !no_sample;
   const uint64_t stride = std::max<uint64_t>(1, n / kSampleKeys) | 1;  // odd: no period-2^k alias
-  const int grid_s = (int)std::min<uint64_t>(std::max<uint64_t>(1, (n / stride + 255) / 256),
-                                             (uint64_t)ctx->sm_count * 4);
+  const int grid_s = (int)std::min<uint64_t>(std::max<uint64_t>(1, (n / stride + 1023) / 1024),
+                                             (uint64_t)ctx->sm_count * 8);
   static int occ_p = 0;  // resident CTAs per SM of the sampled pass (binary property)
   if (!occ_p) {
     LSCAT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, sel_pass_sampled<256>, 256, 0));
     occ_p = std::max(occ_p, 1);
   }
-  const int grid_p = (int)std::min<uint64_t>(std::max<uint64_t>(1, (n + 256 * 4 - 1) / (256 * 4)),
+  const int grid_p = (int)std::min<uint64_t>(std::max<uint64_t>(1, (n + 256 * 8 - 1) / (256 * 8)),
                                              (uint64_t)ctx->sm_count * occ_p);
   auto enqueue_first_sampled = [&](cudaStream_t q) -> lscat_status {
     LSCAT_CUDA(ctx, cudaMemsetAsync(hist, 0, (size_t)kMaxR * kBins * 4, q));
