@@ -29,6 +29,16 @@ __host__ __device__ __forceinline__ uint32_t fx_gain_bin(uint64_t k) {
   if (k == 0) return 0u;
   return k < kGainLo ? 1u : (k >= kGainHi ? kFxBins - 1 : 2u + (uint32_t)((k >> kGainShift) - (kGainLo >> kGainShift)));
 }
+// the same bins from the key's high 32 bits (every bin edge lies on a multiple of 2^42): the
+// selection pass bins in 32-bit arithmetic.  Valid only for keys of the counted bins.
+__host__ __device__ __forceinline__ uint32_t fx_perf_bin_hi(uint32_t h) {
+  return h < (uint32_t)(kPerfLo >> 32) ? 0u : 1u + ((h >> (kPerfShift - 32)) - (uint32_t)(kPerfLo >> kPerfShift));
+}
+__host__ __device__ __forceinline__ uint32_t fx_gain_bin_hi(uint32_t h) {
+  return h < (uint32_t)(kGainLo >> 32) ? 1u
+         : (h >= (uint32_t)(kGainHi >> 32) ? kFxBins - 1 : 2u + ((h >> (kGainShift - 32)) - (uint32_t)(kGainLo >> kGainShift)));
+}
+
 // inclusive key range of bin b of quantity w (0 perf, 1 gain), before clipping to [min, max]
 __host__ __device__ __forceinline__ void fx_bin_range(uint32_t w, uint32_t b, uint64_t* lo, uint64_t* hi) {
   if (w == 0) {

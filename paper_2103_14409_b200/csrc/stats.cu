@@ -867,8 +867,10 @@ __global__ void __launch_bounds__(kT) sel_pass_sampled(const double* __restrict_
 #pragma unroll
       for (int w = 0; w < 2; w++) {
         const uint64_t k = v[w][u];
-        const bool counted = valid_key(k) && (w == 0 ? k < kPerfOne : k != 0);
-        const uint32_t b = counted ? fx_bin(w, k) : 0u;
+        const uint32_t kh = (uint32_t)(k >> 32);  // bins from the high word (32-bit arithmetic)
+        // perf < 1 (and not NaN) / gain > 0 (no gain is below 2^-32 but 0) and not NaN
+        const bool counted = w == 0 ? kh < (uint32_t)(kPerfOne >> 32) : (kh != 0 && kh < 0x7FF00000u);
+        const uint32_t b = counted ? (w == 0 ? fx_perf_bin_hi(kh) : fx_gain_bin_hi(kh)) : 0u;
         if (counted) atomicAdd(&h[w * kFxBins + b], 1u);
         const bool copy = on && counted && cmap[w * kFxBins + b];
         const unsigned m = __ballot_sync(FULL, copy);
