@@ -31,4 +31,6 @@ for mode, l2 in (("warm", L.L2_WARM), ("cold", L.L2_ROTATE)):
         v = rt[i * 32:(i + 1) * 32]
         out[f"{mode}_{n}"] = {"min": round(float(v.min()), 2), "mean": round(float(v.mean()), 2),
                               "max": round(float(v.max()), 2)}
+        if os.environ.get("AB_BY_BLOCK"):
+            out[f"{mode}_{n}"]["by_block"] = [round(float(x), 2) for x in v]
 print(json.dumps(out))

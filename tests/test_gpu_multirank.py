@@ -121,3 +121,68 @@ def test_sampled_selection_multirank(world, point):
 
     res = _run_ranks(world, make, dict(point_sharded=1) if point else {}, f"smp{world}{int(point)}")
     _check(res, ref)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_point_sharded_sweep_then_reduce(world):
+    """a2 -> a9 end to end at world > 1 (local transport, ranks = threads on one GPU): every rank
+    sweeps the points the LPT plan gives it, reduces its point-sharded table with the per-group
+    merge, and every rank's statistics equal the oracle on the union of the ranks' rows."""
+    require_gpu()
+    import torch
+    import importlib
+    importlib.import_module("paper_2103_14409_b200.build").build()
+    import paper_2103_14409_b200 as L
+    ks = [L.K_EUCLID, L.K_MATVEC, L.K_AXPY]
+    ns = [64, 128, 256]
+    bs = [32, 64, 128, 256, 512, 1024]
+    results, tables, errors = [None] * world, [None] * world, []
+
+    def rank_main(r):
+        try:
+            torch.cuda.set_device(0)
+            ctx = L.Ctx(0)
+            ctx.comm_init_local(f"sw{world}", r, world)
+            ctx.register_suite(ks, ns)
+            tab = ctx.sweep(ks, ns, bs, warmup=1, brackets=3, launches=10)
+            tables[r] = tab.to_numpy()
+            o = L.reduce_opts(len(bs), len(ns), point_sharded=1)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                ctx.reduce_table(tab, o, per_group=False, stream=s)
+                st = ctx.stats(o, percentiles=PCTS, stream=s)
+            s.synchronize()
+            results[r] = st
+            ctx.close()
+        except Exception as e:  # noqa: BLE001
+            errors.append((r, repr(e)))
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errors, errors
+    # the union table: every group's rows from all ranks, block ids ascending
+    G = len(ks) * len(ns)
+    assert sum(t["n_rows"] for t in tables) == G * len(bs)
+    rt, bid, off = [], [], [0]
+    for g in range(G):
+        rows = []
+        for t in tables:
+            a, b = t["group_offset"][g], t["group_offset"][g + 1]
+            rows += list(zip(t["block_id"][a:b], t["runtime_ms"][a:b]))
+        rows.sort()
+        assert [x[0] for x in rows] == list(range(len(bs)))      # every point swept exactly once
+        bid += [x[0] for x in rows]
+        rt += [x[1] for x in rows]
+        off.append(len(rt))
+    gm = np.tile(np.arange(len(ns), dtype=np.uint32), len(ks))
+    ref = OT.reduce_table(np.array(rt, np.float32), np.array(bid, np.uint16), np.array(off, np.int64),
+                          group_matrix=gm, opts=OT.Opts(n_blocks=len(bs), n_matrices=len(ns)),
+                          percentiles=PCTS)
+    for st in results:
+        for k, v in ref.counters.items():
+            assert st[k] == v, k
+        assert (st["best_block_hist"] == ref.best_block_hist).all()
+        assert st["pct_perf"] == ref.percentiles["perf"] and st["pct_gain"] == ref.percentiles["gain"]
