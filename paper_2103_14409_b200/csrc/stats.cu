@@ -24,6 +24,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "common.h"
 #include "selbins.h"
 
@@ -88,6 +90,22 @@ __device__ __forceinline__ int bin_of_d(const Range& R, uint64_t d) {
   if (d == R.span) return kBins - 1;
   if (d < R.g) return 1;
   return 2 + (int)((d - R.g) >> R.shift);
+}
+
+// inclusive key range of bin b of range R (the inverse of bin_of_d)
+__device__ __forceinline__ void bin_keys(const Range& R, int b, uint64_t* lo, uint64_t* hi) {
+  if (b == 0) {
+    *lo = *hi = R.lo;
+  } else if (b == kBins - 1) {
+    *lo = *hi = R.hi;
+  } else if (b == 1) {
+    *lo = R.lo + 1;
+    *hi = R.base - 1;
+  } else {
+    *lo = R.base + ((uint64_t)(b - 2) << R.shift);
+    const uint64_t top = R.base + ((uint64_t)(b - 1) << R.shift) - 1;  // may wrap only past hi
+    *hi = (top < *lo || top > R.hi - 1) ? R.hi - 1 : top;
+  }
 }
 
 __device__ Range make_range(uint64_t lo, uint64_t hi, uint64_t count, uint32_t which, uint32_t cap) {
@@ -539,18 +557,7 @@ __device__ void resolve_range(SelState* st, uint32_t* __restrict__ hist,
       const int b = tid * kPer + j;
       t.k = k - cum;
       t.count = c[j];
-      if (b == 0) {
-        t.lo = t.hi = R.lo;
-      } else if (b == kBins - 1) {
-        t.lo = t.hi = R.hi;
-      } else if (b == 1) {
-        t.lo = R.lo + 1;
-        t.hi = R.base - 1;
-      } else {
-        t.lo = R.base + ((uint64_t)(b - 2) << R.shift);
-        const uint64_t top = R.base + ((uint64_t)(b - 1) << R.shift) - 1;  // may wrap only past hi
-        t.hi = (top < t.lo || top > R.hi - 1) ? R.hi - 1 : top;
-      }
+      bin_keys(R, b, &t.lo, &t.hi);
     }
   } else {
     const size_t stride = (size_t)kMaxR * (cap + 1);
@@ -960,6 +967,178 @@ __global__ void __launch_bounds__(1024) sel_check_sampled(SelState* st, SampStat
   plan_ranges(st, cap);
 }
 
+// ---- small inputs on one rank: the whole selection in one cooperative launch ------------
+// <= 2^20 keys per quantity (configs[2]/[3] have 0.07 / 0.16 M): the multi-kernel chain above
+// is latency bound (~7 dependent launches of 7-20 us each).  One cooperative kernel (one CTA
+// per SM, grid-wide barriers between the phases) does: level 0 (the same 8192-bin histogram
+// per quantity over [min, max], privatised per CTA), CTA 0 narrows every target to its bin,
+// a gather of the keys in those bins, one CTA per bin sorts them and picks the targets.  A bin
+// with more than kSmallCap keys sets `fail` and the host runs the chain instead.
+constexpr uint32_t kSmallCap = 8192;  // keys per bin sorted by one CTA (64 KB of smem)
+
+struct SmallSel {
+  uint32_t hist[2][kBins];             // level-0 histograms (atomics from every CTA)
+  unsigned long long rcnt[kMaxT];      // keys gathered per range
+  uint64_t rlo[kMaxT], rhi[kMaxT];     // ranges = the targets' distinct bins
+  uint32_t rwhich[kMaxT];
+  uint64_t tk[kMaxT], tkey[kMaxT];     // per target: rank inside its range, result key
+  uint32_t trange[kMaxT], tdone[kMaxT];
+  uint32_t nr, fail;
+};
+
+__global__ void __launch_bounds__(1024, 1) sel_small(const double* __restrict__ perf,
+                                                     const double* __restrict__ gain, uint64_t lo,
+                                                     uint64_t hi, const uint64_t* __restrict__ partials,
+                                                     const uint64_t* __restrict__ mm, PctArg pct,
+                                                     uint32_t npct, SmallSel* __restrict__ ss,
+                                                     unsigned long long* __restrict__ cand) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ unsigned long long dsm[];  // 64 KB: histograms (u32), prefix (u32), sort (u64)
+  uint32_t* sh = reinterpret_cast<uint32_t*>(dsm);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const unsigned FULL = 0xffffffffu;
+  const uint64_t n_def = partials[LSCAT_P_RATIO_DEFINED];
+  const uint32_t nt = 2 * npct;
+  Range R[2];
+  for (uint32_t w = 0; w < 2; w++) R[w] = make_range(mm[2 * w], mm[2 * w + 1], n_def, w, kSmallCap);
+  const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+  // phase 1: level-0 histograms, privatised per CTA (a gather range needs none)
+  for (uint32_t i = tid; i < 2 * kBins; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  for (uint64_t g = lo + blockIdx.x * (uint64_t)blockDim.x + tid; g < hi; g += T) {
+#pragma unroll
+    for (int w = 0; w < 2; w++) {
+      const uint64_t k = (uint64_t)__double_as_longlong((w ? gain : perf)[g]);
+      const uint64_t d = k - R[w].lo;
+      if (!R[w].gather && d <= R[w].span) atomicAdd(&sh[w * kBins + bin_of_d(R[w], d)], 1u);
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = tid; i < 2 * kBins; i += blockDim.x)
+    if (sh[i]) atomicAdd(&ss->hist[0][0] + i, sh[i]);
+  grid.sync();
+  // phase 2 (CTA 0): every target to its bin; the distinct bins become the ranges
+  if (blockIdx.x == 0) {
+    __shared__ uint32_t wsum[32];
+    __shared__ uint64_t s_lo[kMaxT], s_hi[kMaxT], s_k[kMaxT];
+    __shared__ uint32_t s_done[kMaxT];
+    for (uint32_t w = 0; w < 2; w++) {  // inclusive scan of hist[w] into sh[w * kBins ..]
+      constexpr int kPer = kBins / 1024;
+      uint32_t c[kPer], sum = 0;
+#pragma unroll
+      for (int j = 0; j < kPer; j++) { c[j] = ss->hist[w][tid * kPer + j]; sum += c[j]; }
+      uint32_t inc = sum;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (lane == 31) wsum[tid >> 5] = inc;
+      __syncthreads();
+      if (tid < 32) {
+        uint32_t x = wsum[tid];
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(FULL, x, o);
+          if (tid >= o) x += y;
+        }
+        wsum[tid] = x;
+      }
+      __syncthreads();
+      uint32_t run = inc - sum + ((tid >> 5) ? wsum[(tid >> 5) - 1] : 0u);
+#pragma unroll
+      for (int j = 0; j < kPer; j++) { run += c[j]; sh[w * kBins + tid * kPer + j] = run; }
+      __syncthreads();
+    }
+    if (tid < (int)nt) {
+      const uint32_t w = tid >= (int)npct;
+      const double r = ceil(pct.p[tid % npct] * (double)n_def);  // nearest rank (R-13)
+      uint64_t k = r < 1.0 ? 1 : (r > (double)n_def ? n_def : (uint64_t)r);
+      uint64_t tlo = R[w].lo, thi = R[w].hi;
+      uint32_t done = n_def == 0;
+      if (!done && !R[w].gather) {
+        const uint32_t* P = sh + w * kBins;
+        uint32_t a = 0, b = kBins - 1;  // smallest bin with P[bin] >= k
+        while (a < b) {
+          const uint32_t m = (a + b) / 2;
+          if (P[m] >= k) b = m; else a = m + 1;
+        }
+        const uint32_t below = a ? P[a - 1] : 0u;
+        bin_keys(R[w], (int)a, &tlo, &thi);
+        if (P[a] - below > kSmallCap) atomicOr(&ss->fail, 1u);
+        k -= below;
+      }
+      if (!done && tlo == thi) done = 2;  // a single-valued bin: the key is known
+      s_lo[tid] = tlo; s_hi[tid] = thi; s_k[tid] = k; s_done[tid] = done;
+    }
+    __syncthreads();
+    if (tid == 0) {  // distinct (quantity, bin) -> range ids, in target order
+      uint32_t nr = 0;
+      for (uint32_t i = 0; i < nt; i++) {
+        const uint32_t w = i >= npct;
+        ss->tk[i] = s_k[i];
+        ss->tdone[i] = s_done[i];
+        ss->tkey[i] = s_done[i] == 2 ? s_lo[i] : kNaNKey;
+        if (s_done[i]) continue;
+        uint32_t r = 0;
+        while (r < nr && !(ss->rwhich[r] == w && ss->rlo[r] == s_lo[i] && ss->rhi[r] == s_hi[i])) r++;
+        if (r == nr) { ss->rwhich[r] = w; ss->rlo[r] = s_lo[i]; ss->rhi[r] = s_hi[i]; nr++; }
+        ss->trange[i] = r;
+      }
+      ss->nr = nr;
+    }
+  }
+  grid.sync();
+  // phase 3: gather the keys of the ranges (disjoint bins: at most one range per key)
+  const uint32_t nr = ss->fail ? 0u : ss->nr;
+  if (nr) {
+    for (uint64_t g0 = lo + blockIdx.x * (uint64_t)blockDim.x; g0 < hi; g0 += T) {
+      const uint64_t g = g0 + tid;
+#pragma unroll
+      for (int w = 0; w < 2; w++) {
+        const uint64_t k = g < hi ? (uint64_t)__double_as_longlong((w ? gain : perf)[g]) : kNaNKey;
+        uint32_t r = 0xFFFFFFFFu;
+        for (uint32_t q = 0; q < nr; q++)
+          if (ss->rwhich[q] == (uint32_t)w && ss->rlo[q] <= k && k <= ss->rhi[q]) r = q;
+        const unsigned peers = __match_any_sync(FULL, r);
+        const int leader = __ffs(peers) - 1;
+        unsigned long long base = 0;
+        if (r != 0xFFFFFFFFu && lane == leader) base = atomicAdd(&ss->rcnt[r], (unsigned long long)__popc(peers));
+        base = __shfl_sync(FULL, base, leader);
+        if (r != 0xFFFFFFFFu) {
+          const unsigned long long at = base + __popc(peers & ((1u << lane) - 1u));
+          if (at < kSmallCap) cand[(size_t)r * kSmallCap + at] = k;
+        }
+      }
+    }
+  }
+  grid.sync();
+  // phase 4: CTA r sorts range r's keys and picks its targets
+  if (blockIdx.x < nr) {
+    const uint32_t r = blockIdx.x;
+    const uint32_t n = (uint32_t)min(ss->rcnt[r], (unsigned long long)kSmallCap);
+    uint32_t P2 = 1;
+    while (P2 < n) P2 <<= 1;
+    for (uint32_t i = tid; i < P2; i += blockDim.x) dsm[i] = i < n ? cand[(size_t)r * kSmallCap + i] : ~0ull;
+    __syncthreads();
+    for (uint32_t kk = 2; kk <= P2; kk <<= 1)
+      for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+        for (uint32_t i = tid; i < P2; i += blockDim.x) {
+          const uint32_t ixj = i ^ j;
+          if (ixj > i) {
+            const unsigned long long a = dsm[i], b = dsm[ixj];
+            if ((a > b) == ((i & kk) == 0)) { dsm[i] = b; dsm[ixj] = a; }
+          }
+        }
+        __syncthreads();
+      }
+    if (tid < (int)nt && !ss->tdone[tid] && ss->trange[tid] == r) {
+      const uint64_t k = ss->tk[tid];
+      if (k >= 1 && k <= n) ss->tkey[tid] = dsm[k - 1];
+      else atomicOr(&ss->fail, 2u);  // keys lost: the host falls back
+    }
+  }
+}
+
 lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct, double* out_perf,
                                 double* out_gain, cudaStream_t s) {
   const ReduceState& rs = ctx->rs;
@@ -1013,9 +1192,48 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
                                                     (uint64_t)ctx->sm_count * occ1)
                           : (int)std::min<uint64_t>(std::max<uint64_t>(1, (n + kT1 * 8 - 1) / (kT1 * 8)),
                                                     (uint64_t)ctx->sm_count * occ1);
+  const int lpb = small ? kLevelsPerBatchSmall : kLevelsPerBatch;
   PctArg pa{};
   for (uint32_t i = 0; i < npct; i++) pa.p[i] = pct[i];
-  const int lpb = small ? kLevelsPerBatchSmall : kLevelsPerBatch;
+  static const bool no_small = getenv("LSCAT_SEL_NOSMALL") != nullptr;
+  if (small && world == 1 && !no_small && npct <= kMaxT / 2) {  // one cooperative launch
+    int coop = 0;
+    LSCAT_CUDA(ctx, cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device));
+    constexpr size_t kSmallSmem = (size_t)kSmallCap * 8;  // >= 2 x kBins x 4
+    static_assert(kSmallSmem >= 2 * kBins * 4, "sel_small shared memory");
+    if (coop) {
+      SmallSel* sm = (SmallSel*)scratch(ctx, "sel_small", sizeof(SmallSel), &err);
+      if (err) return cuda_fail(ctx, err, "stats: scratch");
+      auto* scand = (unsigned long long*)scratch(ctx, "sel_small_cand", (size_t)kMaxT * kSmallCap * 8, &err);
+      if (err) return cuda_fail(ctx, err, "stats: scratch");
+      SmallSel* hsm = (SmallSel*)pinned(ctx, "sel_small_h", sizeof(SmallSel), &err);
+      if (err) return cuda_fail(ctx, err, "stats: pinned");
+      LSCAT_CUDA(ctx, ensure_smem_attr((const void*)sel_small, kSmallSmem));
+      LSCAT_CUDA(ctx, cudaMemsetAsync(sm, 0, sizeof(SmallSel), s));
+      const double* perf_p = rs.perf;
+      const double* gain_p = rs.gain;
+      uint64_t lo_ = rs.own_lo, hi_ = rs.own_hi;
+      const uint64_t* part_p = rs.partials;
+      const uint64_t* mm_p = rs.minmax;
+      uint32_t np_ = npct;
+      void* args[] = {(void*)&perf_p, (void*)&gain_p, (void*)&lo_, (void*)&hi_, (void*)&part_p,
+                      (void*)&mm_p, (void*)&pa, (void*)&np_, (void*)&sm, (void*)&scand};
+      LSCAT_CUDA(ctx, cudaLaunchCooperativeKernel((const void*)sel_small, dim3(ctx->sm_count), dim3(1024), args,
+                                                  kSmallSmem, s));
+      ctx->launches++;
+      LSCAT_CUDA(ctx, cudaMemcpyAsync(hsm, sm, sizeof(SmallSel), cudaMemcpyDeviceToHost, s));
+      LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
+      if (!hsm->fail) {
+        for (uint32_t i = 0; i < 2 * npct; i++) {
+          double v;
+          memcpy(&v, &hsm->tkey[i], 8);
+          (i >= npct ? out_gain : out_perf)[i % npct] = v;
+        }
+        return LSCAT_OK;
+      }
+      ctx->sel_fallbacks++;  // a bin too large for one CTA: the multi-kernel chain below
+    }
+  }
   // One batch: lpb levels of pass -> (merge) -> resolve -> plan, then the state
   // is read back (one host sync per batch).
   auto enqueue_levels = [&](cudaStream_t q, bool first) -> lscat_status {
