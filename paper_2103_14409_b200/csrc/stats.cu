@@ -18,6 +18,7 @@
 // are summed and the gathered keys all-gathered between sel_pass and sel_resolve, so every
 // rank takes the same decisions.
 #include <algorithm>
+#include <cstddef>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -977,14 +978,16 @@ __global__ void __launch_bounds__(1024) sel_check_sampled(SelState* st, SampStat
 constexpr uint32_t kSmallCap = 8192;  // keys per bin sorted by one CTA (64 KB of smem)
 
 struct SmallSel {
+  // results first: the host copies back only this head
+  uint64_t tkey[kMaxT];                // per target: result key
+  uint32_t fail, nr;
+  // working state
   uint32_t hist[2][kBins];             // level-0 histograms (atomics from every CTA)
   unsigned long long rcnt[kMaxT];      // keys gathered per range
-  uint64_t rlo[kMaxT], rhi[kMaxT];     // ranges = the targets' distinct bins
-  uint32_t rwhich[kMaxT];
-  uint64_t tk[kMaxT], tkey[kMaxT];     // per target: rank inside its range, result key
+  uint64_t tk[kMaxT];                  // per target: rank inside its range
   uint32_t trange[kMaxT], tdone[kMaxT];
-  uint32_t nr, fail;
 };
+constexpr size_t kSmallHead = offsetof(SmallSel, hist);
 
 __global__ void __launch_bounds__(1024, 1) sel_small(const double* __restrict__ perf,
                                                      const double* __restrict__ gain, uint64_t lo,
@@ -996,6 +999,11 @@ __global__ void __launch_bounds__(1024, 1) sel_small(const double* __restrict__ 
   cg::grid_group grid = cg::this_grid();
   extern __shared__ unsigned long long dsm[];  // 64 KB: histograms (u32), prefix (u32), sort (u64)
   uint32_t* sh = reinterpret_cast<uint32_t*>(dsm);
+  __shared__ uint32_t wsum[32];
+  __shared__ uint64_t s_lo[kMaxT], s_hi[kMaxT], s_k[kMaxT];
+  __shared__ uint32_t s_done[kMaxT], s_first[kMaxT], s_range[kMaxT];
+  __shared__ uint64_t r_lo[kMaxT], r_hi[kMaxT];
+  __shared__ uint32_t r_w[kMaxT], s_nr, s_fail;
   const int tid = threadIdx.x, lane = tid & 31;
   const unsigned FULL = 0xffffffffu;
   const uint64_t n_def = partials[LSCAT_P_RATIO_DEFINED];
@@ -1005,6 +1013,7 @@ __global__ void __launch_bounds__(1024, 1) sel_small(const double* __restrict__ 
   const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
   // phase 1: level-0 histograms, privatised per CTA (a gather range needs none)
   for (uint32_t i = tid; i < 2 * kBins; i += blockDim.x) sh[i] = 0;
+  if (tid == 0) s_fail = 0;
   __syncthreads();
   for (uint64_t g = lo + blockIdx.x * (uint64_t)blockDim.x + tid; g < hi; g += T) {
 #pragma unroll
@@ -1018,78 +1027,93 @@ __global__ void __launch_bounds__(1024, 1) sel_small(const double* __restrict__ 
   for (uint32_t i = tid; i < 2 * kBins; i += blockDim.x)
     if (sh[i]) atomicAdd(&ss->hist[0][0] + i, sh[i]);
   grid.sync();
-  // phase 2 (CTA 0): every target to its bin; the distinct bins become the ranges
-  if (blockIdx.x == 0) {
-    __shared__ uint32_t wsum[32];
-    __shared__ uint64_t s_lo[kMaxT], s_hi[kMaxT], s_k[kMaxT];
-    __shared__ uint32_t s_done[kMaxT];
-    for (uint32_t w = 0; w < 2; w++) {  // inclusive scan of hist[w] into sh[w * kBins ..]
-      constexpr int kPer = kBins / 1024;
-      uint32_t c[kPer], sum = 0;
+  // phase 2 (every CTA, identically): every target to its bin; the distinct bins are the ranges
+  for (uint32_t w = 0; w < 2; w++) {  // inclusive scan of hist[w] into sh[w * kBins ..]
+    constexpr int kPer = kBins / 1024;
+    uint32_t c[kPer], sum = 0;
 #pragma unroll
-      for (int j = 0; j < kPer; j++) { c[j] = ss->hist[w][tid * kPer + j]; sum += c[j]; }
-      uint32_t inc = sum;
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(FULL, inc, o);
-        if (lane >= o) inc += y;
-      }
-      if (lane == 31) wsum[tid >> 5] = inc;
-      __syncthreads();
-      if (tid < 32) {
-        uint32_t x = wsum[tid];
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(FULL, x, o);
-          if (tid >= o) x += y;
-        }
-        wsum[tid] = x;
-      }
-      __syncthreads();
-      uint32_t run = inc - sum + ((tid >> 5) ? wsum[(tid >> 5) - 1] : 0u);
-#pragma unroll
-      for (int j = 0; j < kPer; j++) { run += c[j]; sh[w * kBins + tid * kPer + j] = run; }
-      __syncthreads();
+    for (int j = 0; j < kPer; j++) { c[j] = __ldcg(&ss->hist[w][tid * kPer + j]); sum += c[j]; }
+    uint32_t inc = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, inc, o);
+      if (lane >= o) inc += y;
     }
-    if (tid < (int)nt) {
-      const uint32_t w = tid >= (int)npct;
-      const double r = ceil(pct.p[tid % npct] * (double)n_def);  // nearest rank (R-13)
-      uint64_t k = r < 1.0 ? 1 : (r > (double)n_def ? n_def : (uint64_t)r);
-      uint64_t tlo = R[w].lo, thi = R[w].hi;
-      uint32_t done = n_def == 0;
-      if (!done && !R[w].gather) {
-        const uint32_t* P = sh + w * kBins;
-        uint32_t a = 0, b = kBins - 1;  // smallest bin with P[bin] >= k
-        while (a < b) {
-          const uint32_t m = (a + b) / 2;
-          if (P[m] >= k) b = m; else a = m + 1;
-        }
-        const uint32_t below = a ? P[a - 1] : 0u;
-        bin_keys(R[w], (int)a, &tlo, &thi);
-        if (P[a] - below > kSmallCap) atomicOr(&ss->fail, 1u);
-        k -= below;
+    if (lane == 31) wsum[tid >> 5] = inc;
+    __syncthreads();
+    if (tid < 32) {
+      uint32_t x = wsum[tid];
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, x, o);
+        if (tid >= o) x += y;
       }
-      if (!done && tlo == thi) done = 2;  // a single-valued bin: the key is known
-      s_lo[tid] = tlo; s_hi[tid] = thi; s_k[tid] = k; s_done[tid] = done;
+      wsum[tid] = x;
     }
     __syncthreads();
-    if (tid == 0) {  // distinct (quantity, bin) -> range ids, in target order
-      uint32_t nr = 0;
-      for (uint32_t i = 0; i < nt; i++) {
-        const uint32_t w = i >= npct;
-        ss->tk[i] = s_k[i];
-        ss->tdone[i] = s_done[i];
-        ss->tkey[i] = s_done[i] == 2 ? s_lo[i] : kNaNKey;
-        if (s_done[i]) continue;
-        uint32_t r = 0;
-        while (r < nr && !(ss->rwhich[r] == w && ss->rlo[r] == s_lo[i] && ss->rhi[r] == s_hi[i])) r++;
-        if (r == nr) { ss->rwhich[r] = w; ss->rlo[r] = s_lo[i]; ss->rhi[r] = s_hi[i]; nr++; }
-        ss->trange[i] = r;
+    uint32_t run = inc - sum + ((tid >> 5) ? wsum[(tid >> 5) - 1] : 0u);
+#pragma unroll
+    for (int j = 0; j < kPer; j++) { run += c[j]; sh[w * kBins + tid * kPer + j] = run; }
+    __syncthreads();
+  }
+  if (tid < (int)nt) {
+    const uint32_t w = tid >= (int)npct;
+    const double r = ceil(pct.p[tid % npct] * (double)n_def);  // nearest rank (R-13)
+    uint64_t k = r < 1.0 ? 1 : (r > (double)n_def ? n_def : (uint64_t)r);
+    uint64_t tlo = R[w].lo, thi = R[w].hi;
+    uint32_t done = n_def == 0;
+    if (!done && !R[w].gather) {
+      const uint32_t* P = sh + w * kBins;
+      uint32_t a = 0, b = kBins - 1;  // smallest bin with P[bin] >= k
+      while (a < b) {
+        const uint32_t m = (a + b) / 2;
+        if (P[m] >= k) b = m; else a = m + 1;
       }
-      ss->nr = nr;
+      const uint32_t below = a ? P[a - 1] : 0u;
+      bin_keys(R[w], (int)a, &tlo, &thi);
+      if (tlo != thi && P[a] - below > kSmallCap) atomicOr(&s_fail, 1u);  // too many to sort
+      k -= below;
+    }
+    if (!done && tlo == thi) done = 2;  // a single-valued bin: the key is known
+    s_lo[tid] = tlo; s_hi[tid] = thi; s_k[tid] = k; s_done[tid] = done;
+  }
+  __syncthreads();
+  // distinct (quantity, bin) -> range ids in target order
+  if (tid < (int)nt) {
+    bool first = !s_done[tid];
+    for (int j = 0; j < tid && first; j++)
+      if (!s_done[j] && (j >= (int)npct) == (tid >= (int)npct) && s_lo[j] == s_lo[tid] && s_hi[j] == s_hi[tid])
+        first = false;
+    s_first[tid] = first;
+  }
+  __syncthreads();
+  if (tid < (int)nt) {
+    const uint32_t w = tid >= (int)npct;
+    uint32_t r = 0, src = tid;
+    if (!s_done[tid]) {
+      for (int j = 0; j < tid; j++)  // my range's first occurrence
+        if (!s_done[j] && (j >= (int)npct) == (bool)w && s_lo[j] == s_lo[tid] && s_hi[j] == s_hi[tid]) { src = j; break; }
+      for (uint32_t j = 0; j < src; j++) r += s_first[j];
+      if (src == (uint32_t)tid) { r_w[r] = w; r_lo[r] = s_lo[tid]; r_hi[r] = s_hi[tid]; }
+    }
+    s_range[tid] = r;
+    if (blockIdx.x == 0) {
+      ss->tk[tid] = s_k[tid];
+      ss->tdone[tid] = s_done[tid];
+      ss->tkey[tid] = s_done[tid] == 2 ? s_lo[tid] : kNaNKey;
+      ss->trange[tid] = r;
     }
   }
-  grid.sync();
+  if (tid == 0) {
+    uint32_t nr = 0;
+    for (uint32_t j = 0; j < nt; j++) nr += s_first[j];
+    s_nr = s_fail ? 0u : nr;
+    if (blockIdx.x == 0) {
+      ss->nr = nr;
+      ss->fail = s_fail;
+    }
+  }
+  __syncthreads();
   // phase 3: gather the keys of the ranges (disjoint bins: at most one range per key)
-  const uint32_t nr = ss->fail ? 0u : ss->nr;
+  const uint32_t nr = s_nr;
   if (nr) {
     for (uint64_t g0 = lo + blockIdx.x * (uint64_t)blockDim.x; g0 < hi; g0 += T) {
       const uint64_t g = g0 + tid;
@@ -1098,7 +1122,7 @@ __global__ void __launch_bounds__(1024, 1) sel_small(const double* __restrict__ 
         const uint64_t k = g < hi ? (uint64_t)__double_as_longlong((w ? gain : perf)[g]) : kNaNKey;
         uint32_t r = 0xFFFFFFFFu;
         for (uint32_t q = 0; q < nr; q++)
-          if (ss->rwhich[q] == (uint32_t)w && ss->rlo[q] <= k && k <= ss->rhi[q]) r = q;
+          if (r_w[q] == (uint32_t)w && r_lo[q] <= k && k <= r_hi[q]) r = q;
         const unsigned peers = __match_any_sync(FULL, r);
         const int leader = __ffs(peers) - 1;
         unsigned long long base = 0;
@@ -1112,8 +1136,26 @@ __global__ void __launch_bounds__(1024, 1) sel_small(const double* __restrict__ 
     }
   }
   grid.sync();
-  // phase 4: CTA r sorts range r's keys and picks its targets
-  if (blockIdx.x < nr) {
+  // phase 4: CTA r picks its targets' keys among range r's gathered keys: by rank counting
+  // when they fit one per thread, else a bitonic sort
+  if (blockIdx.x < nr && ss->rcnt[blockIdx.x] <= blockDim.x) {
+    const uint32_t r = blockIdx.x;
+    const uint32_t n = (uint32_t)ss->rcnt[r];
+    for (uint32_t i = tid; i < n; i += blockDim.x) dsm[i] = cand[(size_t)r * kSmallCap + i];
+    __syncthreads();
+    if (tid < (int)n) {  // my key's rank: smaller keys, and equal keys earlier in the list
+      const unsigned long long x = dsm[tid];
+      uint32_t rank = 0;
+      for (uint32_t j = 0; j < n; j++) {
+        const unsigned long long y = dsm[j];
+        rank += (y < x) || (y == x && j < (uint32_t)tid);
+      }
+      for (uint32_t i = 0; i < nt; i++)
+        if (!s_done[i] && s_range[i] == r && s_k[i] == rank + 1) ss->tkey[i] = x;
+    }
+    if (tid < (int)nt && !s_done[tid] && s_range[tid] == r && !(s_k[tid] >= 1 && s_k[tid] <= n))
+      atomicOr(&ss->fail, 2u);  // keys lost: the host falls back
+  } else if (blockIdx.x < nr) {
     const uint32_t r = blockIdx.x;
     const uint32_t n = (uint32_t)min(ss->rcnt[r], (unsigned long long)kSmallCap);
     uint32_t P2 = 1;
@@ -1131,8 +1173,8 @@ __global__ void __launch_bounds__(1024, 1) sel_small(const double* __restrict__ 
         }
         __syncthreads();
       }
-    if (tid < (int)nt && !ss->tdone[tid] && ss->trange[tid] == r) {
-      const uint64_t k = ss->tk[tid];
+    if (tid < (int)nt && !s_done[tid] && s_range[tid] == r) {
+      const uint64_t k = s_k[tid];
       if (k >= 1 && k <= n) ss->tkey[tid] = dsm[k - 1];
       else atomicOr(&ss->fail, 2u);  // keys lost: the host falls back
     }
@@ -1221,8 +1263,15 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
       LSCAT_CUDA(ctx, cudaLaunchCooperativeKernel((const void*)sel_small, dim3(ctx->sm_count), dim3(1024), args,
                                                   kSmallSmem, s));
       ctx->launches++;
-      LSCAT_CUDA(ctx, cudaMemcpyAsync(hsm, sm, sizeof(SmallSel), cudaMemcpyDeviceToHost, s));
+      const bool dbg = getenv("LSCAT_SEL_DEBUG") != nullptr;
+      LSCAT_CUDA(ctx, cudaMemcpyAsync(hsm, sm, dbg ? sizeof(SmallSel) : kSmallHead, cudaMemcpyDeviceToHost, s));
       LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
+      if (dbg) {
+        fprintf(stderr, "sel_small: fail %u nr %u\n", hsm->fail, hsm->nr);
+        for (uint32_t i = 0; i < 2 * npct; i++)
+          fprintf(stderr, "  t%u done %u range %u k %llu key %016llx\n", i, hsm->tdone[i], hsm->trange[i],
+                  (unsigned long long)hsm->tk[i], (unsigned long long)hsm->tkey[i]);
+      }
       if (!hsm->fail) {
         for (uint32_t i = 0; i < 2 * npct; i++) {
           double v;
