@@ -1323,11 +1323,12 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
   const uint64_t stride = std::max<uint64_t>(1, n / kSampleKeys) | 1;  // odd: no period-2^k alias
   const int grid_s = (int)std::min<uint64_t>(std::max<uint64_t>(1, (n / stride + 1023) / 1024),
                                              (uint64_t)ctx->sm_count * 8);
-  static int occ_p = 0;  // resident CTAs per SM of the sampled pass (binary property)
-  if (!occ_p) {
-    LSCAT_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, sel_pass_sampled<256>, 256, 0));
-    occ_p = std::max(occ_p, 1);
-  }
+  static const int occ_p = [] {  // resident CTAs per SM of the sampled pass (binary property;
+    int v = 0;                    // thread-safe one-time query)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, sel_pass_sampled<256>, 256, 0);
+    cudaGetLastError();
+    return std::max(v, 1);
+  }();
   const int grid_p = (int)std::min<uint64_t>(std::max<uint64_t>(1, (n + 256 * 8 - 1) / (256 * 8)),
                                              (uint64_t)ctx->sm_count * occ_p);
   auto enqueue_first_sampled = [&](cudaStream_t q) -> lscat_status {
