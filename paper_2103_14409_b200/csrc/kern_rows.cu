@@ -59,8 +59,18 @@ __device__ __forceinline__ float acc1(float s, float a, float v) {
 
 // A CTA of B threads is split into floor(W/TW) teams of TW warps; each team reduces one row
 // (TW from team_warps, calibrated on B200).
-template <int OP, int B>
-__global__ void __launch_bounds__(B, row_min_blocks<B>()) row_kernel(const float* __restrict__ A,
+// UL = float4 loads of A in flight per thread per pass.  Large N: ROW_U (8) under a 64-register
+// budget; short rows (a launch is latency bound: one or two passes) use lighter variants without
+// the register budget -- 2-deep up to N = 256, 4-deep up to 2048.  Interleaved A/B
+// (scripts/ab_small_rows.sh, plain graph brackets, mean over the 32 blocks): N = 64 2.10 ->
+// 1.72 us, 256 2.23 -> 1.94, 512 2.37 -> 2.02, 1024 2.68 -> 2.63, 2048 4.08 -> 3.97
+// (scripts/launch_floor_probe*.cu: an empty graph launch is 0.44 us).
+constexpr int kSmallRowN = 2048;
+template <int UL, int B>
+constexpr int row_bounds_min_blocks() { return UL >= 8 ? row_min_blocks<B>() : 1; }
+
+template <int OP, int B, int UL>
+__global__ void __launch_bounds__(B, row_bounds_min_blocks<UL, B>()) row_kernel(const float* __restrict__ A,
                                                 const float* __restrict__ v,
                                                 float* __restrict__ out, int N, int TW, float l2keep) {
   constexpr int W = B / 32;
@@ -82,7 +92,7 @@ __global__ void __launch_bounds__(B, row_min_blocks<B>()) row_kernel(const float
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
     if (live) {
       if ((N & 3) == 0) {
-        constexpr int U = ROW_U;
+        constexpr int U = UL;
         const uint64_t pol = l2keep > 0.f ? l2_keep_fraction_policy(l2keep) : 0;
         const float4* a4 = reinterpret_cast<const float4*>(a);
         const float4* v4 = reinterpret_cast<const float4*>(v);
@@ -134,6 +144,22 @@ __global__ void __launch_bounds__(B, row_min_blocks<B>()) row_kernel(const float
 // Larger teams only add the team combine and idle leftover warps.
 inline int team_warps(int /*N*/, int /*B*/) { return 1; }
 
+inline int small_rows() {  // LSCAT_ROW_SMALL=0: the 8-deep variant at every N; =2 also the
+  static const int v = [] {  // 4-deep one up to kSmallRowN (A/B runs)
+    const char* e = getenv("LSCAT_ROW_SMALL");
+    return e ? atoi(e) : 2;
+  }();
+  return v;
+}
+
+inline int small4_max() {  // LSCAT_ROW_SMALL4_MAX: largest N of the 4-deep variant (calibration)
+  static const int v = [] {
+    const char* e = getenv("LSCAT_ROW_SMALL4_MAX");
+    return e ? atoi(e) : 2048;
+  }();
+  return v;
+}
+
 inline bool legacy_grid() {
   static const bool v = [] {
     const char* e = getenv("LSCAT_ROW_GRID");
@@ -147,12 +173,12 @@ struct RowLauncher {
   template <int B>
   struct L {
     static constexpr bool kSupported = true;
-    static cudaError_t attrs(const void** f, size_t* sm) { return kernel_attrs(row_kernel<OP, B>, 0, f, sm); }
+    static cudaError_t attrs(const void** f, size_t* sm) { return kernel_attrs(row_kernel<OP, B, ROW_U>, 0, f, sm); }
     // resident CTAs per SM (a property of the sm_100a binary; thread-safe one-time query)
     static int per_sm() {
       static const int v = [] {
         int r = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, row_kernel<OP, B>, B, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, row_kernel<OP, B, ROW_U>, B, 0);
         cudaGetLastError();
         return r > 0 ? r : 1;
       }();
@@ -199,7 +225,14 @@ struct RowLauncher {
         const long r = (need + slots - 1) / slots;
         grid = (int)((need + r - 1) / r);
       }
-      return launch_k(row_kernel<OP, B>, dim3(grid), dim3(B), 0, s, a.pdl,
+      const int sv = small_rows();
+      if (N <= 256 && sv)  // latency-bound short rows: the lighter variants
+        return launch_k(row_kernel<OP, B, 2>, dim3(grid), dim3(B), 0, s, a.pdl,
+                        (const float*)e.in0, (const float*)e.in1, (float*)e.out, N, tw, keep);
+      if (N <= small4_max() && sv >= 2)
+        return launch_k(row_kernel<OP, B, 4>, dim3(grid), dim3(B), 0, s, a.pdl,
+                        (const float*)e.in0, (const float*)e.in1, (float*)e.out, N, tw, keep);
+      return launch_k(row_kernel<OP, B, ROW_U>, dim3(grid), dim3(B), 0, s, a.pdl,
                       (const float*)e.in0, (const float*)e.in1, (float*)e.out, N, tw, keep);
     }
   };
