@@ -111,6 +111,7 @@ struct lscat_ctx {
   std::map<std::pair<bool, size_t>, int> red_occ;
   int sel_occ0 = 0, sel_occ1 = 0;
   uint64_t sel_fallbacks = 0;  // sampled first levels that missed a target (stats.cu)
+  uint64_t fin_fallbacks = 0;  // sel_finish runs that handed over to the chain (stats.cu)
   std::vector<cudaEvent_t> events;
   // LSCAT_L2_ROTATE (sweep.cu): the (kernel, n) whose input copies the "rot" scratch arena
   // holds, and the arena base its graphs were captured against

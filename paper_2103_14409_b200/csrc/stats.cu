@@ -840,16 +840,18 @@ __global__ void __launch_bounds__(kT) sel_pass_sampled(const double* __restrict_
   __syncthreads();
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
-  auto flush = [&]() {  // CTA-wide: reserve once per quantity, copy the stage out
+  auto flush = [&]() {  // CTA-wide: reserve once per quantity, copy the stage out (keys past
+                        // kCopyStage went straight to the global buffer with their own reservation)
     __syncthreads();
     if (threadIdx.x < 2 && s_nc[threadIdx.x]) {
-      s_base[threadIdx.x] = atomicAdd(&ss->ncopy[threadIdx.x], (unsigned long long)s_nc[threadIdx.x]);
-      atomicAdd(&ss->ncopy_all[threadIdx.x], (unsigned long long)s_nc[threadIdx.x]);
+      const uint32_t n = min(s_nc[threadIdx.x], kCopyStage);
+      s_base[threadIdx.x] = atomicAdd(&ss->ncopy[threadIdx.x], (unsigned long long)n);
+      atomicAdd(&ss->ncopy_all[threadIdx.x], (unsigned long long)n);
     }
     __syncthreads();
 #pragma unroll
     for (int w = 0; w < 2; w++)
-      for (uint32_t i = threadIdx.x; i < s_nc[w]; i += kT) {
+      for (uint32_t i = threadIdx.x; i < min(s_nc[w], kCopyStage); i += kT) {
         const unsigned long long g = s_base[w] + i;
         if (g < kCompactCap) reinterpret_cast<uint64_t*>(cbuf)[(size_t)w * kCompactCap + g] = stage[w][i];
       }
@@ -1181,6 +1183,304 @@ __global__ void __launch_bounds__(1024, 1) sel_small(const double* __restrict__ 
   }
 }
 
+// ---- after the sampled first level, on one rank: the rest of the selection in one launch ----
+// sel_check_sampled leaves every open target in a range [lo, hi] (one fixed bin) whose keys
+// all sit in the copies.  The chain would now run ~4 histogram levels over the copies (two
+// dependent launches each).  One cooperative kernel does it instead: each range's keys are
+// counted into kFinBins sub-bins (global atomics; ranges found by a scan over the <= 18 sorted
+// ranges), CTA r narrows range r's targets to their sub-bins, the keys of those
+// sub-bins are gathered, one CTA per sub-bin sorts them and picks.  The SelState is only read:
+// a sub-bin above kSmallCap keys (or any inconsistency) sets `fail` and the host continues
+// with the chain from the unchanged state.
+constexpr uint32_t kFinBins = 2048;
+constexpr uint32_t kFinRanges = 2 * kIvQ;
+constexpr size_t kFinSmem = (size_t)kSmallCap * 8;  // the sort
+
+struct FinSel {
+  // results first: the host copies back only this head
+  uint64_t tkey[kMaxT];                    // per open target: result key
+  uint32_t fail, pad;
+  uint64_t stamp[5];                       // %globaltimer at the phase boundaries (CTA 0; debug)
+  // working state
+  uint64_t tlo[kMaxT], thi[kMaxT], tk[kMaxT], tcnt[kMaxT];  // per target after the narrowing
+  unsigned long long rcnt[kMaxT];          // keys gathered per sub-range
+  uint32_t hist[kFinRanges][kFinBins];
+};
+constexpr size_t kFinHead = offsetof(FinSel, tlo);
+
+__global__ void __launch_bounds__(1024, 1) sel_finish(const SelState* __restrict__ st,
+                                                      const double* __restrict__ cbuf,
+                                                      FinSel* __restrict__ fs,
+                                                      unsigned long long* __restrict__ cand,
+                                                      uint32_t force_fail) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ unsigned long long dsm[];  // the phase-4 sort
+  __shared__ uint64_t r_lo[kFinRanges], r_hi[kFinRanges];
+  __shared__ uint32_t r_sh[kFinRanges];
+  __shared__ uint64_t q_lo[kMaxT], q_hi[kMaxT];  // sub-ranges (gather): key interval, quantity
+  __shared__ uint32_t q_w[kMaxT], s_qr[kMaxT], s_first[kMaxT], s_nq;
+  __shared__ unsigned long long wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const unsigned FULL = 0xffffffffu;
+  const uint32_t nr = st->nr, nw0 = st->nw0, nt = st->nt;
+  const bool on = !force_fail && !st->sampled_fail && st->src == 1 && st->err == 0 && nr <= kFinRanges;
+  if (!on) {
+    if (blockIdx.x == 0 && tid == 0) fs->fail = 1;
+    return;  // grid-uniform: no grid barrier is reached
+  }
+  auto stamp = [&](int i) {
+    if (blockIdx.x == 0 && tid == 0) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      fs->stamp[i] = t;
+    }
+  };
+  stamp(0);
+  if (nr == 0) {  // every target resolved by the check: nothing to do
+    if (blockIdx.x == 0 && tid == 0) fs->fail = 0;
+    return;
+  }
+  __shared__ uint64_t s_tk[kMaxT];
+  __shared__ uint32_t s_trange[kMaxT], s_topen[kMaxT], s_tw[kMaxT];
+  // After the check every range is one fixed bin of selbins.h (clipped to [min, max]): a key's
+  // range is found from its fixed bin through a byte map (0xFF: no range)
+  __shared__ uint8_t rmap[2 * kFxBins];
+  __shared__ uint32_t gbm[kFinRanges][kFinBins / 32];  // phase 3: sub-bins to gather
+  __shared__ uint32_t s_bad;
+  for (uint32_t i = tid; i < 2 * kFxBins; i += blockDim.x) rmap[i] = 0xFF;
+  for (uint32_t i = tid; i < kFinRanges * (kFinBins / 32); i += blockDim.x) (&gbm[0][0])[i] = 0u;
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  if (tid < (int)nr) {
+    const Range& R = st->r[tid];
+    r_lo[tid] = R.lo;
+    r_hi[tid] = R.hi;
+    const uint64_t span = R.hi - R.lo;
+    uint32_t s = 0;
+    while ((span >> s) >= kFinBins) s++;
+    r_sh[tid] = s;
+    const uint32_t w = R.which;
+    const uint32_t b = fx_bin(w, R.lo);
+    if (b != fx_bin(w, R.hi) || virtual_bin(w, b) || (tid < (int)nw0) != (w == 0)) atomicOr(&s_bad, 1u);
+    else rmap[w * kFxBins + b] = (uint8_t)tid;
+  }
+  if (tid < (int)nt) {  // the targets, read once (phases 2 and 3 loop over them)
+    const Tgt& t = st->t[tid];
+    s_tk[tid] = t.k;
+    s_trange[tid] = t.range;
+    s_topen[tid] = !t.done;
+    s_tw[tid] = t.which;
+  }
+  __syncthreads();
+  if (s_bad) {  // not one fixed bin per range (never, with the check above): the chain
+    if (blockIdx.x == 0 && tid == 0) fs->fail = 16;
+    return;  // CTA-uniform and identical in every CTA: no grid barrier is reached
+  }
+  // phase 1: sub-bin counts of every range (ranges of quantity w: [w ? nw0 : 0, w ? nr : nw0)),
+  // straight to the global histogram: the keys spread over nr x kFinBins bins, so a per-CTA
+  // privatised copy would cost a flush of ~all its bins per CTA.  kU loads in flight per thread.
+  // range of a copied key: its fixed bin's map entry, if the key also lies inside the range's
+  // clipped [lo, hi] (copies of a range's bin outside [min, max] do not exist)
+  auto i_range = [&](int w, uint64_t k) -> uint32_t {
+    const uint32_t kh = (uint32_t)(k >> 32);
+    // counted keys only (perf < 1, finite gain): the padding NaN keys have no bin
+    if (kh >= (w == 0 ? (uint32_t)(kPerfOne >> 32) : 0x7FF00000u)) return 0xFFu;
+    const uint32_t b = w == 0 ? fx_perf_bin_hi(kh) : fx_gain_bin_hi(kh);
+    const uint32_t r = rmap[w * kFxBins + b];
+    return (r != 0xFFu && r_lo[r] <= k && k <= r_hi[r]) ? r : 0xFFu;
+  };
+  constexpr int kU = 8;
+  const uint64_t* keys = reinterpret_cast<const uint64_t*>(cbuf);
+  const uint64_t cstride = (uint64_t)gridDim.x * blockDim.x * kU;
+#pragma unroll 1
+  for (int w = 0; w < 2; w++) {
+    const uint32_t a = w ? nw0 : 0, b = w ? nr : nw0;
+    if (a == b) continue;
+    const uint64_t n = min(st->nc[w], (unsigned long long)kCompactCap);
+    const uint64_t* src = keys + (size_t)w * kCompactCap;
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * kU + tid; base < n; base += cstride) {
+      uint64_t k[kU];
+#pragma unroll
+      for (int u = 0; u < kU; u++) {
+        const uint64_t i = base + (uint64_t)u * blockDim.x;
+        k[u] = i < n ? __ldcg(src + i) : kNaNKey;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; u++) {
+        const uint32_t r = i_range(w, k[u]);
+        if (r != 0xFFu) atomicAdd(&fs->hist[r][(uint32_t)((k[u] - r_lo[r]) >> r_sh[r])], 1u);
+      }
+    }
+  }
+  grid.sync();
+  stamp(1);
+  // phase 2: CTA r narrows range r's open targets to their sub-bins
+  if (blockIdx.x < nr) {
+    const uint32_t r = blockIdx.x;
+    constexpr int kPer = kFinBins / 1024;
+    uint32_t c[kPer];
+    unsigned long long sum = 0;
+#pragma unroll
+    for (int j = 0; j < kPer; j++) { c[j] = __ldcg(&fs->hist[r][tid * kPer + j]); sum += c[j]; }
+    unsigned long long inc = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(FULL, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) wsum[tid >> 5] = inc;
+    __syncthreads();
+    if (tid < 32) {
+      unsigned long long x = wsum[tid];
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(FULL, x, o);
+        if (tid >= o) x += y;
+      }
+      wsum[tid] = x;
+    }
+    __syncthreads();
+    const unsigned long long ex = inc - sum + ((tid >> 5) ? wsum[(tid >> 5) - 1] : 0ull);
+    if (tid == 1023 && ex + sum != st->r[r].count) atomicOr(&fs->fail, 2u);  // keys lost
+    for (uint32_t i = 0; i < nt; i++) {
+      if (!s_topen[i] || s_trange[i] != r) continue;
+      const uint64_t k = s_tk[i];
+      if (tid == 1023 && !(k >= 1 && k <= ex + sum)) atomicOr(&fs->fail, 2u);  // rank outside
+      if (!(ex < k && k <= ex + sum)) continue;
+      unsigned long long cum = ex;
+      int j = 0;
+      while (cum + c[j] < k) cum += c[j++];
+      const uint32_t bb = (uint32_t)(tid * kPer + j);
+      const uint64_t lo = r_lo[r] + ((uint64_t)bb << r_sh[r]);
+      const uint64_t top = lo + ((1ull << r_sh[r]) - 1);
+      const uint64_t hi = (top < lo || top > r_hi[r]) ? r_hi[r] : top;
+      fs->tlo[i] = lo;
+      fs->thi[i] = hi;
+      fs->tk[i] = k - cum;
+      fs->tcnt[i] = c[j];
+      if (c[j] > kSmallCap && hi != lo) atomicOr(&fs->fail, 4u);  // too many to sort
+    }
+  }
+  grid.sync();
+  stamp(2);
+  if (__ldcg(&fs->fail)) return;  // grid-uniform (written before the barrier)
+  // phase 3 (every CTA, identically): distinct open sub-ranges; gather their keys
+  if (tid < (int)nt) {
+    const bool open = s_topen[tid];
+    q_lo[tid] = open ? __ldcg(&fs->tlo[tid]) : 0ull;
+    q_hi[tid] = open ? __ldcg(&fs->thi[tid]) : 0ull;
+    q_w[tid] = s_tw[tid];
+    s_first[tid] = open && q_hi[tid] != q_lo[tid];
+  }
+  __syncthreads();
+  const bool mine_first = tid < (int)nt && s_first[tid];
+  bool dup = false;
+  if (mine_first)
+    for (int j = 0; j < tid; j++)
+      if (s_first[j] && q_w[j] == q_w[tid] && q_lo[j] == q_lo[tid] && q_hi[j] == q_hi[tid]) { dup = true; break; }
+  __syncthreads();
+  if (mine_first && dup) s_first[tid] = 0;
+  __syncthreads();
+  if (tid < (int)nt) {  // sub-range id of every open target (its first occurrence's rank)
+    uint32_t q = 0xFFFFFFFFu;
+    if (s_topen[tid] && q_hi[tid] != q_lo[tid]) {
+      uint32_t src = tid;
+      for (int j = 0; j < tid; j++)
+        if (s_first[j] && q_w[j] == q_w[tid] && q_lo[j] == q_lo[tid] && q_hi[j] == q_hi[tid]) { src = j; break; }
+      q = 0;
+      for (uint32_t j = 0; j < src; j++) q += s_first[j];
+    }
+    s_qr[tid] = q;
+  }
+  if (tid == 0) {
+    uint32_t n = 0;
+    for (uint32_t j = 0; j < nt; j++) n += s_first[j];
+    s_nq = n;
+  }
+  __syncthreads();
+  // compact the distinct sub-ranges to the front: sub-range q = the q-th first occurrence
+  __shared__ uint64_t g_lo[kMaxT], g_hi[kMaxT];
+  __shared__ uint32_t g_w[kMaxT];
+  if (tid < (int)nt && s_first[tid]) {
+    const uint32_t q = s_qr[tid];
+    g_lo[q] = q_lo[tid];
+    g_hi[q] = q_hi[tid];
+    g_w[q] = q_w[tid];
+    const uint32_t r = s_trange[tid];
+    const uint32_t sb = (uint32_t)((q_lo[tid] - r_lo[r]) >> r_sh[r]);
+    atomicOr(&gbm[r][sb >> 5], 1u << (sb & 31));
+  }
+  __syncthreads();
+  const uint32_t nq = s_nq;
+#pragma unroll 1
+  for (int w = 0; w < 2; w++) {
+    const uint64_t n = min(st->nc[w], (unsigned long long)kCompactCap);
+    const uint64_t* src = keys + (size_t)w * kCompactCap;
+    // CTA-uniform trip count (the warp collectives below): every thread runs every chunk
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * kU; base < n; base += cstride) {
+      uint64_t k[kU];
+#pragma unroll
+      for (int u = 0; u < kU; u++) {
+        const uint64_t i = base + (uint64_t)u * blockDim.x + tid;
+        k[u] = i < n ? __ldcg(src + i) : kNaNKey;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; u++) {
+        const uint32_t r = i_range(w, k[u]);
+        bool hit = false;
+        if (r != 0xFFu) {
+          const uint32_t sb = (uint32_t)((k[u] - r_lo[r]) >> r_sh[r]);
+          hit = (gbm[r][sb >> 5] >> (sb & 31)) & 1u;
+        }
+        if (!__any_sync(FULL, hit)) continue;
+        uint32_t q = 0xFFFFFFFFu;
+        if (hit)
+          for (uint32_t j = 0; j < nq; j++)
+            if (g_w[j] == (uint32_t)w && g_lo[j] <= k[u] && k[u] <= g_hi[j]) q = j;
+        const unsigned peers = __match_any_sync(FULL, q);
+        const int leader = __ffs(peers) - 1;
+        unsigned long long at0 = 0;
+        if (q != 0xFFFFFFFFu && lane == leader) at0 = atomicAdd(&fs->rcnt[q], (unsigned long long)__popc(peers));
+        at0 = __shfl_sync(FULL, at0, leader);
+        if (q != 0xFFFFFFFFu) {
+          const unsigned long long at = at0 + __popc(peers & ((1u << lane) - 1u));
+          if (at < kSmallCap) cand[(size_t)q * kSmallCap + at] = k[u];
+        }
+      }
+    }
+  }
+  grid.sync();
+  stamp(3);
+  // phase 4: CTA q sorts sub-range q's keys (bitonic, shared memory) and picks its targets'
+  if (blockIdx.x == 0 && tid < (int)nt) {  // single-valued sub-bins: the key is known
+    if (s_topen[tid] && q_hi[tid] == q_lo[tid]) fs->tkey[tid] = q_lo[tid];
+  }
+  if (blockIdx.x >= nq) return;
+  const uint32_t q = blockIdx.x;
+  const unsigned long long cnt = __ldcg(&fs->rcnt[q]);
+  const uint32_t n = (uint32_t)min(cnt, (unsigned long long)kSmallCap);
+  uint32_t P2 = 1;
+  while (P2 < n) P2 <<= 1;
+  for (uint32_t i = tid; i < P2; i += blockDim.x) dsm[i] = i < n ? __ldcg(&cand[(size_t)q * kSmallCap + i]) : ~0ull;
+  __syncthreads();
+  for (uint32_t kk = 2; kk <= P2; kk <<= 1)
+    for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = tid; i < P2; i += blockDim.x) {
+        const uint32_t ixj = i ^ j;
+        if (ixj > i) {
+          const unsigned long long a = dsm[i], b = dsm[ixj];
+          if ((a > b) == ((i & kk) == 0)) { dsm[i] = b; dsm[ixj] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  if (tid < (int)nt && s_qr[tid] == q) {
+    const uint64_t k = __ldcg(&fs->tk[tid]);
+    if (cnt == __ldcg(&fs->tcnt[tid]) && k >= 1 && k <= n) fs->tkey[tid] = dsm[k - 1];
+    else atomicOr(&fs->fail, 8u);  // keys lost: the host continues with the chain
+  }
+  stamp(4);
+}
+
 lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct, double* out_perf,
                                 double* out_gain, cudaStream_t s) {
   const ReduceState& rs = ctx->rs;
@@ -1331,6 +1631,25 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
   }();
   const int grid_p = (int)std::min<uint64_t>(std::max<uint64_t>(1, (n + 256 * 8 - 1) / (256 * 8)),
                                              (uint64_t)ctx->sm_count * occ_p);
+  // one rank: the levels after the sampled first level run as one cooperative sel_finish
+  // (LSCAT_SEL_NOFINISH=1 keeps the chain)
+  static const bool no_finish = getenv("LSCAT_SEL_NOFINISH") != nullptr;
+  int coop_ok = 0;
+  if (sampled && world == 1 && !no_finish)
+    LSCAT_CUDA(ctx, cudaDeviceGetAttribute(&coop_ok, cudaDevAttrCooperativeLaunch, ctx->device));
+  const bool fin = coop_ok != 0;
+  FinSel* fs = nullptr;
+  FinSel* fsh = nullptr;
+  unsigned long long* fcand = nullptr;
+  if (fin) {
+    fs = (FinSel*)scratch(ctx, "sel_fin", sizeof(FinSel), &err);
+    if (err) return cuda_fail(ctx, err, "stats: scratch");
+    fcand = (unsigned long long*)scratch(ctx, "sel_fin_cand", (size_t)kMaxT * kSmallCap * 8, &err);
+    if (err) return cuda_fail(ctx, err, "stats: scratch");
+    fsh = (FinSel*)pinned(ctx, "sel_fin_h", kFinHead, &err);
+    if (err) return cuda_fail(ctx, err, "stats: pinned");
+    LSCAT_CUDA(ctx, ensure_smem_attr((const void*)sel_finish, kFinSmem));
+  }
   auto enqueue_first_sampled = [&](cudaStream_t q) -> lscat_status {
     LSCAT_CUDA(ctx, cudaMemsetAsync(hist, 0, (size_t)kMaxR * kBins * 4, q));
     LSCAT_CUDA(ctx, cudaMemsetAsync(cand, 0, (size_t)kMaxR * 8, q));
@@ -1354,6 +1673,11 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
     sel_check_sampled<<<1, 1024, 0, q>>>(st, ss, rs.partials, rs.opts.bins_per_unit, rs.minmax, cap,
                                          force_miss ? 1u : 0u);
     LSCAT_CUDA(ctx, cudaGetLastError());
+    if (fin) {  // sel_finish follows (outside the graph); the state as the check left it
+      LSCAT_CUDA(ctx, cudaMemsetAsync(fs, 0, sizeof(FinSel), q));
+      LSCAT_CUDA(ctx, cudaMemcpyAsync(hst, st, sizeof(SelState), cudaMemcpyDeviceToHost, q));
+      return LSCAT_OK;
+    }
     return enqueue_levels(q, false);
   };
   auto enqueue_first = [&](cudaStream_t q) -> lscat_status {
@@ -1376,6 +1700,8 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
       put(ptrs, sizeof ptrs);
       put(&rs.own_lo, 8); put(&rs.own_hi, 8); put(&npct, 4); put(pa.p, npct * 8);
       put(&grid0, 4); put(&grid1, 4); put(&cap, 4); put(&samp, sizeof samp);
+      const bool fin_k = samp && fin;
+      put(&fin_k, sizeof fin_k); put(&fs, sizeof fs);
       cudaGraphExec_t gx = nullptr;
       for (auto& kv : ctx->sel_graphs)
         if (kv.first == key) gx = kv.second;
@@ -1404,10 +1730,24 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
       lscat_status e = enq(s);
       if (e) return e;
     }
-    ctx->launches += (samp ? 4 : 1) + 2 * lpb;
+    if (samp && fin) {
+      const SelState* st_c = st;
+      const double* cb_c = cbuf;
+      // LSCAT_SEL_FIN_FORCE_FAIL=1 (tests): sel_finish hands over to the chain at once
+      static const uint32_t ff = getenv("LSCAT_SEL_FIN_FORCE_FAIL") != nullptr ? 1u : 0u;
+      uint32_t ff_ = ff;
+      void* args[] = {(void*)&st_c, (void*)&cb_c, (void*)&fs, (void*)&fcand, (void*)&ff_};
+      LSCAT_CUDA(ctx, cudaLaunchCooperativeKernel((const void*)sel_finish, dim3(ctx->sm_count), dim3(1024), args,
+                                                  kFinSmem, s));
+      LSCAT_CUDA(ctx, cudaMemcpyAsync(fsh, fs, kFinHead, cudaMemcpyDeviceToHost, s));
+      ctx->launches += 5;
+    } else {
+      ctx->launches += (samp ? 4 : 1) + 2 * lpb;
+    }
     return LSCAT_OK;
   };
   if ((ls = launch_first(sampled))) return ls;
+  bool levels_pending = sampled && fin;  // the first batch ran no levels (sel_finish instead)
   for (int batch = 0;; batch++) {
     if (batch == 8) return fail(ctx, LSCAT_ERR_STATE, "stats: percentile selection did not converge");
     if (batch > 0) {
@@ -1419,8 +1759,31 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
       fprintf(stderr, "sel batch %d: nt %u nr %u nw0 %u open %u err %u src %u compact %u nc %llu %llu sampled %d fail %u\n",
               batch, hst->nt, hst->nr, hst->nw0, hst->open, hst->err, hst->src, hst->compact, hst->nc[0],
               hst->nc[1], (int)sampled, hst->sampled_fail);
+    if (batch == 0 && levels_pending && !hst->sampled_fail) {
+      levels_pending = false;
+      if (debug)
+        fprintf(stderr, "sel_finish: fail %u open %u nr %u nc %llu %llu phases(ns) %lld %lld %lld %lld\n",
+                fsh->fail, hst->open, hst->nr, hst->nc[0], hst->nc[1],
+                (long long)(fsh->stamp[1] - fsh->stamp[0]), (long long)(fsh->stamp[2] - fsh->stamp[1]),
+                (long long)(fsh->stamp[3] - fsh->stamp[2]), (long long)(fsh->stamp[4] - fsh->stamp[3]));
+      if (!fsh->fail && !hst->err) {
+        for (uint32_t i = 0; i < 2 * npct; i++) {
+          const Tgt& t = hst->t[i];
+          const uint64_t key = t.done ? t.key : fsh->tkey[i];
+          double v;
+          memcpy(&v, &key, 8);
+          (t.which ? out_gain : out_perf)[i % npct] = v;
+        }
+        return LSCAT_OK;
+      }
+      ctx->fin_fallbacks++;  // the chain continues from the state the check left
+      if (hst->err) return fail(ctx, LSCAT_ERR_STATE, "stats: percentile selection lost keys (code %u)", hst->err);
+      if (!hst->open) break;
+      continue;
+    }
     if (batch == 0 && sampled && hst->sampled_fail) {  // a sampling miss: the histogram path
       sampled = false;
+      levels_pending = false;
       ctx->sel_fallbacks++;
       if ((ls = launch_first(false))) return ls;
       batch = -1;

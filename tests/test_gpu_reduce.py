@@ -542,3 +542,61 @@ def test_percentiles_sampled_fallback():
                        timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
     assert "sampled 1 fail 1" in r.stderr, r.stderr[-2000:]
+
+
+def _run_child(code, env_add, timeout=900):
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, **env_add)
+    return subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                          timeout=timeout)
+
+
+@pytest.mark.parametrize("knob", ["LSCAT_SEL_FIN_FORCE_FAIL", "LSCAT_SEL_NOFINISH"])
+def test_percentiles_sampled_chain_after_check(knob):
+    """After the sampled first level, one rank finishes the selection in one cooperative launch
+    (sel_finish).  With the finisher handing over at once (forced) or switched off, the
+    multi-level chain continues from the state the check left and stays exact (child process:
+    the switches are read once)."""
+    code = (
+        "from tests.test_gpu_reduce import _compare\n"
+        "from synth import gen_table\n"
+        "t = gen_table(36_000_000, 140_000, preset='t4', nan_rate=0.03, seed=17)\n"
+        "_compare(t, pcts=[0.01, 0.1, 0.25, 0.5, 0.9, 0.99])\n"
+        "print('ok')\n")
+    r = _run_child(code, {knob: "1", "LSCAT_SEL_DEBUG": "1"})
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+    assert "sampled 1 fail 0" in r.stderr, r.stderr[-2000:]
+    if knob == "LSCAT_SEL_FIN_FORCE_FAIL":
+        assert "sel_finish: fail 1" in r.stderr, r.stderr[-2000:]
+    else:
+        assert "sel_finish" not in r.stderr, r.stderr[-2000:]
+
+
+def test_percentiles_sampled_finish_overflow():
+    """sel_finish on a sub-bin of more than 8192 keys (~40 % of 2.5 M ratio-defined groups at
+    four perf values 2^23 ulps apart: one fixed bin, one sub-bin): it hands over to the chain,
+    which gathers / compacts as usual; values exact against the oracle."""
+    code = (
+        "import numpy as np\n"
+        "from tests.test_gpu_reduce import _compare\n"
+        "rng = np.random.default_rng(5)\n"
+        "G = 2_500_000\n"
+        "b = rng.uniform(0.5, 2.0, G).astype(np.float32)\n"
+        "dense = rng.random(G) < 0.4\n"
+        "j = rng.integers(1, 5, G).astype(np.float32)\n"
+        "t = np.where(dense, b * (np.float32(1) + j * np.float32(2.0 ** -22)),\n"
+        "             b * rng.uniform(1.0, 4.0, G).astype(np.float32)).astype(np.float32)\n"
+        "rt = np.empty(2 * G, np.float32)\n"
+        "rt[0::2], rt[1::2] = b, t\n"
+        "tab = dict(runtime_ms=rt, block_id=np.tile(np.array([0, 1], np.uint16), G),\n"
+        "           group_offset=np.arange(0, 2 * G + 1, 2, dtype=np.int64),\n"
+        "           group_matrix=np.zeros(G, np.uint32))\n"
+        "_compare(tab, L=2, M=1, ell=1, pcts=[0.05, 0.3, 0.5, 0.7, 0.95])\n"
+        "print('ok')\n")
+    r = _run_child(code, {"LSCAT_SEL_DEBUG": "1"})
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+    import re
+    assert "sampled 1 fail 0" in r.stderr and re.search(r"sel_finish: fail [1-9]", r.stderr), r.stderr[-2000:]
