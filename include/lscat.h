@@ -274,6 +274,16 @@ typedef struct {
                               /*      thresholds and in 1 % bins.  Precondition: a kernel's */
                               /*      groups are contiguous in table order (sweep, generator */
                               /*      and ingest tables are); 8 extra bytes per group       */
+  uint32_t n_percentiles;     /* > 0 (<= 64): lscat_reduce_table also enqueues the a8       */
+                              /*      selection of these percentiles on its stream, right   */
+                              /*      behind the reduction (one rank, not point-sharded,    */
+                              /*      per-group values kept; R-27), and           */
+                              /*      lscat_stats called with the same list only collects   */
+                              /*      the result (a later selection of another list         */
+                              /*      replaces it).  Otherwise lscat_stats selects as       */
+                              /*      usual.  0: off                                        */
+  uint32_t pad0;
+  const double* percentiles;  /* HOST [n_percentiles] in [0, 1], read during the call      */
 } lscat_reduce_opts;
 
 /* Fills `opts` with the defaults above for a block list of n_blocks with largest id l. */

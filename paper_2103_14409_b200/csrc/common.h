@@ -81,7 +81,11 @@ struct ReduceState {
   double* gain = nullptr;
   uint64_t* partials = nullptr;  // device, len = partials_len (SUM-merged)
   uint64_t* minmax = nullptr;    // device [4]: perf min, perf max, gain min, gain max keys
+  // percentile selection already enqueued by lscat_reduce_table (opts.n_percentiles, R-27)
+  uint32_t early = 0;            // EARLY_NONE / EARLY_SMALL / EARLY_SAMPLED
+  std::vector<double> early_pct;
 };
+enum { EARLY_NONE = 0, EARLY_SMALL = 1, EARLY_SAMPLED = 2 };
 
 struct DevBuf {
   void* p = nullptr;
@@ -139,6 +143,12 @@ void* pinned(lscat_ctx* ctx, const char* name, size_t bytes, cudaError_t* err);
 // Raise a kernel's max-dynamic-shared-memory attribute on the current device to at least
 // `bytes` (device-global state: never lowered, set once per (kernel, device, size increase)).
 cudaError_t ensure_smem_attr(const void* func, size_t bytes);
+// percentile selection enqueued by lscat_reduce_table (stats.cu; R-27), no host sync: the
+// one-launch selection (small tables) or the sampled first level + sel_finish (large tables)
+// on the kept per-group values; *kind = EARLY_NONE when this device / percentile list cannot
+lscat_status early_select(lscat_ctx* ctx, const double* perf, const double* gain, uint64_t lo, uint64_t hi,
+                          const uint64_t* partials, const uint64_t* mm, uint32_t nb, const double* pct,
+                          uint32_t npct, cudaStream_t s, uint32_t* kind);
 // host-side work model
 void kernel_work(uint32_t kernel, uint32_t n, uint64_t* bytes, uint64_t* flops);
 bool block_list_ok(const uint16_t* blocks, uint32_t n);

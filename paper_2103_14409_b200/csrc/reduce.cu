@@ -913,6 +913,9 @@ bool opts_ok(const lscat_reduce_opts* o) {
   if (o->nan_policy > LSCAT_COMPLETE_ONLY) return false;
   if (o->block_profile && (uint64_t)o->n_matrices * o->n_blocks * 12 > 200 * 1024) return false;
   if (o->kernel_rollup > 1 || o->block_profile > 1) return false;
+  if (o->n_percentiles > 64 || (o->n_percentiles && !o->percentiles)) return false;
+  for (uint32_t i = 0; i < o->n_percentiles; i++)
+    if (!(o->percentiles[i] >= 0.0 && o->percentiles[i] <= 1.0)) return false;
   return true;
 }
 
@@ -1156,7 +1159,20 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
     if (ns) return ns;
   }
   if (out->partials) LSCAT_CUDA(ctx, cudaMemcpyAsync(out->partials, p.partials, plen * 8, cudaMemcpyDeviceToDevice, s));
+  // R-27: the percentile selection of opts->percentiles enqueued right behind the reduction
+  // (one rank, not point-sharded, per-group values kept): lscat_stats with the same list only
+  // collects it
+  uint32_t early = EARLY_NONE;
+  const double* perf_k = o->keep_values ? p.o_perf : out->perf;
+  const double* gain_k = o->keep_values ? p.o_gain : out->gain;
+  if (o->n_percentiles && ctx->world == 1 && !o->point_sharded && G && perf_k && gain_k) {
+    lscat_status es = early_select(ctx, perf_k, gain_k, own_lo, own_hi, p.partials, p.minmax, o->bins_per_unit,
+                                   o->percentiles, o->n_percentiles, s, &early);
+    if (es) return es;
+  }
   ReduceState& rs = ctx->rs;
+  rs.early = early;
+  rs.early_pct.assign(o->percentiles, o->percentiles + (early ? o->n_percentiles : 0));
   rs.valid = true;
   rs.opts = *o;
   rs.n_groups = G;

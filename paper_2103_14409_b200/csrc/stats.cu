@@ -626,54 +626,63 @@ __global__ void __launch_bounds__(1024) sel_resolve(SelState* st, uint32_t* __re
 }
 
 // ---- sampled first level (large inputs) -----------------------------------------------
-// Instead of a histogram pass followed by a compaction pass over perf/gain, one pass both
-// counts every key into the fixed bins of selbins.h (exact) and copies out the keys of the
-// bins that, by a sample, hold the targets.  The sample is systematic (every s-th key, s odd)
-// and binned the same way: a target of global rank k has sample rank ~ k ns / n, and the bins
-// of sample ranks k ns / n -/+ (4.5 sqrt(.) + 32) are copied.  After the pass the exact
-// histogram narrows every target to one bin (like a histogram level); if that bin was not
-// copied (a sampling miss) or the copies overflow, the selection restarts on the histogram
-// path, so the result never depends on the sample.  The single-valued bins (perf == 1, gain
-// == 0) are neither counted nor copied: their count is the reducer's perf_hist[nb].
-constexpr int kIvQ = 9;                    // copied bin intervals per quantity (<= percentiles)
-constexpr uint64_t kSampleKeys = 1 << 20;  // about this many samples per quantity
-constexpr uint32_t kCopyStage = 1536;      // per quantity and CTA: copies staged in smem
+// Instead of a histogram pass followed by a compaction pass over perf/gain, one pass counts
+// every key exactly against sample-planned intervals of the fixed bins of selbins.h and copies
+// the keys inside them (R-27):
+//   sample  runs of kSampleRun consecutive keys at kSampleRuns evenly spaced positions (~2^20
+//           keys, 128-byte reads), histogrammed over the fixed bins;
+//   plan    every target's window of sample ranks (rank ~ p ns, +- 4.5 sqrt(.) + 32) as bins,
+//           merged per quantity into <= kIvQ sorted disjoint intervals; the bins inside get an
+//           exact-count slot each, the bins between intervals share one gap counter;
+//   pass    every counted key (perf < 1, finite gain > 0; the single-valued bins perf == 1 <=>
+//           gain == 0 are the reducer's perf_hist[nb]) adds 1 to its slot or gap and the slot
+//           keys are copied;
+//   check   the exact counts in key order (gap 0, interval 0's bins, gap 1, ...) locate every
+//           target: inside a slot it is narrowed to that fixed bin, whose keys all sit in the
+//           copies; in a gap (a sampling miss) or with overflowing copies the selection
+//           restarts on the histogram path, so the result never depends on the sample.
+constexpr int kIvQ = 9;                        // intervals per quantity (<= percentiles)
+constexpr uint32_t kSpSlots = 1024;            // exact-count bins per quantity
+constexpr uint32_t kSpCnt = kSpSlots + kIvQ + 1;  // slots, then gaps 0..niv
+constexpr uint32_t kSpSlotFlag = 0x8000u;      // map entry: slot (else: the gap index)
+constexpr uint64_t kSampleRuns = 1 << 16;      // sampled positions ...
+constexpr uint32_t kSampleRun = 16;            // ... of 16 consecutive keys each
+constexpr uint32_t kSpStage = 64;              // per warp and quantity: copies staged in smem
+static_assert(kIvQ + 1 <= 10, "ten gap fields in two redux words");
 
-struct SampState {
-  uint32_t niv[2];                       // intervals per quantity
-  uint32_t fail;
-  uint32_t pad;
-  uint32_t b1[2][kIvQ], b2[2][kIvQ];     // copied bin intervals (inclusive), sorted, disjoint
-  unsigned long long ncopy_all[2];       // keys copied, summed over ranks (overflow check)
-  unsigned long long ncopy[2];           // keys copied (this rank)
-  uint32_t fh[2][kFxBins];               // exact counts of the counted bins (summed over ranks)
+struct SampPlan {
+  uint32_t fail, pad;
+  uint32_t niv[2], nslot[2];                   // intervals, slots used per quantity
+  uint32_t b1[2][kIvQ], b2[2][kIvQ];           // fixed-bin intervals (inclusive), sorted, disjoint
+  uint32_t slot0[2][kIvQ];                     // slot of each interval's first bin
+  unsigned long long ncopy[2];                 // keys copied (this rank)
+  unsigned long long ncopy_all[2];             // keys copied over all ranks (overflow check)
+  uint32_t cnt[2][kSpCnt];                     // exact counts: slots, then gaps
+  uint16_t map[2][kFxBins];                    // per fixed bin: kSpSlotFlag | slot, or its gap
 };
 
 __device__ __forceinline__ bool valid_key(uint64_t k) { return k < 0x7FF0000000000000ull; }
 __device__ __forceinline__ bool virtual_bin(uint32_t w, uint32_t b) { return w == 0 ? b == kFxBins - 2 : b == 0; }
 __device__ __forceinline__ uint32_t fx_bin(uint32_t w, uint64_t k) { return w == 0 ? fx_perf_bin(k) : fx_gain_bin(k); }
 
+// Sample histogram over the fixed bins (the single-valued bins included).  Thread j reads key
+// (j % kSampleRun) of run j / kSampleRun.
 __global__ void __launch_bounds__(256) sel_sample_hist(const double* __restrict__ perf,
                                                        const double* __restrict__ gain, uint64_t lo,
-                                                       uint64_t hi, uint64_t stride,
+                                                       uint64_t hi, uint64_t rstride,
                                                        uint32_t* __restrict__ shist) {
   __shared__ uint32_t h[2 * kFxBins];
   for (uint32_t i = threadIdx.x; i < 2 * kFxBins; i += blockDim.x) h[i] = 0;
   __syncthreads();
-  const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; lo + j * stride < hi; j += 4 * T) {
-    uint64_t kp[4], kg[4];  // four independent samples in flight per thread
-#pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const uint64_t i = lo + (j + u * T) * stride;
-      kp[u] = i < hi ? (uint64_t)__double_as_longlong(__ldcs(perf + i)) : kNaNKey;
-      kg[u] = i < hi ? (uint64_t)__double_as_longlong(__ldcs(gain + i)) : kNaNKey;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; u++) {
-      if (valid_key(kp[u])) atomicAdd(&h[fx_perf_bin(kp[u])], 1u);
-      if (valid_key(kg[u])) atomicAdd(&h[kFxBins + fx_gain_bin(kg[u])], 1u);
-    }
+  const uint64_t total = kSampleRuns * kSampleRun;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < total;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = lo + (j / kSampleRun) * rstride + (j % kSampleRun);
+    if (i >= hi) continue;
+    const uint64_t kp = (uint64_t)__double_as_longlong(__ldcs(perf + i));
+    const uint64_t kg = (uint64_t)__double_as_longlong(__ldcs(gain + i));
+    if (valid_key(kp)) atomicAdd(&h[fx_perf_bin(kp)], 1u);
+    if (valid_key(kg)) atomicAdd(&h[kFxBins + fx_gain_bin(kg)], 1u);
   }
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < 2 * kFxBins; i += blockDim.x)
@@ -719,69 +728,43 @@ __device__ __forceinline__ uint32_t first_reaching(const unsigned long long* P, 
   return a;
 }
 
-// One CTA: targets, and per quantity the merged bin intervals the sample points at.
-__global__ void __launch_bounds__(1024) sel_plan_sampled(SelState* st, SampState* ss,
-                                                         const uint64_t* __restrict__ partials, uint32_t nb,
-                                                         const uint32_t* __restrict__ shist,
-                                                         const uint64_t* __restrict__ mm, PctArg pct,
-                                                         uint32_t npct, double dmul, double dadd) {
+// One CTA of 1024: every target's window of sample ranks (nearest rank ceil(p ns) among the ns
+// sampled keys, +- dmul sqrt(rank) + dadd) as fixed bins, merged per quantity into sorted
+// disjoint intervals, exact-count slots for their bins and a gap index for every other bin;
+// counters zeroed.  A plan that does not fit (more than kIvQ intervals or kSpSlots bins) sets
+// `fail` with every bin in gap 0: the pass still runs, the check reports a miss.
+__global__ void __launch_bounds__(1024) sel_plan_sampled(SampPlan* __restrict__ sp,
+                                                       const uint32_t* __restrict__ shist, PctArg pct,
+                                                       uint32_t npct, double dmul, double dadd) {
   __shared__ unsigned long long pre[2][kFxBins];
   __shared__ unsigned long long part[1024];
   __shared__ uint32_t tb1[kMaxT], tb2[kMaxT];
+  __shared__ uint32_t s_b1[2][kIvQ], s_b2[2][kIvQ], s_slot0[2][kIvQ], s_niv[2], s_fail;
   const int tid = threadIdx.x;
-  const uint64_t n_def = partials[LSCAT_P_RATIO_DEFINED];
-  // the single-valued bins are left out of the scan (0): the targets' sample ranks are shifted
-  // past them below
   for (uint32_t w = 0; w < 2; w++) scan_bins(shist + w * kFxBins, 0ull, w, pre[w], part);
-  if (tid == 0) {
-    st->nt = 2 * npct;
-    st->err = 0;
-    st->done_ctas = 0;
-    st->src = 0;
-    st->compact = 0;
-    st->n_def = n_def;
-    st->sampled_fail = 0;
-    st->r0_valid = 0;
-    st->nr = 0;
-    ss->fail = 0;
-  }
   if (tid < (int)(2 * npct)) {
-    Tgt t{};
-    t.which = tid >= (int)npct;
-    const double r = ceil(pct.p[tid % npct] * (double)n_def);  // nearest rank (R-13)
-    t.k = r < 1.0 ? 1 : (r > (double)n_def ? n_def : (uint64_t)r);
-    t.done = n_def == 0;
-    t.key = kNaNKey;
-    t.lo = mm[2 * t.which];
-    t.hi = mm[2 * t.which + 1];
-    t.count = n_def;
-    st->t[tid] = t;
-    // sample bins of the target's sample-rank window (sample counts of the single-valued bins
-    // included: they sit in shist like any bin)
+    const uint32_t w = tid >= (int)npct;
+    const unsigned long long* P = pre[w];
+    const unsigned long long vs = shist[w * kFxBins + (w == 0 ? kFxBins - 2 : 0)];
+    const unsigned long long total = P[kFxBins - 1], ns = total + vs;
     uint32_t b1 = 1, b2 = 0;  // empty
-    const unsigned long long* P = pre[t.which];
-    const uint32_t w = t.which;
-    const unsigned long long ns = P[kFxBins - 1] + shist[w * kFxBins + (w == 0 ? kFxBins - 2 : 0)];
-    if (!t.done && ns > 0) {
-      const unsigned long long vs = shist[w * kFxBins + (w == 0 ? kFxBins - 2 : 0)];
-      const double ks = (double)t.k * (double)ns / (double)n_def;
-      const double d = dmul * sqrt(ks > 1.0 ? ks : 1.0) + dadd;
+    if (ns > 0 && total > 0) {
+      const double r = ceil(pct.p[tid % npct] * (double)ns);
+      const double ks = r < 1.0 ? 1.0 : (r > (double)ns ? (double)ns : r);
+      const double d = dmul * sqrt(ks) + dadd;
       // sample ranks among the counted keys: the single-valued bin sits first (gain == 0) or
       // last (perf == 1) in key order
       const double off = w == 1 ? (double)vs : 0.0;
       const double s_lo = fmax(1.0, floor(ks - d - off)), s_hi = fmax(1.0, ceil(ks + d - off));
-      const unsigned long long total = P[kFxBins - 1];
-      if (total > 0) {
-        b1 = first_reaching(P, (unsigned long long)fmin(s_lo, (double)total));
-        b2 = first_reaching(P, (unsigned long long)fmin(s_hi, (double)total));
-      }
+      b1 = first_reaching(P, (unsigned long long)fmin(s_lo, (double)total));
+      b2 = first_reaching(P, (unsigned long long)fmin(s_hi, (double)total));
     }
     tb1[tid] = b1;
     tb2[tid] = b2;
   }
   __syncthreads();
-  if (tid == 0) {  // per quantity: sort the targets' bin intervals, merge overlapping ones
-    bool fail = false;
+  if (tid == 0) {  // per quantity: sort the targets' intervals, merge overlapping / adjacent ones
+    uint32_t fail = 0;
     for (uint32_t w = 0; w < 2; w++) {
       uint32_t idx[kMaxT / 2], n = 0;
       for (uint32_t i = 0; i < npct; i++)
@@ -790,78 +773,95 @@ __global__ void __launch_bounds__(1024) sel_plan_sampled(SelState* st, SampState
         for (uint32_t b = a; b > 0 && tb1[idx[b]] < tb1[idx[b - 1]]; b--) {
           const uint32_t x = idx[b]; idx[b] = idx[b - 1]; idx[b - 1] = x;
         }
-      uint32_t m = 0;
-      for (uint32_t a = 0; a < n; a++) {
+      uint32_t m = 0, slots = 0;
+      for (uint32_t a = 0; a < n && !fail; a++) {
         const uint32_t i = idx[a];
-        if (m > 0 && tb1[i] <= ss->b2[w][m - 1] + 1) {
-          if (tb2[i] > ss->b2[w][m - 1]) ss->b2[w][m - 1] = tb2[i];
+        if (m > 0 && tb1[i] <= s_b2[w][m - 1] + 1) {
+          if (tb2[i] > s_b2[w][m - 1]) s_b2[w][m - 1] = tb2[i];
+        } else if (m == kIvQ) {
+          fail = 1;
         } else {
-          if (m == kIvQ) { fail = true; break; }
-          ss->b1[w][m] = tb1[i];
-          ss->b2[w][m] = tb2[i];
+          s_b1[w][m] = tb1[i];
+          s_b2[w][m] = tb2[i];
           m++;
         }
       }
-      ss->niv[w] = m;
-      ss->ncopy_all[w] = 0;
-      ss->ncopy[w] = 0;
+      for (uint32_t r = 0; r < m; r++) {
+        s_slot0[w][r] = slots;
+        slots += s_b2[w][r] - s_b1[w][r] + 1;
+      }
+      if (slots > kSpSlots) fail = 1;
+      s_niv[w] = m;
+      sp->nslot[w] = slots;
     }
-    if (fail) ss->fail = 1;
+    if (fail) s_niv[0] = s_niv[1] = 0;  // every bin in gap 0
+    s_fail = fail;
+    sp->fail = fail;
+    for (uint32_t w = 0; w < 2; w++) {
+      sp->niv[w] = s_niv[w];
+      sp->ncopy[w] = 0;
+      sp->ncopy_all[w] = 0;
+      for (uint32_t r = 0; r < s_niv[w]; r++) {
+        sp->b1[w][r] = s_b1[w][r];
+        sp->b2[w][r] = s_b2[w][r];
+        sp->slot0[w][r] = s_slot0[w][r];
+      }
+    }
   }
-  for (uint32_t i = tid; i < 2 * kFxBins; i += blockDim.x) (&ss->fh[0][0])[i] = 0;
-  (void)nb;
+  __syncthreads();
+  for (uint32_t i = tid; i < 2 * kFxBins; i += blockDim.x) {
+    const uint32_t w = i / kFxBins, b = i % kFxBins;
+    uint32_t e = 0;  // gap = intervals entirely below b
+    for (uint32_t r = 0; r < s_niv[w]; r++) {
+      if (b > s_b2[w][r]) e = r + 1;
+      else if (b >= s_b1[w][r]) { e = kSpSlotFlag | (s_slot0[w][r] + b - s_b1[w][r]); break; }
+    }
+    sp->map[w][b] = (uint16_t)e;
+  }
+  for (uint32_t i = tid; i < 2 * kSpCnt; i += blockDim.x) (&sp->cnt[0][0])[i] = 0;
 }
 
-// One pass over this rank's keys: exact counts of the counted bins (privatised in shared
-// memory) and copies of the keys in the sample's bin intervals (staged per CTA in shared
-// memory, flushed with one global reservation per CTA and quantity whenever a stage fills).
+// One pass over this rank's keys (kU per quantity in flight per thread): each counted key
+// adds 1 to its slot or gap and the slot keys are copied.  Gaps (most keys, a few hot
+// counters): a packed one-hot (6-bit fields, gaps 0-4 / 5-9 in two words) summed over the warp
+// by two redux.sync adds, lane j accumulating field j in a register; slots (spread over many
+// bins): one shared atomic per key; copies: a per-warp shared stage flushed 32 keys at a time
+// with one reservation.
 template <int kT>
 __global__ void __launch_bounds__(kT) sel_pass_sampled(const double* __restrict__ perf,
                                                        const double* __restrict__ gain, uint64_t lo,
-                                                       uint64_t hi, SampState* __restrict__ ss,
+                                                       uint64_t hi, SampPlan* __restrict__ sp,
                                                        double* __restrict__ cbuf) {
   constexpr int kU = 8;
-  constexpr int kTilesPerCheck = 4;  // stage checked every 4 tiles (copies are ~5 % of keys;
-                                     // a stage that fills in between spills to global atomics)
-  __shared__ uint32_t h[2 * kFxBins];
-  __shared__ uint8_t cmap[2 * kFxBins];
-  __shared__ uint64_t stage[2][kCopyStage];
-  __shared__ uint32_t s_nc[2];
-  __shared__ unsigned long long s_base[2];
-  const bool on = !ss->fail;
-  for (uint32_t i = threadIdx.x; i < 2 * kFxBins; i += kT) { h[i] = 0; cmap[i] = 0; }
-  if (threadIdx.x < 2) s_nc[threadIdx.x] = 0;
-  __syncthreads();
-  if (on)
-    for (uint32_t w = 0; w < 2; w++)
-      for (uint32_t r = 0; r < ss->niv[w]; r++)
-        for (uint32_t b = ss->b1[w][r] + threadIdx.x; b <= ss->b2[w][r]; b += kT)
-          cmap[w * kFxBins + b] = !virtual_bin(w, b);
+  __shared__ uint16_t map[2 * kFxBins];
+  __shared__ uint32_t cnt[2 * kSpCnt];
+  __shared__ uint64_t stage[kT / 32][2][kSpStage];
+  for (uint32_t i = threadIdx.x; i < 2 * kFxBins; i += kT) map[i] = (&sp->map[0][0])[i];
+  for (uint32_t i = threadIdx.x; i < 2 * kSpCnt; i += kT) cnt[i] = 0;
   __syncthreads();
   const unsigned FULL = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  auto flush = [&]() {  // CTA-wide: reserve once per quantity, copy the stage out (keys past
-                        // kCopyStage went straight to the global buffer with their own reservation)
-    __syncthreads();
-    if (threadIdx.x < 2 && s_nc[threadIdx.x]) {
-      const uint32_t n = min(s_nc[threadIdx.x], kCopyStage);
-      s_base[threadIdx.x] = atomicAdd(&ss->ncopy[threadIdx.x], (unsigned long long)n);
-      atomicAdd(&ss->ncopy_all[threadIdx.x], (unsigned long long)n);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t gacc[2] = {0u, 0u}, nst[2] = {0u, 0u};
+  auto flush_stage = [&](uint32_t w, uint32_t n) {  // warp-collective: the first n staged keys
+    uint64_t* sw = stage[wid][w];
+    __syncwarp();
+    unsigned long long base = 0;
+    if (lane == 0) {
+      base = atomicAdd(&sp->ncopy[w], (unsigned long long)n);
+      atomicAdd(&sp->ncopy_all[w], (unsigned long long)n);
     }
-    __syncthreads();
-#pragma unroll
-    for (int w = 0; w < 2; w++)
-      for (uint32_t i = threadIdx.x; i < min(s_nc[w], kCopyStage); i += kT) {
-        const unsigned long long g = s_base[w] + i;
-        if (g < kCompactCap) reinterpret_cast<uint64_t*>(cbuf)[(size_t)w * kCompactCap + g] = stage[w][i];
-      }
-    __syncthreads();
-    if (threadIdx.x < 2) s_nc[threadIdx.x] = 0;
-    __syncthreads();
+    base = __shfl_sync(FULL, base, 0);
+    if ((uint32_t)lane < n && base + lane < kCompactCap)
+      reinterpret_cast<uint64_t*>(cbuf)[(size_t)w * kCompactCap + base + lane] = sw[lane];
+    const uint32_t rest = nst[w] - n;
+    const uint64_t v = (uint32_t)lane < rest ? sw[n + lane] : 0ull;
+    __syncwarp();
+    if ((uint32_t)lane < rest) sw[lane] = v;
+    __syncwarp();
+    nst[w] = rest;
   };
   const uint64_t cstride = (uint64_t)gridDim.x * kT * kU;
-  int tile = 0;
-  for (uint64_t base = lo + blockIdx.x * (uint64_t)kT * kU; base < hi; base += cstride, tile++) {
+  for (uint64_t base = lo + blockIdx.x * (uint64_t)kT * kU; base < hi; base += cstride) {
     uint64_t v[2][kU];
 #pragma unroll
     for (int w = 0; w < 2; w++) {
@@ -875,86 +875,177 @@ __global__ void __launch_bounds__(kT) sel_pass_sampled(const double* __restrict_
 #pragma unroll
     for (int u = 0; u < kU; u++) {
 #pragma unroll
-      for (int w = 0; w < 2; w++) {
+      for (uint32_t w = 0; w < 2; w++) {
         const uint64_t k = v[w][u];
         const uint32_t kh = (uint32_t)(k >> 32);  // bins from the high word (32-bit arithmetic)
         // perf < 1 (and not NaN) / gain > 0 (no gain is below 2^-32 but 0) and not NaN
         const bool counted = w == 0 ? kh < (uint32_t)(kPerfOne >> 32) : (kh != 0 && kh < 0x7FF00000u);
         const uint32_t b = counted ? (w == 0 ? fx_perf_bin_hi(kh) : fx_gain_bin_hi(kh)) : 0u;
-        if (counted) atomicAdd(&h[w * kFxBins + b], 1u);
-        const bool copy = on && counted && cmap[w * kFxBins + b];
-        const unsigned m = __ballot_sync(FULL, copy);
+        const uint32_t e = counted ? (uint32_t)map[w * kFxBins + b] : 0u;
+        const bool slot = counted && (e & kSpSlotFlag);
+        const bool gap = counted && !slot;
+        const uint32_t plo = (gap && e < 5) ? 1u << (6 * e) : 0u;
+        const uint32_t phi = (gap && e >= 5) ? 1u << (6 * (e - 5)) : 0u;
+        const uint32_t rl = __reduce_add_sync(FULL, plo), rh = __reduce_add_sync(FULL, phi);
+        gacc[w] += lane < 10 ? ((lane < 5 ? rl : rh) >> (6 * (lane % 5))) & 63u : 0u;
+        if (slot) atomicAdd(&cnt[w * kSpCnt + (e & (kSpSlotFlag - 1))], 1u);
+        const unsigned m = __ballot_sync(FULL, slot);
         if (m) {
-          const int leader = __ffs(m) - 1;
-          uint32_t at = 0;
-          if (lane == leader) at = atomicAdd(&s_nc[w], (uint32_t)__popc(m));
-          at = __shfl_sync(FULL, at, leader) + __popc(m & ((1u << lane) - 1u));
-          if (copy) {
-            if (at < kCopyStage) {
-              stage[w][at] = k;
-            } else {  // stage full between two checks: straight to the global buffer
-              const unsigned long long g = atomicAdd(&ss->ncopy[w], 1ull);
-              atomicAdd(&ss->ncopy_all[w], 1ull);
-              if (g < kCompactCap) reinterpret_cast<uint64_t*>(cbuf)[(size_t)w * kCompactCap + g] = k;
-            }
-          }
+          if (slot) stage[wid][w][nst[w] + __popc(m & ((1u << lane) - 1u))] = k;
+          nst[w] += __popc(m);
+          if (nst[w] >= 32) flush_stage(w, 32);
         }
       }
     }
-    if (tile % kTilesPerCheck == kTilesPerCheck - 1) {
-      __syncthreads();
-      const bool full = s_nc[0] > kCopyStage / 2 || s_nc[1] > kCopyStage / 2;
-      if (full) flush();  // CTA-uniform
-    }
   }
-  flush();
-  for (uint32_t i = threadIdx.x; i < 2 * kFxBins; i += kT)
-    if (h[i]) atomicAdd(&ss->fh[0][0] + i, h[i]);
+#pragma unroll
+  for (uint32_t w = 0; w < 2; w++) {
+    if (nst[w]) flush_stage(w, nst[w]);
+    if (lane < 10 && gacc[w]) atomicAdd(&cnt[w * kSpCnt + kSpSlots + lane], gacc[w]);
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < 2 * kSpCnt; i += kT)
+    if (cnt[i]) atomicAdd(&sp->cnt[0][0] + i, cnt[i]);
 }
 
-// One CTA of 1024: the exact histogram narrows every target to one bin; a bin that was not
-// copied (a sampling miss) or copies beyond the buffer -> sampled_fail (the host restarts on
-// the histogram path).  Otherwise the passes read the copies from now on and the open
-// targets are planned into ranges.
-__global__ void __launch_bounds__(1024) sel_check_sampled(SelState* st, SampState* ss,
-                                                          const uint64_t* __restrict__ partials,
-                                                          uint32_t nb, const uint64_t* __restrict__ mm,
-                                                          uint32_t cap, uint32_t force_miss) {
-  __shared__ unsigned long long pre[2][kFxBins];
-  __shared__ unsigned long long part[1024];
-  __shared__ uint32_t s_fail;
-  const int tid = threadIdx.x;
+// One CTA of 1024, after the pass (its counts summed over ranks): targets from the exact n_def (sel_init's ranks, R-13),
+// each target located among the exact counts in key order.  Per quantity the counts form the
+// sequence gap 0, interval 0's slots, gap 1, ..., gap niv, plus the single-valued bin (the
+// reducer's perf_hist[nb]: perf == 1 is the largest key, gain == 0 the smallest; the plan's
+// windows never contain it, so it sits after the last gap resp. before gap 0).  A block scan of
+// the sequence, then every target binary-searches its rank.  Inside a slot: narrowed to that
+// fixed bin, whose keys all sit in the copies (the state sel_check_sampled leaves); in a gap, a
+// total that differs from n_def, an unexpected plan or overflowing copies: sampled_fail (the
+// host runs the full selection).
+constexpr uint32_t kSpSeq = kSpCnt + 1;  // slots + gaps + the single-valued bin
+static_assert(kSpSeq <= 2048, "two elements per thread in the check's scan");
+__global__ void __launch_bounds__(1024) sel_check_sampled(SelState* st, const SampPlan* __restrict__ sp,
+                                                        const uint64_t* __restrict__ partials, uint32_t nb,
+                                                        const uint64_t* __restrict__ mm, PctArg pct,
+                                                        uint32_t npct, uint32_t cap, uint32_t force_miss) {
+  __shared__ unsigned long long pre[2][2048];
+  __shared__ uint16_t sbin[2][2048];  // bin of a slot / the single-valued bin; 0xFFFF: a gap
+  __shared__ unsigned long long wsum[32];
+  __shared__ uint32_t s_fail, s_len[2];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const unsigned FULL = 0xffffffffu;
+  const uint64_t n_def = partials[LSCAT_P_RATIO_DEFINED];
   const unsigned long long n_one = partials[LSCAT_P_NCOUNTERS + nb];  // perf == 1 <=> gain == 0
-  for (uint32_t w = 0; w < 2; w++) scan_bins(ss->fh[w], n_one, w, pre[w], part);
-  if (tid == 0)
-    s_fail = force_miss || ss->fail || ss->ncopy_all[0] > kCompactCap || ss->ncopy_all[1] > kCompactCap ||
-             pre[0][kFxBins - 1] != st->n_def || pre[1][kFxBins - 1] != st->n_def;
+  if (tid == 0) {
+    s_fail = force_miss || sp->fail || sp->ncopy_all[0] > kCompactCap || sp->ncopy_all[1] > kCompactCap;
+    for (uint32_t w = 0; w < 2; w++) {
+      s_len[w] = sp->nslot[w] + sp->niv[w] + 2;
+      // the single-valued bin must lie in the end gap (it never enters a sample window)
+      const uint32_t ve = sp->map[w][w == 0 ? kFxBins - 2 : 0];
+      if ((ve & kSpSlotFlag) || ve != (w == 0 ? sp->niv[w] : 0u)) s_fail = 1;
+    }
+  }
   __syncthreads();
-  if (tid < (int)st->nt && !s_fail) {
-    Tgt& t = st->t[tid];
-    if (!t.done) {
+  for (uint32_t w = 0; w < 2; w++) {
+    // element e of the sequence -> count and bin (gain: the single-valued bin first)
+    const uint32_t niv = sp->niv[w], len = s_len[w];
+    for (uint32_t e = tid; e < 2048; e += blockDim.x) {
+      unsigned long long c = 0;
+      uint32_t bin = 0xFFFFu;
+      if (e < len) {
+        const uint32_t q = w == 1 ? e : (e + 1 == len ? 0xFFFFFFFFu : e + 1);  // position after the gain bin
+        if (w == 1 ? e == 0 : e + 1 == len) {
+          c = n_one;
+          bin = w == 0 ? kFxBins - 2 : 0;
+        } else {
+          // q - 1 = position in gap 0, slots..., gap niv; interval iv's slots start at slot0 + iv + 1
+          const uint32_t x = q - 1;
+          uint32_t iv = 0;
+          while (iv < niv && x >= sp->slot0[w][iv] + iv + 1) iv++;
+          // x in [slot0[iv-1] + iv, slot0[iv] + iv]: gap iv sits at slot0[iv] + iv (or the end)
+          const uint32_t gpos = iv < niv ? sp->slot0[w][iv] + iv : sp->nslot[w] + niv;
+          if (x == gpos) {
+            c = sp->cnt[w][kSpSlots + iv];
+          } else {  // a slot of interval iv - 1
+            const uint32_t r = iv - 1, sl = x - r - 1;
+            c = sp->cnt[w][sl];
+            bin = sp->b1[w][r] + (sl - sp->slot0[w][r]);
+          }
+        }
+      }
+      pre[w][e] = c;
+      sbin[w][e] = (uint16_t)bin;
+    }
+  }
+  __syncthreads();
+  for (uint32_t w = 0; w < 2; w++) {  // inclusive scan of 2048 elements, two per thread
+    const unsigned long long a0 = pre[w][2 * tid], a1 = pre[w][2 * tid + 1];
+    unsigned long long inc = a0 + a1;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(FULL, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      unsigned long long x = wsum[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x += y;
+      }
+      wsum[lane] = x;
+    }
+    __syncthreads();
+    const unsigned long long ex = inc - a0 - a1 + (wid ? wsum[wid - 1] : 0ull);
+    pre[w][2 * tid] = ex + a0;
+    pre[w][2 * tid + 1] = ex + a0 + a1;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    st->nt = 2 * npct;
+    st->err = 0;
+    st->done_ctas = 0;
+    st->src = 0;
+    st->compact = 0;
+    st->n_def = n_def;
+    st->sampled_fail = 0;
+    st->r0_valid = 0;
+    st->nr = 0;
+    st->open = 0;
+    if (pre[0][2047] != n_def || pre[1][2047] != n_def) s_fail = 1;  // every key counted once
+  }
+  __syncthreads();
+  if (tid < (int)(2 * npct)) {
+    Tgt t{};
+    t.which = tid >= (int)npct;
+    const double r = ceil(pct.p[tid % npct] * (double)n_def);  // nearest rank (R-13)
+    t.k = r < 1.0 ? 1 : (r > (double)n_def ? n_def : (uint64_t)r);
+    t.done = n_def == 0;
+    t.key = kNaNKey;
+    t.lo = mm[2 * t.which];
+    t.hi = mm[2 * t.which + 1];
+    t.count = n_def;
+    if (!s_fail && !t.done) {
       const uint32_t w = t.which;
       const unsigned long long* P = pre[w];
-      const uint32_t b = first_reaching(P, t.k);
-      const unsigned long long below = b ? P[b - 1] : 0ull;
-      uint64_t blo, bhi;
-      fx_bin_range(w, b, &blo, &bhi);
-      const uint64_t lo = blo > mm[2 * w] ? blo : mm[2 * w], hi = bhi < mm[2 * w + 1] ? bhi : mm[2 * w + 1];
-      bool copied = virtual_bin(w, b);  // single-valued: decided without copies
-      for (uint32_t r = 0; r < ss->niv[w]; r++) copied |= ss->b1[w][r] <= b && b <= ss->b2[w][r];
-      if (!copied) {
-        atomicOr(&s_fail, 1u);
+      uint32_t lo = 0, hi = 2047;  // smallest e with P[e] >= k
+      while (lo < hi) {
+        const uint32_t m = (lo + hi) / 2;
+        if (P[m] >= t.k) hi = m; else lo = m + 1;
+      }
+      const uint32_t bin = sbin[w][lo];
+      if (bin == 0xFFFFu) {
+        atomicOr(&s_fail, 1u);  // inside a gap: a sampling miss
       } else {
-        t.lo = lo;
-        t.hi = hi;
+        const unsigned long long below = lo ? P[lo - 1] : 0ull;
+        uint64_t blo, bhi;
+        fx_bin_range(w, bin, &blo, &bhi);
+        t.lo = blo > mm[2 * w] ? blo : mm[2 * w];
+        t.hi = bhi < mm[2 * w + 1] ? bhi : mm[2 * w + 1];
         t.k -= below;
-        t.count = P[b] - below;
+        t.count = P[lo] - below;
       }
     }
+    st->t[tid] = t;
   }
   __syncthreads();
   if (s_fail) {
-    if (tid == 0) {  // no open ranges: the levels queued behind this are no-ops
+    if (tid == 0) {
       st->sampled_fail = 1;
       st->nr = 0;
       st->open = 0;
@@ -963,8 +1054,8 @@ __global__ void __launch_bounds__(1024) sel_check_sampled(SelState* st, SampStat
   }
   if (tid == 0) {
     st->src = 1;  // the later passes read the copies
-    st->nc[0] = ss->ncopy[0];
-    st->nc[1] = ss->ncopy[1];
+    st->nc[0] = sp->ncopy[0];
+    st->nc[1] = sp->ncopy[1];
   }
   __syncthreads();
   plan_ranges(st, cap);
@@ -1481,6 +1572,161 @@ __global__ void __launch_bounds__(1024, 1) sel_finish(const SelState* __restrict
   stamp(4);
 }
 
+PctArg pct_arg(const double* pct, uint32_t npct) {
+  PctArg pa{};
+  for (uint32_t i = 0; i < npct; i++) pa.p[i] = pct[i];
+  return pa;
+}
+
+bool coop_supported(lscat_ctx* ctx) {
+  int coop = 0;
+  return cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device) == cudaSuccess && coop;
+}
+
+// Device / pinned buffers of the selection, by scratch name (grow-only, shared by every path).
+struct SelBufs {
+  SelState* st = nullptr;
+  SelState* hst = nullptr;  // pinned
+  uint32_t* hist = nullptr;
+  unsigned long long* cand = nullptr;
+  double* cbuf = nullptr;
+  uint32_t* shist = nullptr;
+  SampPlan* sp = nullptr;
+  FinSel* fs = nullptr;
+  FinSel* fsh = nullptr;  // pinned head
+  unsigned long long* fcand = nullptr;
+};
+
+lscat_status sel_bufs(lscat_ctx* ctx, uint32_t cap, SelBufs* b) {
+  cudaError_t err = cudaSuccess;
+  auto S = [&](const char* name, size_t bytes) { void* p = scratch(ctx, name, bytes, &err); return p; };
+  b->st = (SelState*)S("sel_state", sizeof(SelState));
+  if (!err) b->hist = (uint32_t*)S("sel_hist", (size_t)kMaxR * kBins * 4);
+  if (!err) b->cand = (unsigned long long*)S("sel_cand", (size_t)kMaxR * (cap + 1) * 8);
+  if (!err) b->cbuf = (double*)S("sel_cbuf", 2 * kCompactCap * 8);
+  if (!err) b->shist = (uint32_t*)S("sel_shist", 2 * kFxBins * 4);
+  if (!err) b->sp = (SampPlan*)S("sel_samp", sizeof(SampPlan));
+  if (!err) b->fs = (FinSel*)S("sel_fin", sizeof(FinSel));
+  if (!err) b->fcand = (unsigned long long*)S("sel_fin_cand", (size_t)kMaxT * kSmallCap * 8);
+  if (err) return cuda_fail(ctx, err, "selection: scratch");
+  b->hst = (SelState*)pinned(ctx, "sel_state_h", sizeof(SelState), &err);
+  if (!err) b->fsh = (FinSel*)pinned(ctx, "sel_fin_h", kFinHead, &err);
+  if (err) return cuda_fail(ctx, err, "selection: pinned");
+  return LSCAT_OK;
+}
+
+// The sampled first level on stream q: sample, plan, pass, (NCCL sums,) check.  With `fin`
+// (one rank) the state after the check is copied to the host and sel_finish follows
+// (launch_finish); else the caller enqueues levels.
+lscat_status enqueue_sampled(lscat_ctx* ctx, const SelBufs& B, const double* perf, const double* gain,
+                             uint64_t lo, uint64_t hi, const uint64_t* partials, const uint64_t* mm,
+                             uint32_t nb, const PctArg& pa, uint32_t npct, uint32_t cap, bool fin,
+                             cudaStream_t q) {
+  const int world = ctx->world;
+  const uint64_t n = hi - lo;
+  LSCAT_CUDA(ctx, cudaMemsetAsync(B.hist, 0, (size_t)kMaxR * kBins * 4, q));
+  LSCAT_CUDA(ctx, cudaMemsetAsync(B.cand, 0, (size_t)kMaxR * 8, q));
+  LSCAT_CUDA(ctx, cudaMemsetAsync(B.shist, 0, 2 * kFxBins * 4, q));
+  const uint64_t rstride = std::max<uint64_t>(kSampleRun, n / kSampleRuns);
+  const int grid_s = (int)std::min<uint64_t>(kSampleRuns * kSampleRun / 256, (uint64_t)ctx->sm_count * 2);
+  sel_sample_hist<<<grid_s, 256, 0, q>>>(perf, gain, lo, hi, rstride, B.shist);
+  LSCAT_CUDA(ctx, cudaGetLastError());
+  if (world > 1) {
+    lscat_status ns = ctx->comm->allreduce(ctx, {{B.shist, 2 * (size_t)kFxBins, DT::U32, Op::Sum}}, q);
+    if (ns) return ns;
+  }
+  sel_plan_sampled<<<1, 1024, 0, q>>>(B.sp, B.shist, pa, npct, 4.5, 32.0);
+  LSCAT_CUDA(ctx, cudaGetLastError());
+  static const int occ_p = [] {  // resident CTAs per SM of the pass (binary property; one-time)
+    int v = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, sel_pass_sampled<256>, 256, 0);
+    cudaGetLastError();
+    return std::max(v, 1);
+  }();
+  const int grid_p = (int)std::min<uint64_t>(std::max<uint64_t>(1, (n + 256 * 8 - 1) / (256 * 8)),
+                                             (uint64_t)ctx->sm_count * occ_p);
+  sel_pass_sampled<256><<<grid_p, 256, 0, q>>>(perf, gain, lo, hi, B.sp, B.cbuf);
+  LSCAT_CUDA(ctx, cudaGetLastError());
+  if (world > 1) {  // exact counts and copy totals over all ranks
+    lscat_status ns = ctx->comm->allreduce(ctx, {{&B.sp->cnt[0][0], 2 * (size_t)kSpCnt, DT::U32, Op::Sum},
+                                                 {&B.sp->ncopy_all[0], 2, DT::U64, Op::Sum}}, q);
+    if (ns) return ns;
+  }
+  // LSCAT_SEL_FORCE_MISS=1 (tests): every sampled first level reports a miss
+  static const uint32_t force_miss = getenv("LSCAT_SEL_FORCE_MISS") != nullptr ? 1u : 0u;
+  sel_check_sampled<<<1, 1024, 0, q>>>(B.st, B.sp, partials, nb, mm, pa, npct, cap, force_miss);
+  LSCAT_CUDA(ctx, cudaGetLastError());
+  if (fin) {  // sel_finish follows; the state as the check left it
+    LSCAT_CUDA(ctx, cudaMemsetAsync(B.fs, 0, sizeof(FinSel), q));
+    LSCAT_CUDA(ctx, cudaMemcpyAsync(B.hst, B.st, sizeof(SelState), cudaMemcpyDeviceToHost, q));
+  }
+  return LSCAT_OK;
+}
+
+// One rank, after enqueue_sampled(fin): the rest of the selection in one cooperative launch;
+// its result head is copied to the host.
+lscat_status launch_finish(lscat_ctx* ctx, const SelBufs& B, cudaStream_t q) {
+  LSCAT_CUDA(ctx, ensure_smem_attr((const void*)sel_finish, kFinSmem));
+  // LSCAT_SEL_FIN_FORCE_FAIL=1 (tests): sel_finish hands over to the chain at once
+  static const uint32_t ff = getenv("LSCAT_SEL_FIN_FORCE_FAIL") != nullptr ? 1u : 0u;
+  const SelState* st_c = B.st;
+  const double* cb_c = B.cbuf;
+  FinSel* fs = B.fs;
+  unsigned long long* fc = B.fcand;
+  uint32_t ff_ = ff;
+  void* args[] = {(void*)&st_c, (void*)&cb_c, (void*)&fs, (void*)&fc, (void*)&ff_};
+  LSCAT_CUDA(ctx, cudaLaunchCooperativeKernel((const void*)sel_finish, dim3(ctx->sm_count), dim3(1024), args,
+                                              kFinSmem, q));
+  LSCAT_CUDA(ctx, cudaMemcpyAsync(B.fsh, B.fs, kFinHead, cudaMemcpyDeviceToHost, q));
+  ctx->launches++;
+  return LSCAT_OK;
+}
+
+}  // namespace
+
+lscat_status early_select(lscat_ctx* ctx, const double* perf, const double* gain, uint64_t lo, uint64_t hi,
+                          const uint64_t* partials, const uint64_t* mm, uint32_t nb, const double* pct,
+                          uint32_t npct, cudaStream_t s, uint32_t* kind) {
+  *kind = EARLY_NONE;
+  if (ctx->world != 1 || !coop_supported(ctx) || hi <= lo) return LSCAT_OK;
+  static const bool no_small = getenv("LSCAT_SEL_NOSMALL") != nullptr;
+  static const bool no_sample = getenv("LSCAT_SEL_NOSAMPLE") != nullptr;
+  static const bool no_finish = getenv("LSCAT_SEL_NOFINISH") != nullptr;
+  const PctArg pa = pct_arg(pct, npct);
+  cudaError_t err;
+  if (hi - lo <= kSmallKeys) {  // the one-launch selection
+    if (no_small) return LSCAT_OK;
+    SmallSel* sm = (SmallSel*)scratch(ctx, "sel_small", sizeof(SmallSel), &err);
+    if (err) return cuda_fail(ctx, err, "reduce_table: scratch");
+    auto* scand = (unsigned long long*)scratch(ctx, "sel_small_cand", (size_t)kMaxT * kSmallCap * 8, &err);
+    if (err) return cuda_fail(ctx, err, "reduce_table: scratch");
+    SmallSel* hsm = (SmallSel*)pinned(ctx, "sel_small_h", sizeof(SmallSel), &err);
+    if (err) return cuda_fail(ctx, err, "reduce_table: pinned");
+    constexpr size_t kSmallSmem = (size_t)kSmallCap * 8;
+    LSCAT_CUDA(ctx, ensure_smem_attr((const void*)sel_small, kSmallSmem));
+    LSCAT_CUDA(ctx, cudaMemsetAsync(sm, 0, sizeof(SmallSel), s));
+    void* args[] = {(void*)&perf, (void*)&gain, (void*)&lo, (void*)&hi, (void*)&partials,
+                    (void*)&mm, (void*)&pa, (void*)&npct, (void*)&sm, (void*)&scand};
+    LSCAT_CUDA(ctx, cudaLaunchCooperativeKernel((const void*)sel_small, dim3(ctx->sm_count), dim3(1024), args,
+                                                kSmallSmem, s));
+    ctx->launches++;
+    LSCAT_CUDA(ctx, cudaMemcpyAsync(hsm, sm, kSmallHead, cudaMemcpyDeviceToHost, s));
+    *kind = EARLY_SMALL;
+    return LSCAT_OK;
+  }
+  if (npct > (uint32_t)kIvQ || no_sample || no_finish) return LSCAT_OK;
+  SelBufs B;
+  lscat_status bs = sel_bufs(ctx, 8192, &B);
+  if (bs) return bs;
+  if ((bs = enqueue_sampled(ctx, B, perf, gain, lo, hi, partials, mm, nb, pa, npct, 8192, true, s))) return bs;
+  ctx->launches += 4;
+  if ((bs = launch_finish(ctx, B, s))) return bs;
+  *kind = EARLY_SAMPLED;
+  return LSCAT_OK;
+}
+
+namespace {
+
 lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct, double* out_perf,
                                 double* out_gain, cudaStream_t s) {
   const ReduceState& rs = ctx->rs;
@@ -1488,21 +1734,18 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
   const uint32_t cap = world > 1 ? 1024 : 8192;
   const size_t cand_len = (size_t)kMaxR * (cap + 1);
   cudaError_t err;
-  SelState* st = (SelState*)scratch(ctx, "sel_state", sizeof(SelState), &err);
-  if (err) return cuda_fail(ctx, err, "stats: scratch");
-  uint32_t* hist = (uint32_t*)scratch(ctx, "sel_hist", (size_t)kMaxR * kBins * 4, &err);
-  if (err) return cuda_fail(ctx, err, "stats: scratch");
-  auto* cand = (unsigned long long*)scratch(ctx, "sel_cand", cand_len * 8, &err);
-  if (err) return cuda_fail(ctx, err, "stats: scratch");
+  SelBufs B;
+  if (lscat_status bs = sel_bufs(ctx, cap, &B)) return bs;
+  SelState* st = B.st;
+  uint32_t* hist = B.hist;
+  unsigned long long* cand = B.cand;
   unsigned long long* cand_all = cand;
   if (world > 1) {
     cand_all = (unsigned long long*)scratch(ctx, "sel_cand_all", (size_t)world * cand_len * 8, &err);
     if (err) return cuda_fail(ctx, err, "stats: scratch");
   }
-  double* cbuf = (double*)scratch(ctx, "sel_cbuf", 2 * kCompactCap * 8, &err);
-  if (err) return cuda_fail(ctx, err, "stats: scratch");
-  SelState* hst = (SelState*)pinned(ctx, "sel_state_h", sizeof(SelState), &err);
-  if (err) return cuda_fail(ctx, err, "stats: pinned");
+  double* cbuf = B.cbuf;
+  SelState* hst = B.hst;
   constexpr int kT0 = 512, kT1 = 256;
   const int pass_smem = kSmemRanges * kBins * 4, res_smem = (int)cap * 8;
   // kernel attributes and occupancy: once per process (per resolve smem size)
@@ -1537,8 +1780,33 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
   const int lpb = small ? kLevelsPerBatchSmall : kLevelsPerBatch;
   PctArg pa{};
   for (uint32_t i = 0; i < npct; i++) pa.p[i] = pct[i];
+  // R-27: lscat_reduce_table already enqueued the selection of these percentiles
+  const bool early_match = rs.early != EARLY_NONE && rs.early_pct.size() == npct &&
+                           std::equal(rs.early_pct.begin(), rs.early_pct.end(), pct);
+  const bool early_sm = early_match && rs.early == EARLY_SMALL;
+  const bool early_samp = early_match && rs.early == EARLY_SAMPLED;
+  // any other selection reuses the state buffers the early result sits in
+  if (!early_match) ctx->rs.early = EARLY_NONE;
+  static const bool dbg_early = getenv("LSCAT_SEL_DEBUG") != nullptr;
+  if (dbg_early && early_match) fprintf(stderr, "sel early %s\n", early_sm ? "small" : "sampled");
+  if (early_sm) {  // the one-launch selection ran right after the reducer
+    SmallSel* hsm = (SmallSel*)pinned(ctx, "sel_small_h", sizeof(SmallSel), &err);
+    if (err) return cuda_fail(ctx, err, "stats: pinned");
+    LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
+    if (dbg_early) fprintf(stderr, "sel early small: fail %u\n", hsm->fail);
+    if (!hsm->fail) {
+      for (uint32_t i = 0; i < 2 * npct; i++) {
+        double v;
+        memcpy(&v, &hsm->tkey[i], 8);
+        (i >= npct ? out_gain : out_perf)[i % npct] = v;
+      }
+      return LSCAT_OK;
+    }
+    ctx->sel_fallbacks++;  // a bin too large for one CTA: the chain below
+    ctx->rs.early = EARLY_NONE;
+  }
   static const bool no_small = getenv("LSCAT_SEL_NOSMALL") != nullptr;
-  if (small && world == 1 && !no_small && npct <= kMaxT / 2) {  // one cooperative launch
+  if (small && world == 1 && !no_small && !early_sm && npct <= kMaxT / 2) {  // one cooperative launch
     int coop = 0;
     LSCAT_CUDA(ctx, cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device));
     constexpr size_t kSmallSmem = (size_t)kSmallCap * 8;  // >= 2 x kBins x 4
@@ -1609,75 +1877,17 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
     return LSCAT_OK;
   };
   // sampled first level (large inputs, <= kIvQ percentiles; LSCAT_SEL_NOSAMPLE=1 disables it)
-  SampState* ss = (SampState*)scratch(ctx, "sel_samp", sizeof(SampState), &err);
-  if (err) return cuda_fail(ctx, err, "stats: scratch");
-  uint32_t* shist = (uint32_t*)scratch(ctx, "sel_shist", 2 * kFxBins * 4, &err);
-  if (err) return cuda_fail(ctx, err, "stats: scratch");
   static const bool no_sample = getenv("LSCAT_SEL_NOSAMPLE") != nullptr;
-  // interval half-width in sample ranks: dmul sqrt(rank) + dadd
-  // LSCAT_SEL_FORCE_MISS=1 (tests): every sampled first level reports a miss, exercising the
-  // restart on the histogram path
-  static const bool force_miss = getenv("LSCAT_SEL_FORCE_MISS") != nullptr;
-  const double dmul = 4.5, dadd = 32.0;
-  bool sampled = !small && npct <= (uint32_t)kIvQ && !no_sample;
-  const uint64_t stride = std::max<uint64_t>(1, n / kSampleKeys) | 1;  // odd: no period-2^k alias
-  const int grid_s = (int)std::min<uint64_t>(std::max<uint64_t>(1, (n / stride + 1023) / 1024),
-                                             (uint64_t)ctx->sm_count * 8);
-  static const int occ_p = [] {  // resident CTAs per SM of the sampled pass (binary property;
-    int v = 0;                    // thread-safe one-time query)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, sel_pass_sampled<256>, 256, 0);
-    cudaGetLastError();
-    return std::max(v, 1);
-  }();
-  const int grid_p = (int)std::min<uint64_t>(std::max<uint64_t>(1, (n + 256 * 8 - 1) / (256 * 8)),
-                                             (uint64_t)ctx->sm_count * occ_p);
+  bool sampled = early_samp || (!small && npct <= (uint32_t)kIvQ && !no_sample);
   // one rank: the levels after the sampled first level run as one cooperative sel_finish
   // (LSCAT_SEL_NOFINISH=1 keeps the chain)
   static const bool no_finish = getenv("LSCAT_SEL_NOFINISH") != nullptr;
-  int coop_ok = 0;
-  if (sampled && world == 1 && !no_finish)
-    LSCAT_CUDA(ctx, cudaDeviceGetAttribute(&coop_ok, cudaDevAttrCooperativeLaunch, ctx->device));
-  const bool fin = coop_ok != 0;
-  FinSel* fs = nullptr;
-  FinSel* fsh = nullptr;
-  unsigned long long* fcand = nullptr;
-  if (fin) {
-    fs = (FinSel*)scratch(ctx, "sel_fin", sizeof(FinSel), &err);
-    if (err) return cuda_fail(ctx, err, "stats: scratch");
-    fcand = (unsigned long long*)scratch(ctx, "sel_fin_cand", (size_t)kMaxT * kSmallCap * 8, &err);
-    if (err) return cuda_fail(ctx, err, "stats: scratch");
-    fsh = (FinSel*)pinned(ctx, "sel_fin_h", kFinHead, &err);
-    if (err) return cuda_fail(ctx, err, "stats: pinned");
-    LSCAT_CUDA(ctx, ensure_smem_attr((const void*)sel_finish, kFinSmem));
-  }
+  const bool fin = early_samp || (sampled && world == 1 && !no_finish && coop_supported(ctx));
+  FinSel* fsh = B.fsh;
   auto enqueue_first_sampled = [&](cudaStream_t q) -> lscat_status {
-    LSCAT_CUDA(ctx, cudaMemsetAsync(hist, 0, (size_t)kMaxR * kBins * 4, q));
-    LSCAT_CUDA(ctx, cudaMemsetAsync(cand, 0, (size_t)kMaxR * 8, q));
-    LSCAT_CUDA(ctx, cudaMemsetAsync(shist, 0, 2 * kFxBins * 4, q));
-    sel_sample_hist<<<grid_s, 256, 0, q>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, stride, shist);
-    LSCAT_CUDA(ctx, cudaGetLastError());
-    if (world > 1) {
-      lscat_status ns = ctx->comm->allreduce(ctx, {{shist, 2 * (size_t)kFxBins, DT::U32, Op::Sum}}, q);
-      if (ns) return ns;
-    }
-    sel_plan_sampled<<<1, 1024, 0, q>>>(st, ss, rs.partials, rs.opts.bins_per_unit, shist, rs.minmax, pa,
-                                        npct, dmul, dadd);
-    LSCAT_CUDA(ctx, cudaGetLastError());
-    sel_pass_sampled<256><<<grid_p, 256, 0, q>>>(rs.perf, rs.gain, rs.own_lo, rs.own_hi, ss, cbuf);
-    LSCAT_CUDA(ctx, cudaGetLastError());
-    if (world > 1) {  // the exact bin counts and the copy totals over all ranks
-      lscat_status ns = ctx->comm->allreduce(ctx, {{&ss->fh[0][0], 2 * (size_t)kFxBins, DT::U32, Op::Sum},
-                                                   {&ss->ncopy_all[0], 2, DT::U64, Op::Sum}}, q);
-      if (ns) return ns;
-    }
-    sel_check_sampled<<<1, 1024, 0, q>>>(st, ss, rs.partials, rs.opts.bins_per_unit, rs.minmax, cap,
-                                         force_miss ? 1u : 0u);
-    LSCAT_CUDA(ctx, cudaGetLastError());
-    if (fin) {  // sel_finish follows (outside the graph); the state as the check left it
-      LSCAT_CUDA(ctx, cudaMemsetAsync(fs, 0, sizeof(FinSel), q));
-      LSCAT_CUDA(ctx, cudaMemcpyAsync(hst, st, sizeof(SelState), cudaMemcpyDeviceToHost, q));
-      return LSCAT_OK;
-    }
+    lscat_status es = enqueue_sampled(ctx, B, rs.perf, rs.gain, rs.own_lo, rs.own_hi, rs.partials, rs.minmax,
+                                      rs.opts.bins_per_unit, pa, npct, cap, fin, q);
+    if (es || fin) return es;  // sel_finish follows (outside the graph)
     return enqueue_levels(q, false);
   };
   auto enqueue_first = [&](cudaStream_t q) -> lscat_status {
@@ -1696,12 +1906,12 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
     if (world == 1 && !debug) {
       std::string key;
       auto put = [&](const void* v, size_t n_) { key.append(reinterpret_cast<const char*>(v), n_); };
-      const void* ptrs[] = {rs.perf, rs.gain, rs.partials, rs.minmax, st, hist, cand, cbuf, hst, ss, shist};
+      const void* ptrs[] = {rs.perf, rs.gain, rs.partials, rs.minmax, st, hist, cand, cbuf, hst, B.sp, B.shist};
       put(ptrs, sizeof ptrs);
       put(&rs.own_lo, 8); put(&rs.own_hi, 8); put(&npct, 4); put(pa.p, npct * 8);
       put(&grid0, 4); put(&grid1, 4); put(&cap, 4); put(&samp, sizeof samp);
       const bool fin_k = samp && fin;
-      put(&fin_k, sizeof fin_k); put(&fs, sizeof fs);
+      put(&fin_k, sizeof fin_k); put(&B.fs, sizeof B.fs);
       cudaGraphExec_t gx = nullptr;
       for (auto& kv : ctx->sel_graphs)
         if (kv.first == key) gx = kv.second;
@@ -1731,22 +1941,15 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
       if (e) return e;
     }
     if (samp && fin) {
-      const SelState* st_c = st;
-      const double* cb_c = cbuf;
-      // LSCAT_SEL_FIN_FORCE_FAIL=1 (tests): sel_finish hands over to the chain at once
-      static const uint32_t ff = getenv("LSCAT_SEL_FIN_FORCE_FAIL") != nullptr ? 1u : 0u;
-      uint32_t ff_ = ff;
-      void* args[] = {(void*)&st_c, (void*)&cb_c, (void*)&fs, (void*)&fcand, (void*)&ff_};
-      LSCAT_CUDA(ctx, cudaLaunchCooperativeKernel((const void*)sel_finish, dim3(ctx->sm_count), dim3(1024), args,
-                                                  kFinSmem, s));
-      LSCAT_CUDA(ctx, cudaMemcpyAsync(fsh, fs, kFinHead, cudaMemcpyDeviceToHost, s));
-      ctx->launches += 5;
+      if (lscat_status fe = launch_finish(ctx, B, s)) return fe;
+      ctx->launches += 4;
     } else {
       ctx->launches += (samp ? 4 : 1) + 2 * lpb;
     }
     return LSCAT_OK;
   };
-  if ((ls = launch_first(sampled))) return ls;
+  if (!early_samp)
+    if ((ls = launch_first(sampled))) return ls;
   bool levels_pending = sampled && fin;  // the first batch ran no levels (sel_finish instead)
   for (int batch = 0;; batch++) {
     if (batch == 8) return fail(ctx, LSCAT_ERR_STATE, "stats: percentile selection did not converge");
@@ -1755,6 +1958,19 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
       ctx->launches += 2 * lpb;
     }
     LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
+    if (debug && batch == 0 && sampled) {  // the sampled plan and its exact counts
+      std::vector<SampPlan> h(1);
+      LSCAT_CUDA(ctx, cudaMemcpy(h.data(), B.sp, sizeof(SampPlan), cudaMemcpyDeviceToHost));
+      const SampPlan& f = h[0];
+      for (uint32_t w = 0; w < 2; w++) {
+        unsigned long long sum = 0;
+        for (uint32_t i = 0; i < kSpCnt; i++) sum += f.cnt[w][i];
+        fprintf(stderr, "samp q%u: fail %u niv %u nslot %u ncopy %llu counted %llu intervals", w, f.fail,
+                f.niv[w], f.nslot[w], f.ncopy[w], sum);
+        for (uint32_t r = 0; r < f.niv[w]; r++) fprintf(stderr, " [%u,%u]", f.b1[w][r], f.b2[w][r]);
+        fprintf(stderr, "\n");
+      }
+    }
     if (debug)
       fprintf(stderr, "sel batch %d: nt %u nr %u nw0 %u open %u err %u src %u compact %u nc %llu %llu sampled %d fail %u\n",
               batch, hst->nt, hst->nr, hst->nw0, hst->open, hst->err, hst->src, hst->compact, hst->nc[0],
@@ -1785,6 +2001,7 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
       sampled = false;
       levels_pending = false;
       ctx->sel_fallbacks++;
+      ctx->rs.early = EARLY_NONE;
       if ((ls = launch_first(false))) return ls;
       batch = -1;
       continue;

@@ -91,7 +91,8 @@ class ReduceOpts(C.Structure):
     _fields_ = [(n, C.c_uint32) for n in (
         "n_blocks", "largest_block_id", "n_matrices", "nan_policy", "bins_per_unit", "gain_cap",
         "gain_gt_num", "gain_gt_den", "perf_lt_num", "perf_lt_den", "band_lo_num",
-        "band_lo_den", "point_sharded", "keep_values", "block_profile", "kernel_rollup")]
+        "band_lo_den", "point_sharded", "keep_values", "block_profile", "kernel_rollup",
+        "n_percentiles", "pad0")] + [("percentiles", C.c_void_p)]
 
 
 class ReduceOutC(C.Structure):
@@ -237,6 +238,10 @@ def reduce_opts(n_blocks=32, n_matrices=8, **kw) -> ReduceOpts:
         if k in ("gain_gt", "perf_lt", "band_lo"):
             setattr(o, k + "_num", v[0])
             setattr(o, k + "_den", v[1])
+        elif k == "percentiles":  # R-27: selection enqueued by reduce_table (host array kept)
+            o._pct = np.ascontiguousarray(v, dtype=np.float64)
+            o.n_percentiles = o._pct.size
+            o.percentiles = o._pct.ctypes.data if o._pct.size else None
         else:
             setattr(o, k, v)
     return o
@@ -330,6 +335,7 @@ class Ctx:
             raise LscatError(st, f"ctx_create(device={device}) failed (no CUDA device?)")
         self.h = h
         self.device = device
+        self._stats_bufs = {}  # stats(): output struct + host arrays per shape
 
     def close(self):
         self._reduce_keep = None
@@ -460,43 +466,52 @@ class Ctx:
 
     # a8/a10
     def stats(self, opts: ReduceOpts, percentiles=(), hist=True, stream=None) -> dict:
-        so = StatsOutC()
+        pcs = np.ascontiguousarray(percentiles, dtype=np.float64).ravel()
+        ML = opts.n_matrices * opts.n_blocks
         nb, cap = opts.bins_per_unit, opts.gain_cap
-        ph = np.zeros(nb + 1, np.uint64)
-        gh = np.zeros(cap * nb + 1, np.uint64)
-        bh = np.zeros(opts.n_matrices * opts.n_blocks, np.uint64)
-        if hist:
-            so.perf_hist, so.gain_hist, so.best_block_hist = (ph.ctypes.data, gh.ctypes.data,
-                                                              bh.ctypes.data)
-        pc = np.ascontiguousarray(percentiles, dtype=np.float64)
-        pp = np.full(pc.size, np.nan)
-        pg = np.full(pc.size, np.nan)
-        if pc.size:
-            so.percentiles, so.n_percentiles = pc.ctypes.data, pc.size
-            so.pct_perf, so.pct_gain = pp.ctypes.data, pg.ctypes.data
-        pm = np.full(opts.n_matrices * opts.n_blocks, np.nan)
-        pn = np.zeros(opts.n_matrices * opts.n_blocks, np.uint64)
-        if opts.block_profile:
-            so.profile_mean, so.profile_count = pm.ctypes.data, pn.ctypes.data
-        kh = np.zeros(nb + 1, np.uint64)
-        if opts.kernel_rollup:
-            so.kernel_perf_hist = kh.ctypes.data
+        # the output struct and its host arrays are cached per shape (argument marshalling is
+        # on the small tables' critical path); results are returned as copies
+        key = (nb, cap, ML, pcs.size, bool(hist), bool(opts.block_profile), bool(opts.kernel_rollup))
+        bufs = self._stats_bufs.get(key)
+        if bufs is None:
+            so = StatsOutC()
+            ph, gh, bh = (np.zeros(nb + 1, np.uint64), np.zeros(cap * nb + 1, np.uint64),
+                          np.zeros(ML, np.uint64))
+            pc, pp, pg = np.zeros(pcs.size), np.zeros(pcs.size), np.zeros(pcs.size)
+            pm, pn, kh = np.zeros(ML), np.zeros(ML, np.uint64), np.zeros(nb + 1, np.uint64)
+            if hist:
+                so.perf_hist, so.gain_hist, so.best_block_hist = (ph.ctypes.data, gh.ctypes.data,
+                                                                  bh.ctypes.data)
+            if pcs.size:
+                so.percentiles, so.n_percentiles = pc.ctypes.data, pcs.size
+                so.pct_perf, so.pct_gain = pp.ctypes.data, pg.ctypes.data
+            if opts.block_profile:
+                so.profile_mean, so.profile_count = pm.ctypes.data, pn.ctypes.data
+            if opts.kernel_rollup:
+                so.kernel_perf_hist = kh.ctypes.data
+            bufs = (so, ph, gh, bh, pc, pp, pg, pm, pn, kh)
+            self._stats_bufs[key] = bufs
+        so, ph, gh, bh, pc, pp, pg, pm, pn, kh = bufs
+        pc[:] = pcs
+        pp.fill(np.nan)
+        pg.fill(np.nan)
         self._ck(self._lib.lscat_stats(self.h, C.byref(opts), C.byref(so), _stream(stream)),
                  "stats")
-        res = {k: int(getattr(so, k)) for k in COUNTERS}
-        res.update({k: float(getattr(so, k)) for k in DERIVED})
+        raw = bytes(so)  # counters (u64) then the derived doubles, in COUNTERS / DERIVED order
+        res = dict(zip(COUNTERS, np.frombuffer(raw, np.uint64, len(COUNTERS)).tolist()))
+        res.update(zip(DERIVED, np.frombuffer(raw, np.float64, len(DERIVED), 8 * len(COUNTERS)).tolist()))
         if hist:
-            res["perf_hist"], res["gain_hist"] = ph, gh
-            res["best_block_hist"] = bh.reshape(opts.n_matrices, opts.n_blocks)
-        if pc.size:
+            res["perf_hist"], res["gain_hist"] = ph.copy(), gh.copy()
+            res["best_block_hist"] = bh.reshape(opts.n_matrices, opts.n_blocks).copy()
+        if pcs.size:
             res["pct_perf"], res["pct_gain"] = pp.tolist(), pg.tolist()
         if opts.kernel_rollup:
             res.update({k: int(getattr(so, k)) for k in ROLLUP})
             res.update({k: float(getattr(so, k)) for k in ROLLUP_DERIVED})
-            res["kernel_perf_hist"] = kh
+            res["kernel_perf_hist"] = kh.copy()
         if opts.block_profile:
-            res["profile_mean"] = pm.reshape(opts.n_matrices, opts.n_blocks)
-            res["profile_count"] = pn.reshape(opts.n_matrices, opts.n_blocks)
+            res["profile_mean"] = pm.reshape(opts.n_matrices, opts.n_blocks).copy()
+            res["profile_count"] = pn.reshape(opts.n_matrices, opts.n_blocks).copy()
         return res
 
     # group an unordered dataframe into a table

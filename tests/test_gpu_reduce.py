@@ -39,10 +39,11 @@ def _device_table(t, host=False):
     return tab
 
 
-def _opts_pair(L=32, M=8, ell=None, policy=0, rollup=0):
+def _opts_pair(L=32, M=8, ell=None, policy=0, rollup=0, early=None):
     from paper_2103_14409_b200 import reduce_opts
     ell = L - 1 if ell is None else ell
-    g = reduce_opts(L, M, largest_block_id=ell, nan_policy=policy, kernel_rollup=rollup)
+    kw = dict(percentiles=early) if early is not None else {}
+    g = reduce_opts(L, M, largest_block_id=ell, nan_policy=policy, kernel_rollup=rollup, **kw)
     o = OT.Opts(n_blocks=L, largest_block_id=ell, n_matrices=M, nan_policy=policy)
     return g, o
 
@@ -58,9 +59,10 @@ def _check_rollup(st, R):
     assert st["frac_kernels_perf_band"] == R["frac_kernels_perf_band"] or R["n_kernels"] == 0
 
 
-def _compare(t, L=32, M=8, ell=None, policy=0, host=False, pcts=PCTS, rollup=0):
+def _compare(t, L=32, M=8, ell=None, policy=0, host=False, pcts=PCTS, rollup=0, early=False):
+    """early: the percentiles ride in the reduce options (R-27: selected while reducing)."""
     c = ctx()
-    g_opts, o_opts = _opts_pair(L, M, ell, policy, rollup)
+    g_opts, o_opts = _opts_pair(L, M, ell, policy, rollup, early=pcts if early else None)
     tab = _device_table(t, host=host)
     out = c.reduce_table(tab, g_opts)
     st = c.stats(g_opts, percentiles=pcts)
@@ -600,3 +602,95 @@ def test_percentiles_sampled_finish_overflow():
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
     import re
     assert "sampled 1 fail 0" in r.stderr and re.search(r"sel_finish: fail [1-9]", r.stderr), r.stderr[-2000:]
+
+
+# ---- R-27: the selection enqueued by reduce_table (percentiles in the reduce options) ------
+def test_early_selection_small_tables():
+    """configs[2]-shaped table: the one-launch selection enqueued right after the reducer;
+    values exact against the oracle, then a different percentile list (the usual path) and
+    the early list again (the early result was invalidated: the usual path, still exact)."""
+    t = gen_table(2_140_796, 8363, preset="gtx980", nan_rate=0.03, seed=980)
+    _compare(t, early=True)
+    from paper_2103_14409_b200 import reduce_opts
+    c = ctx()
+    tab = _device_table(t)
+    g = reduce_opts(32, 8, percentiles=PCTS)
+    c.reduce_table(tab, g, per_group=False)
+    other = [0.3, 0.6]
+    st2 = c.stats(g, percentiles=other)
+    st1 = c.stats(g, percentiles=PCTS)
+    ref = OT.reduce_table(t["runtime_ms"], t["block_id"], t["group_offset"],
+                          group_matrix=t["group_matrix"], opts=OT.Opts(), percentiles=PCTS)
+    ref2 = OT.reduce_table(t["runtime_ms"], t["block_id"], t["group_offset"],
+                           group_matrix=t["group_matrix"], opts=OT.Opts(), percentiles=other)
+    assert st1["pct_perf"] == ref.percentiles["perf"] and st1["pct_gain"] == ref.percentiles["gain"]
+    assert st2["pct_perf"] == ref2.percentiles["perf"] and st2["pct_gain"] == ref2.percentiles["gain"]
+
+
+PCT9 = [0.01, 0.05, 0.1, 0.25, 0.5, 0.75, 0.9, 0.95, 0.99]
+
+
+@pytest.mark.parametrize("preset,seed", [("t4", 31), ("gtx980", 32)])
+def test_early_sampled_ragged(preset, seed):
+    """More than 2^20 groups with the percentiles in the reduce options: the sampled first
+    level (fixed-bin intervals from a sample, one pass counting every key into its slot or gap
+    and copying the slot keys, the exact check) and sel_finish enqueued behind the reducer:
+    values exact against the oracle (child process: the debug switch is read once)."""
+    code = (
+        "from tests.test_gpu_reduce import _compare, PCT9\n"
+        "from synth import gen_table\n"
+        f"t = gen_table(40_000_000, 150_000, preset='{preset}', nan_rate=0.03, seed={seed})\n"
+        "_compare(t, pcts=PCT9, early=True)\n"
+        "print('ok')\n")
+    r = _run_child(code, {"LSCAT_SEL_DEBUG": "1"})
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+    assert "sel early sampled" in r.stderr and "sampled 1 fail 0" in r.stderr, r.stderr[-2000:]
+    assert "sel_finish: fail 0" in r.stderr, r.stderr[-2000:]
+
+
+def test_early_sampled_uniform_table():
+    """The uniform 32-row reducer (configs[4]'s kernel) with the selection enqueued behind it:
+    1.5 M groups without an offset array, every counter and the values exact against the
+    oracle."""
+    from paper_2103_14409_b200 import reduce_opts
+    c = ctx()
+    n, K = 48_000_000, 187_500
+    h = gen_table(n, K, preset="t4", seed=99)
+    tab = _uniform_device_table(h["runtime_ms"], h["block_id"])
+    g = reduce_opts(32, 8, percentiles=PCT9)
+    c.reduce_table(tab, g, per_group=False)
+    st = c.stats(g, percentiles=PCT9)
+    ref = OT.reduce_table(h["runtime_ms"], h["block_id"], rows_per_group=32, opts=OT.Opts(),
+                          percentiles=PCT9)
+    for k, v in ref.counters.items():
+        assert st[k] == v, (k, st[k], v)
+    assert (st["perf_hist"] == ref.perf_hist).all() and (st["gain_hist"] == ref.gain_hist).all()
+    assert st["pct_perf"] == ref.percentiles["perf"] and st["pct_gain"] == ref.percentiles["gain"]
+
+
+def test_early_sampled_forced_miss():
+    """An enqueued sampled first level that misses (forced: LSCAT_SEL_FORCE_MISS=1) makes
+    lscat_stats run the histogram path over the kept perf/gain values: still exact."""
+    code = (
+        "from tests.test_gpu_reduce import _compare, PCT9\n"
+        "from synth import gen_table\n"
+        "t = gen_table(36_000_000, 140_000, preset='gtx980', nan_rate=0.03, seed=7)\n"
+        "_compare(t, pcts=PCT9, early=True)\n"
+        "print('ok')\n")
+    r = _run_child(code, {"LSCAT_SEL_FORCE_MISS": "1", "LSCAT_SEL_DEBUG": "1"})
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+    assert "sel early sampled" in r.stderr and "sampled 1 fail 1" in r.stderr, r.stderr[-2000:]
+
+
+def test_early_sampled_finish_fallback():
+    """The enqueued sel_finish handing over at once (forced): the chain continues over the
+    sampled pass's copies, exact."""
+    code = (
+        "from tests.test_gpu_reduce import _compare, PCT9\n"
+        "from synth import gen_table\n"
+        "t = gen_table(36_000_000, 140_000, preset='t4', nan_rate=0.03, seed=17)\n"
+        "_compare(t, pcts=PCT9, early=True)\n"
+        "print('ok')\n")
+    r = _run_child(code, {"LSCAT_SEL_FIN_FORCE_FAIL": "1", "LSCAT_SEL_DEBUG": "1"})
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+    assert "sel early sampled" in r.stderr and "sel_finish: fail 1" in r.stderr, r.stderr[-2000:]
