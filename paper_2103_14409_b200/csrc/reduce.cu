@@ -337,9 +337,9 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 // 8 x 16 B of runtimes and 4 x 16 B of block ids per lane, coalesced, placed in an
 // XOR-swizzled layout (chunk c of group g at c ^ (g & 7) resp. c ^ ((g >> 1) & 3)) so that
 // the per-group 128-bit reads below (lane j <- group j) are bank-conflict free.
-__device__ __forceinline__ void uniform_prefetch(const RP& p, uint64_t base, float4* d, uint4* di, int lane) {
-  const float4* src = reinterpret_cast<const float4*>(p.rt + base * 32);
-  const uint4* isrc = reinterpret_cast<const uint4*>(p.bid + base * 32);
+__device__ __forceinline__ void uniform_prefetch_rows(const RP& p, uint64_t row0, float4* d, uint4* di, int lane) {
+  const float4* src = reinterpret_cast<const float4*>(p.rt + row0);
+  const uint4* isrc = reinterpret_cast<const uint4*>(p.bid + row0);
 #pragma unroll
   for (int i = 0; i < 8; i++) {
     const int f = lane + 32 * i, g = f >> 3, c = f & 7;
@@ -351,6 +351,10 @@ __device__ __forceinline__ void uniform_prefetch(const RP& p, uint64_t base, flo
     cp_async16(di + g * 4 + (c ^ ((g >> 1) & 3)), isrc + h);
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+__device__ __forceinline__ void uniform_prefetch(const RP& p, uint64_t base, float4* d, uint4* di, int lane) {
+  uniform_prefetch_rows(p, base * 32, d, di, lane);
 }
 
 __device__ __forceinline__ uint4 lds128(uint32_t saddr) {
@@ -549,7 +553,18 @@ __global__ void __launch_bounds__(kThreads, 2) reduce_groups_kernel(RP p) {
     const int64_t total = R1 - R0;
     GroupAcc mine;
     acc_init(mine);
-    if (maxlen <= 32 && total >= 0 && total <= kStageRows) {
+    const uint32_t minlen = __reduce_min_sync(FULL, lane < nj ? (uint32_t)(hi - lo) : 32u);
+    if (nj == 32 && maxlen == 32 && minlen == 32 && p.vec && (R0 & 7) == 0) {
+      // a batch of 32 full 32-row groups (configs[2]/[3] apart from the last group): the
+      // uniform tables' swizzled cp.async stage and one-pass fold, in this warp's stage
+      float4* d = reinterpret_cast<float4*>(s_rt);
+      uint4* di = reinterpret_cast<uint4*>(s_id);
+      uniform_prefetch_rows(p, (uint64_t)R0, d, di, lane);
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      __syncwarp();
+      uniform_fold(p, (uint32_t)__cvta_generic_to_shared(d), (uint32_t)__cvta_generic_to_shared(di), lane, mine);
+      __syncwarp();
+    } else if (maxlen <= 32 && total >= 0 && total <= kStageRows) {
       const int tot = (int)total;
       constexpr int kU = 16;  // rows in flight per lane
       for (int r0 = 0; r0 < tot; r0 += 32 * kU) {

@@ -647,7 +647,7 @@ constexpr uint32_t kSpCnt = kSpSlots + kIvQ + 1;  // slots, then gaps 0..niv
 constexpr uint32_t kSpSlotFlag = 0x8000u;      // map entry: slot (else: the gap index)
 constexpr uint64_t kSampleRuns = 1 << 16;      // sampled positions ...
 constexpr uint32_t kSampleRun = 16;            // ... of 16 consecutive keys each
-constexpr uint32_t kSpStage = 64;              // per warp and quantity: copies staged in smem
+constexpr uint32_t kSpStage = 96;              // per warp and quantity: copies staged in smem
 static_assert(kIvQ + 1 <= 10, "ten gap fields in two redux words");
 
 struct SampPlan {
@@ -821,88 +821,159 @@ __global__ void __launch_bounds__(1024) sel_plan_sampled(SampPlan* __restrict__ 
   for (uint32_t i = tid; i < 2 * kSpCnt; i += blockDim.x) (&sp->cnt[0][0])[i] = 0;
 }
 
-// One pass over this rank's keys (kU per quantity in flight per thread): each counted key
-// adds 1 to its slot or gap and the slot keys are copied.  Gaps (most keys, a few hot
-// counters): a packed one-hot (6-bit fields, gaps 0-4 / 5-9 in two words) summed over the warp
-// by two redux.sync adds, lane j accumulating field j in a register; slots (spread over many
-// bins): one shared atomic per key; copies: a per-warp shared stage flushed 32 keys at a time
-// with one reservation.
+// One pass over this rank's keys (kU per quantity in flight per thread, full tiles without
+// bounds checks, the tail tile with them): each counted key adds 1 to its slot or gap and the
+// slot keys are copied.  Per key: the fixed bin from the key's high word, one shared map
+// lookup (uncounted keys read an extra "none" entry).  Gaps (most keys): per-lane 8-bit
+// counters packed in registers (gaps 0-7 in a u64, 8-9 in a u32), flushed to shared memory
+// every 31 tiles (<= 248 keys per field); slots: one shared atomic per key; copies: a per-warp
+// shared stage flushed 32 keys at a time with one reservation.
+constexpr uint16_t kSpNone = 0x4000u;  // map entry of an uncounted key
+#ifndef SP_MINB
+#define SP_MINB 3  // resident CTAs ptxas budgets registers for (1 / 3 / 4 measured: 1.34 / 1.33 / 1.33 ms reduce + selection at 10^9 rows, pass 177 / 157 / 221 us under ncu)
+#endif
 template <int kT>
-__global__ void __launch_bounds__(kT) sel_pass_sampled(const double* __restrict__ perf,
+__global__ void __launch_bounds__(kT, SP_MINB) sel_pass_sampled(const double* __restrict__ perf,
                                                        const double* __restrict__ gain, uint64_t lo,
                                                        uint64_t hi, SampPlan* __restrict__ sp,
                                                        double* __restrict__ cbuf) {
-  constexpr int kU = 8;
-  __shared__ uint16_t map[2 * kFxBins];
+  constexpr int kU = 8, kFlushTiles = 31;
+  static_assert(kFlushTiles * kU < 256, "8-bit gap fields");
+  __shared__ uint16_t map[2][kFxBins + 1];
   __shared__ uint32_t cnt[2 * kSpCnt];
   __shared__ uint64_t stage[kT / 32][2][kSpStage];
-  for (uint32_t i = threadIdx.x; i < 2 * kFxBins; i += kT) map[i] = (&sp->map[0][0])[i];
+  for (uint32_t i = threadIdx.x; i < 2 * (kFxBins + 1); i += kT) {
+    const uint32_t w = i / (kFxBins + 1), b = i % (kFxBins + 1);
+    map[w][b] = b < kFxBins ? sp->map[w][b] : kSpNone;
+  }
   for (uint32_t i = threadIdx.x; i < 2 * kSpCnt; i += kT) cnt[i] = 0;
   __syncthreads();
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint32_t gacc[2] = {0u, 0u}, nst[2] = {0u, 0u};
-  auto flush_stage = [&](uint32_t w, uint32_t n) {  // warp-collective: the first n staged keys
-    uint64_t* sw = stage[wid][w];
+  uint64_t glo[2] = {0ull, 0ull};
+  uint32_t ghi[2] = {0u, 0u}, nst[2] = {0u, 0u};
+  auto flush_gaps = [&]() {
+#pragma unroll
+    for (int w = 0; w < 2; w++) {
+#pragma unroll
+      for (int g = 0; g < 10; g++) {
+        const uint32_t c = g < 8 ? (uint32_t)(glo[w] >> (8 * g)) & 255u : (ghi[w] >> (8 * (g - 8))) & 255u;
+        if (c) atomicAdd(&cnt[w * kSpCnt + kSpSlots + g], c);
+      }
+      glo[w] = 0ull;
+      ghi[w] = 0u;
+    }
+  };
+  auto flush_stage = [&](uint32_t w) {  // warp-collective: every staged key, one reservation
+    const uint64_t* sw = stage[wid][w];
     __syncwarp();
     unsigned long long base = 0;
     if (lane == 0) {
-      base = atomicAdd(&sp->ncopy[w], (unsigned long long)n);
-      atomicAdd(&sp->ncopy_all[w], (unsigned long long)n);
+      base = atomicAdd(&sp->ncopy[w], (unsigned long long)nst[w]);
+      atomicAdd(&sp->ncopy_all[w], (unsigned long long)nst[w]);
     }
     base = __shfl_sync(FULL, base, 0);
-    if ((uint32_t)lane < n && base + lane < kCompactCap)
-      reinterpret_cast<uint64_t*>(cbuf)[(size_t)w * kCompactCap + base + lane] = sw[lane];
-    const uint32_t rest = nst[w] - n;
-    const uint64_t v = (uint32_t)lane < rest ? sw[n + lane] : 0ull;
+    for (uint32_t i = lane; i < nst[w]; i += 32)
+      if (base + i < kCompactCap) reinterpret_cast<uint64_t*>(cbuf)[(size_t)w * kCompactCap + base + i] = sw[i];
     __syncwarp();
-    if ((uint32_t)lane < rest) sw[lane] = v;
-    __syncwarp();
-    nst[w] = rest;
+    nst[w] = 0;
   };
-  const uint64_t cstride = (uint64_t)gridDim.x * kT * kU;
-  for (uint64_t base = lo + blockIdx.x * (uint64_t)kT * kU; base < hi; base += cstride) {
-    uint64_t v[2][kU];
+  // per key: slot / gap counts; returns whether the key is copied
+  auto count = [&](int w, uint64_t k) -> uint32_t {
+    const uint32_t kh = (uint32_t)(k >> 32);  // bins from the high word (32-bit arithmetic)
+    uint32_t b;
+    if (w == 0)  // perf < 1 (NaN keys are above)
+      b = kh < (uint32_t)(kPerfOne >> 32) ? fx_perf_bin_hi(kh) : kFxBins;
+    else         // 0 < gain (no gain is below 2^-32 but 0), not NaN
+      b = kh - 1u < 0x7FEFFFFFu ? fx_gain_bin_hi(kh) : kFxBins;
+    const uint32_t e = map[w][b];
+    glo[w] += e < 8u ? 1ull << (8 * e) : 0ull;
+    ghi[w] += e - 8u < 2u ? 1u << (8 * (e - 8u)) : 0u;
+    const bool slot = (e & kSpSlotFlag) != 0;
+    if (slot) atomicAdd(&cnt[w * kSpCnt + (e & (kSpSlotFlag - 1))], 1u);
+    return slot ? 1u : 0u;
+  };
+  // per tile and quantity: the lanes' copied keys (bit u of mask: key u) placed by one warp
+  // scan, staged (or, above the stage, written with their own reservation)
+  auto copy_tile = [&](int w, uint32_t mask, const uint64_t* v) {
+    const uint32_t c = __popc(mask);
+    uint32_t inc = c;
 #pragma unroll
-    for (int w = 0; w < 2; w++) {
-      const uint64_t* src = reinterpret_cast<const uint64_t*>(w ? gain : perf);
-#pragma unroll
-      for (int u = 0; u < kU; u++) {
-        const uint64_t i = base + threadIdx.x + (uint64_t)kT * u;
-        v[w][u] = i < hi ? __ldcs(src + i) : kNaNKey;
-      }
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, inc, o);
+      if (lane >= o) inc += y;
     }
+    const uint32_t total = __shfl_sync(FULL, inc, 31);
+    if (total == 0) return;
+    if (nst[w] + total > kSpStage) flush_stage(w);
+    uint32_t pos = inc - c;
+    if (total > kSpStage) {  // more than a stage in one tile: straight out
+      unsigned long long base = 0;
+      if (lane == 0) {
+        base = atomicAdd(&sp->ncopy[w], (unsigned long long)total);
+        atomicAdd(&sp->ncopy_all[w], (unsigned long long)total);
+      }
+      base = __shfl_sync(FULL, base, 0);
+#pragma unroll
+      for (int u = 0; u < kU; u++)
+        if ((mask >> u) & 1u) {
+          if (base + pos < kCompactCap) reinterpret_cast<uint64_t*>(cbuf)[(size_t)w * kCompactCap + base + pos] = v[u];
+          pos++;
+        }
+      return;
+    }
+    pos += nst[w];
+#pragma unroll
+    for (int u = 0; u < kU; u++)
+      if ((mask >> u) & 1u) stage[wid][w][pos++] = v[u];
+    nst[w] += total;
+    if (nst[w] >= 32) flush_stage(w);
+  };
+  const uint64_t* P = reinterpret_cast<const uint64_t*>(perf) + lo;
+  const uint64_t* Q = reinterpret_cast<const uint64_t*>(gain) + lo;
+  const uint64_t n = hi - lo, full = n / (kT * kU);
+  int since = 0;
+  for (uint64_t t = blockIdx.x; t < full; t += gridDim.x) {
+    const uint64_t off = t * (kT * kU) + threadIdx.x;
+    uint64_t vp[kU], vg[kU];
 #pragma unroll
     for (int u = 0; u < kU; u++) {
+      vp[u] = __ldcs(P + off + u * kT);
+      vg[u] = __ldcs(Q + off + u * kT);
+    }
+    uint32_t mp = 0, mg = 0;
 #pragma unroll
-      for (uint32_t w = 0; w < 2; w++) {
-        const uint64_t k = v[w][u];
-        const uint32_t kh = (uint32_t)(k >> 32);  // bins from the high word (32-bit arithmetic)
-        // perf < 1 (and not NaN) / gain > 0 (no gain is below 2^-32 but 0) and not NaN
-        const bool counted = w == 0 ? kh < (uint32_t)(kPerfOne >> 32) : (kh != 0 && kh < 0x7FF00000u);
-        const uint32_t b = counted ? (w == 0 ? fx_perf_bin_hi(kh) : fx_gain_bin_hi(kh)) : 0u;
-        const uint32_t e = counted ? (uint32_t)map[w * kFxBins + b] : 0u;
-        const bool slot = counted && (e & kSpSlotFlag);
-        const bool gap = counted && !slot;
-        const uint32_t plo = (gap && e < 5) ? 1u << (6 * e) : 0u;
-        const uint32_t phi = (gap && e >= 5) ? 1u << (6 * (e - 5)) : 0u;
-        const uint32_t rl = __reduce_add_sync(FULL, plo), rh = __reduce_add_sync(FULL, phi);
-        gacc[w] += lane < 10 ? ((lane < 5 ? rl : rh) >> (6 * (lane % 5))) & 63u : 0u;
-        if (slot) atomicAdd(&cnt[w * kSpCnt + (e & (kSpSlotFlag - 1))], 1u);
-        const unsigned m = __ballot_sync(FULL, slot);
-        if (m) {
-          if (slot) stage[wid][w][nst[w] + __popc(m & ((1u << lane) - 1u))] = k;
-          nst[w] += __popc(m);
-          if (nst[w] >= 32) flush_stage(w, 32);
-        }
-      }
+    for (int u = 0; u < kU; u++) {
+      mp |= count(0, vp[u]) << u;
+      mg |= count(1, vg[u]) << u;
+    }
+    copy_tile(0, mp, vp);
+    copy_tile(1, mg, vg);
+    if (++since == kFlushTiles) {
+      flush_gaps();
+      since = 0;
     }
   }
+  flush_gaps();
+  if (blockIdx.x == gridDim.x - 1) {  // the tail tile
+    const uint64_t off = full * (kT * kU) + threadIdx.x;
+    uint64_t vp[kU], vg[kU];
+    uint32_t mp = 0, mg = 0;
 #pragma unroll
-  for (uint32_t w = 0; w < 2; w++) {
-    if (nst[w]) flush_stage(w, nst[w]);
-    if (lane < 10 && gacc[w]) atomicAdd(&cnt[w * kSpCnt + kSpSlots + lane], gacc[w]);
+    for (int u = 0; u < kU; u++) {
+      const uint64_t i = off + u * kT;
+      vp[u] = i < n ? __ldcs(P + i) : kNaNKey;
+      vg[u] = i < n ? __ldcs(Q + i) : kNaNKey;
+      mp |= count(0, vp[u]) << u;
+      mg |= count(1, vg[u]) << u;
+    }
+    copy_tile(0, mp, vp);
+    copy_tile(1, mg, vg);
   }
+  flush_gaps();
+#pragma unroll
+  for (uint32_t w = 0; w < 2; w++)
+    if (nst[w]) flush_stage(w);
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < 2 * kSpCnt; i += kT)
     if (cnt[i]) atomicAdd(&sp->cnt[0][0] + i, cnt[i]);
