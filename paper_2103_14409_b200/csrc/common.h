@@ -110,6 +110,18 @@ struct lscat_ctx {
   // percentile selection: first batch (init + 3 levels + state read-back) as a graph, keyed by
   // every pointer / size / percentile it bakes in (stats.cu; world == 1)
   std::vector<std::pair<std::string, cudaGraphExec_t>> sel_graphs;
+  // lscat_reduce_table on small device tables (one rank): everything it enqueues as one cached
+  // graph, keyed by its arguments; valid while no scratch / pinned buffer was (re)allocated
+  struct RedGraph {
+    std::string key;
+    cudaGraphExec_t gx = nullptr;  // null: seen once (captured on the next call) or not capturable
+    bool tried = false;        // a capture was attempted
+    uint64_t gen = 0;          // scratch_gen at capture
+    lscat::ReduceState rs;     // the context state the call leaves
+    uint64_t launches = 0;     // kernels one call launches
+  };
+  std::vector<RedGraph> red_graphs;
+  uint64_t scratch_gen = 0;    // bumped by every scratch / pinned (re)allocation
   // kernel attributes / occupancy already set or queried on this context's device (host calls
   // kept off the launch path of the small tables)
   std::map<std::pair<bool, size_t>, int> red_occ;
@@ -143,6 +155,7 @@ void* pinned(lscat_ctx* ctx, const char* name, size_t bytes, cudaError_t* err);
 // Raise a kernel's max-dynamic-shared-memory attribute on the current device to at least
 // `bytes` (device-global state: never lowered, set once per (kernel, device, size increase)).
 cudaError_t ensure_smem_attr(const void* func, size_t bytes);
+constexpr uint64_t kEarlySmallGroups = 1ull << 20;  // = stats.cu kSmallKeys (one-launch selection)
 // percentile selection enqueued by lscat_reduce_table (stats.cu; R-27), no host sync: the
 // one-launch selection (small tables) or the sampled first level + sel_finish (large tables)
 // on the kept per-group values; *kind = EARLY_NONE when this device / percentile list cannot

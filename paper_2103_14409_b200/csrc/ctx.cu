@@ -59,6 +59,7 @@ void* scratch(lscat_ctx* ctx, const char* name, size_t bytes, cudaError_t* err) 
     b.bytes = 0;
     size_t want = std::max(bytes, (size_t)256);
     *err = cudaMalloc(&b.p, want);
+    ctx->scratch_gen++;
     if (*err != cudaSuccess) return nullptr;
     b.bytes = want;
   }
@@ -74,6 +75,7 @@ void* pinned(lscat_ctx* ctx, const char* name, size_t bytes, cudaError_t* err) {
     b.bytes = 0;
     size_t want = std::max(bytes, (size_t)4096);
     *err = cudaMallocHost(&b.p, want);
+    ctx->scratch_gen++;
     if (*err != cudaSuccess) return nullptr;
     b.bytes = want;
   }
@@ -190,6 +192,8 @@ void lscat_ctx_destroy(lscat_ctx* c) {
   cudaDeviceSynchronize();
   for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
   for (auto& kv : c->sel_graphs) cudaGraphExecDestroy(kv.second);
+  for (auto& rg : c->red_graphs)
+    if (rg.gx) cudaGraphExecDestroy(rg.gx);
   for (auto ev : c->events) cudaEventDestroy(ev);
   for (auto& kv : c->suite) {
     cudaFree(kv.second.in0);

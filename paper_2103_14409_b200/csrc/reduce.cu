@@ -960,8 +960,8 @@ void lscat_reduce_opts_default(lscat_reduce_opts* o, uint32_t n_blocks, uint32_t
 
 size_t lscat_partials_len(const lscat_reduce_opts* o) { return opts_ok(o) ? partials_len(*o) : 0; }
 
-lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lscat_reduce_opts* o,
-                                lscat_reduce_out* out, void* stream) {
+static lscat_status reduce_enqueue(lscat_ctx* ctx, const lscat_table* T, const lscat_reduce_opts* o,
+                                   lscat_reduce_out* out, void* stream) {
   LSCAT_CHECK_CTX(ctx);
   if (!T || !opts_ok(o)) return fail(ctx, LSCAT_ERR_INVALID_ARG, "reduce_table: bad table or options");
   if (!T->runtime_ms || !T->block_id || (!T->rows_per_group && !T->group_offset) ||
@@ -1198,6 +1198,83 @@ lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lsca
   rs.partials = p.partials;
   rs.minmax = p.minmax;
   if (T->mem == LSCAT_MEM_HOST) LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
+  return LSCAT_OK;
+}
+
+// Small device tables on one rank are launch-latency bound (configs[2]/[3]: ~5 dependent
+// launches, memsets and copies for ~50 us of kernels): the sequence reduce_enqueue issues is
+// captured once per argument set (the second call with the same arguments runs it normally
+// and then captures the same calls into a graph) and later calls replay it with one
+// cudaGraphLaunch.  A cached graph is used only while no scratch / pinned buffer has been
+// (re)allocated since its capture.  LSCAT_REDUCE_NOGRAPH=1 disables it.
+lscat_status lscat_reduce_table(lscat_ctx* ctx, const lscat_table* T, const lscat_reduce_opts* o,
+                                lscat_reduce_out* out, void* stream) {
+  using RedGraph = lscat_ctx::RedGraph;
+  LSCAT_CHECK_CTX(ctx);
+  static const bool no_graph = getenv("LSCAT_REDUCE_NOGRAPH") != nullptr;
+  const bool graphable = !no_graph && ctx->world == 1 && T && opts_ok(o) && T->mem == LSCAT_MEM_DEVICE &&
+                         T->n_groups > 0 && T->n_groups <= kEarlySmallGroups;
+  if (!graphable) return reduce_enqueue(ctx, T, o, out, stream);
+  std::string key;
+  auto put = [&](const void* v, size_t n) { key.append(reinterpret_cast<const char*>(v), n); };
+  put(T, sizeof *T);
+  lscat_reduce_opts oc = *o;
+  oc.percentiles = nullptr;  // by value below
+  put(&oc, sizeof oc);
+  if (o->n_percentiles) put(o->percentiles, o->n_percentiles * sizeof(double));
+  lscat_reduce_out oo{};
+  if (out) oo = *out;
+  put(&oo, sizeof oo);
+  put(&stream, sizeof stream);
+  auto drop_oldest = [&]() {
+    if (ctx->red_graphs.size() < 8) return;
+    if (ctx->red_graphs.front().gx) cudaGraphExecDestroy(ctx->red_graphs.front().gx);
+    ctx->red_graphs.erase(ctx->red_graphs.begin());
+  };
+  RedGraph* hit = nullptr;
+  for (auto& rg : ctx->red_graphs)
+    if (rg.key == key && rg.gen == ctx->scratch_gen) hit = &rg;
+  if (hit && hit->gx) {
+    LSCAT_CUDA(ctx, cudaSetDevice(ctx->device));
+    LSCAT_CUDA(ctx, cudaGraphLaunch(hit->gx, (cudaStream_t)stream));
+    ctx->rs = hit->rs;
+    ctx->rs.opts = *o;
+    ctx->launches += hit->launches;
+    return LSCAT_OK;
+  }
+  const uint64_t l0 = ctx->launches;
+  lscat_status st = reduce_enqueue(ctx, T, o, out, stream);
+  if (st || (hit && hit->tried)) return st;  // not capturable with these arguments
+  const uint64_t gen = ctx->scratch_gen, l1 = ctx->launches;
+  if (!hit) {  // first call with these arguments: remember them (per-call outputs never repeat)
+    drop_oldest();
+    RedGraph rg;
+    rg.key = std::move(key);
+    rg.gen = gen;
+    ctx->red_graphs.push_back(std::move(rg));
+    return LSCAT_OK;
+  }
+  // second call: capture the same sequence for the next ones
+  const lscat::ReduceState rs = ctx->rs;
+  hit->tried = true;
+  cudaStream_t cs = ctx->capture_stream;
+  if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+    const lscat_status cst = reduce_enqueue(ctx, T, o, out, cs);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(cs, &g);
+    cudaGraphExec_t gx = nullptr;
+    if (!cst && ce == cudaSuccess && g && ctx->scratch_gen == gen && cudaGraphInstantiate(&gx, g, 0) == cudaSuccess) {
+      hit->gx = gx;
+      hit->rs = rs;
+      hit->launches = l1 - l0;
+    }
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();  // a capture that failed leaves no sticky error; the call itself succeeded
+    if (cst && ctx->poisoned) return cst;
+  }
+  ctx->rs = rs;
+  ctx->launches = l1;
+  ctx->err.clear();
   return LSCAT_OK;
 }
 

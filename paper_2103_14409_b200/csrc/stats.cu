@@ -1758,6 +1758,7 @@ lscat_status launch_finish(lscat_ctx* ctx, const SelBufs& B, cudaStream_t q) {
 lscat_status early_select(lscat_ctx* ctx, const double* perf, const double* gain, uint64_t lo, uint64_t hi,
                           const uint64_t* partials, const uint64_t* mm, uint32_t nb, const double* pct,
                           uint32_t npct, cudaStream_t s, uint32_t* kind) {
+  static_assert(kEarlySmallGroups == kSmallKeys, "small-table threshold");
   *kind = EARLY_NONE;
   if (ctx->world != 1 || !coop_supported(ctx) || hi <= lo) return LSCAT_OK;
   static const bool no_small = getenv("LSCAT_SEL_NOSMALL") != nullptr;

@@ -1,0 +1,8 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+python __graft_entry__.py build > gpurun_out/build.log 2>&1 || { echo BUILD FAILED; tail -30 gpurun_out/build.log; exit 1; }
+timeout 1800 python -m pytest tests/test_gpu_reduce.py tests/test_gpu_multirank.py -x -q > gpurun_out/pytest_reduce.log 2>&1; echo "reduce tests rc=$?"; tail -3 gpurun_out/pytest_reduce.log
+timeout 600 python scripts/table_bench_early.py > gpurun_out/table_early.json 2> gpurun_out/table_early.err; echo "table rc=$?"
+timeout 300 python scripts/small_table_probe.py 2140796 8 > gpurun_out/small_probe.txt 2>&1
+LSCAT_REDUCE_NOGRAPH=1 timeout 300 python scripts/small_table_probe.py 2140796 8 > gpurun_out/small_probe_nograph.txt 2>&1
+echo done

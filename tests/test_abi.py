@@ -101,6 +101,21 @@ def test_reduce_opts_and_partials(lib):
     assert lib.partials_len(o) == 24 + 101 + 1001 + 8 * 32
 
 
+def test_reduce_opts_percentiles(lib):
+    """R-27: the percentile list in the reduce options (struct layout = the header's: 16 u32,
+    n_percentiles, pad, a pointer); the defaults leave it off and the library's option check
+    (lscat_partials_len returns 0 for rejected options) accepts <= 64 values in [0, 1]."""
+    o = lib.reduce_opts(32, 8)
+    assert C.sizeof(o) == 16 * 4 + 8 + 8 and (o.n_percentiles, o.percentiles) == (0, None)
+    good = lib.reduce_opts(32, 8, percentiles=[0.0, 0.5, 0.99, 1.0])
+    assert good.n_percentiles == 4 and lib.partials_len(good) == lib.partials_len(o)
+    assert list(np.ctypeslib.as_array(C.cast(good.percentiles, C.POINTER(C.c_double)), (4,))) == [0.0, 0.5, 0.99, 1.0]
+    for bad in ([0.5, 1.5], [-0.1], [float("nan")], [0.5] * 65):
+        assert lib.partials_len(lib.reduce_opts(32, 8, percentiles=bad)) == 0, bad
+    o.n_percentiles = 3  # a count without an array
+    assert lib.partials_len(o) == 0
+
+
 def test_gen_shape(lib):
     L = lib.load()
     o = lib.lscat.GenOpts(2140796, 8363, 32, 31, 8, 1, 0.03, 980, 0, 0, 1, 0) \

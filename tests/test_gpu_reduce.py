@@ -694,3 +694,32 @@ def test_early_sampled_finish_fallback():
     r = _run_child(code, {"LSCAT_SEL_FIN_FORCE_FAIL": "1", "LSCAT_SEL_DEBUG": "1"})
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
     assert "sel early sampled" in r.stderr and "sel_finish: fail 1" in r.stderr, r.stderr[-2000:]
+
+
+def test_small_table_graph_replay():
+    """lscat_reduce_table on a small device table is captured on its second call with the same
+    arguments and replayed as one graph afterwards: repeated calls (with and without the early
+    percentiles, per-group outputs, a larger table reduced in between that reallocates the
+    scratch the graph was captured against) stay exact against the oracle."""
+    from paper_2103_14409_b200 import reduce_opts
+    c = ctx()
+    t = gen_table(300_000, 1200, preset="t4", nan_rate=0.03, seed=55)
+    big = gen_table(3_000_000, 12_000, preset="gtx980", nan_rate=0.03, seed=56)
+    ref = OT.reduce_table(t["runtime_ms"], t["block_id"], t["group_offset"], group_matrix=t["group_matrix"],
+                          opts=OT.Opts(), percentiles=PCTS)
+    tab, tab_big = _device_table(t), _device_table(big)
+    for early in (True, False):
+        g = reduce_opts(32, 8, **(dict(percentiles=PCTS) if early else {}))
+        for i in range(5):
+            if i == 3:  # grows the reducer / selection scratch: the cached graph must not be replayed
+                gb = reduce_opts(32, 8, percentiles=PCTS)
+                c.reduce_table(tab_big, gb, per_group=False)
+                c.stats(gb, percentiles=PCTS)
+            out = c.reduce_table(tab, g, per_group=(i == 4))
+            st = c.stats(g, percentiles=PCTS)
+            for k, v in ref.counters.items():
+                assert st[k] == v, (early, i, k, st[k], v)
+            assert (st["perf_hist"] == ref.perf_hist).all() and (st["gain_hist"] == ref.gain_hist).all()
+            assert st["pct_perf"] == ref.percentiles["perf"] and st["pct_gain"] == ref.percentiles["gain"]
+            if i == 4:
+                assert (out["best_block_id"].cpu().numpy().view(np.uint16) == ref.best_block).all()
