@@ -689,7 +689,8 @@ __global__ void __launch_bounds__(256) sel_sample_hist(const double* __restrict_
     if (h[i]) atomicAdd(&shist[i], h[i]);
 }
 
-// Inclusive scan of a quantity's kFxBins counts into pre[] (1024 threads; part is scratch).
+// Inclusive scan of a quantity's kFxBins counts into pre[] (1024 threads; part: 32 + 1024 words
+// of scratch).
 __device__ void scan_bins(const uint32_t* __restrict__ c_in, unsigned long long virt, uint32_t w,
                           unsigned long long* pre, unsigned long long* part) {
   constexpr int kPer = (kFxBins + 1023) / 1024;
@@ -701,15 +702,28 @@ __device__ void scan_bins(const uint32_t* __restrict__ c_in, unsigned long long 
     c[j] = b < kFxBins ? (virtual_bin(w, b) ? virt : (unsigned long long)c_in[b]) : 0ull;
     sum += c[j];
   }
-  part[tid] = sum;
-  __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {
-    const unsigned long long y = tid >= o ? part[tid - o] : 0ull;
-    __syncthreads();
-    part[tid] += y;
-    __syncthreads();
+  // warp-shuffle scan of the per-thread sums, then of the 32 warp totals (part[0..31])
+  const int lane = tid & 31, wid = tid >> 5;
+  unsigned long long inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
   }
-  unsigned long long run = part[tid] - sum;
+  if (lane == 31) part[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    unsigned long long x = part[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    part[lane] = x;
+  }
+  __syncthreads();
+  part[32 + tid] = inc + (wid ? part[wid - 1] : 0ull);  // inclusive scan of the thread sums
+  unsigned long long run = part[32 + tid] - sum;
 #pragma unroll
   for (int j = 0; j < kPer; j++) {
     const uint32_t b = (uint32_t)tid * kPer + j;
@@ -737,7 +751,7 @@ __global__ void __launch_bounds__(1024) sel_plan_sampled(SampPlan* __restrict__ 
                                                        const uint32_t* __restrict__ shist, PctArg pct,
                                                        uint32_t npct, double dmul, double dadd) {
   __shared__ unsigned long long pre[2][kFxBins];
-  __shared__ unsigned long long part[1024];
+  __shared__ unsigned long long part[32 + 1024];
   __shared__ uint32_t tb1[kMaxT], tb2[kMaxT];
   __shared__ uint32_t s_b1[2][kIvQ], s_b2[2][kIvQ], s_slot0[2][kIvQ], s_niv[2], s_fail;
   const int tid = threadIdx.x;
@@ -1300,10 +1314,10 @@ __global__ void __launch_bounds__(1024, 1) sel_small(const double* __restrict__ 
     }
   }
   grid.sync();
-  // phase 4: CTA r picks its targets' keys among range r's gathered keys: by rank counting
-  // when they fit one per thread, else a bitonic sort
-  if (blockIdx.x < nr && ss->rcnt[blockIdx.x] <= blockDim.x) {
-    const uint32_t r = blockIdx.x;
+  // phase 4: CTA r (mod the grid) picks its targets' keys among range r's gathered keys: by
+  // rank counting when they fit one per thread, else a bitonic sort
+  for (uint32_t r = blockIdx.x; r < nr; r += gridDim.x) {
+  if (ss->rcnt[r] <= blockDim.x) {
     const uint32_t n = (uint32_t)ss->rcnt[r];
     for (uint32_t i = tid; i < n; i += blockDim.x) dsm[i] = cand[(size_t)r * kSmallCap + i];
     __syncthreads();
@@ -1319,8 +1333,7 @@ __global__ void __launch_bounds__(1024, 1) sel_small(const double* __restrict__ 
     }
     if (tid < (int)nt && !s_done[tid] && s_range[tid] == r && !(s_k[tid] >= 1 && s_k[tid] <= n))
       atomicOr(&ss->fail, 2u);  // keys lost: the host falls back
-  } else if (blockIdx.x < nr) {
-    const uint32_t r = blockIdx.x;
+  } else {
     const uint32_t n = (uint32_t)min(ss->rcnt[r], (unsigned long long)kSmallCap);
     uint32_t P2 = 1;
     while (P2 < n) P2 <<= 1;
@@ -1343,6 +1356,22 @@ __global__ void __launch_bounds__(1024, 1) sel_small(const double* __restrict__ 
       else atomicOr(&ss->fail, 2u);  // keys lost: the host falls back
     }
   }
+  __syncthreads();  // the next range reuses dsm
+  }
+}
+
+// Grid of sel_small: one CTA per 512 keys, at most one per SM (tiny inputs get fewer CTAs and
+// cheaper grid barriers).  Calibration on configs[2]/[3] (LSCAT_SMALL_KEYS_PER_CTA = 512 / 2048
+// / 4096 / 8192 / 16384): reduce + early selection 0.090 / 0.091 / 0.101 / 0.106 / 0.127 ms and
+// 0.116 / 0.116 / 0.119 / 0.130 / 0.155 ms (profiles/r02_sel_small_grid.txt): the CTAs' loads
+// in flight win over the flush and barrier costs.
+uint32_t small_grid(const lscat_ctx* ctx, uint64_t n) {
+  static const uint64_t per = [] {
+    const char* e = getenv("LSCAT_SMALL_KEYS_PER_CTA");
+    const long long v = e ? atoll(e) : 0;
+    return v > 0 ? (uint64_t)v : (uint64_t)512;
+  }();
+  return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(ctx->sm_count, (n + per - 1) / per));
 }
 
 // ---- after the sampled first level, on one rank: the rest of the selection in one launch ----
@@ -1695,8 +1724,10 @@ lscat_status enqueue_sampled(lscat_ctx* ctx, const SelBufs& B, const double* per
                              cudaStream_t q) {
   const int world = ctx->world;
   const uint64_t n = hi - lo;
-  LSCAT_CUDA(ctx, cudaMemsetAsync(B.hist, 0, (size_t)kMaxR * kBins * 4, q));
-  LSCAT_CUDA(ctx, cudaMemsetAsync(B.cand, 0, (size_t)kMaxR * 8, q));
+  if (!fin) {  // the chain follows at once (with sel_finish: cleared only if it hands over)
+    LSCAT_CUDA(ctx, cudaMemsetAsync(B.hist, 0, (size_t)kMaxR * kBins * 4, q));
+    LSCAT_CUDA(ctx, cudaMemsetAsync(B.cand, 0, (size_t)kMaxR * 8, q));
+  }
   LSCAT_CUDA(ctx, cudaMemsetAsync(B.shist, 0, 2 * kFxBins * 4, q));
   const uint64_t rstride = std::max<uint64_t>(kSampleRun, n / kSampleRuns);
   const int grid_s = (int)std::min<uint64_t>(kSampleRuns * kSampleRun / 256, (uint64_t)ctx->sm_count * 2);
@@ -1779,8 +1810,8 @@ lscat_status early_select(lscat_ctx* ctx, const double* perf, const double* gain
     LSCAT_CUDA(ctx, cudaMemsetAsync(sm, 0, sizeof(SmallSel), s));
     void* args[] = {(void*)&perf, (void*)&gain, (void*)&lo, (void*)&hi, (void*)&partials,
                     (void*)&mm, (void*)&pa, (void*)&npct, (void*)&sm, (void*)&scand};
-    LSCAT_CUDA(ctx, cudaLaunchCooperativeKernel((const void*)sel_small, dim3(ctx->sm_count), dim3(1024), args,
-                                                kSmallSmem, s));
+    LSCAT_CUDA(ctx, cudaLaunchCooperativeKernel((const void*)sel_small, dim3(small_grid(ctx, hi - lo)), dim3(1024),
+                                                args, kSmallSmem, s));
     ctx->launches++;
     LSCAT_CUDA(ctx, cudaMemcpyAsync(hsm, sm, kSmallHead, cudaMemcpyDeviceToHost, s));
     *kind = EARLY_SMALL;
@@ -1900,8 +1931,8 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
       uint32_t np_ = npct;
       void* args[] = {(void*)&perf_p, (void*)&gain_p, (void*)&lo_, (void*)&hi_, (void*)&part_p,
                       (void*)&mm_p, (void*)&pa, (void*)&np_, (void*)&sm, (void*)&scand};
-      LSCAT_CUDA(ctx, cudaLaunchCooperativeKernel((const void*)sel_small, dim3(ctx->sm_count), dim3(1024), args,
-                                                  kSmallSmem, s));
+      LSCAT_CUDA(ctx, cudaLaunchCooperativeKernel((const void*)sel_small, dim3(small_grid(ctx, rs.own_hi - rs.own_lo)),
+                                                  dim3(1024), args, kSmallSmem, s));
       ctx->launches++;
       const bool dbg = getenv("LSCAT_SEL_DEBUG") != nullptr;
       LSCAT_CUDA(ctx, cudaMemcpyAsync(hsm, sm, dbg ? sizeof(SmallSel) : kSmallHead, cudaMemcpyDeviceToHost, s));
@@ -2023,9 +2054,15 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
   if (!early_samp)
     if ((ls = launch_first(sampled))) return ls;
   bool levels_pending = sampled && fin;  // the first batch ran no levels (sel_finish instead)
+  bool chain_cleared = !(sampled && fin);  // the sampled path with sel_finish skips the chain's memsets
   for (int batch = 0;; batch++) {
     if (batch == 8) return fail(ctx, LSCAT_ERR_STATE, "stats: percentile selection did not converge");
     if (batch > 0) {
+      if (!chain_cleared) {  // sel_finish handed over: the chain's histograms / counters first
+        LSCAT_CUDA(ctx, cudaMemsetAsync(hist, 0, (size_t)kMaxR * kBins * 4, s));
+        LSCAT_CUDA(ctx, cudaMemsetAsync(cand, 0, (size_t)kMaxR * 8, s));
+        chain_cleared = true;
+      }
       if ((ls = enqueue_levels(s, false))) return ls;
       ctx->launches += 2 * lpb;
     }
