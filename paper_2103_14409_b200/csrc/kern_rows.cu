@@ -174,16 +174,19 @@ struct RowLauncher {
   struct L {
     static constexpr bool kSupported = true;
     static cudaError_t attrs(const void** f, size_t* sm) { return kernel_attrs(row_kernel<OP, B, ROW_U>, 0, f, sm); }
-    // resident CTAs per SM (a property of the sm_100a binary; thread-safe one-time query)
-    static int per_sm() {
+    // resident CTAs per SM of the UL variant (a property of the sm_100a binary; thread-safe
+    // one-time query)
+    template <int UL>
+    static int per_sm_v() {
       static const int v = [] {
         int r = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, row_kernel<OP, B, ROW_U>, B, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, row_kernel<OP, B, UL>, B, 0);
         cudaGetLastError();
         return r > 0 ? r : 1;
       }();
       return v;
     }
+    static int per_sm() { return per_sm_v<ROW_U>(); }
     static cudaError_t launch(const LaunchArgs& a, cudaStream_t s) {
       const SuiteEntry& e = *a.e;
       const int N = (int)e.n;
@@ -214,8 +217,10 @@ struct RowLauncher {
       // blocks / resident CTAs) row blocks per CTA over the fewest CTAs that need no more than
       // r -- every CTA (and warp) streams the same number of rows and none idles through a
       // partial last round (LSCAT_ROW_GRID=legacy: the round-1 grid, for A/B runs).
+      const int sv = small_rows();
+      const int ul = (N <= 256 && sv) ? 2 : (N <= small4_max() && sv >= 2) ? 4 : ROW_U;
       const long need = (N + teams - 1) / teams;
-      const long slots = (long)sms * per_sm();
+      const long slots = (long)sms * (ul == 2 ? per_sm_v<2>() : ul == 4 ? per_sm_v<4>() : per_sm());
       int grid;
       if (legacy_grid()) {
         grid = (int)((ROW_PERSIST_BIG && B > 512 && need > sms) ? sms : need);
@@ -225,11 +230,10 @@ struct RowLauncher {
         const long r = (need + slots - 1) / slots;
         grid = (int)((need + r - 1) / r);
       }
-      const int sv = small_rows();
-      if (N <= 256 && sv)  // latency-bound short rows: the lighter variants
+      if (ul == 2)  // latency-bound short rows: the lighter variants
         return launch_k(row_kernel<OP, B, 2>, dim3(grid), dim3(B), 0, s, a.pdl,
                         (const float*)e.in0, (const float*)e.in1, (float*)e.out, N, tw, keep);
-      if (N <= small4_max() && sv >= 2)
+      if (ul == 4)
         return launch_k(row_kernel<OP, B, 4>, dim3(grid), dim3(B), 0, s, a.pdl,
                         (const float*)e.in0, (const float*)e.in1, (float*)e.out, N, tw, keep);
       return launch_k(row_kernel<OP, B, ROW_U>, dim3(grid), dim3(B), 0, s, a.pdl,
