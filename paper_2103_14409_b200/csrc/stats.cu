@@ -753,7 +753,7 @@ __global__ void __launch_bounds__(1024) sel_plan_sampled(SampPlan* __restrict__ 
   __shared__ unsigned long long pre[2][kFxBins];
   __shared__ unsigned long long part[32 + 1024];
   __shared__ uint32_t tb1[kMaxT], tb2[kMaxT];
-  __shared__ uint32_t s_b1[2][kIvQ], s_b2[2][kIvQ], s_slot0[2][kIvQ], s_niv[2], s_fail;
+  __shared__ uint32_t s_b1[2][kIvQ], s_b2[2][kIvQ], s_slot0[2][kIvQ], s_niv[2];
   const int tid = threadIdx.x;
   for (uint32_t w = 0; w < 2; w++) scan_bins(shist + w * kFxBins, 0ull, w, pre[w], part);
   if (tid < (int)(2 * npct)) {
@@ -809,7 +809,6 @@ __global__ void __launch_bounds__(1024) sel_plan_sampled(SampPlan* __restrict__ 
       sp->nslot[w] = slots;
     }
     if (fail) s_niv[0] = s_niv[1] = 0;  // every bin in gap 0
-    s_fail = fail;
     sp->fail = fail;
     for (uint32_t w = 0; w < 2; w++) {
       sp->niv[w] = s_niv[w];
@@ -841,7 +840,9 @@ __global__ void __launch_bounds__(1024) sel_plan_sampled(SampPlan* __restrict__ 
 // lookup (uncounted keys read an extra "none" entry).  Gaps (most keys): per-lane 8-bit
 // counters packed in registers (gaps 0-7 in a u64, 8-9 in a u32), flushed to shared memory
 // every 31 tiles (<= 248 keys per field); slots: one shared atomic per key; copies: a per-warp
-// shared stage flushed 32 keys at a time with one reservation.
+// shared stage flushed 32 keys at a time with one reservation.  Per-thread shared gap counters
+// instead of the packed registers: 96 M instead of 102 M warp instructions, same time (157-161
+// us at 10^9 rows, profiles/r02_sel_pass_gaps_ab.txt): the pass is latency, not issue, bound.
 constexpr uint16_t kSpNone = 0x4000u;  // map entry of an uncounted key
 #ifndef SP_MINB
 #define SP_MINB 3  // resident CTAs ptxas budgets registers for (1 / 3 / 4 measured: 1.34 / 1.33 / 1.33 ms reduce + selection at 10^9 rows, pass 177 / 157 / 221 us under ncu)
