@@ -674,15 +674,24 @@ __global__ void __launch_bounds__(256) sel_sample_hist(const double* __restrict_
   __shared__ uint32_t h[2 * kFxBins];
   for (uint32_t i = threadIdx.x; i < 2 * kFxBins; i += blockDim.x) h[i] = 0;
   __syncthreads();
-  const uint64_t total = kSampleRuns * kSampleRun;
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < total;
-       j += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t i = lo + (j / kSampleRun) * rstride + (j % kSampleRun);
-    if (i >= hi) continue;
-    const uint64_t kp = (uint64_t)__double_as_longlong(__ldcs(perf + i));
-    const uint64_t kg = (uint64_t)__double_as_longlong(__ldcs(gain + i));
-    if (valid_key(kp)) atomicAdd(&h[fx_perf_bin(kp)], 1u);
-    if (valid_key(kg)) atomicAdd(&h[kFxBins + fx_gain_bin(kg)], 1u);
+  // four samples of each quantity in flight per thread (the loop is load-latency bound)
+  constexpr int kV = 4;
+  const uint64_t total = kSampleRuns * kSampleRun, T = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j0 < total; j0 += kV * T) {
+    uint64_t kp[kV], kg[kV];
+#pragma unroll
+    for (int v = 0; v < kV; v++) {
+      const uint64_t j = j0 + v * T;
+      const uint64_t i = lo + (j / kSampleRun) * rstride + (j % kSampleRun);
+      const bool in = j < total && i < hi;
+      kp[v] = in ? (uint64_t)__double_as_longlong(__ldcs(perf + i)) : kNaNKey;
+      kg[v] = in ? (uint64_t)__double_as_longlong(__ldcs(gain + i)) : kNaNKey;
+    }
+#pragma unroll
+    for (int v = 0; v < kV; v++) {
+      if (valid_key(kp[v])) atomicAdd(&h[fx_perf_bin(kp[v])], 1u);
+      if (valid_key(kg[v])) atomicAdd(&h[kFxBins + fx_gain_bin(kg[v])], 1u);
+    }
   }
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < 2 * kFxBins; i += blockDim.x)
@@ -777,51 +786,67 @@ __global__ void __launch_bounds__(1024) sel_plan_sampled(SampPlan* __restrict__ 
     tb2[tid] = b2;
   }
   __syncthreads();
-  if (tid == 0) {  // per quantity: sort the targets' intervals, merge overlapping / adjacent ones
-    uint32_t fail = 0;
-    for (uint32_t w = 0; w < 2; w++) {
-      uint32_t idx[kMaxT / 2], n = 0;
-      for (uint32_t i = 0; i < npct; i++)
-        if (tb1[w * npct + i] <= tb2[w * npct + i]) idx[n++] = w * npct + i;
-      for (uint32_t a = 1; a < n; a++)
-        for (uint32_t b = a; b > 0 && tb1[idx[b]] < tb1[idx[b - 1]]; b--) {
-          const uint32_t x = idx[b]; idx[b] = idx[b - 1]; idx[b - 1] = x;
-        }
-      uint32_t m = 0, slots = 0;
-      for (uint32_t a = 0; a < n && !fail; a++) {
-        const uint32_t i = idx[a];
-        if (m > 0 && tb1[i] <= s_b2[w][m - 1] + 1) {
-          if (tb2[i] > s_b2[w][m - 1]) s_b2[w][m - 1] = tb2[i];
-        } else if (m == kIvQ) {
-          fail = 1;
-        } else {
-          s_b1[w][m] = tb1[i];
-          s_b2[w][m] = tb2[i];
-          m++;
-        }
-      }
-      for (uint32_t r = 0; r < m; r++) {
-        s_slot0[w][r] = slots;
-        slots += s_b2[w][r] - s_b1[w][r] + 1;
-      }
-      if (slots > kSpSlots) fail = 1;
-      s_niv[w] = m;
-      sp->nslot[w] = slots;
-    }
-    if (fail) s_niv[0] = s_niv[1] = 0;  // every bin in gap 0
-    sp->fail = fail;
-    for (uint32_t w = 0; w < 2; w++) {
-      sp->niv[w] = s_niv[w];
-      sp->ncopy[w] = 0;
-      sp->ncopy_all[w] = 0;
-      for (uint32_t r = 0; r < s_niv[w]; r++) {
-        sp->b1[w][r] = s_b1[w][r];
-        sp->b2[w][r] = s_b2[w][r];
-        sp->slot0[w][r] = s_slot0[w][r];
-      }
+  // per quantity: the targets' non-empty intervals sorted by (b1, target) by a parallel rank
+  // count, then merged (overlapping / adjacent) by one thread over the sorted shared arrays
+  __shared__ uint32_t srt1[kMaxT], srt2[kMaxT], s_n[2];
+  if (tid < 2) s_n[tid] = 0;
+  __syncthreads();
+  if (tid < (int)(2 * npct)) {
+    const uint32_t w = tid >= (int)npct, base = w * npct;
+    if (tb1[tid] <= tb2[tid]) {
+      uint32_t r = 0;
+      for (uint32_t j = base; j < base + npct; j++)
+        r += tb1[j] <= tb2[j] && (tb1[j] < tb1[tid] || (tb1[j] == tb1[tid] && j < (uint32_t)tid));
+      srt1[base + r] = tb1[tid];
+      srt2[base + r] = tb2[tid];
+      atomicAdd(&s_n[w], 1u);
     }
   }
   __syncthreads();
+  if (tid < 2) {  // thread w merges quantity w
+    const uint32_t w = tid, base = w * npct, n = s_n[w];
+    uint32_t m = 0, slots = 0, fail = 0;
+    for (uint32_t a = 0; a < n && !fail; a++) {
+      const uint32_t b1 = srt1[base + a], b2 = srt2[base + a];
+      if (m > 0 && b1 <= s_b2[w][m - 1] + 1) {
+        if (b2 > s_b2[w][m - 1]) s_b2[w][m - 1] = b2;
+      } else if (m == kIvQ) {
+        fail = 1;
+      } else {
+        s_b1[w][m] = b1;
+        s_b2[w][m] = b2;
+        m++;
+      }
+    }
+    for (uint32_t r = 0; r < m; r++) {
+      s_slot0[w][r] = slots;
+      slots += s_b2[w][r] - s_b1[w][r] + 1;
+    }
+    if (slots > kSpSlots) fail = 1;
+    s_niv[w] = m;
+    sp->nslot[w] = slots;
+    s_n[w] = fail;  // reused: this quantity's plan failed
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const uint32_t fail = s_n[0] | s_n[1];
+    if (fail) s_niv[0] = s_niv[1] = 0;  // every bin in gap 0
+    sp->fail = fail;
+  }
+  __syncthreads();
+  if (tid < 2 * (int)kIvQ) {
+    const uint32_t w = tid / kIvQ, r = tid % kIvQ;
+    if (r < s_niv[w]) {
+      sp->b1[w][r] = s_b1[w][r];
+      sp->b2[w][r] = s_b2[w][r];
+      sp->slot0[w][r] = s_slot0[w][r];
+    }
+    if (r == 0) {
+      sp->niv[w] = s_niv[w];
+      sp->ncopy[w] = 0;
+      sp->ncopy_all[w] = 0;
+    }
+  }
   for (uint32_t i = tid; i < 2 * kFxBins; i += blockDim.x) {
     const uint32_t w = i / kFxBins, b = i % kFxBins;
     uint32_t e = 0;  // gap = intervals entirely below b
@@ -1013,10 +1038,20 @@ __global__ void __launch_bounds__(1024) sel_check_sampled(SelState* st, const Sa
   __shared__ uint16_t sbin[2][2048];  // bin of a slot / the single-valued bin; 0xFFFF: a gap
   __shared__ unsigned long long wsum[32];
   __shared__ uint32_t s_fail, s_len[2];
+  __shared__ uint32_t q_niv[2], q_nslot[2], q_b1[2][kIvQ], q_slot0[2][kIvQ];  // the plan, in smem
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const unsigned FULL = 0xffffffffu;
   const uint64_t n_def = partials[LSCAT_P_RATIO_DEFINED];
   const unsigned long long n_one = partials[LSCAT_P_NCOUNTERS + nb];  // perf == 1 <=> gain == 0
+  if (tid < 2 * (int)kIvQ) {
+    const uint32_t w = tid / kIvQ, r = tid % kIvQ;
+    q_b1[w][r] = sp->b1[w][r];
+    q_slot0[w][r] = sp->slot0[w][r];
+    if (r == 0) {
+      q_niv[w] = sp->niv[w];
+      q_nslot[w] = sp->nslot[w];
+    }
+  }
   if (tid == 0) {
     s_fail = force_miss || sp->fail || sp->ncopy_all[0] > kCompactCap || sp->ncopy_all[1] > kCompactCap;
     for (uint32_t w = 0; w < 2; w++) {
@@ -1029,7 +1064,7 @@ __global__ void __launch_bounds__(1024) sel_check_sampled(SelState* st, const Sa
   __syncthreads();
   for (uint32_t w = 0; w < 2; w++) {
     // element e of the sequence -> count and bin (gain: the single-valued bin first)
-    const uint32_t niv = sp->niv[w], len = s_len[w];
+    const uint32_t niv = q_niv[w], len = s_len[w];
     for (uint32_t e = tid; e < 2048; e += blockDim.x) {
       unsigned long long c = 0;
       uint32_t bin = 0xFFFFu;
@@ -1042,15 +1077,15 @@ __global__ void __launch_bounds__(1024) sel_check_sampled(SelState* st, const Sa
           // q - 1 = position in gap 0, slots..., gap niv; interval iv's slots start at slot0 + iv + 1
           const uint32_t x = q - 1;
           uint32_t iv = 0;
-          while (iv < niv && x >= sp->slot0[w][iv] + iv + 1) iv++;
+          while (iv < niv && x >= q_slot0[w][iv] + iv + 1) iv++;
           // x in [slot0[iv-1] + iv, slot0[iv] + iv]: gap iv sits at slot0[iv] + iv (or the end)
-          const uint32_t gpos = iv < niv ? sp->slot0[w][iv] + iv : sp->nslot[w] + niv;
+          const uint32_t gpos = iv < niv ? q_slot0[w][iv] + iv : q_nslot[w] + niv;
           if (x == gpos) {
             c = sp->cnt[w][kSpSlots + iv];
           } else {  // a slot of interval iv - 1
             const uint32_t r = iv - 1, sl = x - r - 1;
             c = sp->cnt[w][sl];
-            bin = sp->b1[w][r] + (sl - sp->slot0[w][r]);
+            bin = q_b1[w][r] + (sl - q_slot0[w][r]);
           }
         }
       }
@@ -1698,7 +1733,26 @@ struct SelBufs {
   unsigned long long* fcand = nullptr;
 };
 
+// One shared-memory carve-out (maximum shared) for every kernel of the selection paths, as for
+// the reducer and the level chain: a kernel whose carve-out differs from its predecessor's
+// waits for the SMs to be reconfigured (measured at 10^9 rows: the one-CTA plan and check
+// kernels took 18 / 16 us between events, mostly that wait).  Once per device.
+lscat_status sel_carveout(lscat_ctx* ctx) {
+  static bool done[64] = {};
+  const int d = ctx->device;
+  if (d >= 0 && d < 64 && done[d]) return LSCAT_OK;
+  const void* fs[] = {(const void*)sel_sample_hist, (const void*)sel_plan_sampled,
+                      (const void*)sel_pass_sampled<256>, (const void*)sel_check_sampled,
+                      (const void*)sel_finish, (const void*)sel_small};
+  for (const void* f : fs)
+    LSCAT_CUDA(ctx, cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         (int)cudaSharedmemCarveoutMaxShared));
+  if (d >= 0 && d < 64) done[d] = true;
+  return LSCAT_OK;
+}
+
 lscat_status sel_bufs(lscat_ctx* ctx, uint32_t cap, SelBufs* b) {
+  if (lscat_status cs = sel_carveout(ctx)) return cs;
   cudaError_t err = cudaSuccess;
   auto S = [&](const char* name, size_t bytes) { void* p = scratch(ctx, name, bytes, &err); return p; };
   b->st = (SelState*)S("sel_state", sizeof(SelState));
@@ -1716,6 +1770,37 @@ lscat_status sel_bufs(lscat_ctx* ctx, uint32_t cap, SelBufs* b) {
   return LSCAT_OK;
 }
 
+// LSCAT_SEL_TIMING=1 (calibration): CUDA events between the stages of the sampled selection,
+// printed once the selection is collected (stderr).  Not used inside graph capture.
+std::vector<std::pair<const char*, cudaEvent_t>>& sel_events() {
+  static std::vector<std::pair<const char*, cudaEvent_t>> v;
+  return v;
+}
+void sel_mark(const char* name, cudaStream_t q) {
+  static const bool on = getenv("LSCAT_SEL_TIMING") != nullptr;
+  if (!on) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(q, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEventRecord(e, q);
+  sel_events().push_back({name, e});
+}
+void sel_print_events() {
+  auto& v = sel_events();
+  if (v.empty()) return;
+  cudaEventSynchronize(v.back().second);
+  fprintf(stderr, "sel timing (us):");
+  for (size_t i = 1; i < v.size(); i++) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, v[i - 1].second, v[i].second);
+    fprintf(stderr, " %s %.1f", v[i].first, ms * 1e3f);
+  }
+  fprintf(stderr, "\n");
+  for (auto& e : v) cudaEventDestroy(e.second);
+  v.clear();
+}
+
 // The sampled first level on stream q: sample, plan, pass, (NCCL sums,) check.  With `fin`
 // (one rank) the state after the check is copied to the host and sel_finish follows
 // (launch_finish); else the caller enqueues levels.
@@ -1729,17 +1814,20 @@ lscat_status enqueue_sampled(lscat_ctx* ctx, const SelBufs& B, const double* per
     LSCAT_CUDA(ctx, cudaMemsetAsync(B.hist, 0, (size_t)kMaxR * kBins * 4, q));
     LSCAT_CUDA(ctx, cudaMemsetAsync(B.cand, 0, (size_t)kMaxR * 8, q));
   }
+  sel_mark("start", q);
   LSCAT_CUDA(ctx, cudaMemsetAsync(B.shist, 0, 2 * kFxBins * 4, q));
   const uint64_t rstride = std::max<uint64_t>(kSampleRun, n / kSampleRuns);
   const int grid_s = (int)std::min<uint64_t>(kSampleRuns * kSampleRun / 256, (uint64_t)ctx->sm_count * 2);
   sel_sample_hist<<<grid_s, 256, 0, q>>>(perf, gain, lo, hi, rstride, B.shist);
   LSCAT_CUDA(ctx, cudaGetLastError());
+  sel_mark("sample", q);
   if (world > 1) {
     lscat_status ns = ctx->comm->allreduce(ctx, {{B.shist, 2 * (size_t)kFxBins, DT::U32, Op::Sum}}, q);
     if (ns) return ns;
   }
   sel_plan_sampled<<<1, 1024, 0, q>>>(B.sp, B.shist, pa, npct, 4.5, 32.0);
   LSCAT_CUDA(ctx, cudaGetLastError());
+  sel_mark("plan", q);
   static const int occ_p = [] {  // resident CTAs per SM of the pass (binary property; one-time)
     int v = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, sel_pass_sampled<256>, 256, 0);
@@ -1750,6 +1838,7 @@ lscat_status enqueue_sampled(lscat_ctx* ctx, const SelBufs& B, const double* per
                                              (uint64_t)ctx->sm_count * occ_p);
   sel_pass_sampled<256><<<grid_p, 256, 0, q>>>(perf, gain, lo, hi, B.sp, B.cbuf);
   LSCAT_CUDA(ctx, cudaGetLastError());
+  sel_mark("pass", q);
   if (world > 1) {  // exact counts and copy totals over all ranks
     lscat_status ns = ctx->comm->allreduce(ctx, {{&B.sp->cnt[0][0], 2 * (size_t)kSpCnt, DT::U32, Op::Sum},
                                                  {&B.sp->ncopy_all[0], 2, DT::U64, Op::Sum}}, q);
@@ -1759,6 +1848,7 @@ lscat_status enqueue_sampled(lscat_ctx* ctx, const SelBufs& B, const double* per
   static const uint32_t force_miss = getenv("LSCAT_SEL_FORCE_MISS") != nullptr ? 1u : 0u;
   sel_check_sampled<<<1, 1024, 0, q>>>(B.st, B.sp, partials, nb, mm, pa, npct, cap, force_miss);
   LSCAT_CUDA(ctx, cudaGetLastError());
+  sel_mark("check", q);
   if (fin) {  // sel_finish follows; the state as the check left it
     LSCAT_CUDA(ctx, cudaMemsetAsync(B.fs, 0, sizeof(FinSel), q));
     LSCAT_CUDA(ctx, cudaMemcpyAsync(B.hst, B.st, sizeof(SelState), cudaMemcpyDeviceToHost, q));
@@ -1780,6 +1870,7 @@ lscat_status launch_finish(lscat_ctx* ctx, const SelBufs& B, cudaStream_t q) {
   void* args[] = {(void*)&st_c, (void*)&cb_c, (void*)&fs, (void*)&fc, (void*)&ff_};
   LSCAT_CUDA(ctx, cudaLaunchCooperativeKernel((const void*)sel_finish, dim3(ctx->sm_count), dim3(1024), args,
                                               kFinSmem, q));
+  sel_mark("finish", q);
   LSCAT_CUDA(ctx, cudaMemcpyAsync(B.fsh, B.fs, kFinHead, cudaMemcpyDeviceToHost, q));
   ctx->launches++;
   return LSCAT_OK;
@@ -1796,6 +1887,7 @@ lscat_status early_select(lscat_ctx* ctx, const double* perf, const double* gain
   static const bool no_small = getenv("LSCAT_SEL_NOSMALL") != nullptr;
   static const bool no_sample = getenv("LSCAT_SEL_NOSAMPLE") != nullptr;
   static const bool no_finish = getenv("LSCAT_SEL_NOFINISH") != nullptr;
+  if (lscat_status cs = sel_carveout(ctx)) return cs;
   const PctArg pa = pct_arg(pct, npct);
   cudaError_t err;
   if (hi - lo <= kSmallKeys) {  // the one-launch selection
@@ -2068,6 +2160,7 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
       ctx->launches += 2 * lpb;
     }
     LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
+    if (batch == 0 && sampled) sel_print_events();
     if (debug && batch == 0 && sampled) {  // the sampled plan and its exact counts
       std::vector<SampPlan> h(1);
       LSCAT_CUDA(ctx, cudaMemcpy(h.data(), B.sp, sizeof(SampPlan), cudaMemcpyDeviceToHost));
