@@ -774,6 +774,57 @@ __device__ void kernel_fin(const RollupArgs& q, uint64_t c, unsigned __int128 S,
   else atomicAdd(&hist64[bin], 1ull);
 }
 
+// multiply-high reciprocals m_c = floor((2^64 - 1) / c) + 1 of c = 2..32 (m_0, m_1 unused)
+__constant__ uint64_t kRcp32[33] = {
+    0x0000000000000000ull, 0x0000000000000000ull, 0x8000000000000000ull,
+    0x5555555555555556ull, 0x4000000000000000ull, 0x3333333333333334ull,
+    0x2aaaaaaaaaaaaaabull, 0x2492492492492493ull, 0x2000000000000000ull,
+    0x1c71c71c71c71c72ull, 0x199999999999999aull, 0x1745d1745d1745d2ull,
+    0x1555555555555556ull, 0x13b13b13b13b13b2ull, 0x124924924924924aull,
+    0x1111111111111112ull, 0x1000000000000000ull, 0x0f0f0f0f0f0f0f10ull,
+    0x0e38e38e38e38e39ull, 0x0d79435e50d79436ull, 0x0ccccccccccccccdull,
+    0x0c30c30c30c30c31ull, 0x0ba2e8ba2e8ba2e9ull, 0x0b21642c8590b217ull,
+    0x0aaaaaaaaaaaaaabull, 0x0a3d70a3d70a3d71ull, 0x09d89d89d89d89d9ull,
+    0x097b425ed097b426ull, 0x0924924924924925ull, 0x08d3dcb08d3dcb09ull,
+    0x0888888888888889ull, 0x0842108421084211ull, 0x0800000000000000ull,
+};
+
+// kernel_fin for kernels of <= 32 groups (S <= c 2^52 <= 2^57): the same integers with 64-bit
+// arithmetic and 64 x 64 -> 128-bit products by mul.hi (no 128-bit multiplies or f64 division).
+__device__ __forceinline__ bool mul_lt(uint64_t a, uint64_t b, uint64_t c, uint64_t d) {  // a b < c d
+  const uint64_t h1 = __umul64hi(a, b), h2 = __umul64hi(c, d);
+  return h1 < h2 || (h1 == h2 && a * b < c * d);
+}
+__device__ void kernel_fin_small(const RollupArgs& q, uint32_t c, uint64_t S, bool not_best, KAcc& a,
+                                 uint32_t* hist32) {
+  if (c == 0) return;
+  const uint64_t cd = (uint64_t)c << 52;  // kernel-mean perf = S / cd
+  const bool lt = mul_lt(q.pld, S, q.pln, cd);
+  const bool band = lt && !mul_lt(q.bld, S, q.bln, cd);
+  // divisions by c <= 32 as a multiply-high by m = floor((2^64 - 1) / c) + 1 (c > 1), then one
+  // exact fix-up step each way (64-bit integer division is a long software sequence)
+  const uint64_t m = kRcp32[c];
+  auto divc = [&](uint64_t x) -> uint64_t {
+    if (c == 1) return x;
+    uint64_t d = __umul64hi(x, m);
+    if (d * c > x) d--;
+    if ((d + 1) * c <= x) d++;
+    return d;
+  };
+  // bin = floor(nb S / cd) = floor(floor(nb S / 2^52) / c)
+  const uint64_t nbS_lo = (uint64_t)q.nb * S, nbS_hi = __umul64hi((uint64_t)q.nb, S);
+  uint64_t bin = divc((nbS_hi << 12) | (nbS_lo >> 52));
+  if (bin > q.nb) bin = q.nb;  // perf <= 1 (defensive: the histogram has nb + 1 bins)
+  const uint64_t kfx = divc(S);  // floor(S / c) <= 2^52
+  a.v[0] += 1;
+  a.v[1] += not_best;
+  a.v[2] += lt;
+  a.v[3] += band;
+  a.v[4] += kfx >> 21;
+  a.v[5] += kfx & ((1ull << 21) - 1);
+  atomicAdd(&hist32[bin], 1u);
+}
+
 __device__ __forceinline__ void write_bnd(const RollupArgs& q, int slot, uint32_t k, uint64_t c,
                                           unsigned __int128 S, bool nbst) {
   uint64_t* b = q.bnd + slot * kBndWords;
@@ -872,6 +923,53 @@ __global__ void __launch_bounds__(256) rollup_kernel(RollupArgs q) {
     if (cv && lane == 0) {  // the last kernel reaches hi: it may continue on the next rank
       write_bnd(q, cfirst ? 0 : 1, ck, cc, cS, cn != 0);
     }
+  }
+#pragma unroll
+  for (int i = 0; i < 6; i++) {
+    unsigned long long x = acc.v[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0 && x) atomicAdd(&cnt[i], x);
+  }
+  __syncthreads();
+  unsigned long long* gc = reinterpret_cast<unsigned long long*>(q.part);
+  for (uint32_t i = threadIdx.x; i < kRollupWords; i += blockDim.x)
+    if (cnt[i]) atomicAdd(&gc[i], cnt[i]);
+  for (uint32_t i = threadIdx.x; i <= q.nb; i += blockDim.x)
+    if (hist[i]) atomicAdd(&gc[kRollupWords + i], (unsigned long long)hist[i]);
+}
+
+// Implicit kernel ids with a power-of-two M <= 32 (configs[4]): lane j of a warp takes
+// kernel k = kb + j whole (its M records read sequentially: a warp reads 32 M contiguous
+// records), sums c, S (< 2^58) and the not-best flag in registers and finalises the kernel, or
+// writes the boundary record when the kernel reaches past this rank's range (it may continue on
+// a neighbouring rank).  Same totals as rollup_kernel, with every lane finalising a kernel.
+__global__ void __launch_bounds__(256) rollup_uniform_kernel(RollupArgs q) {
+  extern __shared__ unsigned long long rs[];
+  unsigned long long* cnt = rs;                                  // [kRollupWords]
+  uint32_t* hist = reinterpret_cast<uint32_t*>(rs + kRollupWords);  // [nb + 1]
+  for (uint32_t i = threadIdx.x; i < kRollupWords; i += blockDim.x) cnt[i] = 0;
+  for (uint32_t i = threadIdx.x; i <= q.nb; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  KAcc acc{};
+  const uint32_t M = q.M;
+  const uint64_t alo = q.first_group + q.lo, ahi = q.first_group + q.hi;  // absolute range
+  const uint64_t k0 = alo >> q.mshift, k1 = (ahi + M - 1) >> q.mshift;   // kernels touched
+  const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = k0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < k1; k += T) {
+    const uint64_t g0 = k << q.mshift;  // the kernel's first absolute group
+    uint32_t c = 0, nbst = 0;
+    uint64_t S = 0;
+    for (uint32_t i = 0; i < M; i++) {
+      const uint64_t ga = g0 + i;
+      const uint64_t r = (ga >= alo && ga < ahi) ? q.krec[ga - q.first_group] : 0ull;
+      const uint32_t rd = (uint32_t)((r >> 53) & 1);
+      c += rd;
+      S += rd ? (r & ((1ull << 53) - 1)) : 0ull;
+      nbst |= rd & (uint32_t)((r >> 54) & 1);
+    }
+    if (g0 >= alo && g0 + M <= ahi) kernel_fin_small(q, c, S, nbst != 0, acc, hist);
+    else write_bnd(q, g0 < alo ? 0 : 1, (uint32_t)k, c, (unsigned __int128)S, nbst != 0);
   }
 #pragma unroll
   for (int i = 0; i < 6; i++) {
@@ -1148,7 +1246,18 @@ static lscat_status reduce_enqueue(lscat_ctx* ctx, const lscat_table* T, const l
     const size_t rsm = kRollupWords * 8 + (o->bins_per_unit + 1) * 4;
     if (rsm > 48 * 1024) LSCAT_CUDA(ctx, ensure_smem_attr((const void*)rollup_kernel, rsm));
     const uint64_t ng = q.hi - q.lo;
-    if (ng) {
+    // implicit ids, M a power of two <= 32: aligned-chunk kernel (LSCAT_ROLLUP_GENERAL=1: the
+    // general segmented one, for A/B)
+    static const bool general = getenv("LSCAT_ROLLUP_GENERAL") != nullptr;
+    const bool uni = !q.gkern && q.mshift >= 0 && q.M <= 32 && !general;
+    if (uni && rsm > 48 * 1024) LSCAT_CUDA(ctx, ensure_smem_attr((const void*)rollup_uniform_kernel, rsm));
+    if (ng && uni) {
+      const uint64_t nk = (ng + 2 * q.M) / q.M;  // kernels touched (upper bound)
+      const int g4 = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)ctx->sm_count * 8, (nk + 255) / 256));
+      rollup_uniform_kernel<<<g4, 256, rsm, s>>>(q);
+      ctx->launches++;
+      LSCAT_CUDA(ctx, cudaGetLastError());
+    } else if (ng) {
       const int g4 = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)ctx->sm_count * 8, (ng + 255) / 256));
       rollup_kernel<<<g4, 256, rsm, s>>>(q);
       ctx->launches++;

@@ -186,3 +186,26 @@ def test_point_sharded_sweep_then_reduce(world):
             assert st[k] == v, k
         assert (st["best_block_hist"] == ref.best_block_hist).all()
         assert st["pct_perf"] == ref.percentiles["perf"] and st["pct_gain"] == ref.percentiles["gain"]
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_implicit_kernel_rollup_shards(world):
+    """The per-kernel roll-up with implicit kernel ids (no group_kernel array: kernel =
+    (first_group + g) / 8, configs[4]'s layout) runs the aligned-chunk roll-up kernel;
+    group-aligned shards whose boundaries cut kernels hand those kernels to the boundary merge.
+    Roll-up values bit-exact against the oracle on the whole table."""
+    require_gpu()
+    K = 20_003                          # G / 2, G / 3 not multiples of 8: shards cut kernels
+    n = 32 * 8 * K                      # G = 8 K: every kernel has exactly 8 groups
+    full = gen_table(n, K, preset="t4", seed=77)
+    G = full["n_groups"]
+    ref = OT.reduce_table(full["runtime_ms"], full["block_id"], full["group_offset"],
+                          group_matrix=full["group_matrix"], percentiles=PCTS,
+                          group_kernel=np.arange(G, dtype=np.uint32) // 8, kernel_rollup=True)
+
+    def make(ctx, r):
+        return ctx.gen_table(n, K, preset=0, seed=77, group_begin=G * r // world,
+                             group_end=G * (r + 1) // world if world > 1 else 0, offsets=False)
+
+    res = _run_ranks(world, make, dict(kernel_rollup=1), f"ir{world}")
+    _check(res, ref)
