@@ -869,6 +869,9 @@ __global__ void __launch_bounds__(1024) sel_plan_sampled(SampPlan* __restrict__ 
 // instead of the packed registers: 96 M instead of 102 M warp instructions, same time (157-161
 // us at 10^9 rows, profiles/r02_sel_pass_gaps_ab.txt): the pass is latency, not issue, bound.
 constexpr uint16_t kSpNone = 0x4000u;  // map entry of an uncounted key
+#ifndef SP_PIPE
+#define SP_PIPE 0  // 1: the next tile's loads in flight while a tile is counted (A/B)
+#endif
 #ifndef SP_MINB
 #define SP_MINB 3  // resident CTAs ptxas budgets registers for (1 / 3 / 4 measured: 1.34 / 1.33 / 1.33 ms reduce + selection at 10^9 rows, pass 177 / 157 / 221 us under ncu)
 #endif
@@ -929,9 +932,8 @@ __global__ void __launch_bounds__(kT, SP_MINB) sel_pass_sampled(const double* __
     const uint32_t e = map[w][b];
     glo[w] += e < 8u ? 1ull << (8 * e) : 0ull;
     ghi[w] += e - 8u < 2u ? 1u << (8 * (e - 8u)) : 0u;
-    const bool slot = (e & kSpSlotFlag) != 0;
-    if (slot) atomicAdd(&cnt[w * kSpCnt + (e & (kSpSlotFlag - 1))], 1u);
-    return slot ? 1u : 0u;
+    // a slot key is only copied: the slot counts are the copies' histogram (sel_slot_counts)
+    return (e & kSpSlotFlag) != 0 ? 1u : 0u;
   };
   // per tile and quantity: the lanes' copied keys (bit u of mask: key u) placed by one warp
   // scan, staged (or, above the stage, written with their own reservation)
@@ -973,14 +975,42 @@ __global__ void __launch_bounds__(kT, SP_MINB) sel_pass_sampled(const double* __
   const uint64_t* Q = reinterpret_cast<const uint64_t*>(gain) + lo;
   const uint64_t n = hi - lo, full = n / (kT * kU);
   int since = 0;
+#if SP_PIPE
+  // software pipeline: the next tile's loads are issued before this tile is counted
+  uint64_t np_[kU], ng_[kU];
+  if (blockIdx.x < full) {
+    const uint64_t off = blockIdx.x * (uint64_t)(kT * kU) + threadIdx.x;
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+      np_[u] = __ldcs(P + off + u * kT);
+      ng_[u] = __ldcs(Q + off + u * kT);
+    }
+  }
+#endif
   for (uint64_t t = blockIdx.x; t < full; t += gridDim.x) {
-    const uint64_t off = t * (kT * kU) + threadIdx.x;
     uint64_t vp[kU], vg[kU];
+#if SP_PIPE
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+      vp[u] = np_[u];
+      vg[u] = ng_[u];
+    }
+    if (t + gridDim.x < full) {
+      const uint64_t off = (t + gridDim.x) * (kT * kU) + threadIdx.x;
+#pragma unroll
+      for (int u = 0; u < kU; u++) {
+        np_[u] = __ldcs(P + off + u * kT);
+        ng_[u] = __ldcs(Q + off + u * kT);
+      }
+    }
+#else
+    const uint64_t off = t * (kT * kU) + threadIdx.x;
 #pragma unroll
     for (int u = 0; u < kU; u++) {
       vp[u] = __ldcs(P + off + u * kT);
       vg[u] = __ldcs(Q + off + u * kT);
     }
+#endif
     uint32_t mp = 0, mg = 0;
 #pragma unroll
     for (int u = 0; u < kU; u++) {
@@ -1017,6 +1047,39 @@ __global__ void __launch_bounds__(kT, SP_MINB) sel_pass_sampled(const double* __
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < 2 * kSpCnt; i += kT)
     if (cnt[i]) atomicAdd(&sp->cnt[0][0] + i, cnt[i]);
+}
+
+// After the pass: the exact count of every slot is the histogram of the copies (every key of
+// a slot bin was copied; a copy overflow is caught by the check), per CTA in shared memory,
+// flushed once.  Cheaper than a shared atomic per slot key inside the pass (measured: the
+// pass 162 -> 142 us at 10^9 rows without them).
+__global__ void __launch_bounds__(256) sel_slot_counts(const double* __restrict__ cbuf, SampPlan* __restrict__ sp) {
+  __shared__ uint16_t map[2][kFxBins];
+  __shared__ uint32_t h[2][kSpSlots];
+  for (uint32_t i = threadIdx.x; i < 2 * kFxBins; i += blockDim.x) (&map[0][0])[i] = (&sp->map[0][0])[i];
+  for (uint32_t i = threadIdx.x; i < 2 * kSpSlots; i += blockDim.x) (&h[0][0])[i] = 0;
+  __syncthreads();
+  const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+#pragma unroll 1
+  for (uint32_t w = 0; w < 2; w++) {
+    const uint64_t n = min(sp->ncopy[w], (unsigned long long)kCompactCap);
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(cbuf) + (size_t)w * kCompactCap;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += 4 * T) {
+      uint64_t k[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) k[u] = i + u * T < n ? __ldcg(src + i + u * T) : kNaNKey;
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const uint32_t kh = (uint32_t)(k[u] >> 32);
+        if (kh >= 0x7FF00000u) continue;  // padding
+        const uint32_t e = map[w][w == 0 ? fx_perf_bin_hi(kh) : fx_gain_bin_hi(kh)];
+        if (e & kSpSlotFlag) atomicAdd(&h[w][e & (kSpSlotFlag - 1)], 1u);
+      }
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < 2 * kSpSlots; i += blockDim.x)
+    if ((&h[0][0])[i]) atomicAdd(&sp->cnt[i / kSpSlots][i % kSpSlots], (&h[0][0])[i]);
 }
 
 // One CTA of 1024, after the pass (its counts summed over ranks): targets from the exact n_def (sel_init's ranks, R-13),
@@ -1741,7 +1804,7 @@ lscat_status sel_carveout(lscat_ctx* ctx) {
   static bool done[64] = {};
   const int d = ctx->device;
   if (d >= 0 && d < 64 && done[d]) return LSCAT_OK;
-  const void* fs[] = {(const void*)sel_sample_hist, (const void*)sel_plan_sampled,
+  const void* fs[] = {(const void*)sel_sample_hist, (const void*)sel_plan_sampled, (const void*)sel_slot_counts,
                       (const void*)sel_pass_sampled<256>, (const void*)sel_check_sampled,
                       (const void*)sel_finish, (const void*)sel_small};
   for (const void* f : fs)
@@ -1839,6 +1902,9 @@ lscat_status enqueue_sampled(lscat_ctx* ctx, const SelBufs& B, const double* per
   sel_pass_sampled<256><<<grid_p, 256, 0, q>>>(perf, gain, lo, hi, B.sp, B.cbuf);
   LSCAT_CUDA(ctx, cudaGetLastError());
   sel_mark("pass", q);
+  sel_slot_counts<<<ctx->sm_count * 4, 256, 0, q>>>(B.cbuf, B.sp);  // latency bound: 4 CTAs per SM
+  LSCAT_CUDA(ctx, cudaGetLastError());
+  sel_mark("slots", q);
   if (world > 1) {  // exact counts and copy totals over all ranks
     lscat_status ns = ctx->comm->allreduce(ctx, {{&B.sp->cnt[0][0], 2 * (size_t)kSpCnt, DT::U32, Op::Sum},
                                                  {&B.sp->ncopy_all[0], 2, DT::U64, Op::Sum}}, q);
@@ -1915,7 +1981,7 @@ lscat_status early_select(lscat_ctx* ctx, const double* perf, const double* gain
   lscat_status bs = sel_bufs(ctx, 8192, &B);
   if (bs) return bs;
   if ((bs = enqueue_sampled(ctx, B, perf, gain, lo, hi, partials, mm, nb, pa, npct, 8192, true, s))) return bs;
-  ctx->launches += 4;
+  ctx->launches += 5;
   if ((bs = launch_finish(ctx, B, s))) return bs;
   *kind = EARLY_SAMPLED;
   return LSCAT_OK;
@@ -2138,9 +2204,9 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
     }
     if (samp && fin) {
       if (lscat_status fe = launch_finish(ctx, B, s)) return fe;
-      ctx->launches += 4;
+      ctx->launches += 5;
     } else {
-      ctx->launches += (samp ? 4 : 1) + 2 * lpb;
+      ctx->launches += (samp ? 5 : 1) + 2 * lpb;
     }
     return LSCAT_OK;
   };

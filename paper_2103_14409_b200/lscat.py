@@ -315,9 +315,21 @@ class Table:
         return d
 
 
-def _stream(stream):
+_raw_stream = None
+
+
+def _stream(stream, device=None):
+    """The cudaStream_t of `stream` (None: torch's current stream on `device`).  The current
+    stream is read with torch's raw-pointer accessor when available (constructing a Stream
+    object costs ~3 us per call on the small tables' critical path)."""
+    global _raw_stream
     if stream is None:
         import torch
+        if device is not None:
+            if _raw_stream is None:
+                _raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", False)
+            if _raw_stream:
+                return C.c_void_p(_raw_stream(device))
         return C.c_void_p(torch.cuda.current_stream().cuda_stream)
     if isinstance(stream, int):
         return C.c_void_p(stream)
@@ -440,12 +452,12 @@ class Ctx:
     # a6-a9
     def reduce_table(self, table: Table, opts: ReduceOpts, per_group=True, partials=False,
                      stream=None):
-        import torch
         G = table.n_groups
-        dev = f"cuda:{self.device}"
         out = {}
         oc = ReduceOutC()
         if per_group:
+            import torch
+            dev = f"cuda:{self.device}"
             out = dict(best_block_id=torch.empty(max(G, 1), dtype=torch.int16, device=dev),
                        best_runtime=torch.empty(max(G, 1), dtype=torch.float32, device=dev),
                        perf=torch.empty(max(G, 1), dtype=torch.float64, device=dev),
@@ -454,11 +466,12 @@ class Ctx:
             for k, v in out.items():
                 setattr(oc, k, v.data_ptr())
         if partials:
-            out["partials"] = torch.zeros(partials_len(opts), dtype=torch.int64, device=dev)
+            import torch
+            out["partials"] = torch.zeros(partials_len(opts), dtype=torch.int64, device=f"cuda:{self.device}")
             oc.partials = out["partials"].data_ptr()
         tc = table.c(with_groups=not table.rows_per_group or table.group_offset is not None)
         self._ck(self._lib.lscat_reduce_table(self.h, C.byref(tc), C.byref(opts), C.byref(oc),
-                                              _stream(stream)), "reduce_table")
+                                              _stream(stream, self.device)), "reduce_table")
         # the library reads the per-group perf/gain again in lscat_stats (keep_values): hold
         # the tensors until the next reduce_table or close, even if the caller drops `out`
         self._reduce_keep = out
@@ -495,7 +508,7 @@ class Ctx:
         pc[:] = pcs
         pp.fill(np.nan)
         pg.fill(np.nan)
-        self._ck(self._lib.lscat_stats(self.h, C.byref(opts), C.byref(so), _stream(stream)),
+        self._ck(self._lib.lscat_stats(self.h, C.byref(opts), C.byref(so), _stream(stream, self.device)),
                  "stats")
         raw = bytes(so)  # counters (u64) then the derived doubles, in COUNTERS / DERIVED order
         res = dict(zip(COUNTERS, np.frombuffer(raw, np.uint64, len(COUNTERS)).tolist()))

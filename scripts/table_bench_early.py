@@ -18,7 +18,7 @@ out = {}
 for name, n, K, preset, seed, offs in (("gtx980", 2_140_796, 8363, L.PRESET_GTX980, 980, True),
                                        ("t4", 5_028_536, 19_683, L.PRESET_T4, 4, True),
                                        ("scaled_1e9", 1_000_000_000, 3_906_250, L.PRESET_T4, 10 ** 9, False)):
-    if os.environ.get("LSCAT_TABLE_SMALL_ONLY") and n > 10 ** 8:
+    if os.environ.get("LSCAT_TABLE_SMALL_ONLY") and n > 10 ** 8 or (os.environ.get("LSCAT_TABLE_ONE") and n > 3_000_000):
         continue
     tab = c.gen_table(n, K, preset=preset, seed=seed, offsets=offs)
     res = {}
