@@ -880,31 +880,33 @@ __global__ void __launch_bounds__(kT, SP_MINB) sel_pass_sampled(const double* __
                                                        const double* __restrict__ gain, uint64_t lo,
                                                        uint64_t hi, SampPlan* __restrict__ sp,
                                                        double* __restrict__ cbuf) {
-  constexpr int kU = 8, kFlushTiles = 31;
-  static_assert(kFlushTiles * kU < 256, "8-bit gap fields");
-  __shared__ uint16_t map[2][kFxBins + 1];
-  __shared__ uint32_t cnt[2 * kSpCnt];
+  constexpr int kU = 8, kFlushTiles = 7;
+  static_assert(kFlushTiles * kU < 64, "6-bit gap fields");
+  // per fixed bin (+ an entry for uncounted keys) one word: the slot flag in bit 63, else the
+  // gap's increment 1 << 6 g (ten 6-bit fields: one 64-bit add counts a key)
+  __shared__ uint64_t incm[2][kFxBins + 1];
+  __shared__ uint32_t cnt[2][kIvQ + 1];  // gap counters (slots: sel_slot_counts)
   __shared__ uint64_t stage[kT / 32][2][kSpStage];
   for (uint32_t i = threadIdx.x; i < 2 * (kFxBins + 1); i += kT) {
     const uint32_t w = i / (kFxBins + 1), b = i % (kFxBins + 1);
-    map[w][b] = b < kFxBins ? sp->map[w][b] : kSpNone;
+    const uint32_t e = b < kFxBins ? sp->map[w][b] : kSpNone;
+    incm[w][b] = (e & kSpSlotFlag) ? (1ull << 63) : (e < 10u ? 1ull << (6 * e) : 0ull);
   }
-  for (uint32_t i = threadIdx.x; i < 2 * kSpCnt; i += kT) cnt[i] = 0;
+  if (threadIdx.x < 2 * (kIvQ + 1)) (&cnt[0][0])[threadIdx.x] = 0;
   __syncthreads();
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint64_t glo[2] = {0ull, 0ull};
-  uint32_t ghi[2] = {0u, 0u}, nst[2] = {0u, 0u};
+  uint64_t gacc[2] = {0ull, 0ull};
+  uint32_t nst[2] = {0u, 0u};
   auto flush_gaps = [&]() {
 #pragma unroll
     for (int w = 0; w < 2; w++) {
 #pragma unroll
       for (int g = 0; g < 10; g++) {
-        const uint32_t c = g < 8 ? (uint32_t)(glo[w] >> (8 * g)) & 255u : (ghi[w] >> (8 * (g - 8))) & 255u;
-        if (c) atomicAdd(&cnt[w * kSpCnt + kSpSlots + g], c);
+        const uint32_t c = (uint32_t)(gacc[w] >> (6 * g)) & 63u;
+        if (c) atomicAdd(&cnt[w][g], c);
       }
-      glo[w] = 0ull;
-      ghi[w] = 0u;
+      gacc[w] = 0ull;
     }
   };
   auto flush_stage = [&](uint32_t w) {  // warp-collective: every staged key, one reservation
@@ -929,11 +931,10 @@ __global__ void __launch_bounds__(kT, SP_MINB) sel_pass_sampled(const double* __
       b = kh < (uint32_t)(kPerfOne >> 32) ? fx_perf_bin_hi(kh) : kFxBins;
     else         // 0 < gain (no gain is below 2^-32 but 0), not NaN
       b = kh - 1u < 0x7FEFFFFFu ? fx_gain_bin_hi(kh) : kFxBins;
-    const uint32_t e = map[w][b];
-    glo[w] += e < 8u ? 1ull << (8 * e) : 0ull;
-    ghi[w] += e - 8u < 2u ? 1u << (8 * (e - 8u)) : 0u;
+    const uint64_t v = incm[w][b];
+    gacc[w] += v & ((1ull << 60) - 1);
     // a slot key is only copied: the slot counts are the copies' histogram (sel_slot_counts)
-    return (e & kSpSlotFlag) != 0 ? 1u : 0u;
+    return (uint32_t)(v >> 63);
   };
   // per tile and quantity: the lanes' copied keys (bit u of mask: key u) placed by one warp
   // scan, staged (or, above the stage, written with their own reservation)
@@ -1045,8 +1046,10 @@ __global__ void __launch_bounds__(kT, SP_MINB) sel_pass_sampled(const double* __
   for (uint32_t w = 0; w < 2; w++)
     if (nst[w]) flush_stage(w);
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < 2 * kSpCnt; i += kT)
-    if (cnt[i]) atomicAdd(&sp->cnt[0][0] + i, cnt[i]);
+  if (threadIdx.x < 2 * (kIvQ + 1)) {
+    const uint32_t w = threadIdx.x / (kIvQ + 1), g = threadIdx.x % (kIvQ + 1);
+    if (cnt[w][g]) atomicAdd(&sp->cnt[w][kSpSlots + g], cnt[w][g]);
+  }
 }
 
 // After the pass: the exact count of every slot is the histogram of the copies (every key of
