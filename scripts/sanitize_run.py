@@ -49,6 +49,18 @@ c.ingest(T(gk.astype(np.uint32), np.int32), T(gm.astype(np.uint32), np.int32),
 c.aggregation_experiment(torch.rand(1000, device="cuda") + 1, k=10, reps=200, seed=1)
 c.occupancy_block(L.K_EUCLID, list(range(32, 1025, 32)))
 c.timeout_curve(tab, [1e-3, 1.0], 1, 2, 2)
+if "--round2" in sys.argv:  # round-2 paths: early selection, graph replay, sampled pass, roll-up
+    P9 = [0.01, 0.05, 0.1, 0.25, 0.5, 0.75, 0.9, 0.95, 0.99]
+    small = c.gen_table(200_000, 800, preset=0, seed=5)
+    oe = L.reduce_opts(32, 8, percentiles=P9, kernel_rollup=1)
+    for _ in range(3):  # the third call replays the captured graph
+        c.reduce_table(small, oe, per_group=False)
+        c.stats(oe, percentiles=P9)
+    big = c.gen_table(32 * (1 << 20) + 32 * 4096, (1 << 20) // 8 + 512, preset=0, seed=6, offsets=False)
+    ob = L.reduce_opts(32, 8, percentiles=P9, kernel_rollup=1)
+    c.reduce_table(big, ob, per_group=False)  # > 2^20 groups: sampled selection + sel_finish
+    c.stats(ob, percentiles=P9)
+    c.stats(ob, percentiles=[0.3, 0.6])  # another list: the usual selection
 if "--gemm-multi" in sys.argv:  # persistent GEMM with two tiles per CTA (153 tiles)
     c.register_suite([L.K_GEMM_BF16], [2056])
     for b in (192, 256):
