@@ -317,7 +317,8 @@ def main():
     if cold_ms:
         mean_ms = float(np.mean(cold_ms))
         achieved = nbytes / (mean_ms * 1e-3) / 1e9
-        tr = load_traffic().get("euclid_8192_cold")
+        trs = load_traffic()  # the capture of the timed block when there is one
+        tr = trs.get(f"euclid_8192_b{colds[-1][0]}_cold", trs.get("euclid_8192_cold"))
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(achieved / hbm_peak, 4), "traffic": tr,
                 "kernel": f"euclid N=8192 block={colds[-1][0]}", "peak_kind": peak_kind,

@@ -18,6 +18,7 @@
 // are summed and the gathered keys all-gathered between sel_pass and sel_resolve, so every
 // rank takes the same decisions.
 #include <algorithm>
+#include <atomic>
 #include <cstddef>
 #include <cmath>
 #include <cstdio>
@@ -120,8 +121,15 @@ __device__ Range make_range(uint64_t lo, uint64_t hi, uint64_t count, uint32_t w
   R.base = (hi > kGapKeys && hi - kGapKeys > lo + 1) ? hi - kGapKeys : lo + 1;
   uint32_t s = 0;
   if (R.base < hi) {
-    const uint64_t span = hi - 1 - R.base;  // largest (k - base) of a middle key
-    while ((span >> s) > (uint64_t)(kBins - 4)) s++;
+    // the smallest s with (span >> s) <= kBins - 4, span = the largest (k - base) of a middle
+    // key: from the bit lengths, then at most one step (every thread of sel_small runs this,
+    // a shift-by-one loop cost up to ~50 dependent iterations per quantity)
+    const uint64_t span = hi - 1 - R.base;
+    constexpr uint64_t M = (uint64_t)(kBins - 4);
+    if (span > M) {
+      s = (uint32_t)((64 - __clzll((long long)span)) - (64 - __clzll((long long)M)));
+      if ((span >> s) > M) s++;
+    }
   }
   R.shift = s;
   R.span = hi - lo;
@@ -1261,6 +1269,7 @@ struct SmallSel {
   // results first: the host copies back only this head
   uint64_t tkey[kMaxT];                // per target: result key
   uint32_t fail, nr;
+  uint64_t stamp[8];                   // %globaltimer at the phase boundaries (CTA 0; debug)
   // working state
   uint32_t hist[2][kBins];             // level-0 histograms (atomics from every CTA)
   unsigned long long rcnt[kMaxT];      // keys gathered per range
@@ -1291,6 +1300,14 @@ __global__ void __launch_bounds__(1024, 1) sel_small(const double* __restrict__ 
   Range R[2];
   for (uint32_t w = 0; w < 2; w++) R[w] = make_range(mm[2 * w], mm[2 * w + 1], n_def, w, kSmallCap);
   const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+  auto stamp = [&](int i) {
+    if (blockIdx.x == 0 && tid == 0) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      ss->stamp[i] = t;
+    }
+  };
+  stamp(0);
   // phase 1: level-0 histograms, privatised per CTA (a gather range needs none)
   for (uint32_t i = tid; i < 2 * kBins; i += blockDim.x) sh[i] = 0;
   if (tid == 0) s_fail = 0;
@@ -1307,12 +1324,18 @@ __global__ void __launch_bounds__(1024, 1) sel_small(const double* __restrict__ 
   for (uint32_t i = tid; i < 2 * kBins; i += blockDim.x)
     if (sh[i]) atomicAdd(&ss->hist[0][0] + i, sh[i]);
   grid.sync();
-  // phase 2 (every CTA, identically): every target to its bin; the distinct bins are the ranges
-  for (uint32_t w = 0; w < 2; w++) {  // inclusive scan of hist[w] into sh[w * kBins ..]
+  stamp(1);
+  // phase 2 (every CTA, identically): every target to its bin; the distinct bins are the ranges.
+  // Both histograms are staged in shared memory with coalesced loads first: the scan's
+  // thread-contiguous reads straight from L2 (4-byte lanes at a 32-byte stride) fetched every
+  // sector 8 times, 512 KB per CTA (5.8 us of the kernel on configs[3], LSCAT_SEL_DEBUG stamps).
+  for (uint32_t i = tid; i < 2 * kBins; i += blockDim.x) sh[i] = __ldcg(&ss->hist[0][0] + i);
+  __syncthreads();
+  for (uint32_t w = 0; w < 2; w++) {  // inclusive scan of hist[w] into sh[w * kBins ..], in place
     constexpr int kPer = kBins / 1024;
     uint32_t c[kPer], sum = 0;
 #pragma unroll
-    for (int j = 0; j < kPer; j++) { c[j] = __ldcg(&ss->hist[w][tid * kPer + j]); sum += c[j]; }
+    for (int j = 0; j < kPer; j++) { c[j] = sh[w * kBins + tid * kPer + j]; sum += c[j]; }
     uint32_t inc = sum;
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(FULL, inc, o);
@@ -1334,64 +1357,130 @@ __global__ void __launch_bounds__(1024, 1) sel_small(const double* __restrict__ 
     for (int j = 0; j < kPer; j++) { run += c[j]; sh[w * kBins + tid * kPer + j] = run; }
     __syncthreads();
   }
-  if (tid < (int)nt) {
-    const uint32_t w = tid >= (int)npct;
-    const double r = ceil(pct.p[tid % npct] * (double)n_def);  // nearest rank (R-13)
-    uint64_t k = r < 1.0 ? 1 : (r > (double)n_def ? n_def : (uint64_t)r);
-    uint64_t tlo = R[w].lo, thi = R[w].hi;
-    uint32_t done = n_def == 0;
-    if (!done && !R[w].gather) {
-      const uint32_t* P = sh + w * kBins;
-      uint32_t a = 0, b = kBins - 1;  // smallest bin with P[bin] >= k
-      while (a < b) {
-        const uint32_t m = (a + b) / 2;
-        if (P[m] >= k) b = m; else a = m + 1;
+  stamp(3);
+  if (nt <= 32) {
+    // one warp, lane i = target i: the same bins, distinct (quantity, bin) pairs and range ids
+    // (ranks of the first occurrences in target order) as the general path below, from
+    // match_any / ballot in registers instead of O(nt^2) shared-memory loops between barriers
+    if (tid < 32) {
+      const bool act = tid < (int)nt;
+      const uint32_t w = act && tid >= (int)npct;
+      uint64_t k = 0, tlo = 0, thi = 0;
+      uint32_t done = 1;
+      bool too_many = false;
+      if (act) {
+        const Range& Rw = w ? R[1] : R[0];
+        const double r = ceil(pct.p[tid % npct] * (double)n_def);  // nearest rank (R-13)
+        k = r < 1.0 ? 1 : (r > (double)n_def ? n_def : (uint64_t)r);
+        tlo = Rw.lo;
+        thi = Rw.hi;
+        done = n_def == 0;
+        if (!done && !Rw.gather) {
+          const uint32_t* P = sh + w * kBins;
+          uint32_t a = 0, b = kBins - 1;  // smallest bin with P[bin] >= k
+          while (a < b) {
+            const uint32_t m = (a + b) / 2;
+            if (P[m] >= k) b = m; else a = m + 1;
+          }
+          const uint32_t below = a ? P[a - 1] : 0u;
+          bin_keys(Rw, (int)a, &tlo, &thi);
+          too_many = tlo != thi && P[a] - below > kSmallCap;  // too many to sort
+          k -= below;
+        }
+        if (!done && tlo == thi) done = 2;  // a single-valued bin: the key is known
       }
-      const uint32_t below = a ? P[a - 1] : 0u;
-      bin_keys(R[w], (int)a, &tlo, &thi);
-      if (tlo != thi && P[a] - below > kSmallCap) atomicOr(&s_fail, 1u);  // too many to sort
-      k -= below;
+      const bool open = act && !done;
+      // lanes that are not open get a class of their own
+      const unsigned m = __match_any_sync(FULL, tlo) & __match_any_sync(FULL, thi) &
+                         __match_any_sync(FULL, open ? w : 2u + (uint32_t)tid);
+      const int src = __ffs(m) - 1;
+      const bool first = open && src == tid;
+      const unsigned firsts = __ballot_sync(FULL, first);
+      const uint32_t fail = __ballot_sync(FULL, too_many) ? 1u : 0u;
+      const uint32_t r = open ? (uint32_t)__popc(firsts & ((1u << src) - 1u)) : 0u;
+      if (first) { r_w[r] = w; r_lo[r] = tlo; r_hi[r] = thi; }
+      if (act) {
+        s_lo[tid] = tlo; s_hi[tid] = thi; s_k[tid] = k; s_done[tid] = done;
+        s_first[tid] = first;
+        s_range[tid] = r;
+        if (blockIdx.x == 0) {
+          ss->tk[tid] = k;
+          ss->tdone[tid] = done;
+          ss->tkey[tid] = done == 2 ? tlo : kNaNKey;
+          ss->trange[tid] = r;
+        }
+      }
+      if (tid == 0) {
+        const uint32_t nr = (uint32_t)__popc(firsts);
+        s_fail = fail;
+        s_nr = fail ? 0u : nr;
+        if (blockIdx.x == 0) {
+          ss->nr = nr;
+          ss->fail = fail;
+        }
+      }
     }
-    if (!done && tlo == thi) done = 2;  // a single-valued bin: the key is known
-    s_lo[tid] = tlo; s_hi[tid] = thi; s_k[tid] = k; s_done[tid] = done;
+  } else {
+    if (tid < (int)nt) {
+      const uint32_t w = tid >= (int)npct;
+      const double r = ceil(pct.p[tid % npct] * (double)n_def);  // nearest rank (R-13)
+      uint64_t k = r < 1.0 ? 1 : (r > (double)n_def ? n_def : (uint64_t)r);
+      uint64_t tlo = R[w].lo, thi = R[w].hi;
+      uint32_t done = n_def == 0;
+      if (!done && !R[w].gather) {
+        const uint32_t* P = sh + w * kBins;
+        uint32_t a = 0, b = kBins - 1;  // smallest bin with P[bin] >= k
+        while (a < b) {
+          const uint32_t m = (a + b) / 2;
+          if (P[m] >= k) b = m; else a = m + 1;
+        }
+        const uint32_t below = a ? P[a - 1] : 0u;
+        bin_keys(R[w], (int)a, &tlo, &thi);
+        if (tlo != thi && P[a] - below > kSmallCap) atomicOr(&s_fail, 1u);  // too many to sort
+        k -= below;
+      }
+      if (!done && tlo == thi) done = 2;  // a single-valued bin: the key is known
+      s_lo[tid] = tlo; s_hi[tid] = thi; s_k[tid] = k; s_done[tid] = done;
+    }
+    __syncthreads();
+    // distinct (quantity, bin) -> range ids in target order
+    if (tid < (int)nt) {
+      bool first = !s_done[tid];
+      for (int j = 0; j < tid && first; j++)
+        if (!s_done[j] && (j >= (int)npct) == (tid >= (int)npct) && s_lo[j] == s_lo[tid] && s_hi[j] == s_hi[tid])
+          first = false;
+      s_first[tid] = first;
+    }
+    __syncthreads();
+    if (tid < (int)nt) {
+      const uint32_t w = tid >= (int)npct;
+      uint32_t r = 0, src = tid;
+      if (!s_done[tid]) {
+        for (int j = 0; j < tid; j++)  // my range's first occurrence
+          if (!s_done[j] && (j >= (int)npct) == (bool)w && s_lo[j] == s_lo[tid] && s_hi[j] == s_hi[tid]) { src = j; break; }
+        for (uint32_t j = 0; j < src; j++) r += s_first[j];
+        if (src == (uint32_t)tid) { r_w[r] = w; r_lo[r] = s_lo[tid]; r_hi[r] = s_hi[tid]; }
+      }
+      s_range[tid] = r;
+      if (blockIdx.x == 0) {
+        ss->tk[tid] = s_k[tid];
+        ss->tdone[tid] = s_done[tid];
+        ss->tkey[tid] = s_done[tid] == 2 ? s_lo[tid] : kNaNKey;
+        ss->trange[tid] = r;
+      }
+    }
+    if (tid == 0) {
+      uint32_t nr = 0;
+      for (uint32_t j = 0; j < nt; j++) nr += s_first[j];
+      s_nr = s_fail ? 0u : nr;
+      if (blockIdx.x == 0) {
+        ss->nr = nr;
+        ss->fail = s_fail;
+      }
+    }
   }
   __syncthreads();
-  // distinct (quantity, bin) -> range ids in target order
-  if (tid < (int)nt) {
-    bool first = !s_done[tid];
-    for (int j = 0; j < tid && first; j++)
-      if (!s_done[j] && (j >= (int)npct) == (tid >= (int)npct) && s_lo[j] == s_lo[tid] && s_hi[j] == s_hi[tid])
-        first = false;
-    s_first[tid] = first;
-  }
-  __syncthreads();
-  if (tid < (int)nt) {
-    const uint32_t w = tid >= (int)npct;
-    uint32_t r = 0, src = tid;
-    if (!s_done[tid]) {
-      for (int j = 0; j < tid; j++)  // my range's first occurrence
-        if (!s_done[j] && (j >= (int)npct) == (bool)w && s_lo[j] == s_lo[tid] && s_hi[j] == s_hi[tid]) { src = j; break; }
-      for (uint32_t j = 0; j < src; j++) r += s_first[j];
-      if (src == (uint32_t)tid) { r_w[r] = w; r_lo[r] = s_lo[tid]; r_hi[r] = s_hi[tid]; }
-    }
-    s_range[tid] = r;
-    if (blockIdx.x == 0) {
-      ss->tk[tid] = s_k[tid];
-      ss->tdone[tid] = s_done[tid];
-      ss->tkey[tid] = s_done[tid] == 2 ? s_lo[tid] : kNaNKey;
-      ss->trange[tid] = r;
-    }
-  }
-  if (tid == 0) {
-    uint32_t nr = 0;
-    for (uint32_t j = 0; j < nt; j++) nr += s_first[j];
-    s_nr = s_fail ? 0u : nr;
-    if (blockIdx.x == 0) {
-      ss->nr = nr;
-      ss->fail = s_fail;
-    }
-  }
-  __syncthreads();
+  stamp(4);
   // phase 3: gather the keys of the ranges (disjoint bins: at most one range per key)
   const uint32_t nr = s_nr;
   if (nr) {
@@ -1415,7 +1504,9 @@ __global__ void __launch_bounds__(1024, 1) sel_small(const double* __restrict__ 
       }
     }
   }
+  stamp(5);
   grid.sync();
+  stamp(2);
   // phase 4: CTA r (mod the grid) picks its targets' keys among range r's gathered keys: by
   // rank counting when they fit one per thread, else a bitonic sort
   for (uint32_t r = blockIdx.x; r < nr; r += gridDim.x) {
@@ -1804,16 +1895,16 @@ struct SelBufs {
 // waits for the SMs to be reconfigured (measured at 10^9 rows: the one-CTA plan and check
 // kernels took 18 / 16 us between events, mostly that wait).  Once per device.
 lscat_status sel_carveout(lscat_ctx* ctx) {
-  static bool done[64] = {};
+  static std::atomic<bool> done[64] = {};  // ranks of the local transport are threads
   const int d = ctx->device;
-  if (d >= 0 && d < 64 && done[d]) return LSCAT_OK;
+  if (d >= 0 && d < 64 && done[d].load(std::memory_order_acquire)) return LSCAT_OK;
   const void* fs[] = {(const void*)sel_sample_hist, (const void*)sel_plan_sampled, (const void*)sel_slot_counts,
                       (const void*)sel_pass_sampled<256>, (const void*)sel_check_sampled,
                       (const void*)sel_finish, (const void*)sel_small};
   for (const void* f : fs)
     LSCAT_CUDA(ctx, cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                                          (int)cudaSharedmemCarveoutMaxShared));
-  if (d >= 0 && d < 64) done[d] = true;
+  if (d >= 0 && d < 64) done[d].store(true, std::memory_order_release);
   return LSCAT_OK;
 }
 
@@ -2058,7 +2149,11 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
     SmallSel* hsm = (SmallSel*)pinned(ctx, "sel_small_h", sizeof(SmallSel), &err);
     if (err) return cuda_fail(ctx, err, "stats: pinned");
     LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
-    if (dbg_early) fprintf(stderr, "sel early small: fail %u\n", hsm->fail);
+    if (dbg_early)
+      fprintf(stderr, "sel early small: fail %u nr %u phases(ns) %lld %lld (scan %lld targets %lld gather %lld barrier %lld)\n",
+              hsm->fail, hsm->nr, (long long)(hsm->stamp[1] - hsm->stamp[0]), (long long)(hsm->stamp[2] - hsm->stamp[1]),
+              (long long)(hsm->stamp[3] - hsm->stamp[1]), (long long)(hsm->stamp[4] - hsm->stamp[3]),
+              (long long)(hsm->stamp[5] - hsm->stamp[4]), (long long)(hsm->stamp[2] - hsm->stamp[5]));
     if (!hsm->fail) {
       for (uint32_t i = 0; i < 2 * npct; i++) {
         double v;
@@ -2100,7 +2195,9 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
       LSCAT_CUDA(ctx, cudaMemcpyAsync(hsm, sm, dbg ? sizeof(SmallSel) : kSmallHead, cudaMemcpyDeviceToHost, s));
       LSCAT_CUDA(ctx, cudaStreamSynchronize(s));
       if (dbg) {
-        fprintf(stderr, "sel_small: fail %u nr %u\n", hsm->fail, hsm->nr);
+        fprintf(stderr, "sel_small: fail %u nr %u phases(ns) %lld %lld\n", hsm->fail, hsm->nr,
+                (long long)(hsm->stamp[1] - hsm->stamp[0]), (long long)(hsm->stamp[2] - hsm->stamp[1]));
+        for (uint32_t r = 0; r < hsm->nr && r < kMaxT; r++) fprintf(stderr, "  range %u keys %llu\n", r, hsm->rcnt[r]);
         for (uint32_t i = 0; i < 2 * npct; i++)
           fprintf(stderr, "  t%u done %u range %u k %llu key %016llx\n", i, hsm->tdone[i], hsm->trange[i],
                   (unsigned long long)hsm->tk[i], (unsigned long long)hsm->tkey[i]);

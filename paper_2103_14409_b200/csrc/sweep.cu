@@ -251,7 +251,9 @@ extern "C" lscat_status lscat_sweep(lscat_ctx* ctx, const uint32_t* kernels, uin
   auto harvest = [&](PointState& ps) -> lscat_status {
     if (!ps.pending) return LSCAT_OK;
     ps.pending = false;
-    lscat_status w = wait_event(ctx, EV(ps.slot, ps.nk), deadline);
+    // with GLOBALTIMER the stamps' copy to the host follows the last bracket's event: wait for
+    // the event recorded after that copy (reading the pinned stamps earlier raced with the copy)
+    lscat_status w = wait_event(ctx, EV(ps.slot, gtimer ? K + 2 : ps.nk), deadline);
     if (w) return w;
     double total = ps.warm_ms;
     const unsigned long long* sh = gtimer ? stamp_h + (size_t)ps.slot * (K + 1) : nullptr;
@@ -384,9 +386,12 @@ extern "C" lscat_status lscat_sweep(lscat_ctx* ctx, const uint32_t* kernels, uin
     }
     ps.nk = k;
     ctx->launches += (uint64_t)k * R;
-    if (gtimer)
+    if (gtimer) {
       LSCAT_CUDA(ctx, cudaMemcpyAsync(stamp_h + (size_t)ps.slot * (K + 1), stamp_d + (size_t)ps.slot * (K + 1),
                                       (size_t)(k + 1) * 8, cudaMemcpyDeviceToHost, s));
+      // EV(K + 2) (the warm-up's end, already waited for above) now marks the copy's completion
+      LSCAT_CUDA(ctx, cudaEventRecord(EV(ps.slot, K + 2), s));
+    }
     if (o->verify && k == K && kern != LSCAT_K_SPIN) {  // the last timed launch's output
       const SuiteEntry* last = args[(R - 1) % nargs].e;
       LSCAT_CUDA(ctx, cudaMemcpyAsync((uint8_t*)o->verify_host + voff[i], last->out, last->out_bytes,
