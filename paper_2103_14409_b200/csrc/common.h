@@ -83,6 +83,8 @@ struct ReduceState {
   uint64_t* minmax = nullptr;    // device [4]: perf min, perf max, gain min, gain max keys
   // percentile selection already enqueued by lscat_reduce_table (opts.n_percentiles, R-27)
   uint32_t early = 0;            // EARLY_NONE / EARLY_SMALL / EARLY_SAMPLED
+  // pinned host copy of the partials, enqueued by the reduce call (EARLY_SMALL; else null)
+  const uint64_t* partials_h = nullptr;
   std::vector<double> early_pct;
 };
 enum { EARLY_NONE = 0, EARLY_SMALL = 1, EARLY_SAMPLED = 2 };
@@ -107,6 +109,9 @@ struct lscat_ctx {
   // graphs: (kernel, n, block_idx, chunk) -> exec
   std::map<std::tuple<uint32_t, uint32_t, uint32_t, uint32_t>, cudaGraphExec_t> graphs;
   cudaStream_t capture_stream = nullptr;
+  // side branch of a reduce call (the host copy of the partials next to the early selection)
+  cudaStream_t aux_stream = nullptr;
+  cudaEvent_t aux_fork = nullptr, aux_join = nullptr;
   // percentile selection: first batch (init + 3 levels + state read-back) as a graph, keyed by
   // every pointer / size / percentile it bakes in (stats.cu; world == 1)
   std::vector<std::pair<std::string, cudaGraphExec_t>> sel_graphs;

@@ -205,6 +205,9 @@ void lscat_ctx_destroy(lscat_ctx* c) {
   for (auto& kv : c->pinned) cudaFreeHost(kv.second.p);
   delete c->comm;
   if (c->capture_stream) cudaStreamDestroy(c->capture_stream);
+  if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
+  if (c->aux_fork) cudaEventDestroy(c->aux_fork);
+  if (c->aux_join) cudaEventDestroy(c->aux_join);
   delete c;
 }
 

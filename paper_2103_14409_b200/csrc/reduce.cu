@@ -1289,13 +1289,34 @@ static lscat_status reduce_enqueue(lscat_ctx* ctx, const lscat_table* T, const l
   uint32_t early = EARLY_NONE;
   const double* perf_k = o->keep_values ? p.o_perf : out->perf;
   const double* gain_k = o->keep_values ? p.o_gain : out->gain;
+  const uint64_t* partials_h = nullptr;
   if (o->n_percentiles && ctx->world == 1 && !o->point_sharded && G && perf_k && gain_k) {
+    // lscat_stats follows: on small tables its host copy of the partials runs here, on a side
+    // branch next to the one-launch selection instead of after it (configs[2]/[3])
+    const bool side = G <= kEarlySmallGroups;
+    if (side) {
+      if (!ctx->aux_stream) {
+        LSCAT_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
+        LSCAT_CUDA(ctx, cudaEventCreateWithFlags(&ctx->aux_fork, cudaEventDisableTiming));
+        LSCAT_CUDA(ctx, cudaEventCreateWithFlags(&ctx->aux_join, cudaEventDisableTiming));
+      }
+      uint64_t* hP = (uint64_t*)pinned(ctx, "stats_partials", plen * 8, &err);
+      if (err) return cuda_fail(ctx, err, "reduce_table: pinned");
+      LSCAT_CUDA(ctx, cudaEventRecord(ctx->aux_fork, s));
+      LSCAT_CUDA(ctx, cudaStreamWaitEvent(ctx->aux_stream, ctx->aux_fork, 0));
+      LSCAT_CUDA(ctx, cudaMemcpyAsync(hP, p.partials, plen * 8, cudaMemcpyDeviceToHost, ctx->aux_stream));
+      LSCAT_CUDA(ctx, cudaEventRecord(ctx->aux_join, ctx->aux_stream));
+      partials_h = hP;
+    }
     lscat_status es = early_select(ctx, perf_k, gain_k, own_lo, own_hi, p.partials, p.minmax, o->bins_per_unit,
                                    o->percentiles, o->n_percentiles, s, &early);
+    if (side) LSCAT_CUDA(ctx, cudaStreamWaitEvent(s, ctx->aux_join, 0));  // joined before any return
     if (es) return es;
+    if (early != EARLY_SMALL) partials_h = nullptr;
   }
   ReduceState& rs = ctx->rs;
   rs.early = early;
+  rs.partials_h = partials_h;
   rs.early_pct.assign(o->percentiles, o->percentiles + (early ? o->n_percentiles : 0));
   rs.valid = true;
   rs.opts = *o;

@@ -1263,7 +1263,8 @@ __global__ void __launch_bounds__(1024) sel_check_sampled(SelState* st, const Sa
 // per quantity over [min, max], privatised per CTA), CTA 0 narrows every target to its bin,
 // a gather of the keys in those bins, one CTA per bin sorts them and picks the targets.  A bin
 // with more than kSmallCap keys sets `fail` and the host runs the chain instead.
-constexpr uint32_t kSmallCap = 8192;  // keys per bin sorted by one CTA (64 KB of smem)
+constexpr uint32_t kSmallCap = 8192;  // keys per bin selected by one CTA (64 KB of smem)
+constexpr uint32_t kRankCountMax = 128;  // phase 4: rank counting up to this many keys
 
 struct SmallSel {
   // results first: the host copies back only this head
@@ -1508,10 +1509,16 @@ __global__ void __launch_bounds__(1024, 1) sel_small(const double* __restrict__ 
   grid.sync();
   stamp(2);
   // phase 4: CTA r (mod the grid) picks its targets' keys among range r's gathered keys: by
-  // rank counting when they fit one per thread, else a bitonic sort
+  // rank counting when there are few (one key per thread, O(n^2) compares), else by a radix
+  // select in shared memory (8-bit digits of the key below the range's common prefix; one
+  // histogram pass per digit and target).  A bitonic sort of up to 8192 keys took ~20 us and
+  // rank counting at n = 1024 as long (issue bound: n compares in every thread).
+  __shared__ uint32_t s_dh[256];
+  __shared__ unsigned long long s_pre;
+  __shared__ uint64_t s_kk;
   for (uint32_t r = blockIdx.x; r < nr; r += gridDim.x) {
-  if (ss->rcnt[r] <= blockDim.x) {
-    const uint32_t n = (uint32_t)ss->rcnt[r];
+  const uint32_t n = (uint32_t)min(ss->rcnt[r], (unsigned long long)kSmallCap);
+  if (ss->rcnt[r] <= kRankCountMax) {
     for (uint32_t i = tid; i < n; i += blockDim.x) dsm[i] = cand[(size_t)r * kSmallCap + i];
     __syncthreads();
     if (tid < (int)n) {  // my key's rank: smaller keys, and equal keys earlier in the list
@@ -1527,26 +1534,54 @@ __global__ void __launch_bounds__(1024, 1) sel_small(const double* __restrict__ 
     if (tid < (int)nt && !s_done[tid] && s_range[tid] == r && !(s_k[tid] >= 1 && s_k[tid] <= n))
       atomicOr(&ss->fail, 2u);  // keys lost: the host falls back
   } else {
-    const uint32_t n = (uint32_t)min(ss->rcnt[r], (unsigned long long)kSmallCap);
-    uint32_t P2 = 1;
-    while (P2 < n) P2 <<= 1;
-    for (uint32_t i = tid; i < P2; i += blockDim.x) dsm[i] = i < n ? cand[(size_t)r * kSmallCap + i] : ~0ull;
-    __syncthreads();
-    for (uint32_t kk = 2; kk <= P2; kk <<= 1)
-      for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
-        for (uint32_t i = tid; i < P2; i += blockDim.x) {
-          const uint32_t ixj = i ^ j;
-          if (ixj > i) {
-            const unsigned long long a = dsm[i], b = dsm[ixj];
-            if ((a > b) == ((i & kk) == 0)) { dsm[i] = b; dsm[ixj] = a; }
+    for (uint32_t i = tid; i < n; i += blockDim.x) dsm[i] = cand[(size_t)r * kSmallCap + i];
+    // every key of the range lies in [r_lo, r_hi]: the digits above their highest differing
+    // bit are common
+    const uint64_t diff = r_lo[r] ^ r_hi[r];
+    const int top = diff ? 64 - __clzll((long long)diff) : 0;  // bits below the common prefix
+    for (uint32_t i = 0; i < nt; i++) {  // CTA-uniform loop over the range's targets
+      if (s_done[i] || s_range[i] != r) continue;
+      const uint64_t k0 = s_k[i];
+      if (!(k0 >= 1 && k0 <= n)) {
+        if (tid == 0) atomicOr(&ss->fail, 2u);  // keys lost: the host falls back
+        continue;
+      }
+      if (tid == 0) { s_pre = r_lo[r] & ~((top >= 64) ? ~0ull : ((1ull << top) - 1)); s_kk = k0; }
+      for (int sh0 = ((top + 7) / 8) * 8 - 8; sh0 >= 0; sh0 -= 8) {
+        if (tid < 256) s_dh[tid] = 0;
+        __syncthreads();  // (also: the keys and the prefix are in place)
+        const unsigned long long pre = s_pre;
+        const unsigned long long hmask = (sh0 + 8 >= 64) ? 0ull : (~0ull << (sh0 + 8));
+        for (uint32_t j = tid; j < n; j += blockDim.x) {
+          const unsigned long long x = dsm[j];
+          if ((x & hmask) == (pre & hmask)) atomicAdd(&s_dh[(uint32_t)(x >> sh0) & 255u], 1u);
+        }
+        __syncthreads();
+        if (tid < 32) {  // the digit holding the kk-th of the keys with this prefix
+          uint32_t c[8], sum = 0;
+#pragma unroll
+          for (int q = 0; q < 8; q++) { c[q] = s_dh[tid * 8 + q]; sum += c[q]; }
+          uint32_t inc = sum;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, inc, o);
+            if (lane >= o) inc += y;
+          }
+          const uint64_t kk = s_kk;
+          const uint32_t ex = inc - sum;
+          if (tid == 31 && inc < kk) atomicOr(&ss->fail, 2u);  // keys lost: the host falls back
+          if (ex < kk && kk <= inc) {  // exactly one lane
+            uint32_t cum = ex;
+            int q = 0;
+            while (cum + c[q] < kk) cum += c[q++];
+            s_pre = (pre & hmask) | ((unsigned long long)(tid * 8 + q) << sh0);
+            s_kk = kk - cum;
           }
         }
         __syncthreads();
       }
-    if (tid < (int)nt && !s_done[tid] && s_range[tid] == r) {
-      const uint64_t k = s_k[tid];
-      if (k >= 1 && k <= n) ss->tkey[tid] = dsm[k - 1];
-      else atomicOr(&ss->fail, 2u);  // keys lost: the host falls back
+      if (tid == 0) ss->tkey[i] = s_pre;
+      __syncthreads();  // s_pre / s_kk are reset for the next target
     }
   }
   __syncthreads();  // the next range reuses dsm
@@ -2154,6 +2189,12 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
               hsm->fail, hsm->nr, (long long)(hsm->stamp[1] - hsm->stamp[0]), (long long)(hsm->stamp[2] - hsm->stamp[1]),
               (long long)(hsm->stamp[3] - hsm->stamp[1]), (long long)(hsm->stamp[4] - hsm->stamp[3]),
               (long long)(hsm->stamp[5] - hsm->stamp[4]), (long long)(hsm->stamp[2] - hsm->stamp[5]));
+    if (dbg_early) {  // keys per range (the working state after the head: a separate copy)
+      std::vector<SmallSel> full(1);
+      const SmallSel* smd = (const SmallSel*)scratch(ctx, "sel_small", sizeof(SmallSel), &err);
+      if (!err && cudaMemcpy(full.data(), smd, sizeof(SmallSel), cudaMemcpyDeviceToHost) == cudaSuccess)
+        for (uint32_t r = 0; r < hsm->nr && r < kMaxT; r++) fprintf(stderr, "  range %u keys %llu\n", r, full[0].rcnt[r]);
+    }
     if (!hsm->fail) {
       for (uint32_t i = 0; i < 2 * npct; i++) {
         double v;
@@ -2413,9 +2454,15 @@ extern "C" lscat_status lscat_stats(lscat_ctx* ctx, const lscat_reduce_opts* o, 
   const size_t plen = LSCAT_P_NCOUNTERS + (nb + 1) + (ng + 1) + nbb * (o->block_profile ? 3 : 1) +
                       (o->kernel_rollup ? 8 + nb + 1 : 0);
   cudaError_t err;
+  // the reduce call already enqueued the host copy when it enqueued the one-launch selection
+  // for exactly these percentiles (rs.partials_h; same buffer, same length)
+  const bool pre_copied = rs.partials_h && rs.early == EARLY_SMALL && out->n_percentiles &&
+                          rs.early_pct.size() == out->n_percentiles &&
+                          memcmp(rs.early_pct.data(), out->percentiles, out->n_percentiles * 8) == 0;
   uint64_t* hP = (uint64_t*)pinned(ctx, "stats_partials", plen * 8, &err);
   if (err) return cuda_fail(ctx, err, "stats: pinned");
-  LSCAT_CUDA(ctx, cudaMemcpyAsync(hP, rs.partials, plen * 8, cudaMemcpyDeviceToHost, s));
+  if (!pre_copied || hP != rs.partials_h)
+    LSCAT_CUDA(ctx, cudaMemcpyAsync(hP, rs.partials, plen * 8, cudaMemcpyDeviceToHost, s));
   if (out->n_percentiles) {
     // a8 on the device; its first host sync also completes the partials copy above
     lscat_status st = select_percentiles(ctx, out->percentiles, out->n_percentiles, out->pct_perf,
