@@ -502,17 +502,20 @@ class Ctx:
                 so.profile_mean, so.profile_count = pm.ctypes.data, pn.ctypes.data
             if opts.kernel_rollup:
                 so.kernel_perf_hist = kh.ctypes.data
-            bufs = (so, ph, gh, bh, pc, pp, pg, pm, pn, kh)
+            # views over the struct's counters and derived doubles (no per-call bytes() copy)
+            cv = np.frombuffer(so, np.uint64, len(COUNTERS))
+            dv = np.frombuffer(so, np.float64, len(DERIVED), 8 * len(COUNTERS))
+            bufs = (so, ph, gh, bh, pc, pp, pg, pm, pn, kh, cv, dv)
             self._stats_bufs[key] = bufs
-        so, ph, gh, bh, pc, pp, pg, pm, pn, kh = bufs
+        so, ph, gh, bh, pc, pp, pg, pm, pn, kh, cv, dv = bufs
         pc[:] = pcs
         pp.fill(np.nan)
         pg.fill(np.nan)
         self._ck(self._lib.lscat_stats(self.h, C.byref(opts), C.byref(so), _stream(stream, self.device)),
                  "stats")
-        raw = bytes(so)  # counters (u64) then the derived doubles, in COUNTERS / DERIVED order
-        res = dict(zip(COUNTERS, np.frombuffer(raw, np.uint64, len(COUNTERS)).tolist()))
-        res.update(zip(DERIVED, np.frombuffer(raw, np.float64, len(DERIVED), 8 * len(COUNTERS)).tolist()))
+        # counters (u64) then the derived doubles, in COUNTERS / DERIVED order
+        res = dict(zip(COUNTERS, cv.tolist()))
+        res.update(zip(DERIVED, dv.tolist()))
         if hist:
             res["perf_hist"], res["gain_hist"] = ph.copy(), gh.copy()
             res["best_block_hist"] = bh.reshape(opts.n_matrices, opts.n_blocks).copy()
