@@ -287,6 +287,21 @@ class Table:
                      torch.empty(max(cap_groups, 1), dtype=torch.int32, **kw),
                      mem=MEM_DEVICE if device != "cpu" else MEM_HOST)
 
+    def __setattr__(self, k, v):  # any attribute change drops the cached C view
+        object.__setattr__(self, k, v)
+        if k != "_cview":
+            object.__setattr__(self, "_cview", None)
+
+    def c_input(self, with_groups=True) -> TableC:
+        """c() for calls that only read the table (lscat_reduce_table takes a const table):
+        built once and reused until an attribute changes (building it costs ~4 us per call on
+        the small tables' critical path)."""
+        cv = getattr(self, "_cview", None)
+        if cv is None or cv[0] != with_groups:
+            cv = (with_groups, self.c(with_groups))
+            object.__setattr__(self, "_cview", cv)
+        return cv[1]
+
     def c(self, with_groups=True) -> TableC:
         def p(t):
             return None if t is None else t.data_ptr()
@@ -469,7 +484,7 @@ class Ctx:
             import torch
             out["partials"] = torch.zeros(partials_len(opts), dtype=torch.int64, device=f"cuda:{self.device}")
             oc.partials = out["partials"].data_ptr()
-        tc = table.c(with_groups=not table.rows_per_group or table.group_offset is not None)
+        tc = table.c_input(with_groups=not table.rows_per_group or table.group_offset is not None)
         self._ck(self._lib.lscat_reduce_table(self.h, C.byref(tc), C.byref(opts), C.byref(oc),
                                               _stream(stream, self.device)), "reduce_table")
         # the library reads the per-group perf/gain again in lscat_stats (keep_values): hold
