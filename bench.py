@@ -710,7 +710,8 @@ def table_benches(ctx, L, hbm_peak, rank, world, barrier, allmax, cpu_rows=False
                     lt.append(e0.elapsed_time(e1))
                 res["local_ms_no_merge"] = round(allmax(statistics.median(lt)), 4)
             # the per-kernel roll-up of P:258 (R-26) on the same shard: its extra time and values
-            ok_ = L.reduce_opts(32, 8, point_sharded=1 if (point and world > 1) else 0, kernel_rollup=1)
+            ok_ = L.reduce_opts(32, 8, point_sharded=1 if (point and world > 1) else 0, kernel_rollup=1,
+                                percentiles=PCTS)
             run(ctx, ok_)
             kt = []
             for _ in range(5):

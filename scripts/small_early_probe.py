@@ -18,7 +18,8 @@ if which == "gtx980":
     tab = c.gen_table(2_140_796, 8363, preset=L.PRESET_GTX980, seed=980)
 else:
     tab = c.gen_table(5_028_536, 19_683, preset=L.PRESET_T4, seed=4)
-o = L.reduce_opts(32, 8, percentiles=PCTS)
+rollup = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+o = L.reduce_opts(32, 8, percentiles=PCTS, kernel_rollup=rollup)
 s = torch.cuda.current_stream()
 flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 for i in range(reps):
