@@ -309,6 +309,29 @@ def test_percentiles_wide_key_span_many_targets():
     assert st["pct_gain"][-1] > 1e59 and st["pct_perf"][0] < 1e-59
 
 
+@pytest.mark.parametrize("early", [False, True])
+def test_small_selection_ties_and_wide_bins(early):
+    """The one-launch small-table selection (<= 2^20 groups) where the targets' level-0 bins hold
+    thousands of keys with heavy ties (40 % of the groups take one of 50 perf values, ~2400
+    groups each, a few values per bin) and the bins span ~2^40 key units (perf over ~1.6
+    binades): the per-bin radix select runs several 8-bit digits with long runs of equal keys;
+    also bins of 129-1000 keys and the rank-counting path below 128.  Exact against the oracle,
+    with the percentiles given to lscat_stats and in the reduce options (R-27)."""
+    rng = np.random.default_rng(23)
+    G = 300_000
+    b = rng.choice(np.array([0.5, 1.0, 2.0, 4.0], np.float32), G)   # powers of two: b / (b tv) == 1 / tv
+    tied = rng.random(G) < 0.4
+    tv = np.where(tied, rng.choice(np.linspace(1.05, 1.2, 50).astype(np.float32), G),
+                  rng.uniform(1.0, 3.0, G).astype(np.float32)).astype(np.float32)
+    rt = np.empty(2 * G, np.float32)
+    rt[0::2], rt[1::2] = b, (b * tv).astype(np.float32)
+    tab = dict(runtime_ms=rt, block_id=np.tile(np.array([0, 1], np.uint16), G),
+               group_offset=np.arange(0, 2 * G + 1, 2, dtype=np.int64),
+               group_matrix=np.zeros(G, np.uint32))
+    pcts = [0.001, 0.01, 0.05, 0.1, 0.2, 0.25, 0.3, 0.35, 0.4, 0.5, 0.6, 0.75, 0.9, 0.99, 0.999, 1.0]
+    _compare(tab, L=2, M=1, ell=1, pcts=pcts, early=early)
+
+
 def test_percentiles_dense_bin_compaction():
     """a8 where one level-0 bin holds ~35 % of the ratio-defined groups as distinct keys
     (perf = 1 - j * 2^-20): the level-1 range is too large to gather, so the device copies the
