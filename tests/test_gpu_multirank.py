@@ -84,6 +84,32 @@ def test_point_sharded_merge(world):
         assert (out["best_block_id"].view(np.uint16) == ref.best_block).all()
 
 
+def test_point_sharded_host_tables():
+    """The e2e leg of bench.py at N > 1: every rank reduces a pinned HOST table of its own
+    points (staged through device scratch by the library) with the point-sharded merge; the
+    merged statistics equal the whole-table oracle (local transport, 2 ranks)."""
+    require_gpu()
+    import torch
+    from paper_2103_14409_b200 import MEM_HOST
+    n, K = 300_000, 1201
+    full = gen_table(n, K, preset="t4", seed=37)
+    ref = OT.reduce_table(full["runtime_ms"], full["block_id"], full["group_offset"],
+                          group_matrix=full["group_matrix"], percentiles=PCTS)
+
+    def make(ctx, r):
+        d = ctx.gen_table(n, K, preset=0, seed=37, block_mod=2, block_rem=r)
+        for k in ("runtime_ms", "block_id", "status", "group_offset", "group_kernel", "group_matrix"):
+            v = getattr(d, k)
+            if v is not None:
+                setattr(d, k, v.cpu().pin_memory())
+        torch.cuda.synchronize()
+        d.mem = MEM_HOST
+        return d
+
+    res = _run_ranks(2, make, dict(point_sharded=1), "psh2")
+    _check(res, ref)
+
+
 @pytest.mark.parametrize("world", [2, 3, 8])
 def test_group_aligned_merge(world):
     require_gpu()
