@@ -128,3 +128,26 @@ def test_gen_shape(lib):
     o = GenOpts(5028536, 19683, 32, 31, 8, 0, 0.03, 4, 0, 0, 4, 1)       # point shard 1 of 4
     assert L.lscat_gen_table_shape(C.byref(o), C.byref(nr), C.byref(ng)) == 0
     assert ng.value == 157142 and nr.value == 157141 * 8 + 6             # last group: 24 rows
+
+
+def test_table_c_view_cache():
+    """The binding's cached C view of a table (reduce calls take a const table): reused while
+    nothing changes, rebuilt after any attribute assignment, and equal to a fresh one."""
+    import torch
+    from paper_2103_14409_b200 import Table
+    n, G = 100, 4
+    t = Table(torch.zeros(n), torch.zeros(n, dtype=torch.int16), None,
+              torch.arange(0, n + 1, n // G, dtype=torch.int64), None, torch.zeros(G, dtype=torch.int32),
+              n_rows=n, n_groups=G)
+    a = t.c_input()
+    assert t.c_input() is a
+    fresh = t.c()
+    for f, _ in fresh._fields_:
+        assert getattr(a, f) == getattr(fresh, f), f
+    t.n_rows = 50
+    b = t.c_input()
+    assert b is not a and b.n_rows == 50
+    t.runtime_ms = torch.zeros(n)
+    c = t.c_input()
+    assert c is not b and c.runtime_ms == t.runtime_ms.data_ptr()
+    assert t.c_input(with_groups=False).group_offset is None
