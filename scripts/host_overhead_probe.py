@@ -32,6 +32,7 @@ res = {}
 res["current_stream"] = t(lambda: torch.cuda.current_stream())
 res["_stream(None)"] = t(lambda: M._stream(None))
 res["table.c"] = t(lambda: tab.c(with_groups=True))
+res["table.c_input"] = t(lambda: tab.c_input(with_groups=True))
 tc = tab.c(with_groups=True)
 oc = M.ReduceOutC()
 sp = M._stream(None)
