@@ -1514,8 +1514,9 @@ __global__ void __launch_bounds__(1024, 1) sel_small(const double* __restrict__ 
   // histogram pass per digit and target).  A bitonic sort of up to 8192 keys took ~20 us and
   // rank counting at n = 1024 as long (issue bound: n compares in every thread).
   __shared__ uint32_t s_dh[256];
-  __shared__ unsigned long long s_pre;
+  __shared__ unsigned long long s_pre, s_surv[kRankCountMax];
   __shared__ uint64_t s_kk;
+  __shared__ uint32_t s_cnt, s_m;
   for (uint32_t r = blockIdx.x; r < nr; r += gridDim.x) {
   const uint32_t n = (uint32_t)min(ss->rcnt[r], (unsigned long long)kSmallCap);
   if (ss->rcnt[r] <= kRankCountMax) {
@@ -1546,10 +1547,16 @@ __global__ void __launch_bounds__(1024, 1) sel_small(const double* __restrict__ 
         if (tid == 0) atomicOr(&ss->fail, 2u);  // keys lost: the host falls back
         continue;
       }
-      if (tid == 0) { s_pre = r_lo[r] & ~((top >= 64) ? ~0ull : ((1ull << top) - 1)); s_kk = k0; }
+      if (tid == 0) { s_pre = r_lo[r] & ~((top >= 64) ? ~0ull : ((1ull << top) - 1)); s_kk = k0; s_cnt = n; }
+      __syncthreads();  // s_cnt is read at the loop head (and the keys are in place)
+      // digits until the keys with the chosen prefix are few: those are then ranked directly
+      // (after the first digit typically ~n / 256 keys remain; each further digit pass costs
+      // three barriers, ~1.4 us)
+      int sh_end = 0;
       for (int sh0 = ((top + 7) / 8) * 8 - 8; sh0 >= 0; sh0 -= 8) {
+        if (s_cnt <= kRankCountMax) { sh_end = sh0 + 8; break; }  // CTA-uniform
         if (tid < 256) s_dh[tid] = 0;
-        __syncthreads();  // (also: the keys and the prefix are in place)
+        __syncthreads();
         const unsigned long long pre = s_pre;
         const unsigned long long hmask = (sh0 + 8 >= 64) ? 0ull : (~0ull << (sh0 + 8));
         // (warp-aggregating these atomics with match.any measured slower: 7.0 -> 7.9 us)
@@ -1577,12 +1584,40 @@ __global__ void __launch_bounds__(1024, 1) sel_small(const double* __restrict__ 
             while (cum + c[q] < kk) cum += c[q++];
             s_pre = (pre & hmask) | ((unsigned long long)(tid * 8 + q) << sh0);
             s_kk = kk - cum;
+            s_cnt = c[q];
           }
         }
         __syncthreads();
       }
-      if (tid == 0) ss->tkey[i] = s_pre;
-      __syncthreads();  // s_pre / s_kk are reset for the next target
+      if (sh_end == 0) {  // every digit chosen: s_pre is the key
+        if (tid == 0) ss->tkey[i] = s_pre;
+      } else {  // rank the s_cnt keys with the prefix above bit sh_end
+        const unsigned long long pmask = sh_end >= 64 ? 0ull : (~0ull << sh_end);
+        const unsigned long long pre = s_pre & pmask;
+        if (tid == 0) s_m = 0;
+        __syncthreads();
+        for (uint32_t j = tid; j < n; j += blockDim.x) {
+          const unsigned long long x = dsm[j];
+          if ((x & pmask) == pre) {
+            const uint32_t at = atomicAdd(&s_m, 1u);
+            if (at < kRankCountMax) s_surv[at] = x;
+          }
+        }
+        __syncthreads();
+        const uint32_t m = s_m;
+        const uint64_t kk = s_kk;
+        if (tid == 0 && (m > kRankCountMax || !(kk >= 1 && kk <= m))) atomicOr(&ss->fail, 2u);  // keys lost
+        if (tid < (int)m && m <= kRankCountMax) {  // the survivors' order is arbitrary; the value is unique
+          const unsigned long long x = s_surv[tid];
+          uint32_t rank = 0;
+          for (uint32_t j = 0; j < m; j++) {
+            const unsigned long long y = s_surv[j];
+            rank += (y < x) || (y == x && j < (uint32_t)tid);
+          }
+          if (rank + 1 == kk) ss->tkey[i] = x;
+        }
+      }
+      __syncthreads();  // s_pre / s_kk / s_cnt / s_surv are reset for the next target
     }
   }
   __syncthreads();  // the next range reuses dsm
