@@ -1289,7 +1289,7 @@ __global__ void __launch_bounds__(1024, 1) sel_small(const double* __restrict__ 
   cg::grid_group grid = cg::this_grid();
   extern __shared__ unsigned long long dsm[];  // 64 KB: histograms (u32), prefix (u32), sort (u64)
   uint32_t* sh = reinterpret_cast<uint32_t*>(dsm);
-  __shared__ uint32_t wsum[32];
+  __shared__ uint32_t wsum[32], wsum2[32];
   __shared__ uint64_t s_lo[kMaxT], s_hi[kMaxT], s_k[kMaxT];
   __shared__ uint32_t s_done[kMaxT], s_first[kMaxT], s_range[kMaxT];
   __shared__ uint64_t r_lo[kMaxT], r_hi[kMaxT];
@@ -1330,32 +1330,51 @@ __global__ void __launch_bounds__(1024, 1) sel_small(const double* __restrict__ 
   // Both histograms are staged in shared memory with coalesced loads first: the scan's
   // thread-contiguous reads straight from L2 (4-byte lanes at a 32-byte stride) fetched every
   // sector 8 times, 512 KB per CTA (5.8 us of the kernel on configs[3], LSCAT_SEL_DEBUG stamps).
-  for (uint32_t i = tid; i < 2 * kBins; i += blockDim.x) sh[i] = __ldcg(&ss->hist[0][0] + i);
-  __syncthreads();
-  for (uint32_t w = 0; w < 2; w++) {  // inclusive scan of hist[w] into sh[w * kBins ..], in place
-    constexpr int kPer = kBins / 1024;
-    uint32_t c[kPer], sum = 0;
+  {
+    constexpr int kL = 2 * kBins / 1024;  // 1024 threads (the scans below assume it too)
+    uint32_t v[kL];
 #pragma unroll
-    for (int j = 0; j < kPer; j++) { c[j] = sh[w * kBins + tid * kPer + j]; sum += c[j]; }
-    uint32_t inc = sum;
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(FULL, inc, o);
-      if (lane >= o) inc += y;
+    for (int j = 0; j < kL; j++) v[j] = __ldcg(&ss->hist[0][0] + j * 1024 + tid);  // all in flight
+#pragma unroll
+    for (int j = 0; j < kL; j++) sh[j * 1024 + tid] = v[j];
+  }
+  __syncthreads();
+  {  // inclusive scans of hist[0] and hist[1] into sh[w * kBins ..], in place, both at once
+    constexpr int kPer = kBins / 1024;
+    uint32_t c[2][kPer], sum[2] = {0u, 0u}, inc[2];
+#pragma unroll
+    for (int w = 0; w < 2; w++) {
+#pragma unroll
+      for (int j = 0; j < kPer; j++) { c[w][j] = sh[w * kBins + tid * kPer + j]; sum[w] += c[w][j]; }
+      inc[w] = sum[w];
     }
-    if (lane == 31) wsum[tid >> 5] = inc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y0 = __shfl_up_sync(FULL, inc[0], o), y1 = __shfl_up_sync(FULL, inc[1], o);
+      if (lane >= o) { inc[0] += y0; inc[1] += y1; }
+    }
+    if (lane == 31) { wsum[tid >> 5] = inc[0]; wsum2[tid >> 5] = inc[1]; }
     __syncthreads();
     if (tid < 32) {
-      uint32_t x = wsum[tid];
+      uint32_t x0 = wsum[tid], x1 = wsum2[tid];
+#pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(FULL, x, o);
-        if (tid >= o) x += y;
+        const uint32_t y0 = __shfl_up_sync(FULL, x0, o), y1 = __shfl_up_sync(FULL, x1, o);
+        if (tid >= o) { x0 += y0; x1 += y1; }
       }
-      wsum[tid] = x;
+      wsum[tid] = x0;
+      wsum2[tid] = x1;
     }
     __syncthreads();
-    uint32_t run = inc - sum + ((tid >> 5) ? wsum[(tid >> 5) - 1] : 0u);
+    uint32_t run0 = inc[0] - sum[0] + ((tid >> 5) ? wsum[(tid >> 5) - 1] : 0u);
+    uint32_t run1 = inc[1] - sum[1] + ((tid >> 5) ? wsum2[(tid >> 5) - 1] : 0u);
 #pragma unroll
-    for (int j = 0; j < kPer; j++) { run += c[j]; sh[w * kBins + tid * kPer + j] = run; }
+    for (int j = 0; j < kPer; j++) {
+      run0 += c[0][j];
+      run1 += c[1][j];
+      sh[tid * kPer + j] = run0;
+      sh[kBins + tid * kPer + j] = run1;
+    }
     __syncthreads();
   }
   stamp(3);
