@@ -1843,39 +1843,65 @@ __global__ void __launch_bounds__(1024, 1) sel_finish(const SelState* __restrict
   stamp(2);
   if (__ldcg(&fs->fail)) return;  // grid-uniform (written before the barrier)
   // phase 3 (every CTA, identically): distinct open sub-ranges; gather their keys
-  if (tid < (int)nt) {
-    const bool open = s_topen[tid];
-    q_lo[tid] = open ? __ldcg(&fs->tlo[tid]) : 0ull;
-    q_hi[tid] = open ? __ldcg(&fs->thi[tid]) : 0ull;
-    q_w[tid] = s_tw[tid];
-    s_first[tid] = open && q_hi[tid] != q_lo[tid];
-  }
-  __syncthreads();
-  const bool mine_first = tid < (int)nt && s_first[tid];
-  bool dup = false;
-  if (mine_first)
-    for (int j = 0; j < tid; j++)
-      if (s_first[j] && q_w[j] == q_w[tid] && q_lo[j] == q_lo[tid] && q_hi[j] == q_hi[tid]) { dup = true; break; }
-  __syncthreads();
-  if (mine_first && dup) s_first[tid] = 0;
-  __syncthreads();
-  if (tid < (int)nt) {  // sub-range id of every open target (its first occurrence's rank)
-    uint32_t q = 0xFFFFFFFFu;
-    if (s_topen[tid] && q_hi[tid] != q_lo[tid]) {
-      uint32_t src = tid;
-      for (int j = 0; j < tid; j++)
-        if (s_first[j] && q_w[j] == q_w[tid] && q_lo[j] == q_lo[tid] && q_hi[j] == q_hi[tid]) { src = j; break; }
-      q = 0;
-      for (uint32_t j = 0; j < src; j++) q += s_first[j];
+  if (nt <= 32) {
+    // one warp, lane i = target i: first occurrences and sub-range ids from match_any / ballot
+    // (the same values as the general path below, without its O(nt^2) loops between barriers)
+    if (tid < 32) {
+      const bool act = tid < (int)nt;
+      const bool open = act && s_topen[tid];
+      const uint64_t lo = open ? __ldcg(&fs->tlo[tid]) : 0ull, hi = open ? __ldcg(&fs->thi[tid]) : 0ull;
+      const uint32_t w = act ? s_tw[tid] : 0u;
+      const bool cand = open && hi != lo;
+      const unsigned m = __match_any_sync(FULL, lo) & __match_any_sync(FULL, hi) &
+                         __match_any_sync(FULL, cand ? w : 2u + (uint32_t)tid);
+      const int src = __ffs(m) - 1;
+      const bool first = cand && src == tid;
+      const unsigned firsts = __ballot_sync(FULL, first);
+      if (act) {
+        q_lo[tid] = lo;
+        q_hi[tid] = hi;
+        q_w[tid] = w;
+        s_first[tid] = first;
+        s_qr[tid] = cand ? (uint32_t)__popc(firsts & ((1u << src) - 1u)) : 0xFFFFFFFFu;
+      }
+      if (tid == 0) s_nq = (uint32_t)__popc(firsts);
     }
-    s_qr[tid] = q;
+    __syncthreads();
+  } else {
+    if (tid < (int)nt) {
+      const bool open = s_topen[tid];
+      q_lo[tid] = open ? __ldcg(&fs->tlo[tid]) : 0ull;
+      q_hi[tid] = open ? __ldcg(&fs->thi[tid]) : 0ull;
+      q_w[tid] = s_tw[tid];
+      s_first[tid] = open && q_hi[tid] != q_lo[tid];
+    }
+    __syncthreads();
+    const bool mine_first = tid < (int)nt && s_first[tid];
+    bool dup = false;
+    if (mine_first)
+      for (int j = 0; j < tid; j++)
+        if (s_first[j] && q_w[j] == q_w[tid] && q_lo[j] == q_lo[tid] && q_hi[j] == q_hi[tid]) { dup = true; break; }
+    __syncthreads();
+    if (mine_first && dup) s_first[tid] = 0;
+    __syncthreads();
+    if (tid < (int)nt) {  // sub-range id of every open target (its first occurrence's rank)
+      uint32_t q = 0xFFFFFFFFu;
+      if (s_topen[tid] && q_hi[tid] != q_lo[tid]) {
+        uint32_t src = tid;
+        for (int j = 0; j < tid; j++)
+          if (s_first[j] && q_w[j] == q_w[tid] && q_lo[j] == q_lo[tid] && q_hi[j] == q_hi[tid]) { src = j; break; }
+        q = 0;
+        for (uint32_t j = 0; j < src; j++) q += s_first[j];
+      }
+      s_qr[tid] = q;
+    }
+    if (tid == 0) {
+      uint32_t n = 0;
+      for (uint32_t j = 0; j < nt; j++) n += s_first[j];
+      s_nq = n;
+    }
+    __syncthreads();
   }
-  if (tid == 0) {
-    uint32_t n = 0;
-    for (uint32_t j = 0; j < nt; j++) n += s_first[j];
-    s_nq = n;
-  }
-  __syncthreads();
   // compact the distinct sub-ranges to the front: sub-range q = the q-th first occurrence
   __shared__ uint64_t g_lo[kMaxT], g_hi[kMaxT];
   __shared__ uint32_t g_w[kMaxT];
