@@ -141,11 +141,18 @@ __device__ __forceinline__ uint64_t t_count(const SelState* st, int i) { return 
 
 // Merge the open targets into disjoint ranges sorted by (which, lo).  One CTA; thread i < nt
 // owns target i.  Called by sel_init and by the last CTA of sel_resolve.
+__device__ void plan_ranges_warp(SelState* st, uint32_t cap, int nt);
+
 __device__ void plan_ranges(SelState* st, uint32_t cap) {
   __shared__ uint64_t slo[kMaxT], shi[kMaxT];
   __shared__ uint32_t sw[kMaxT], sopen[kMaxT], sfirst[kMaxT];
   const int i = threadIdx.x;
   const int nt = (int)st->nt;
+  if (nt <= 32) {  // one warp (every thread of the CTA calls this)
+    if (i < 32) plan_ranges_warp(st, cap, nt);
+    __syncthreads();
+    return;
+  }
   bool open = false;
   if (i < nt) {
     Tgt& t = st->t[i];
@@ -190,6 +197,69 @@ __device__ void plan_ranges(SelState* st, uint32_t cap) {
       st->compact = 0;
     } else if (st->src == 0 && nr > 0 && s_keys[0] <= kCompactCap && s_keys[1] <= kCompactCap &&
                2 * (s_keys[0] + s_keys[1]) <= st->n_def) {
+      st->compact = 1;
+      st->nc[0] = st->nc[1] = 0;
+    }
+  }
+}
+
+// plan_ranges for <= 32 targets in one warp (lane i = target i): the same ranges, range ids
+// (rank by (which, lo) among the first occurrences) and counters, from match_any / ballot and
+// shuffles instead of O(nt^2) shared-memory loops between barriers.
+__device__ void plan_ranges_warp(SelState* st, uint32_t cap, int nt) {
+  const unsigned FULL = 0xffffffffu;
+  const int i = threadIdx.x;
+  const bool act = i < nt;
+  uint64_t lo = 0, hi = 0, cnt = 0;
+  uint32_t w = 0;
+  bool open = false;
+  if (act) {
+    Tgt& t = st->t[i];
+    if (!t.done && t.lo == t.hi) { t.done = 1; t.key = t.lo; }
+    open = !t.done;
+    lo = t.lo;
+    hi = t.hi;
+    w = t.which;
+    cnt = t.count;
+  }
+  const unsigned m = __match_any_sync(FULL, lo) & __match_any_sync(FULL, hi) &
+                     __match_any_sync(FULL, open ? w : 2u + (uint32_t)i);
+  const bool first = open && __ffs(m) - 1 == i;
+  const unsigned firsts = __ballot_sync(FULL, first);
+  const uint32_t nr = (uint32_t)__popc(firsts);
+  const uint32_t nw0 = (uint32_t)__popc(__ballot_sync(FULL, first && w == 0));
+  const uint32_t nopen = (uint32_t)__popc(__ballot_sync(FULL, open));
+  uint32_t rank = 0;
+  for (unsigned f = firsts; f; f &= f - 1) {  // warp-uniform
+    const int j = __ffs(f) - 1;
+    const uint32_t wj = __shfl_sync(FULL, w, j);
+    const uint64_t lj = __shfl_sync(FULL, lo, j);
+    rank += (wj < w || (wj == w && lj < lo)) ? 1u : 0u;
+  }
+  bool gather = true;
+  if (open) {
+    st->t[i].range = rank;
+    if (first) {
+      const Range R = make_range(lo, hi, cnt, w, cap);
+      st->r[rank] = R;
+      gather = R.gather;
+    }
+  }
+  // keys of the non-gather ranges per quantity (the compaction decision below)
+  unsigned long long k0 = (first && !gather && w == 0) ? cnt : 0ull, k1 = (first && !gather && w == 1) ? cnt : 0ull;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    k0 += __shfl_xor_sync(FULL, k0, o);
+    k1 += __shfl_xor_sync(FULL, k1, o);
+  }
+  if (i == 0) {
+    st->nr = nr;
+    st->nw0 = nw0;
+    st->open = nopen;
+    if (st->compact) {  // the pass that just ran copied the keys: read the copies from now on
+      st->src = 1;
+      st->compact = 0;
+    } else if (st->src == 0 && nr > 0 && k0 <= kCompactCap && k1 <= kCompactCap && 2 * (k0 + k1) <= st->n_def) {
       st->compact = 1;
       st->nc[0] = st->nc[1] = 0;
     }
