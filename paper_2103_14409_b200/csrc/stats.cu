@@ -737,6 +737,7 @@ struct SampPlan {
   unsigned long long ncopy_all[2];             // keys copied over all ranks (overflow check)
   uint32_t cnt[2][kSpCnt];                     // exact counts: slots, then gaps
   uint16_t map[2][kFxBins];                    // per fixed bin: kSpSlotFlag | slot, or its gap
+  unsigned long long stamp[6];                 // %globaltimer in sel_plan_sampled (debug)
 };
 
 __device__ __forceinline__ bool valid_key(uint64_t k) { return k < 0x7FF0000000000000ull; }
@@ -842,7 +843,16 @@ __global__ void __launch_bounds__(1024) sel_plan_sampled(SampPlan* __restrict__ 
   __shared__ uint32_t tb1[kMaxT], tb2[kMaxT];
   __shared__ uint32_t s_b1[2][kIvQ], s_b2[2][kIvQ], s_slot0[2][kIvQ], s_niv[2];
   const int tid = threadIdx.x;
+  auto stamp = [&](int i) {
+    if (tid == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      sp->stamp[i] = t;
+    }
+  };
+  stamp(0);
   for (uint32_t w = 0; w < 2; w++) scan_bins(shist + w * kFxBins, 0ull, w, pre[w], part);
+  stamp(1);
   if (tid < (int)(2 * npct)) {
     const uint32_t w = tid >= (int)npct;
     const unsigned long long* P = pre[w];
@@ -864,6 +874,7 @@ __global__ void __launch_bounds__(1024) sel_plan_sampled(SampPlan* __restrict__ 
     tb2[tid] = b2;
   }
   __syncthreads();
+  stamp(2);
   // per quantity: the targets' non-empty intervals sorted by (b1, target) by a parallel rank
   // count, then merged (overlapping / adjacent) by one thread over the sorted shared arrays
   __shared__ uint32_t srt1[kMaxT], srt2[kMaxT], s_n[2];
@@ -925,16 +936,25 @@ __global__ void __launch_bounds__(1024) sel_plan_sampled(SampPlan* __restrict__ 
       sp->ncopy_all[w] = 0;
     }
   }
+  stamp(3);
+  // per fixed bin: its slot, or its gap = the number of intervals entirely below it; branch-free
+  // over the (sorted, disjoint) intervals of its quantity (the early-exit loop of dependent
+  // shared loads took ~3.7 us)
   for (uint32_t i = tid; i < 2 * kFxBins; i += blockDim.x) {
-    const uint32_t w = i / kFxBins, b = i % kFxBins;
-    uint32_t e = 0;  // gap = intervals entirely below b
-    for (uint32_t r = 0; r < s_niv[w]; r++) {
-      if (b > s_b2[w][r]) e = r + 1;
-      else if (b >= s_b1[w][r]) { e = kSpSlotFlag | (s_slot0[w][r] + b - s_b1[w][r]); break; }
+    const uint32_t w = i / kFxBins, b = i % kFxBins, niv = s_niv[w];
+    uint32_t below = 0, slot = 0xFFFFFFFFu;
+#pragma unroll
+    for (uint32_t r = 0; r < (uint32_t)kIvQ; r++) {
+      const bool v = r < niv;
+      const uint32_t b1 = s_b1[w][r], b2 = s_b2[w][r];
+      below += (v && b > b2) ? 1u : 0u;
+      if (v && b >= b1 && b <= b2) slot = s_slot0[w][r] + b - b1;
     }
-    sp->map[w][b] = (uint16_t)e;
+    sp->map[w][b] = (uint16_t)(slot != 0xFFFFFFFFu ? (kSpSlotFlag | slot) : below);
   }
   for (uint32_t i = tid; i < 2 * kSpCnt; i += blockDim.x) (&sp->cnt[0][0])[i] = 0;
+  __syncthreads();
+  stamp(4);
 }
 
 // One pass over this rank's keys (kU per quantity in flight per thread, full tiles without
@@ -2534,6 +2554,10 @@ lscat_status select_percentiles(lscat_ctx* ctx, const double* pct, uint32_t npct
       for (uint32_t w = 0; w < 2; w++) {
         unsigned long long sum = 0;
         for (uint32_t i = 0; i < kSpCnt; i++) sum += f.cnt[w][i];
+        if (w == 0)
+          fprintf(stderr, "plan phases(ns): scans %lld targets %lld merge %lld map %lld\n",
+                  (long long)(f.stamp[1] - f.stamp[0]), (long long)(f.stamp[2] - f.stamp[1]),
+                  (long long)(f.stamp[3] - f.stamp[2]), (long long)(f.stamp[4] - f.stamp[3]));
         fprintf(stderr, "samp q%u: fail %u niv %u nslot %u ncopy %llu counted %llu intervals", w, f.fail,
                 f.niv[w], f.nslot[w], f.ncopy[w], sum);
         for (uint32_t r = 0; r < f.niv[w]; r++) fprintf(stderr, " [%u,%u]", f.b1[w][r], f.b2[w][r]);
