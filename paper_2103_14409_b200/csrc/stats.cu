@@ -740,6 +740,27 @@ struct SampPlan {
   unsigned long long stamp[6];                 // %globaltimer in sel_plan_sampled (debug)
 };
 
+// Programmatic dependent launch between the sampled path's kernels on one rank: the next kernel
+// is launched while its producer drains and waits here for the producer's completion and
+// memory (no early trigger: the kernels never overlap).  A no-op without the launch attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                       Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 __device__ __forceinline__ bool valid_key(uint64_t k) { return k < 0x7FF0000000000000ull; }
 __device__ __forceinline__ bool virtual_bin(uint32_t w, uint32_t b) { return w == 0 ? b == kFxBins - 2 : b == 0; }
 __device__ __forceinline__ uint32_t fx_bin(uint32_t w, uint64_t k) { return w == 0 ? fx_perf_bin(k) : fx_gain_bin(k); }
@@ -838,6 +859,7 @@ __device__ __forceinline__ uint32_t first_reaching(const unsigned long long* P, 
 __global__ void __launch_bounds__(1024) sel_plan_sampled(SampPlan* __restrict__ sp,
                                                        const uint32_t* __restrict__ shist, PctArg pct,
                                                        uint32_t npct, double dmul, double dadd) {
+  pdl_wait();  // launched with programmatic stream serialization after its producer (one rank)
   __shared__ unsigned long long pre[2][kFxBins];
   __shared__ unsigned long long part[32 + 1024];
   __shared__ uint32_t tb1[kMaxT], tb2[kMaxT];
@@ -978,6 +1000,7 @@ __global__ void __launch_bounds__(kT, SP_MINB) sel_pass_sampled(const double* __
                                                        const double* __restrict__ gain, uint64_t lo,
                                                        uint64_t hi, SampPlan* __restrict__ sp,
                                                        double* __restrict__ cbuf) {
+  pdl_wait();  // launched with programmatic stream serialization after its producer (one rank)
   constexpr int kU = 8, kFlushTiles = 7;
   static_assert(kFlushTiles * kU < 64, "6-bit gap fields");
   // per fixed bin (+ an entry for uncounted keys) one word: the slot flag in bit 63, else the
@@ -1155,6 +1178,7 @@ __global__ void __launch_bounds__(kT, SP_MINB) sel_pass_sampled(const double* __
 // flushed once.  Cheaper than a shared atomic per slot key inside the pass (measured: the
 // pass 162 -> 142 us at 10^9 rows without them).
 __global__ void __launch_bounds__(256) sel_slot_counts(const double* __restrict__ cbuf, SampPlan* __restrict__ sp) {
+  pdl_wait();  // launched with programmatic stream serialization after its producer (one rank)
   __shared__ uint16_t map[2][kFxBins];
   __shared__ uint32_t h[2][kSpSlots];
   for (uint32_t i = threadIdx.x; i < 2 * kFxBins; i += blockDim.x) (&map[0][0])[i] = (&sp->map[0][0])[i];
@@ -1198,6 +1222,7 @@ __global__ void __launch_bounds__(1024) sel_check_sampled(SelState* st, const Sa
                                                         const uint64_t* __restrict__ partials, uint32_t nb,
                                                         const uint64_t* __restrict__ mm, PctArg pct,
                                                         uint32_t npct, uint32_t cap, uint32_t force_miss) {
+  pdl_wait();  // launched with programmatic stream serialization after its producer (one rank)
   __shared__ unsigned long long pre[2][2048];
   __shared__ uint16_t sbin[2][2048];  // bin of a slot / the single-valued bin; 0xFFFF: a gap
   __shared__ unsigned long long wsum[32];
@@ -2144,9 +2169,12 @@ std::vector<std::pair<const char*, cudaEvent_t>>& sel_events() {
   static std::vector<std::pair<const char*, cudaEvent_t>> v;
   return v;
 }
-void sel_mark(const char* name, cudaStream_t q) {
+bool sel_timing_on() {
   static const bool on = getenv("LSCAT_SEL_TIMING") != nullptr;
-  if (!on) return;
+  return on;
+}
+void sel_mark(const char* name, cudaStream_t q) {
+  if (!sel_timing_on()) return;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(q, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
   cudaEvent_t e;
@@ -2193,8 +2221,8 @@ lscat_status enqueue_sampled(lscat_ctx* ctx, const SelBufs& B, const double* per
     lscat_status ns = ctx->comm->allreduce(ctx, {{B.shist, 2 * (size_t)kFxBins, DT::U32, Op::Sum}}, q);
     if (ns) return ns;
   }
-  sel_plan_sampled<<<1, 1024, 0, q>>>(B.sp, B.shist, pa, npct, 4.5, 32.0);
-  LSCAT_CUDA(ctx, cudaGetLastError());
+  const bool pdl = world == 1 && !sel_timing_on();  // (stage events between the kernels: plain launches)
+  LSCAT_CUDA(ctx, launch_pdl(sel_plan_sampled, dim3(1), dim3(1024), 0, q, pdl, B.sp, B.shist, pa, npct, 4.5, 32.0));
   sel_mark("plan", q);
   static const int occ_p = [] {  // resident CTAs per SM of the pass (binary property; one-time)
     int v = 0;
@@ -2204,11 +2232,10 @@ lscat_status enqueue_sampled(lscat_ctx* ctx, const SelBufs& B, const double* per
   }();
   const int grid_p = (int)std::min<uint64_t>(std::max<uint64_t>(1, (n + 256 * 8 - 1) / (256 * 8)),
                                              (uint64_t)ctx->sm_count * occ_p);
-  sel_pass_sampled<256><<<grid_p, 256, 0, q>>>(perf, gain, lo, hi, B.sp, B.cbuf);
-  LSCAT_CUDA(ctx, cudaGetLastError());
+  LSCAT_CUDA(ctx, launch_pdl(sel_pass_sampled<256>, dim3(grid_p), dim3(256), 0, q, pdl, perf, gain, lo, hi, B.sp, B.cbuf));
   sel_mark("pass", q);
-  sel_slot_counts<<<ctx->sm_count * 4, 256, 0, q>>>(B.cbuf, B.sp);  // latency bound: 4 CTAs per SM
-  LSCAT_CUDA(ctx, cudaGetLastError());
+  LSCAT_CUDA(ctx, launch_pdl(sel_slot_counts, dim3(ctx->sm_count * 4), dim3(256), 0, q, pdl,  // 4 CTAs per SM
+                             B.cbuf, B.sp));
   sel_mark("slots", q);
   if (world > 1) {  // exact counts and copy totals over all ranks
     lscat_status ns = ctx->comm->allreduce(ctx, {{&B.sp->cnt[0][0], 2 * (size_t)kSpCnt, DT::U32, Op::Sum},
@@ -2217,8 +2244,8 @@ lscat_status enqueue_sampled(lscat_ctx* ctx, const SelBufs& B, const double* per
   }
   // LSCAT_SEL_FORCE_MISS=1 (tests): every sampled first level reports a miss
   static const uint32_t force_miss = getenv("LSCAT_SEL_FORCE_MISS") != nullptr ? 1u : 0u;
-  sel_check_sampled<<<1, 1024, 0, q>>>(B.st, B.sp, partials, nb, mm, pa, npct, cap, force_miss);
-  LSCAT_CUDA(ctx, cudaGetLastError());
+  LSCAT_CUDA(ctx, launch_pdl(sel_check_sampled, dim3(1), dim3(1024), 0, q, pdl && world == 1, B.st, B.sp, partials,
+                             nb, mm, pa, npct, cap, force_miss));
   sel_mark("check", q);
   if (fin) {  // sel_finish follows; the state as the check left it
     LSCAT_CUDA(ctx, cudaMemsetAsync(B.fs, 0, sizeof(FinSel), q));
