@@ -1767,7 +1767,8 @@ __global__ void __launch_bounds__(1024, 1) sel_small(const double* __restrict__ 
 // cheaper grid barriers).  Calibration on configs[2]/[3] (LSCAT_SMALL_KEYS_PER_CTA = 512 / 2048
 // / 4096 / 8192 / 16384): reduce + early selection 0.090 / 0.091 / 0.101 / 0.106 / 0.127 ms and
 // 0.116 / 0.116 / 0.119 / 0.130 / 0.155 ms (profiles/r02_sel_small_grid.txt): the CTAs' loads
-// in flight win over the flush and barrier costs.
+// in flight win over the flush and barrier costs.  Re-checked after the session-3 rework
+// (256 / 512 / 1024 / 2048): 71.6-76.5 / 83.0-86.8 us, within the run-to-run spread.
 uint32_t small_grid(const lscat_ctx* ctx, uint64_t n) {
   static const uint64_t per = [] {
     const char* e = getenv("LSCAT_SMALL_KEYS_PER_CTA");
